@@ -1,0 +1,121 @@
+"""ORACLE — TEST INFRASTRUCTURE ONLY.
+
+Plain CPU references for symmetric sparse MTTKRP (SySTeC, arXiv 2406.09266).
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s
+``cpu_baseline`` / ``--impl reference`` leg may import this package.  It shares
+no code with the CUDA path (``paper_2406_09266_b200``) and never imports it.
+
+* :func:`mttkrp` / :func:`mttkrp_rows` — the expansion oracle (plain C,
+  ``mttkrp_oracle.c``): every stored canonical entry is expanded to its
+  distinct permutations and the naive non-symmetric MTTKRP runs in fp64
+  (north_star; PAPER.md:859-865 for the MTTKRP definition
+  for "as many assignments as unique permutations").  Also returns S, the sum
+  of absolute terms used to normalise the parity error.
+* :mod:`oracle.symmetric_ref` — the per-position multiplicity-coefficient
+  formula, written independently in fp64 numpy (pin P4 of SURVEY.md §8(c)).
+
+Pins: see tests/test_oracle_pins.py (P1-P10).  No function here is "parity
+unpinned".
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "mttkrp_oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+_lib = None
+
+
+def build(force: bool = False) -> str:
+    """Compile the plain-C oracle with gcc (no GPU code involved)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + f".{os.getpid()}.tmp"
+        subprocess.check_call(["gcc", "-O2", "-std=c11", "-fPIC", "-shared", "-pthread",
+                               "-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        build()
+        lib = ctypes.CDLL(_LIB)
+        i64, i32, vp = ctypes.c_int64, ctypes.c_int, ctypes.c_void_p
+        lib.oracle_mttkrp.argtypes = [i32, i64, i64, vp, vp, vp, i32, vp, vp, i32, i64]
+        lib.oracle_mttkrp.restype = i32
+        lib.oracle_mttkrp_rows.argtypes = [i32, i64, i64, vp, vp, vp, i32, i64, vp, vp, vp, i32]
+        lib.oracle_mttkrp_rows.restype = i32
+        lib.oracle_count_expanded.argtypes = [i32, i64, vp]
+        lib.oracle_count_expanded.restype = i64
+        _lib = lib
+    return _lib
+
+
+def default_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def _prep(order, idx, vals, B):
+    idx = np.ascontiguousarray(idx, dtype=np.int32).reshape(-1, order)
+    vals = np.ascontiguousarray(vals, dtype=np.float32).reshape(-1)
+    B = np.ascontiguousarray(B, dtype=np.float32)
+    if vals.shape[0] != idx.shape[0]:
+        raise ValueError("idx and vals disagree on nnz")
+    if B.ndim != 2:
+        raise ValueError("B must be [dim][R]")
+    return idx, vals, B
+
+
+def _ptr(a):
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+def mttkrp(order: int, dim: int, idx, vals, B, threads: int | None = None,
+           mem_budget_bytes: int = 0):
+    """Expansion oracle.  Returns (C, S), fp64 [dim][R]."""
+    idx, vals, B = _prep(order, idx, vals, B)
+    if B.shape[0] != dim:
+        raise ValueError("B must have dim rows")
+    R = B.shape[1]
+    C = np.empty((dim, R), np.float64)
+    S = np.empty((dim, R), np.float64)
+    T = threads if threads else default_threads()
+    rc = _load().oracle_mttkrp(order, dim, idx.shape[0], _ptr(idx), _ptr(vals), _ptr(B), R,
+                               _ptr(C), _ptr(S), T, mem_budget_bytes)
+    if rc == 3:
+        raise IndexError("index outside [0, dim)")
+    if rc != 0:
+        raise RuntimeError(f"oracle_mttkrp failed with status {rc}")
+    return C, S
+
+
+def mttkrp_rows(order: int, dim: int, idx, vals, B, rows, threads: int | None = None):
+    """Expansion oracle restricted to output rows ``rows``: (C, S) [len(rows)][R]."""
+    idx, vals, B = _prep(order, idx, vals, B)
+    rows = np.ascontiguousarray(rows, dtype=np.int64)
+    R = B.shape[1]
+    C = np.empty((rows.shape[0], R), np.float64)
+    S = np.empty((rows.shape[0], R), np.float64)
+    T = threads if threads else default_threads()
+    rc = _load().oracle_mttkrp_rows(order, dim, idx.shape[0], _ptr(idx), _ptr(vals), _ptr(B), R,
+                                    rows.shape[0], _ptr(rows), _ptr(C), _ptr(S), T)
+    if rc == 3:
+        raise IndexError("index outside [0, dim)")
+    if rc != 0:
+        raise RuntimeError(f"oracle_mttkrp_rows failed with status {rc}")
+    return C, S
+
+
+def count_expanded(order: int, idx) -> int:
+    """Σ over entries of the number of distinct permutations (expanded nnz)."""
+    idx = np.ascontiguousarray(idx, dtype=np.int32).reshape(-1, order)
+    return int(_load().oracle_count_expanded(order, idx.shape[0], _ptr(idx)))
