@@ -1,0 +1,344 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 symmetric sparse MTTKRP (SySTeC hot path).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl systec|reference]
+
+A step = one execute of the whole hot path on one batch: zero C + the MTTKRP
+kernel over every stored non-zero of the config (inputs resident in HBM, the
+plan — canonicalised sorted stream — built once before timing, as the paper
+excludes rearrangement).  With N > 1 (torchrun) the sorted
+stream is split into N contiguous nnz-balanced slices, each rank computes a
+partial C, and C is summed with one NCCL all-reduce per step:
+strong scaling of one problem.
+
+Prints ONE JSON line on rank 0.  See DESIGN.md §Measurement for every field.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "stored nonzeros/sec and achieved HBM GB/s (fraction of roofline) for symmetric MTTKRP"
+UNIT = "nnz/s"
+L2_FLUSH_BYTES = 256 << 20
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--impl", default="systec", choices=["systec", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--opts", default="", help="kernel options, e.g. K=33,stages=2,pos1_accumulate=1")
+    return ap.parse_args()
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def load_traffic(config):
+    """DRAM bytes per launch of the kernel from the committed ncu summary."""
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d.get(config, {}).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, index=0, period=0.02):
+        self.samples, self.reasons, self.max_mhz = [], 0, None
+        self.period, self.index = period, index
+        self._stop = threading.Event()
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            pass
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                self.reasons |= int(self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h))
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def report(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml unavailable"], "samples": 0}
+        names = [n for b, n in self.REASONS.items() if self.reasons & b and n != "gpu_idle"]
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": names, "samples": len(self.samples)}
+
+
+def bytes_eff(order, nnz, G, R, dim):
+    """SURVEY.md §8(d) / DESIGN.md: indices + values + one B row per distinct
+    index of each stored entry + one write of C."""
+    return nnz * (4 * order + 4) + G * R * 4 + dim * R * 4
+
+
+def cpu_baseline(w, target_wall=4.0, max_entries=None):
+    """The oracle as it stands on the host cores, on a bounded sample (the
+    first m stored entries), scaled up until one run takes ~target_wall s."""
+    import oracle
+    T = oracle.default_threads()
+    m = min(w.nnz, 50_000)
+    while True:
+        t0 = time.perf_counter()
+        oracle.mttkrp(w.order, w.dim, w.idx[:m], w.vals[:m], w.B, threads=T)
+        dt = time.perf_counter() - t0
+        if dt >= target_wall or m >= w.nnz or (max_entries and m >= max_entries):
+            break
+        m = min(w.nnz, int(m * max(2.0, min(8.0, target_wall / max(dt, 1e-3)))))
+    return {"value": m / dt, "unit": UNIT, "cores": T, "kind": "oracle",
+            "sample": f"first {m} of {w.nnz} stored entries of {w.name} (sorted order), "
+                      f"full expansion + fp64 accumulation into [dim][R], {dt:.2f} s wall on {T} threads"}
+
+
+def run_reference(args, w):
+    """--impl reference: the oracle, as it stands, on the host cores."""
+    import oracle
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    T = oracle.default_threads()
+    budget = 150.0 / max(1, args.steps + args.warmup)           # seconds per step
+    m = min(w.nnz, 20_000)
+    while True:                                                   # calibrate the sample
+        t0 = time.perf_counter()
+        oracle.mttkrp(w.order, w.dim, w.idx[:m], w.vals[:m], w.B, threads=T)
+        dt = time.perf_counter() - t0
+        if dt >= 0.5 * budget or m >= w.nnz:
+            break
+        m = min(w.nnz, int(m * max(2.0, min(8.0, 0.6 * budget / max(dt, 1e-3)))))
+    for _ in range(args.warmup):
+        oracle.mttkrp(w.order, w.dim, w.idx[:m], w.vals[:m], w.B, threads=T)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        oracle.mttkrp(w.order, w.dim, w.idx[:m], w.vals[:m], w.B, threads=T)
+        times.append(time.perf_counter() - t0)
+    tot = sum(times)
+    value = m * args.steps / tot
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": config_dict(w, args),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": T, "kind": "oracle",
+                             "sample": f"first {m} of {w.nnz} stored entries per step"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def config_dict(w, args):
+    from synth import CONFIGS
+    return {"workload": f"{w.name}: {CONFIGS[w.name].describe}" if w.name in CONFIGS else w.name,
+            "order": w.order, "dim": w.dim, "nnz": w.nnz, "R": w.R,
+            "l2": "flushed between timed steps (256 MiB write outside the events)",
+            "parallelism": f"nnz-slices x{args.gpus} + all-reduce(C)" if args.gpus > 1 else "1 GPU"}
+
+
+def parse_opts(s):
+    out = {}
+    for kv in filter(None, s.split(",")):
+        k, v = kv.split("=")
+        out[k.strip()] = int(v)
+    return out
+
+
+def main():
+    args = parse()
+    from synth import generate
+    w = generate(args.config)
+    if args.impl == "reference":
+        run_reference(args, w)
+        return
+
+    import torch
+    import paper_2406_09266_b200 as systec
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream()
+
+    # this rank's slice of the sorted stream (whole stream at N = 1)
+    lo, hi = w.nnz * rank // world, w.nnz * (rank + 1) // world
+    idx_d = torch.from_numpy(w.idx[lo:hi]).to(dev)
+    vals_d = torch.from_numpy(w.vals[lo:hi]).to(dev)
+    B_d = torch.from_numpy(w.B).to(dev)
+    C_d = torch.empty((w.dim, w.R), dtype=torch.float32, device=dev)
+    plan = systec.Plan(w.order, w.dim, idx_d, vals_d)
+    del idx_d, vals_d
+    st = plan.stats()
+    opts = parse_opts(args.opts)
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+
+    def step(timed_events=None):
+        if timed_events:
+            timed_events[0].record(stream)
+        C_d.zero_()
+        if timed_events:
+            timed_events[1].record(stream)
+        plan.execute(B_d, C_d, no_zero=1, **opts)
+        if timed_events:
+            timed_events[2].record(stream)
+        if dist is not None:
+            dist.all_reduce(C_d)
+        if timed_events:
+            timed_events[3].record(stream)
+
+    for _ in range(max(3, args.warmup)):
+        flush.fill_(1.0)
+        step()
+    torch.cuda.synchronize()
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for k in range(args.steps):
+            flush.fill_(float(k))              # L2 flush between timed steps, outside the events
+            step(ev[k])
+        torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    step_ms = [e[0].elapsed_time(e[3]) for e in ev]
+    kern_ms = [e[1].elapsed_time(e[2]) for e in ev]
+    tot_ms = float(np.sum(step_ms))
+    if dist is not None:
+        t = torch.tensor([tot_ms, float(np.sum(kern_ms))], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot_ms, kern_tot = t.tolist()
+    else:
+        kern_tot = float(np.sum(kern_ms))
+    ms_per_step = tot_ms / args.steps
+    kern_avg_ms = kern_tot / args.steps
+
+    # warm back-to-back (B L2-resident from the previous call): context number
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(20):
+        plan.execute(B_d, C_d, **opts)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    warm_ms = e0.elapsed_time(e1) / 20
+
+    value = w.nnz / (ms_per_step * 1e-3)          # all ranks together process the whole tensor
+    # roofline of the dominant kernel (mttkrp_sym_kernel) on this rank's slice
+    G_all = st["G"]
+    if dist is not None:
+        t = torch.tensor([G_all], device=dev, dtype=torch.float64)
+        dist.all_reduce(t)
+        G_all = int(t.item())
+    local_bytes = bytes_eff(w.order, hi - lo, st["G"], w.R, w.dim)
+    achieved = local_bytes / (kern_avg_ms * 1e-3) / 1e9
+    peak, peak_kind = load_peaks()
+    traffic = load_traffic(w.name) if world == 1 else None
+
+    line = None
+    if rank == 0:
+        launch = plan.last_launch()
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": config_dict(w, args),
+            "eff_gbs": bytes_eff(w.order, w.nnz, G_all, w.R, w.dim) / (ms_per_step * 1e-3) / 1e9,
+            "bytes_eff_per_step": bytes_eff(w.order, w.nnz, G_all, w.R, w.dim),
+            "frac_of_8tbs": bytes_eff(w.order, w.nnz, G_all, w.R, w.dim) / (ms_per_step * 1e-3) / 8e12,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": "mttkrp_sym_kernel", "kernel_ms": kern_avg_ms,
+                         "peak_kind": f"{peak_kind} copy bandwidth (MEASURED_PEAKS.json hbm_gbs)",
+                         "algorithmic_bytes_per_launch": local_bytes},
+            "warm_ms_per_step": warm_ms,
+            "gpu_launches": args.steps,
+            "launch": launch,
+            "plan_stats": {k: st[k] for k in ("G", "expanded", "lead_runs", "max_lead_run", "pos1_runs")},
+        }
+        line["clocks"] = clk.report()
+
+    # end to end through the public host-buffer call: H2D idx/vals/B from pinned
+    # memory, prepare, execute, D2H C — every step
+    if rank == 0 and world == 1 and not args.no_e2e:
+        pin_idx = torch.from_numpy(w.idx).pin_memory()
+        pin_vals = torch.from_numpy(w.vals).pin_memory()
+        pin_B = torch.from_numpy(w.B).pin_memory()
+        pin_C = torch.empty((w.dim, w.R), dtype=torch.float32).pin_memory()
+        systec.mttkrp_host(w.order, w.dim, pin_idx, pin_vals, pin_B, C=pin_C)   # warm-up
+        ts = []
+        for _ in range(args.e2e_steps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            a.record(stream)
+            systec.mttkrp_host(w.order, w.dim, pin_idx, pin_vals, pin_B, C=pin_C)
+            b.record(stream)
+            b.synchronize()
+            ts.append(a.elapsed_time(b))
+        e2e_ms = float(np.mean(ts))
+        line["e2e"] = {"value": w.nnz / (e2e_ms * 1e-3), "unit": UNIT,
+                       "h2d_bytes_per_step": w.idx.nbytes + w.vals.nbytes + w.B.nbytes,
+                       "d2h_bytes_per_step": pin_C.numel() * 4, "ms_per_step": e2e_ms,
+                       "includes": "H2D + validate/canonicalise/sort-check/gather/stats + execute + D2H"}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(w)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    plan.destroy()
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

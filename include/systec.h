@@ -1,0 +1,173 @@
+/*
+ * systec.h — C ABI of the B200-native symmetric sparse MTTKRP
+ * (the hot path of SySTeC, arXiv 2406.09266).
+ *
+ * The operation ("The assignments for the 3-, 4-, and
+ * 5-dimensional kernels"):
+ *
+ *     C[i, r] = sum_{j_1..j_{n-1}} A[i, j_1, .., j_{n-1}] * prod_t B[j_t, r]
+ *
+ * where A is a FULLY SYMMETRIC order-n sparse tensor (Def. Symmetry,
+ * PAPER.md:141-147) given by its stored entries.  Every stored entry
+ * (idx_e, v_e) stands for its whole orbit: A[x] = sum of v_e over the stored
+ * entries with sort(x) == sort(idx_e).  Tuples may be given in any order
+ * inside the tuple (they are canonicalised, Def. Canonical PAPER.md:162-167,
+ * by sorting ascending) and entries in any order; repeated canonical
+ * coordinates add (MTTKRP is linear in A).  Each stored entry is read once and
+ * updates each of its DISTINCT index positions once, weighted by the number of
+ * distinct permutations that put that index first (the unique symmetry group
+ * S_P|E, after distributive grouping PAPER.md:577-591).
+ *
+ * Conventions shared by every entry point
+ *   - all array pointers are DEVICE pointers unless the name says _host;
+ *   - every device call is ordered on `stream` (0 = legacy default stream);
+ *   - indices are 0-based (the paper's Julia listings are 1-based);
+ *   - row-major layouts: idx[nnz][order] int32, B[dim][R] fp32, C[dim][R] fp32;
+ *   - the caller owns idx, vals, B and C; the library never frees them and
+ *     never writes idx, vals or B;
+ *   - nothing throws across the ABI: every call returns a systec_status, and
+ *     systec_last_cuda_error() gives the cudaError_t behind SYSTEC_ERR_CUDA;
+ *   - on an argument error (SYSTEC_ERR_ARG / _UNSUPPORTED / _ALIAS) C is not
+ *     touched.
+ *   - supported: order 2..5 (3, 4, 5 are the paper's MTTKRP; 2 is symmetric
+ *     SpMM), 1 <= dim < 2^31, 0 <= nnz < 2^31, R >= 1, and
+ *     order * ceil(log2 dim) <= 64 (one 64-bit sort key).  R % 4 == 0 with
+ *     16-byte aligned B and C takes the float4 path; any other R takes the
+ *     scalar GPU path (never a CPU path).
+ */
+#ifndef SYSTEC_H
+#define SYSTEC_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define SYSTEC_API __attribute__((visibility("default")))
+#else
+#define SYSTEC_API
+#endif
+
+typedef struct CUstream_st *systec_stream_t;   /* == cudaStream_t */
+
+typedef enum {
+    SYSTEC_OK = 0,
+    SYSTEC_ERR_ARG = 1,          /* null pointer with nnz>0, dim<1, nnz<0, R<1, bad option   */
+    SYSTEC_ERR_UNSUPPORTED = 2,  /* order outside 2..5, order*ceil(log2 dim) > 64, nnz>=2^31 */
+    SYSTEC_ERR_INDEX = 3,        /* some idx outside [0, dim) (detected on the device)      */
+    SYSTEC_ERR_ALIAS = 4,        /* C overlaps B, idx or vals                               */
+    SYSTEC_ERR_NOMEM = 5,        /* device or host allocation failed                        */
+    SYSTEC_ERR_CUDA = 6          /* a CUDA runtime call failed; see systec_last_cuda_error  */
+} systec_status;
+
+/* Statistics of a prepared plan (filled once, at plan creation). */
+typedef struct systec_stats {
+    int64_t nnz;                 /* stored entries                                            */
+    int64_t dim;
+    int32_t order;
+    int32_t key_bits;            /* bits per index in the 64-bit sort key = ceil(log2 dim)     */
+    int64_t G;                   /* sum over entries of the number of distinct indices d_e     */
+    int64_t expanded;            /* sum over entries of the orbit size n!/prod m! (naive work) */
+    int64_t pattern_hist[16];    /* entries per equality-pattern code (bit t: c_t == c_{t+1})  */
+    int64_t lead_runs;           /* runs of equal leading index c_0 in sorted order            */
+    int64_t max_lead_run;        /* longest such run                                           */
+    int64_t pos1_runs;           /* runs of equal c_1 in sorted order                          */
+    int32_t input_was_sorted;    /* 1: input already canonical and lexicographically sorted    */
+    int32_t pad0;
+    int64_t bad_entry;           /* first entry with an index outside [0,dim), else -1         */
+} systec_stats;
+
+/* Kernel tuning options for systec_plan_execute_ex; zero fields = defaults. */
+typedef struct systec_exec_opts {
+    int32_t warps_per_block;     /* 0 = default (8)                                            */
+    int32_t blocks_per_sm;       /* 0 = as many as fit (occupancy calculator)                  */
+    int32_t pos1_accumulate;     /* 0 = auto from stats, 1 = on, -1 = off                      */
+    int32_t force_scalar;        /* 1 = scalar (non-float4) path even when float4 is possible  */
+    int32_t no_zero;             /* 1 = accumulate into C instead of overwriting it            */
+    int32_t l2_hints;            /* 0 = default (on), -1 = off                                 */
+    int32_t reserved[10];
+} systec_exec_opts;
+
+typedef struct systec_plan_s *systec_plan;
+
+/*
+ * One-shot call with the paper's signature (north_star):
+ * plan_create + plan_execute + plan_destroy.  idx/vals/B/C are DEVICE
+ * pointers; C [dim][R] is OVERWRITTEN.  Synchronises `stream` inside plan
+ * creation (validation verdict and statistics); the execute part is async.
+ */
+SYSTEC_API int systec_mttkrp(int order, int64_t dim, int64_t nnz, const int32_t *idx, const float *vals,
+                  const float *B, int R, float *C, systec_stream_t stream);
+
+/*
+ * The same operation on HOST buffers (the end-to-end call): copies idx, vals
+ * and B to the device, runs the path, copies C back and synchronises.
+ * Host buffers may be pageable or pinned (pinned is faster).  Device scratch
+ * comes from the stream-ordered pool and is returned before the call ends.
+ */
+SYSTEC_API int systec_mttkrp_host(int order, int64_t dim, int64_t nnz, const int32_t *idx_host,
+                       const float *vals_host, const float *B_host, int R, float *C_host,
+                       systec_stream_t stream);
+
+/*
+ * Plan creation: validate (range check on the device), canonicalise every
+ * tuple (ascending sort), sort entries lexicographically (skipped when the
+ * input already is), and store the prepared structure-of-arrays copy
+ * (order x int32 + 1 x fp32 per entry, owned by the plan).  idx and vals may
+ * be freed once this returns.  Synchronises `stream` twice: once to read the
+ * device validation verdict (which also decides whether the sort can be
+ * skipped) and once to read the statistics.
+ * Errors: ARG, UNSUPPORTED, INDEX (plan not created, *out = NULL, and
+ * systec_last_bad_entry() names the first offending entry), NOMEM, CUDA.
+ */
+SYSTEC_API int systec_plan_create(systec_plan *out, int order, int64_t dim, int64_t nnz,
+                       const int32_t *idx, const float *vals, systec_stream_t stream);
+
+/*
+ * Execute: C[dim][R] = MTTKRP(plan, B).  Zeroes C and launches the kernel on
+ * `stream`; never allocates, never synchronises (CUDA-graph capturable).
+ * Concurrent executions of one plan on different streams are safe when
+ * their C buffers differ.  Errors: ARG, ALIAS, CUDA (launch failure).
+ */
+SYSTEC_API int systec_plan_execute(systec_plan plan, const float *B, int R, float *C, systec_stream_t stream);
+
+/* Execute with tuning options (NULL = defaults).  Same semantics. */
+SYSTEC_API int systec_plan_execute_ex(systec_plan plan, const float *B, int R, float *C,
+                           const systec_exec_opts *opts, systec_stream_t stream);
+
+/* Copy the plan's statistics to host memory. */
+SYSTEC_API int systec_plan_stats(systec_plan plan, systec_stats *host_out);
+
+/*
+ * Device pointers to the prepared stream (read-only views, owned by the plan):
+ * coords[t] = c_t[nnz] int32 for t < order, *vals = v[nnz] fp32, in
+ * lexicographic order of the canonical tuples.  For tests and tools.
+ */
+SYSTEC_API int systec_plan_prepared(systec_plan plan, const int32_t **coords /* [order] */, const float **vals);
+
+/* Copy the prepared stream into caller-owned DEVICE buffers, ordered on
+ * `stream`: coords_dst [order][nnz] int32 (row t = c_t), vals_dst [nnz] fp32. */
+SYSTEC_API int systec_plan_copy_prepared(systec_plan plan, int32_t *coords_dst, float *vals_dst,
+                                         systec_stream_t stream);
+
+/* Launch geometry of the last execute of this plan (for bench reporting). */
+SYSTEC_API int systec_plan_last_launch(systec_plan plan, int32_t *grid_x, int32_t *grid_y, int32_t *block,
+                            int32_t *smem_bytes, int32_t *kernel_id);
+
+/* Free the plan's device memory (stream-ordered on the creation stream). */
+SYSTEC_API int systec_plan_destroy(systec_plan plan);
+
+SYSTEC_API const char *systec_status_string(int status);
+SYSTEC_API int systec_last_cuda_error(void);
+/* ABI version: 100 * major + minor. */
+SYSTEC_API int systec_version(void);
+/* Entry index of the first out-of-range tuple seen by the last failed
+ * plan creation on this thread (SYSTEC_ERR_INDEX), else -1. */
+SYSTEC_API int64_t systec_last_bad_entry(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SYSTEC_H */

@@ -1,0 +1,330 @@
+// abi.cu — the extern "C" boundary of libsystec (declared in include/systec.h).
+// Argument checking, plan lifetime, stream-ordered memory and error mapping;
+// every step of the computation itself runs in the kernels of prepare.cu and
+// mttkrp.cu.  There is no host compute path.
+#include <climits>
+#include <cstring>
+#include <new>
+
+#include "internal.cuh"
+
+namespace systec {
+
+static thread_local int g_last_cuda_error = 0;
+static thread_local int64_t g_last_bad_entry = -1;
+void set_last_cuda_error(cudaError_t e) { g_last_cuda_error = static_cast<int>(e); }
+
+namespace {
+
+int cuda_fail(cudaError_t e) {
+    set_last_cuda_error(e);
+    return e == cudaErrorMemoryAllocation ? SYSTEC_ERR_NOMEM : SYSTEC_ERR_CUDA;
+}
+
+int ceil_log2(int64_t dim) {
+    int b = 0;
+    while ((int64_t(1) << b) < dim) ++b;
+    return b < 1 ? 1 : b;
+}
+
+bool overlap(const void *a, size_t na, const void *b, size_t nb) {
+    if (!a || !b || na == 0 || nb == 0) return false;
+    const uintptr_t x = reinterpret_cast<uintptr_t>(a), y = reinterpret_cast<uintptr_t>(b);
+    return x < y + nb && y < x + na;
+}
+
+void ensure_pool_keeps_memory() {
+    static bool done = false;
+    if (done) return;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    done = true;
+}
+
+int check_shape(int order, int64_t dim, int64_t nnz, int *bits_out) {
+    if (dim < 1 || nnz < 0) return SYSTEC_ERR_ARG;
+    if (order < 2 || order > 5) return SYSTEC_ERR_UNSUPPORTED;
+    if (dim > INT32_MAX || nnz > INT32_MAX - 64) return SYSTEC_ERR_UNSUPPORTED;
+    const int bits = ceil_log2(dim);
+    if (bits * order > 64) return SYSTEC_ERR_UNSUPPORTED;
+    *bits_out = bits;
+    return SYSTEC_OK;
+}
+
+// Builds the plan.  `pooled` plans keep their storage in the stream-ordered pool.
+int plan_create_impl(Plan **out, int order, int64_t dim, int64_t nnz, const int32_t *idx, const float *vals,
+                     cudaStream_t s, bool pooled) {
+    *out = nullptr;
+    int bits = 0;
+    int rc = check_shape(order, dim, nnz, &bits);
+    if (rc) return rc;
+    if (nnz > 0 && (!idx || !vals)) return SYSTEC_ERR_ARG;
+    ensure_pool_keeps_memory();
+
+    Plan *p = new (std::nothrow) Plan();
+    if (!p) return SYSTEC_ERR_NOMEM;
+    p->order = order;
+    p->dim = dim;
+    p->nnz = nnz;
+    p->ld = ((nnz + 3) & ~int64_t(3)) + 4;
+    p->key_bits = bits;
+    p->pooled = pooled;
+    p->stream = s;
+    const size_t bytes = static_cast<size_t>(order + 1) * p->ld * 4;
+    cudaError_t e = pooled ? cudaMallocAsync(&p->storage, bytes, s) : cudaMalloc(&p->storage, bytes);
+    if (e != cudaSuccess) {
+        delete p;
+        return cuda_fail(e);
+    }
+    p->coords = static_cast<int32_t *>(p->storage);
+    p->vals = reinterpret_cast<float *>(p->coords + static_cast<size_t>(order) * p->ld);
+
+    DevStats *dst = nullptr;
+    unsigned long long *keys = nullptr, *keys2 = nullptr;
+    uint32_t *perm = nullptr, *perm2 = nullptr;
+    DevStats hst;
+    auto cleanup = [&]() {
+        if (dst) cudaFreeAsync(dst, s);
+        if (keys) cudaFreeAsync(keys, s);
+        if (keys2) cudaFreeAsync(keys2, s);
+        if (perm) cudaFreeAsync(perm, s);
+        if (perm2) cudaFreeAsync(perm2, s);
+    };
+    auto fail = [&](cudaError_t err) {
+        cleanup();
+        if (pooled) cudaFreeAsync(p->storage, s); else cudaFree(p->storage);
+        delete p;
+        return cuda_fail(err);
+    };
+    const size_t nk = static_cast<size_t>(nnz > 0 ? nnz : 1);
+    if ((e = cudaMallocAsync(&dst, sizeof(DevStats), s)) != cudaSuccess) return fail(e);
+    if ((e = cudaMallocAsync(&keys, nk * 8, s)) != cudaSuccess) return fail(e);
+    if ((e = cudaMallocAsync(&perm, nk * 4, s)) != cudaSuccess) return fail(e);
+    std::memset(&hst, 0, sizeof(hst));
+    hst.bad_entry = ULLONG_MAX;
+    if ((e = cudaMemcpyAsync(dst, &hst, sizeof(hst), cudaMemcpyHostToDevice, s)) != cudaSuccess) return fail(e);
+
+    // a1: validate + canonicalise + pack keys
+    if ((e = launch_canonicalize(order, dim, nnz, bits, idx, keys, perm, dst, s)) != cudaSuccess) return fail(e);
+    if ((e = cudaMemcpyAsync(&hst, dst, sizeof(hst), cudaMemcpyDeviceToHost, s)) != cudaSuccess) return fail(e);
+    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return fail(e);  // sync 1: validation verdict
+    if (hst.err) {
+        g_last_bad_entry = static_cast<int64_t>(hst.bad_entry);
+        cleanup();
+        if (pooled) cudaFreeAsync(p->storage, s); else cudaFree(p->storage);
+        delete p;
+        return SYSTEC_ERR_INDEX;
+    }
+    const bool sorted = hst.unsorted == 0;
+    // a2: lexicographic sort (only when needed) + SoA gather
+    const unsigned long long *skeys = keys;
+    const uint32_t *sperm = nullptr;
+    if (!sorted && nnz > 1) {
+        if ((e = cudaMallocAsync(&keys2, nk * 8, s)) != cudaSuccess) return fail(e);
+        if ((e = cudaMallocAsync(&perm2, nk * 4, s)) != cudaSuccess) return fail(e);
+        if ((e = sort_keys(nnz, bits * order, keys, keys2, perm, perm2, s, pooled)) != cudaSuccess) return fail(e);
+        skeys = keys2;
+        sperm = perm2;
+    }
+    if ((e = launch_gather(order, nnz, p->ld, bits, skeys, sperm, vals, p->coords, p->vals, s)) != cudaSuccess)
+        return fail(e);
+    if ((e = launch_stats(order, nnz, p->ld, p->coords, dst, s)) != cudaSuccess) return fail(e);
+    if ((e = cudaMemcpyAsync(&hst, dst, sizeof(hst), cudaMemcpyDeviceToHost, s)) != cudaSuccess) return fail(e);
+    cleanup();
+    dst = nullptr; keys = nullptr; keys2 = nullptr; perm = nullptr; perm2 = nullptr;
+    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) {  // sync 2: statistics
+        if (pooled) cudaFreeAsync(p->storage, s); else cudaFree(p->storage);
+        delete p;
+        return cuda_fail(e);
+    }
+    systec_stats &st = p->stats;
+    st.nnz = nnz;
+    st.dim = dim;
+    st.order = order;
+    st.key_bits = bits;
+    st.G = static_cast<int64_t>(hst.G);
+    st.expanded = static_cast<int64_t>(hst.expanded);
+    for (int c = 0; c < 16; ++c) st.pattern_hist[c] = static_cast<int64_t>(hst.hist[c]);
+    st.lead_runs = static_cast<int64_t>(hst.lead_runs);
+    st.max_lead_run = static_cast<int64_t>(hst.max_lead_run);
+    st.pos1_runs = static_cast<int64_t>(hst.pos1_runs);
+    st.input_was_sorted = sorted ? 1 : 0;
+    st.bad_entry = -1;
+    *out = p;
+    return SYSTEC_OK;
+}
+
+int execute_impl(Plan *p, const float *B, int R, float *C, const systec_exec_opts *opts, cudaStream_t s) {
+    if (!p || !B || !C || R < 1) return SYSTEC_ERR_ARG;
+    const size_t bytes = static_cast<size_t>(p->dim) * R * sizeof(float);
+    if (overlap(B, bytes, C, bytes)) return SYSTEC_ERR_ALIAS;
+    if (overlap(C, bytes, p->storage, static_cast<size_t>(p->order + 1) * p->ld * 4)) return SYSTEC_ERR_ALIAS;
+    systec_exec_opts o;
+    std::memset(&o, 0, sizeof(o));
+    if (opts) o = *opts;
+    if (o.warps_per_block < 0 || o.warps_per_block > 8 || o.blocks_per_sm < 0) return SYSTEC_ERR_ARG;
+    cudaError_t e = launch_mttkrp(*p, B, R, C, o, s);
+    if (e == cudaErrorInvalidValue) return SYSTEC_ERR_ARG;
+    if (e != cudaSuccess) return cuda_fail(e);
+    return SYSTEC_OK;
+}
+
+void destroy_impl(Plan *p) {
+    if (!p) return;
+    if (p->pooled) cudaFreeAsync(p->storage, p->stream);
+    else cudaFree(p->storage);
+    delete p;
+}
+
+}  // namespace
+}  // namespace systec
+
+using systec::Plan;
+
+extern "C" {
+
+int systec_plan_create(systec_plan *out, int order, int64_t dim, int64_t nnz, const int32_t *idx,
+                       const float *vals, systec_stream_t stream) {
+    if (!out) return SYSTEC_ERR_ARG;
+    Plan *p = nullptr;
+    int rc = systec::plan_create_impl(&p, order, dim, nnz, idx, vals, reinterpret_cast<cudaStream_t>(stream), false);
+    *out = reinterpret_cast<systec_plan>(p);
+    return rc;
+}
+
+int systec_plan_execute(systec_plan plan, const float *B, int R, float *C, systec_stream_t stream) {
+    return systec::execute_impl(reinterpret_cast<Plan *>(plan), B, R, C, nullptr,
+                                reinterpret_cast<cudaStream_t>(stream));
+}
+
+int systec_plan_execute_ex(systec_plan plan, const float *B, int R, float *C, const systec_exec_opts *opts,
+                           systec_stream_t stream) {
+    return systec::execute_impl(reinterpret_cast<Plan *>(plan), B, R, C, opts,
+                                reinterpret_cast<cudaStream_t>(stream));
+}
+
+int systec_plan_stats(systec_plan plan, systec_stats *host_out) {
+    if (!plan || !host_out) return SYSTEC_ERR_ARG;
+    *host_out = reinterpret_cast<Plan *>(plan)->stats;
+    return SYSTEC_OK;
+}
+
+int systec_plan_prepared(systec_plan plan, const int32_t **coords, const float **vals) {
+    if (!plan || !coords || !vals) return SYSTEC_ERR_ARG;
+    Plan *p = reinterpret_cast<Plan *>(plan);
+    for (int t = 0; t < p->order; ++t) coords[t] = p->coords + static_cast<size_t>(t) * p->ld;
+    *vals = p->vals;
+    return SYSTEC_OK;
+}
+
+int systec_plan_copy_prepared(systec_plan plan, int32_t *coords_dst, float *vals_dst, systec_stream_t stream) {
+    if (!plan || !coords_dst || !vals_dst) return SYSTEC_ERR_ARG;
+    Plan *p = reinterpret_cast<Plan *>(plan);
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (p->nnz == 0) return SYSTEC_OK;
+    cudaError_t e = cudaMemcpy2DAsync(coords_dst, static_cast<size_t>(p->nnz) * 4, p->coords,
+                                      static_cast<size_t>(p->ld) * 4, static_cast<size_t>(p->nnz) * 4, p->order,
+                                      cudaMemcpyDeviceToDevice, s);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(vals_dst, p->vals, static_cast<size_t>(p->nnz) * 4, cudaMemcpyDeviceToDevice, s);
+    return e == cudaSuccess ? SYSTEC_OK : systec::cuda_fail(e);
+}
+
+int systec_plan_last_launch(systec_plan plan, int32_t *grid_x, int32_t *grid_y, int32_t *block, int32_t *smem,
+                            int32_t *kernel_id) {
+    if (!plan) return SYSTEC_ERR_ARG;
+    Plan *p = reinterpret_cast<Plan *>(plan);
+    if (grid_x) *grid_x = p->last_grid_x;
+    if (grid_y) *grid_y = p->last_grid_y;
+    if (block) *block = p->last_block;
+    if (smem) *smem = p->last_smem;
+    if (kernel_id) *kernel_id = p->last_kernel;
+    return SYSTEC_OK;
+}
+
+int systec_plan_destroy(systec_plan plan) {
+    systec::destroy_impl(reinterpret_cast<Plan *>(plan));
+    return SYSTEC_OK;
+}
+
+int systec_mttkrp(int order, int64_t dim, int64_t nnz, const int32_t *idx, const float *vals, const float *B,
+                  int R, float *C, systec_stream_t stream) {
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    int bits = 0;
+    int rc = systec::check_shape(order, dim, nnz, &bits);
+    if (rc) return rc;
+    if (!B || !C || R < 1 || (nnz > 0 && (!idx || !vals))) return SYSTEC_ERR_ARG;
+    const size_t cb = static_cast<size_t>(dim) * R * sizeof(float);
+    if (systec::overlap(C, cb, B, cb) || systec::overlap(C, cb, idx, static_cast<size_t>(nnz) * order * 4) ||
+        systec::overlap(C, cb, vals, static_cast<size_t>(nnz) * 4))
+        return SYSTEC_ERR_ALIAS;
+    Plan *p = nullptr;
+    rc = systec::plan_create_impl(&p, order, dim, nnz, idx, vals, s, true);
+    if (rc) return rc;
+    rc = systec::execute_impl(p, B, R, C, nullptr, s);
+    systec::destroy_impl(p);
+    return rc;
+}
+
+int systec_mttkrp_host(int order, int64_t dim, int64_t nnz, const int32_t *idx_host, const float *vals_host,
+                       const float *B_host, int R, float *C_host, systec_stream_t stream) {
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    int bits = 0;
+    int rc = systec::check_shape(order, dim, nnz, &bits);
+    if (rc) return rc;
+    if (!B_host || !C_host || R < 1 || (nnz > 0 && (!idx_host || !vals_host))) return SYSTEC_ERR_ARG;
+    systec::ensure_pool_keeps_memory();
+    const size_t ib = static_cast<size_t>(nnz) * order * 4, vb = static_cast<size_t>(nnz) * 4;
+    const size_t bb = static_cast<size_t>(dim) * R * 4;
+    char *buf = nullptr;
+    const size_t ib_al = (ib + 255) & ~size_t(255), vb_al = (vb + 255) & ~size_t(255), bb_al = (bb + 255) & ~size_t(255);
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void **>(&buf), ib_al + vb_al + 2 * bb_al + 256, s);
+    if (e != cudaSuccess) return systec::cuda_fail(e);
+    int32_t *d_idx = reinterpret_cast<int32_t *>(buf);
+    float *d_vals = reinterpret_cast<float *>(buf + ib_al);
+    float *d_B = reinterpret_cast<float *>(buf + ib_al + vb_al);
+    float *d_C = reinterpret_cast<float *>(buf + ib_al + vb_al + bb_al);
+    Plan *p = nullptr;
+    rc = SYSTEC_OK;
+    do {
+        if (ib && (e = cudaMemcpyAsync(d_idx, idx_host, ib, cudaMemcpyHostToDevice, s)) != cudaSuccess) break;
+        if (vb && (e = cudaMemcpyAsync(d_vals, vals_host, vb, cudaMemcpyHostToDevice, s)) != cudaSuccess) break;
+        if ((e = cudaMemcpyAsync(d_B, B_host, bb, cudaMemcpyHostToDevice, s)) != cudaSuccess) break;
+        rc = systec::plan_create_impl(&p, order, dim, nnz, d_idx, d_vals, s, true);
+        if (rc) break;
+        rc = systec::execute_impl(p, d_B, R, d_C, nullptr, s);
+        if (rc) break;
+        if ((e = cudaMemcpyAsync(C_host, d_C, bb, cudaMemcpyDeviceToHost, s)) != cudaSuccess) break;
+    } while (false);
+    if (p) systec::destroy_impl(p);
+    cudaFreeAsync(buf, s);
+    if (e != cudaSuccess) return systec::cuda_fail(e);
+    if (rc) return rc;
+    e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return systec::cuda_fail(e);
+    return SYSTEC_OK;
+}
+
+const char *systec_status_string(int status) {
+    switch (status) {
+        case SYSTEC_OK: return "ok";
+        case SYSTEC_ERR_ARG: return "invalid argument";
+        case SYSTEC_ERR_UNSUPPORTED: return "unsupported order/dim/nnz";
+        case SYSTEC_ERR_INDEX: return "index outside [0, dim)";
+        case SYSTEC_ERR_ALIAS: return "output aliases an input";
+        case SYSTEC_ERR_NOMEM: return "out of memory";
+        case SYSTEC_ERR_CUDA: return "CUDA error";
+        default: return "unknown status";
+    }
+}
+
+int systec_last_cuda_error(void) { return systec::g_last_cuda_error; }
+int systec_version(void) { return 100; }
+int64_t systec_last_bad_entry(void) { return systec::g_last_bad_entry; }
+
+}  // extern "C"

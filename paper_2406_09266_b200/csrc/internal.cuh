@@ -1,0 +1,59 @@
+// internal.cuh — plan object and launcher declarations shared by the .cu files
+// of libsystec (not part of the public ABI; see include/systec.h).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/systec.h"
+
+namespace systec {
+
+// Prepared, canonicalised, lexicographically sorted structure-of-arrays stream.
+struct Plan {
+    int order = 0;
+    int64_t dim = 0;
+    int64_t nnz = 0;
+    int64_t ld = 0;            // padded length of every array (multiple of 4, >= nnz)
+    int key_bits = 0;
+    int32_t *coords = nullptr; // [order][ld] int32: c_t of entry e at coords[t*ld + e]
+    float *vals = nullptr;     // [ld] fp32
+    void *storage = nullptr;   // one allocation holding coords + vals
+    bool pooled = false;       // storage from the stream-ordered pool (freed async)
+    cudaStream_t stream = nullptr;
+    systec_stats stats{};
+    // last launch (for reporting)
+    int last_grid_x = 0, last_grid_y = 0, last_block = 0, last_smem = 0, last_kernel = -1;
+};
+
+// Device-side counters filled by the prepare kernels (all unsigned 64-bit).
+struct DevStats {
+    unsigned long long err;            // bit 0: index out of range
+    unsigned long long unsorted;       // 1 if canonical keys are not non-decreasing
+    unsigned long long bad_entry;      // min entry with a bad index (ULLONG_MAX if none)
+    unsigned long long G;
+    unsigned long long expanded;
+    unsigned long long hist[16];
+    unsigned long long lead_runs;
+    unsigned long long max_lead_run;
+    unsigned long long pos1_runs;
+};
+
+// prepare.cu
+cudaError_t launch_canonicalize(int order, int64_t dim, int64_t nnz, int bits, const int32_t *idx,
+                                unsigned long long *keys, uint32_t *perm, DevStats *st,
+                                cudaStream_t s);
+cudaError_t sort_keys(int64_t nnz, int end_bit, unsigned long long *keys_in, unsigned long long *keys_out,
+                      uint32_t *perm_in, uint32_t *perm_out, cudaStream_t s, bool pooled);
+cudaError_t launch_gather(int order, int64_t nnz, int64_t ld, int bits, const unsigned long long *keys,
+                          const uint32_t *perm /* null = identity */, const float *vals_in,
+                          int32_t *coords, float *vals_out, cudaStream_t s);
+cudaError_t launch_stats(int order, int64_t nnz, int64_t ld, const int32_t *coords, DevStats *st,
+                         cudaStream_t s);
+
+// mttkrp.cu
+cudaError_t launch_mttkrp(Plan &p, const float *B, int R, float *C, const systec_exec_opts &o,
+                          cudaStream_t s);
+
+void set_last_cuda_error(cudaError_t e);
+
+}  // namespace systec

@@ -1,0 +1,226 @@
+// prepare.cu — device-side validation, canonicalisation, lexicographic sort and
+// structure-of-arrays gather of the stored COO entries.
+//
+// Paper basis: a fully symmetric tensor is determined by its canonical triangle
+// (Def. Symmetry, Def. Canonical), so every
+// input tuple is replaced by its ascending sort; the symmetrised kernel then
+// walks only canonical coordinates ("if p_1 <= ... <= p_n").
+// The concordant, sorted traversal order corresponds to building the CSF /
+// concordising step of PAPER.md:482-503.  The paper excludes this
+// rearrangement from its timings; so do we (plan creation).
+#include <cub/device/device_radix_sort.cuh>
+
+#include "internal.cuh"
+
+namespace systec {
+
+namespace {
+
+template <int N>
+__device__ __forceinline__ void sort_net(int32_t (&c)[N]) {
+    // odd-even transposition network, fully unrolled (N <= 5)
+#pragma unroll
+    for (int r = 0; r < N; ++r) {
+#pragma unroll
+        for (int t = r & 1; t + 1 < N; t += 2) {
+            const int32_t a = c[t], b = c[t + 1];
+            c[t] = min(a, b);
+            c[t + 1] = max(a, b);
+        }
+    }
+}
+
+template <int N>
+__device__ __forceinline__ unsigned long long pack_key(const int32_t (&c)[N], int bits) {
+    unsigned long long k = 0;
+#pragma unroll
+    for (int t = 0; t < N; ++t) k = (k << bits) | static_cast<unsigned long long>(static_cast<uint32_t>(c[t]));
+    return k;
+}
+
+template <int N>
+__device__ __forceinline__ bool load_canonical(const int32_t *idx, int64_t e, int64_t dim, int32_t (&c)[N]) {
+    bool ok = true;
+#pragma unroll
+    for (int t = 0; t < N; ++t) {
+        c[t] = idx[e * N + t];
+        ok &= (c[t] >= 0) & (static_cast<int64_t>(c[t]) < dim);
+    }
+    sort_net<N>(c);
+    return ok;
+}
+
+template <int N>
+__global__ void canonicalize_kernel(const int32_t *__restrict__ idx, int64_t nnz, int64_t dim, int bits,
+                                    unsigned long long *__restrict__ keys, uint32_t *__restrict__ perm,
+                                    DevStats *st) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        int32_t c[N];
+        const bool ok = load_canonical<N>(idx, e, dim, c);
+        if (!ok) {
+            atomicOr(&st->err, 1ull);
+            atomicMin(&st->bad_entry, static_cast<unsigned long long>(e));
+            keys[e] = 0;
+            perm[e] = static_cast<uint32_t>(e);
+            continue;
+        }
+        const unsigned long long k = pack_key<N>(c, bits);
+        keys[e] = k;
+        perm[e] = static_cast<uint32_t>(e);
+        if (e > 0) {
+            int32_t q[N];
+            if (load_canonical<N>(idx, e - 1, dim, q) && pack_key<N>(q, bits) > k) st->unsorted = 1ull;
+        }
+    }
+}
+
+template <int N>
+__global__ void gather_kernel(int64_t nnz, int64_t ld, int bits, const unsigned long long *__restrict__ keys,
+                              const uint32_t *__restrict__ perm, const float *__restrict__ vals_in,
+                              int32_t *__restrict__ coords, float *__restrict__ vals_out) {
+    const unsigned long long mask = (bits >= 64) ? ~0ull : ((1ull << bits) - 1ull);
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < ld;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        if (e < nnz) {
+            unsigned long long k = keys[e];
+#pragma unroll
+            for (int t = N - 1; t >= 0; --t) {
+                coords[t * ld + e] = static_cast<int32_t>(k & mask);
+                k >>= bits;
+            }
+            vals_out[e] = vals_in[perm ? perm[e] : e];
+        } else {  // padding read by the bulk copies of the last chunk; never used
+#pragma unroll
+            for (int t = 0; t < N; ++t) coords[t * ld + e] = 0;
+            vals_out[e] = 0.0f;
+        }
+    }
+}
+
+__device__ __forceinline__ long long dfact(int k) {
+    long long f = 1;
+    for (int i = 2; i <= k; ++i) f *= i;
+    return f;
+}
+
+template <int N>
+__global__ void stats_kernel(int64_t nnz, int64_t ld, const int32_t *__restrict__ coords, DevStats *st) {
+    __shared__ unsigned long long s_hist[16];
+    __shared__ unsigned long long s_sum[4];  // G, expanded, lead_runs, pos1_runs
+    if (threadIdx.x < 16) s_hist[threadIdx.x] = 0;
+    if (threadIdx.x < 4) s_sum[threadIdx.x] = 0;
+    __syncthreads();
+    unsigned long long G = 0, expanded = 0, lead = 0, pos1 = 0, maxrun = 0;
+    const int32_t *c0 = coords;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        int32_t c[N];
+#pragma unroll
+        for (int t = 0; t < N; ++t) c[t] = coords[t * ld + e];
+        int code = 0, distinct = 1, run = 1;
+        long long denom = 1;
+#pragma unroll
+        for (int t = 1; t < N; ++t) {
+            if (c[t] == c[t - 1]) {
+                code |= 1 << (t - 1);
+                ++run;
+            } else {
+                ++distinct;
+                denom *= dfact(run);
+                run = 1;
+            }
+        }
+        denom *= dfact(run);
+        G += distinct;
+        expanded += static_cast<unsigned long long>(dfact(N) / denom);
+        atomicAdd(&s_hist[code], 1ull);
+        if (e == 0 || c0[e - 1] != c[0]) ++lead;
+        if (N >= 2 && (e == 0 || coords[ld + e - 1] != c[1])) ++pos1;
+        if (e == nnz - 1 || c0[e + 1] != c[0]) {  // end of a leading run: its start by binary search
+            int64_t lo = 0, hi = e;
+            while (lo < hi) {
+                const int64_t mid = (lo + hi) >> 1;
+                if (c0[mid] < c[0]) lo = mid + 1; else hi = mid;
+            }
+            const unsigned long long len = static_cast<unsigned long long>(e - lo + 1);
+            maxrun = len > maxrun ? len : maxrun;
+        }
+    }
+    atomicAdd(&s_sum[0], G);
+    atomicAdd(&s_sum[1], expanded);
+    atomicAdd(&s_sum[2], lead);
+    atomicAdd(&s_sum[3], pos1);
+    if (maxrun) atomicMax(&st->max_lead_run, maxrun);
+    __syncthreads();
+    if (threadIdx.x < 16 && s_hist[threadIdx.x]) atomicAdd(&st->hist[threadIdx.x], s_hist[threadIdx.x]);
+    if (threadIdx.x == 0) {
+        atomicAdd(&st->G, s_sum[0]);
+        atomicAdd(&st->expanded, s_sum[1]);
+        atomicAdd(&st->lead_runs, s_sum[2]);
+        atomicAdd(&st->pos1_runs, s_sum[3]);
+    }
+}
+
+int grid_for(int64_t n, int threads) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t want = (n + threads - 1) / threads;
+    const int64_t cap = static_cast<int64_t>(sms) * 16;
+    return static_cast<int>(want < 1 ? 1 : (want > cap ? cap : want));
+}
+
+}  // namespace
+
+#define SYSTEC_ORDER_SWITCH(order, ...)          \
+    switch (order) {                             \
+        case 2: { constexpr int N = 2; __VA_ARGS__; } break; \
+        case 3: { constexpr int N = 3; __VA_ARGS__; } break; \
+        case 4: { constexpr int N = 4; __VA_ARGS__; } break; \
+        case 5: { constexpr int N = 5; __VA_ARGS__; } break; \
+        default: return cudaErrorInvalidValue;   \
+    }
+
+cudaError_t launch_canonicalize(int order, int64_t dim, int64_t nnz, int bits, const int32_t *idx,
+                                unsigned long long *keys, uint32_t *perm, DevStats *st, cudaStream_t s) {
+    if (nnz == 0) return cudaSuccess;
+    const int th = 256;
+    SYSTEC_ORDER_SWITCH(order, canonicalize_kernel<N><<<grid_for(nnz, th), th, 0, s>>>(idx, nnz, dim, bits, keys, perm, st));
+    return cudaGetLastError();
+}
+
+cudaError_t sort_keys(int64_t nnz, int end_bit, unsigned long long *keys_in, unsigned long long *keys_out,
+                      uint32_t *perm_in, uint32_t *perm_out, cudaStream_t s, bool pooled) {
+    size_t temp = 0;
+    cudaError_t e = cub::DeviceRadixSort::SortPairs(nullptr, temp, keys_in, keys_out, perm_in, perm_out,
+                                                    static_cast<int>(nnz), 0, end_bit, s);
+    if (e != cudaSuccess) return e;
+    void *tmp = nullptr;
+    e = cudaMallocAsync(&tmp, temp ? temp : 16, s);
+    if (e != cudaSuccess) return e;
+    e = cub::DeviceRadixSort::SortPairs(tmp, temp, keys_in, keys_out, perm_in, perm_out,
+                                        static_cast<int>(nnz), 0, end_bit, s);
+    cudaError_t f = cudaFreeAsync(tmp, s);
+    (void)pooled;
+    return e != cudaSuccess ? e : f;
+}
+
+cudaError_t launch_gather(int order, int64_t nnz, int64_t ld, int bits, const unsigned long long *keys,
+                          const uint32_t *perm, const float *vals_in, int32_t *coords, float *vals_out,
+                          cudaStream_t s) {
+    if (ld == 0) return cudaSuccess;
+    const int th = 256;
+    SYSTEC_ORDER_SWITCH(order, gather_kernel<N><<<grid_for(ld, th), th, 0, s>>>(nnz, ld, bits, keys, perm, vals_in, coords, vals_out));
+    return cudaGetLastError();
+}
+
+cudaError_t launch_stats(int order, int64_t nnz, int64_t ld, const int32_t *coords, DevStats *st,
+                         cudaStream_t s) {
+    if (nnz == 0) return cudaSuccess;
+    const int th = 256;
+    SYSTEC_ORDER_SWITCH(order, stats_kernel<N><<<grid_for(nnz, th), th, 0, s>>>(nnz, ld, coords, st));
+    return cudaGetLastError();
+}
+
+}  // namespace systec

@@ -1,0 +1,242 @@
+"""Thin ctypes binding of libsystec (include/systec.h).  Argument marshalling
+only: every step of the computation runs in the library's CUDA kernels.
+PyTorch provides device memory and streams.  There is no CPU fallback: if the
+shared library is missing or cannot be loaded this module raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libsystec.so")
+
+OK, ERR_ARG, ERR_UNSUPPORTED, ERR_INDEX, ERR_ALIAS, ERR_NOMEM, ERR_CUDA = range(7)
+_ERRORS = {ERR_ARG: ValueError, ERR_UNSUPPORTED: NotImplementedError, ERR_INDEX: IndexError,
+           ERR_ALIAS: ValueError, ERR_NOMEM: MemoryError, ERR_CUDA: RuntimeError}
+
+
+class SystecStats(ctypes.Structure):
+    _fields_ = [("nnz", ctypes.c_int64), ("dim", ctypes.c_int64), ("order", ctypes.c_int32),
+                ("key_bits", ctypes.c_int32), ("G", ctypes.c_int64), ("expanded", ctypes.c_int64),
+                ("pattern_hist", ctypes.c_int64 * 16), ("lead_runs", ctypes.c_int64),
+                ("max_lead_run", ctypes.c_int64), ("pos1_runs", ctypes.c_int64),
+                ("input_was_sorted", ctypes.c_int32), ("pad0", ctypes.c_int32),
+                ("bad_entry", ctypes.c_int64)]
+
+
+class SystecExecOpts(ctypes.Structure):
+    _fields_ = [("warps_per_block", ctypes.c_int32), ("blocks_per_sm", ctypes.c_int32),
+                ("pos1_accumulate", ctypes.c_int32), ("force_scalar", ctypes.c_int32),
+                ("no_zero", ctypes.c_int32), ("l2_hints", ctypes.c_int32),
+                ("reserved", ctypes.c_int32 * 10)]
+
+
+EXPORTS = ["systec_mttkrp", "systec_mttkrp_host", "systec_plan_create", "systec_plan_execute",
+           "systec_plan_execute_ex", "systec_plan_stats", "systec_plan_prepared",
+           "systec_plan_copy_prepared", "systec_plan_last_launch", "systec_plan_destroy",
+           "systec_status_string", "systec_last_cuda_error", "systec_version", "systec_last_bad_entry"]
+
+_lib = None
+
+
+def load(path: str | None = None):
+    """Load libsystec.so (fails loudly when it is missing)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    p = path or LIB_PATH
+    if not os.path.exists(p):
+        raise ImportError(f"libsystec.so not built at {p}; run __graft_entry__.build() "
+                          "(there is no CPU fallback)")
+    lib = ctypes.CDLL(p)
+    i32, i64, vp = ctypes.c_int, ctypes.c_int64, ctypes.c_void_p
+    lib.systec_mttkrp.argtypes = [i32, i64, i64, vp, vp, vp, i32, vp, vp]
+    lib.systec_mttkrp_host.argtypes = [i32, i64, i64, vp, vp, vp, i32, vp, vp]
+    lib.systec_plan_create.argtypes = [ctypes.POINTER(vp), i32, i64, i64, vp, vp, vp]
+    lib.systec_plan_execute.argtypes = [vp, vp, i32, vp, vp]
+    lib.systec_plan_execute_ex.argtypes = [vp, vp, i32, vp, ctypes.POINTER(SystecExecOpts), vp]
+    lib.systec_plan_stats.argtypes = [vp, ctypes.POINTER(SystecStats)]
+    lib.systec_plan_prepared.argtypes = [vp, ctypes.POINTER(vp), ctypes.POINTER(vp)]
+    lib.systec_plan_copy_prepared.argtypes = [vp, vp, vp, vp]
+    lib.systec_plan_last_launch.argtypes = [vp] + [ctypes.POINTER(ctypes.c_int32)] * 5
+    lib.systec_plan_destroy.argtypes = [vp]
+    lib.systec_status_string.argtypes = [i32]
+    lib.systec_status_string.restype = ctypes.c_char_p
+    lib.systec_last_cuda_error.argtypes = []
+    lib.systec_version.argtypes = []
+    lib.systec_last_bad_entry.argtypes = []
+    lib.systec_last_bad_entry.restype = i64
+    for name in EXPORTS:
+        if name not in ("systec_status_string", "systec_last_bad_entry"):
+            getattr(lib, name).restype = i32
+    _lib = lib
+    return lib
+
+
+class SystecError(RuntimeError):
+    pass
+
+
+def _check(rc: int, what: str):
+    if rc == OK:
+        return
+    lib = load()
+    msg = f"{what}: {lib.systec_status_string(rc).decode()}"
+    if rc == ERR_CUDA:
+        msg += f" (cudaError {lib.systec_last_cuda_error()})"
+    if rc == ERR_INDEX:
+        msg += f" (first bad entry {lib.systec_last_bad_entry()})"
+    raise _ERRORS.get(rc, SystecError)(msg)
+
+
+def _stream_handle(stream):
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def _dev(t, dtype, name):
+    import torch
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise TypeError(f"{name} must be a CUDA tensor")
+    if t.dtype != dtype:
+        raise TypeError(f"{name} must be {dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    return ctypes.c_void_p(t.data_ptr() if t.numel() else 0)
+
+
+def _opts(**kw) -> SystecExecOpts:
+    o = SystecExecOpts()
+    for k, v in kw.items():
+        if k == "K":
+            o.reserved[0] = int(v)
+        elif k == "stages":
+            o.reserved[1] = int(v)
+        else:
+            setattr(o, k, int(v))
+    return o
+
+
+class Plan:
+    """A prepared (validated, canonicalised, sorted) symmetric tensor on the GPU:
+    ``systec_plan_create``.  ``idx`` [nnz][order] int32 and ``vals`` [nnz] fp32
+    are CUDA tensors; they may be freed after construction."""
+
+    def __init__(self, order: int, dim: int, idx, vals, stream=None):
+        import torch
+        lib = load()
+        nnz = int(vals.shape[0])
+        if idx.dim() != 2 or idx.shape[1] != order or idx.shape[0] != nnz:
+            raise ValueError("idx must be [nnz][order]")
+        h = ctypes.c_void_p()
+        _check(lib.systec_plan_create(ctypes.byref(h), order, dim, nnz, _dev(idx, torch.int32, "idx"),
+                                      _dev(vals, torch.float32, "vals"), _stream_handle(stream)),
+               "systec_plan_create")
+        self._h = h
+        self.order, self.dim, self.nnz = order, dim, nnz
+
+    def execute(self, B, C=None, stream=None, **opts):
+        """``systec_plan_execute(_ex)``: returns C [dim][R] fp32 (overwritten)."""
+        import torch
+        lib = load()
+        if B.dim() != 2 or B.shape[0] != self.dim:
+            raise ValueError("B must be [dim][R]")
+        R = int(B.shape[1])
+        if C is None:
+            C = torch.empty((self.dim, R), dtype=torch.float32, device=B.device)
+        if tuple(C.shape) != (self.dim, R):
+            raise ValueError("C must be [dim][R]")
+        bp, cp = _dev(B, torch.float32, "B"), _dev(C, torch.float32, "C")
+        s = _stream_handle(stream)
+        if opts:
+            o = _opts(**opts)
+            _check(lib.systec_plan_execute_ex(self._h, bp, R, cp, ctypes.byref(o), s), "systec_plan_execute_ex")
+        else:
+            _check(lib.systec_plan_execute(self._h, bp, R, cp, s), "systec_plan_execute")
+        return C
+
+    def stats(self) -> dict:
+        st = SystecStats()
+        _check(load().systec_plan_stats(self._h, ctypes.byref(st)), "systec_plan_stats")
+        d = {k: getattr(st, k) for k, _ in SystecStats._fields_ if k != "pad0"}
+        d["pattern_hist"] = list(st.pattern_hist)
+        return d
+
+    def prepared(self):
+        """Copy of the prepared stream: (coords [order][nnz] int32, vals [nnz] fp32) CUDA tensors."""
+        import torch
+        coords = torch.empty((self.order, self.nnz), dtype=torch.int32, device="cuda")
+        vals = torch.empty(self.nnz, dtype=torch.float32, device="cuda")
+        if self.nnz:
+            _check(load().systec_plan_copy_prepared(self._h, ctypes.c_void_p(coords.data_ptr()),
+                                                    ctypes.c_void_p(vals.data_ptr()), _stream_handle(None)),
+                   "systec_plan_copy_prepared")
+        return coords, vals
+
+    def last_launch(self) -> dict:
+        vals = [ctypes.c_int32() for _ in range(5)]
+        _check(load().systec_plan_last_launch(self._h, *[ctypes.byref(v) for v in vals]), "systec_plan_last_launch")
+        return dict(zip(["grid_x", "grid_y", "block", "smem_bytes", "kernel_id"], [v.value for v in vals]))
+
+    def destroy(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            load().systec_plan_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.destroy()
+        except Exception:
+            pass
+
+
+def plan_create(order, dim, idx, vals, stream=None) -> Plan:
+    return Plan(order, dim, idx, vals, stream)
+
+
+def mttkrp(order: int, dim: int, idx, vals, B, C=None, stream=None):
+    """One-shot ``systec_mttkrp`` on CUDA tensors; returns C [dim][R] (overwritten)."""
+    import torch
+    lib = load()
+    nnz = int(vals.shape[0])
+    if idx.dim() != 2 or idx.shape[1] != order or idx.shape[0] != nnz:
+        raise ValueError("idx must be [nnz][order]")
+    R = int(B.shape[1])
+    if C is None:
+        C = torch.empty((dim, R), dtype=torch.float32, device=B.device)
+    _check(lib.systec_mttkrp(order, dim, nnz, _dev(idx, torch.int32, "idx"), _dev(vals, torch.float32, "vals"),
+                             _dev(B, torch.float32, "B"), R, _dev(C, torch.float32, "C"), _stream_handle(stream)),
+           "systec_mttkrp")
+    return C
+
+
+def mttkrp_host(order: int, dim: int, idx, vals, B, C=None, stream=None):
+    """``systec_mttkrp_host`` on host arrays (numpy or pinned CPU tensors); returns C."""
+    lib = load()
+
+    def host_ptr(a, dtype, name):
+        if hasattr(a, "data_ptr"):          # torch CPU tensor (possibly pinned)
+            if a.is_cuda or not a.is_contiguous():
+                raise TypeError(f"{name} must be a contiguous host tensor")
+            return ctypes.c_void_p(a.data_ptr() if a.numel() else 0), a
+        arr = np.ascontiguousarray(a, dtype=dtype)
+        return ctypes.c_void_p(arr.ctypes.data if arr.size else 0), arr
+
+    nnz = int(vals.shape[0])
+    R = int(B.shape[1])
+    if C is None:
+        C = np.empty((dim, R), np.float32)
+    ip, _i = host_ptr(idx, np.int32, "idx")
+    vp_, _v = host_ptr(vals, np.float32, "vals")
+    bp, _b = host_ptr(B, np.float32, "B")
+    cp, _c = host_ptr(C, np.float32, "C")
+    if not hasattr(C, "data_ptr") and _c is not C:
+        raise ValueError("C must be a contiguous float32 array")
+    _check(lib.systec_mttkrp_host(order, dim, nnz, ip, vp_, bp, R, cp, _stream_handle(stream)),
+           "systec_mttkrp_host")
+    return C

@@ -1,0 +1,85 @@
+"""The C ABI library without a GPU: it loads, exports every symbol that
+include/systec.h declares, and the host-side argument checks answer before any
+CUDA call.  No compute calls here."""
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_symbols():
+    with open(os.path.join(ROOT, "include", "systec.h")) as f:
+        src = f.read()
+    return sorted(set(re.findall(r"SYSTEC_API\s+[\w\s\*]*?\b(systec_\w+)\s*\(", src)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    import __graft_entry__
+    __graft_entry__.build()
+    from paper_2406_09266_b200 import load
+    return load()
+
+
+def test_header_declares_the_north_star_call():
+    syms = header_symbols()
+    assert "systec_mttkrp" in syms and "systec_plan_execute" in syms and len(syms) >= 12
+
+
+def test_library_exports_every_header_symbol(lib):
+    from paper_2406_09266_b200 import EXPORTS
+    for name in header_symbols():
+        assert hasattr(lib, name), name
+    assert set(header_symbols()) == set(EXPORTS)
+
+
+def test_status_strings_and_version(lib):
+    assert lib.systec_status_string(0) == b"ok"
+    assert lib.systec_status_string(3) == b"index outside [0, dim)"
+    assert lib.systec_version() == 100
+    assert lib.systec_last_bad_entry() == -1
+
+
+def test_host_argument_checks_need_no_gpu(lib):
+    vp = ctypes.c_void_p
+    # order outside 2..5 -> UNSUPPORTED, before any CUDA call
+    assert lib.systec_mttkrp(7, 10, 0, None, None, vp(16), 4, vp(4096), None) == 2
+    assert lib.systec_mttkrp(1, 10, 0, None, None, vp(16), 4, vp(4096), None) == 2
+    # dim < 1, nnz < 0 -> ARG
+    assert lib.systec_mttkrp(3, 0, 0, None, None, vp(16), 4, vp(4096), None) == 1
+    assert lib.systec_mttkrp(3, 10, -1, None, None, vp(16), 4, vp(4096), None) == 1
+    # key wider than 64 bits (5 * 20 bits) -> UNSUPPORTED
+    assert lib.systec_mttkrp(5, 1 << 20, 0, None, None, vp(16), 4, vp(1 << 30), None) == 2
+    # null idx with nnz > 0 -> ARG
+    assert lib.systec_mttkrp(3, 10, 5, None, None, vp(16), 4, vp(4096), None) == 1
+    # R < 1 -> ARG
+    assert lib.systec_mttkrp(3, 10, 0, None, None, vp(16), 0, vp(4096), None) == 1
+    # C overlapping B -> ALIAS
+    assert lib.systec_mttkrp(3, 10, 0, None, None, vp(4096), 4, vp(4096 + 16), None) == 4
+    # plan-less calls
+    assert lib.systec_plan_execute(None, vp(16), 4, vp(4096), None) == 1
+    assert lib.systec_plan_stats(None, None) == 1
+    out = ctypes.c_void_p()
+    assert lib.systec_plan_create(ctypes.byref(out), 6, 10, 0, None, None, None) == 2
+    assert not out.value
+
+
+def test_product_path_has_no_oracle_dependency():
+    """The CUDA path never imports, links or calls oracle/ (and vice versa)."""
+    pkg = os.path.join(ROOT, "paper_2406_09266_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for fn in files:
+            if fn.endswith((".py", ".cu", ".cuh", ".h")):
+                with open(os.path.join(dirpath, fn)) as f:
+                    text = f.read()
+                assert not re.search(r"^\s*(import|from)\s+oracle", text, re.M), fn
+                assert "mttkrp_oracle" not in text and "liboracle" not in text, fn
+    for fn in os.listdir(os.path.join(ROOT, "oracle")):
+        if fn.endswith((".py", ".c")):
+            with open(os.path.join(ROOT, "oracle", fn)) as f:
+                text = f.read()
+            assert not re.search(r"^\s*(import|from)\s+paper_2406_09266_b200", text, re.M), fn
+            assert "libsystec" not in text and '#include "systec.h"' not in text, fn

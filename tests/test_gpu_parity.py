@@ -1,0 +1,216 @@
+"""Parity of the CUDA path (through the C ABI) with the CPU oracle.
+GPU tests: run with `pytest -m gpu` on a B200."""
+import numpy as np
+import pytest
+
+import oracle
+from synth import generate, integer_workload, scramble, small_random
+from synth.workloads import make
+
+from gpu_util import TOL, contraction_invariant, parity, sample_rows, to_dev
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def systec():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import __graft_entry__
+    __graft_entry__.build()
+    import paper_2406_09266_b200 as s
+    return s
+
+
+def run(systec, w, idx=None, vals=None, **opts):
+    import torch
+    idx = w.idx if idx is None else idx
+    vals = w.vals if vals is None else vals
+    di, dv, dB = to_dev(idx, vals, w.B)
+    plan = systec.Plan(w.order, w.dim, di, dv)
+    C = plan.execute(dB, **opts)
+    torch.cuda.synchronize()
+    out = C.cpu().numpy()
+    plan.destroy()
+    return out
+
+
+# ---------------------------------------------------------------- small, several tiles + ragged tail
+@pytest.mark.parametrize("n,dim,nnz,R", [
+    (3, 64, 2000, 8), (3, 300, 5003, 32), (3, 97, 777, 16),
+    (4, 40, 6001, 16), (4, 25, 1234, 4), (5, 18, 4099, 16), (5, 12, 999, 32), (2, 500, 3001, 32),
+])
+def test_parity_small(systec, n, dim, nnz, R):
+    w = small_random(n, dim, nnz, R, seed=nnz + n, diag_frac=0.15)
+    Cref, S = oracle.mttkrp(n, dim, w.idx, w.vals, w.B)
+    parity(run(systec, w), Cref, S)
+
+
+@pytest.mark.parametrize("R", [1, 2, 3, 4, 5, 8, 12, 16, 31, 32, 33, 64, 100, 128, 129, 256])
+def test_rank_sweep(systec, R):
+    w = small_random(3, 120, 3000, R, seed=R, diag_frac=0.2)
+    Cref, S = oracle.mttkrp(3, 120, w.idx, w.vals, w.B)
+    parity(run(systec, w), Cref, S)
+    parity(run(systec, w, force_scalar=1), Cref, S)
+
+
+@pytest.mark.parametrize("n", [3, 4, 5])
+def test_integer_valued_bit_exact(systec, n):
+    """Values and B in {-2..2}: every partial sum is an exactly representable
+    integer, so the atomic order cannot matter — GPU == oracle exactly."""
+    w = integer_workload(small_random(n, 30, 3000, 16, seed=n, diag_frac=0.3), seed=n)
+    Cref, _ = oracle.mttkrp(n, 30, w.idx, w.vals, w.B)
+    assert np.max(np.abs(Cref)) < 2 ** 24
+    Cg = run(systec, w)
+    assert np.array_equal(Cg.astype(np.float64), Cref)
+    Cg2 = run(systec, w, pos1_accumulate=1, K=5, stages=3)
+    assert np.array_equal(Cg2.astype(np.float64), Cref)
+
+
+def test_unsorted_noncanonical_input(systec):
+    w = small_random(4, 30, 5000, 16, seed=3, diag_frac=0.2)
+    si, sv = scramble(w.idx, w.vals, seed=9)
+    Cref, S = oracle.mttkrp(4, 30, w.idx, w.vals, w.B)
+    parity(run(systec, w, idx=si, vals=sv), Cref, S)
+
+
+def test_duplicates_add(systec):
+    w = small_random(3, 50, 2000, 8, seed=4, diag_frac=0.2)
+    idx = np.concatenate([w.idx, w.idx[::3]])
+    vals = np.concatenate([w.vals, w.vals[::3]])
+    Cref, S = oracle.mttkrp(3, 50, idx, vals, w.B)
+    parity(run(systec, w, idx=idx, vals=vals), Cref, S)
+
+
+def test_option_variants_agree(systec):
+    w = small_random(3, 200, 20000, 32, seed=5, diag_frac=0.1)
+    Cref, S = oracle.mttkrp(3, 200, w.idx, w.vals, w.B)
+    for opts in [dict(), dict(pos1_accumulate=1), dict(pos1_accumulate=-1), dict(l2_hints=-1),
+                 dict(warps_per_block=4), dict(warps_per_block=1, blocks_per_sm=1), dict(K=1), dict(K=7),
+                 dict(K=64, stages=4), dict(stages=3)]:
+        parity(run(systec, w, **opts), Cref, S)
+
+
+def test_hub_rows_long_runs(systec):
+    """Zipf-skewed input: long equal-leading-index runs cross chunk and warp
+    boundaries (the carried position-0 sums)."""
+    w = make("zipf_small", 3, 5000, 200000, 32, seed=3, mode="zipf", zipf_s=1.1)
+    Cref, S = oracle.mttkrp(3, w.dim, w.idx, w.vals, w.B)
+    parity(run(systec, w), Cref, S)
+    parity(run(systec, w, pos1_accumulate=1), Cref, S)
+
+
+def test_empty_and_degenerate(systec):
+    import torch
+    w = small_random(3, 10, 1, 4, seed=1)
+    Cref, S = oracle.mttkrp(3, 10, w.idx, w.vals, w.B)
+    parity(run(systec, w), Cref, S)
+    # nnz = 0: C is overwritten with zeros
+    di, dv, dB = to_dev(np.zeros((0, 3), np.int32), np.zeros(0, np.float32), w.B)
+    C = torch.full((10, 4), 7.0, device="cuda")
+    systec.mttkrp(3, 10, di, dv, dB, C)
+    torch.cuda.synchronize()
+    assert not C.any()
+    # dim = 1: every entry is all-equal
+    w1 = make("d1", 4, 1, 1, 3, seed=0)
+    Cref, S = oracle.mttkrp(4, 1, w1.idx, w1.vals, w1.B)
+    parity(run(systec, w1), Cref, S)
+
+
+def test_index_out_of_range_reports_entry(systec):
+    w = small_random(3, 20, 100, 4, seed=2)
+    idx = w.idx.copy()
+    idx[37, 1] = 20
+    di, dv, dB = to_dev(idx, w.vals, w.B)
+    with pytest.raises(IndexError, match="first bad entry 37"):
+        systec.Plan(3, 20, di, dv)
+    idx[37, 1] = -1
+    di, dv, _ = to_dev(idx, w.vals, w.B)
+    with pytest.raises(IndexError):
+        systec.mttkrp(3, 20, di, dv, dB)
+
+
+def test_misaligned_views_take_scalar_path(systec):
+    import torch
+    w = small_random(3, 64, 3000, 8, seed=6, diag_frac=0.2)
+    Cref, S = oracle.mttkrp(3, 64, w.idx, w.vals, w.B)
+    di, dv = to_dev(w.idx, w.vals)
+    Bbig = torch.zeros(64 * 8 + 1, device="cuda")
+    Bbig[1:] = torch.from_numpy(w.B.reshape(-1)).cuda()
+    Bv = Bbig[1:].view(64, 8)
+    Cbig = torch.zeros(64 * 8 + 1, device="cuda")
+    Cv = Cbig[1:].view(64, 8)
+    plan = systec.Plan(3, 64, di, dv)
+    plan.execute(Bv, Cv)
+    torch.cuda.synchronize()
+    parity(Cv.cpu().numpy(), Cref, S)
+    assert plan.last_launch()["kernel_id"] // 100 % 10 == 1     # scalar path
+
+
+def test_one_shot_and_host_calls(systec):
+    import torch
+    w = small_random(5, 15, 3000, 16, seed=8, diag_frac=0.3)
+    Cref, S = oracle.mttkrp(5, 15, w.idx, w.vals, w.B)
+    di, dv, dB = to_dev(w.idx, w.vals, w.B)
+    C = systec.mttkrp(5, 15, di, dv, dB)
+    torch.cuda.synchronize()
+    parity(C.cpu().numpy(), Cref, S)
+    Ch = systec.mttkrp_host(5, 15, w.idx, w.vals, w.B)
+    parity(Ch, Cref, S)
+    pin = [torch.from_numpy(a).pin_memory() for a in (w.idx, w.vals, w.B)]
+    Cp = torch.empty((15, 16), dtype=torch.float32).pin_memory()
+    systec.mttkrp_host(5, 15, *pin, C=Cp)
+    parity(Cp.numpy(), Cref, S)
+
+
+def test_prepare_canonicalises_sorts_and_counts(systec):
+    import torch
+    w = small_random(4, 25, 4000, 4, seed=12, diag_frac=0.3)
+    si, sv = scramble(w.idx, w.vals, seed=2)
+    di, dv = to_dev(si, sv)
+    plan = systec.Plan(4, 25, di, dv)
+    coords, pv = plan.prepared()
+    torch.cuda.synchronize()
+    got = coords.cpu().numpy().T
+    assert np.array_equal(got, w.idx)                   # w.idx is the canonical lexicographic order
+    assert np.array_equal(pv.cpu().numpy(), w.vals)
+    st = plan.stats()
+    c = w.idx.astype(np.int64)
+    assert st["G"] == int(np.sum(1 + np.sum(c[:, 1:] != c[:, :-1], axis=1)))
+    code = np.zeros(len(c), np.int64)
+    for t in range(3):
+        code |= (c[:, t] == c[:, t + 1]).astype(np.int64) << t
+    assert st["pattern_hist"][:8] == np.bincount(code, minlength=8).tolist()
+    assert st["lead_runs"] == len(np.unique(c[:, 0]))
+    assert st["max_lead_run"] == int(np.bincount(c[:, 0]).max())
+    assert st["expanded"] == oracle.count_expanded(4, w.idx)
+    assert st["input_was_sorted"] == 0
+    plan2 = systec.Plan(4, 25, *to_dev(w.idx, w.vals))
+    assert plan2.stats()["input_was_sorted"] == 1
+
+
+@pytest.mark.parametrize("name", ["c1"])
+def test_config_c1_full(systec, name):
+    w = generate(name)
+    Cref, S = oracle.mttkrp(w.order, w.dim, w.idx, w.vals, w.B)
+    err = parity(run(systec, w), Cref, S)
+    si, sv = scramble(w.idx, w.vals, seed=1)
+    parity(run(systec, w, idx=si, vals=sv), Cref, S)
+    print(f"{name}: max_rel_err={err:.3e}")
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name", ["c2", "c3", "c4", "c5"])
+def test_config_full_size_sampled(systec, name):
+    """BASELINE.json full sizes, default launch configuration (the one bench.py
+    times): sampled output rows checked against the oracle row by row, and the
+    full-contraction invariant P7 over all of C."""
+    w = generate(name)
+    Cg = run(systec, w)
+    rows = sample_rows(w)
+    Cref, S = oracle.mttkrp_rows(w.order, w.dim, w.idx, w.vals, w.B, rows)
+    err = parity(Cg[rows], Cref, S)
+    inv = contraction_invariant(w, Cg)
+    assert inv <= TOL, inv
+    print(f"{name}: rows={len(rows)} max_rel_err={err:.3e} P7={inv:.3e}")

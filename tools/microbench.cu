@@ -1,0 +1,229 @@
+// microbench.cu — measures the bounds the symmetric MTTKRP actually runs into
+// on this B200: HBM stream read, L2 random-row gather of
+// B-like tables, vector red.global throughput into random C rows, and the
+// same-row contention rate.  Prints one JSON object.
+//
+//   nvcc -std=c++17 -O3 -gencode arch=compute_100a,code=sm_100a -o tools/microbench tools/microbench.cu
+#include <cstdio>
+#include <cstdint>
+#include <vector>
+#include <cuda_runtime.h>
+
+#define CK(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) { fprintf(stderr, "%s:%d %s\n", __FILE__, __LINE__, cudaGetErrorString(e_)); return 1; } } while (0)
+
+__global__ void stream_read(const float4 *__restrict__ a, size_t n4, float *sink) {
+    float4 acc = make_float4(0, 0, 0, 0);
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n4; i += (size_t)gridDim.x * blockDim.x) {
+        float4 v = __ldg(a + i);
+        acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+    }
+    if (acc.x + acc.y + acc.z + acc.w == 12345.f) *sink = acc.x;
+}
+
+__device__ __forceinline__ uint32_t hash32(uint32_t x) {
+    x ^= x >> 16; x *= 0x7feb352dU; x ^= x >> 15; x *= 0x846ca68bU; x ^= x >> 16;
+    return x;
+}
+
+// each group of 8 lanes gathers one 128-byte row (R = 32 floats) per iteration
+__global__ void gather_rows(const float *__restrict__ B, uint32_t rows, int iters, float *sink) {
+    const int lane = threadIdx.x & 31, g = lane >> 3, j = lane & 7;
+    const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    float4 acc = make_float4(0, 0, 0, 0);
+#pragma unroll 4
+    for (int it = 0; it < iters; ++it) {
+        const uint32_t r = hash32(gw * 131071u + it * 4u + g) % rows;
+        float4 v = __ldg(reinterpret_cast<const float4 *>(B + (size_t)r * 32) + j);
+        acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+    }
+    if (acc.x + acc.y + acc.z + acc.w == 12345.f) *sink = acc.x;
+}
+
+__global__ void red_rows(float *C, uint32_t rows, int iters) {
+    const int lane = threadIdx.x & 31, g = lane >> 3, j = lane & 7;
+    const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const float4 v = make_float4(1.f, 1.f, 1.f, 1.f);
+    for (int it = 0; it < iters; ++it) {
+        const uint32_t r = hash32(gw * 131071u + it * 4u + g) % rows;
+        float *p = C + (size_t)r * 32 + j * 4;
+        asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
+    }
+}
+
+__global__ void red_rows_scalar(float *C, uint32_t rows, int iters) {
+    const int lane = threadIdx.x & 31, g = lane >> 3, j = lane & 7;
+    const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    for (int it = 0; it < iters; ++it) {
+        const uint32_t r = hash32(gw * 131071u + it * 4u + g) % rows;
+        float *p = C + (size_t)r * 32 + j * 4;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) atomicAdd(p + q, 1.f);
+    }
+}
+
+// gather 3 rows + red 2 rows per "entry": the c2 inner loop without index streaming
+__global__ void mttkrp_like(const float *__restrict__ B, float *C, uint32_t rows, int iters) {
+    const int lane = threadIdx.x & 31, g = lane >> 3, j = lane & 7;
+    const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    for (int it = 0; it < iters; ++it) {
+        const uint32_t h = gw * 131071u + it * 4u + g;
+        const uint32_t r0 = hash32(h) % rows, r1 = hash32(h ^ 0x9e3779b9u) % rows, r2 = hash32(h ^ 0x85ebca6bu) % rows;
+        float4 a = __ldg(reinterpret_cast<const float4 *>(B + (size_t)r0 * 32) + j);
+        float4 b = __ldg(reinterpret_cast<const float4 *>(B + (size_t)r1 * 32) + j);
+        float4 c = __ldg(reinterpret_cast<const float4 *>(B + (size_t)r2 * 32) + j);
+        float4 u = make_float4(a.x * b.x, a.y * b.y, a.z * b.z, a.w * b.w);
+        float4 w = make_float4(a.x * c.x, a.y * c.y, a.z * c.z, a.w * c.w);
+        float *p1 = C + (size_t)r1 * 32 + j * 4, *p2 = C + (size_t)r2 * 32 + j * 4;
+        asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p1), "f"(w.x), "f"(w.y), "f"(w.z), "f"(w.w) : "memory");
+        asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p2), "f"(u.x), "f"(u.y), "f"(u.z), "f"(u.w) : "memory");
+    }
+}
+
+int main() {
+    int dev = 0, sms = 0, l2 = 0, smem = 0, clk = 0;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    CK(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev));
+    CK(cudaDeviceGetAttribute(&smem, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev));
+    CK(cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, dev));
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    float *sink;
+    CK(cudaMalloc(&sink, 4));
+    printf("{\"sms\": %d, \"l2_bytes\": %d, \"smem_per_sm\": %d, \"clock_khz\": %d", sms, l2, smem, clk);
+
+    // 1) HBM stream read, 4 GiB
+    {
+        size_t bytes = size_t(4) << 30;
+        float4 *a;
+        CK(cudaMalloc(&a, bytes));
+        CK(cudaMemset(a, 0, bytes));
+        float best = 1e30f;
+        for (int r = 0; r < 5; ++r) {
+            CK(cudaEventRecord(e0));
+            stream_read<<<sms * 8, 512>>>(a, bytes / 16, sink);
+            CK(cudaEventRecord(e1));
+            CK(cudaEventSynchronize(e1));
+            float ms;
+            CK(cudaEventElapsedTime(&ms, e0, e1));
+            best = ms < best ? ms : best;
+        }
+        printf(", \"hbm_read_gbs\": %.1f", bytes / (best * 1e-3) / 1e9);
+        CK(cudaFree(a));
+    }
+    // 2) L2 / HBM random 128-B row gathers for several table sizes
+    const double tables_mb[] = {0.064, 0.64, 12.8, 64.0, 128.0, 512.0};
+    printf(", \"gather_128B_rows_gbs\": {");
+    for (int t = 0; t < 6; ++t) {
+        uint32_t rows = (uint32_t)(tables_mb[t] * 1e6 / 128);
+        float *B;
+        CK(cudaMalloc(&B, (size_t)rows * 128));
+        CK(cudaMemset(B, 0, (size_t)rows * 128));
+        const int iters = 256, blocks = sms * 8, threads = 256;
+        float best = 1e30f;
+        for (int r = 0; r < 4; ++r) {
+            CK(cudaEventRecord(e0));
+            gather_rows<<<blocks, threads>>>(B, rows, iters, sink);
+            CK(cudaEventRecord(e1));
+            CK(cudaEventSynchronize(e1));
+            float ms;
+            CK(cudaEventElapsedTime(&ms, e0, e1));
+            best = ms < best ? ms : best;
+        }
+        double bytes = (double)blocks * threads / 8 * iters * 128;
+        printf("%s\"%.3fMB\": %.1f", t ? ", " : "", tables_mb[t], bytes / (best * 1e-3) / 1e9);
+        CK(cudaFree(B));
+    }
+    printf("}");
+    // 3) red.global.add.v4.f32 into random 128-B rows
+    const double ctab_mb[] = {0.064, 0.64, 12.8, 128.0};
+    printf(", \"red_v4_128B_rows_gbs\": {");
+    for (int t = 0; t < 4; ++t) {
+        uint32_t rows = (uint32_t)(ctab_mb[t] * 1e6 / 128);
+        float *C;
+        CK(cudaMalloc(&C, (size_t)rows * 128));
+        CK(cudaMemset(C, 0, (size_t)rows * 128));
+        const int iters = 128, blocks = sms * 8, threads = 256;
+        float best = 1e30f;
+        for (int r = 0; r < 4; ++r) {
+            CK(cudaEventRecord(e0));
+            red_rows<<<blocks, threads>>>(C, rows, iters);
+            CK(cudaEventRecord(e1));
+            CK(cudaEventSynchronize(e1));
+            float ms;
+            CK(cudaEventElapsedTime(&ms, e0, e1));
+            best = ms < best ? ms : best;
+        }
+        double bytes = (double)blocks * threads / 8 * iters * 128;
+        printf("%s\"%.3fMB\": %.1f", t ? ", " : "", ctab_mb[t], bytes / (best * 1e-3) / 1e9);
+        CK(cudaFree(C));
+    }
+    printf("}");
+    // 3b) scalar atomicAdd, 12.8 MB
+    {
+        uint32_t rows = 100000;
+        float *C;
+        CK(cudaMalloc(&C, (size_t)rows * 128));
+        CK(cudaMemset(C, 0, (size_t)rows * 128));
+        const int iters = 64, blocks = sms * 8, threads = 256;
+        float best = 1e30f;
+        for (int r = 0; r < 3; ++r) {
+            CK(cudaEventRecord(e0));
+            red_rows_scalar<<<blocks, threads>>>(C, rows, iters);
+            CK(cudaEventRecord(e1));
+            CK(cudaEventSynchronize(e1));
+            float ms;
+            CK(cudaEventElapsedTime(&ms, e0, e1));
+            best = ms < best ? ms : best;
+        }
+        double bytes = (double)blocks * threads / 8 * iters * 128;
+        printf(", \"red_scalar_12.8MB_gbs\": %.1f", bytes / (best * 1e-3) / 1e9);
+        CK(cudaFree(C));
+    }
+    // 4) same-row contention: all groups red into 1 row / 64 rows
+    {
+        float *C;
+        CK(cudaMalloc(&C, 64 * 128));
+        for (uint32_t rows : {1u, 64u}) {
+            CK(cudaMemset(C, 0, 64 * 128));
+            const int iters = 16, blocks = sms * 2, threads = 256;
+            CK(cudaEventRecord(e0));
+            red_rows<<<blocks, threads>>>(C, rows, iters);
+            CK(cudaEventRecord(e1));
+            CK(cudaEventSynchronize(e1));
+            float ms;
+            CK(cudaEventElapsedTime(&ms, e0, e1));
+            double reds = (double)blocks * threads / 8 * iters;
+            printf(", \"same_row_red_rows_per_us_%u\": %.1f", rows, reds / (ms * 1e3));
+        }
+        CK(cudaFree(C));
+    }
+    // 5) the c2-shaped inner loop without the index stream: 3 gathers + 2 reds per entry
+    {
+        uint32_t rows = 100000;
+        float *B, *C;
+        CK(cudaMalloc(&B, (size_t)rows * 128));
+        CK(cudaMalloc(&C, (size_t)rows * 128));
+        CK(cudaMemset(B, 0, (size_t)rows * 128));
+        CK(cudaMemset(C, 0, (size_t)rows * 128));
+        const int iters = 128, blocks = sms * 8, threads = 256;
+        float best = 1e30f;
+        for (int r = 0; r < 4; ++r) {
+            CK(cudaEventRecord(e0));
+            mttkrp_like<<<blocks, threads>>>(B, C, rows, iters);
+            CK(cudaEventRecord(e1));
+            CK(cudaEventSynchronize(e1));
+            float ms;
+            CK(cudaEventElapsedTime(&ms, e0, e1));
+            best = ms < best ? ms : best;
+        }
+        double entries = (double)blocks * threads / 8 * iters;
+        printf(", \"c2_like_entries_per_s\": %.4e, \"c2_like_ms_per_10M\": %.4f", entries / (best * 1e-3),
+               best * 1e7 / entries);
+        CK(cudaFree(B));
+        CK(cudaFree(C));
+    }
+    printf("}\n");
+    return 0;
+}
