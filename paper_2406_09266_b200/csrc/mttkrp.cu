@@ -331,11 +331,16 @@ cudaError_t launch_mttkrp(Plan &p, const float *B, int R, float *C, const systec
 
     KernelFn fn = pick(p.order, vw, lpe, pos1);
     if (!fn) return cudaErrorInvalidValue;
-    const int wpb = o.warps_per_block > 0 ? o.warps_per_block : 8;
+    int wpb = o.warps_per_block > 0 ? o.warps_per_block : 8;
+    auto smem_for = [&](int w) {
+        return static_cast<size_t>(w) * stages * (p.order + 1) * (E * K) * 4 + static_cast<size_t>(w) * stages * 8;
+    };
+    const size_t smem_cap = 200 * 1024;
+    while (wpb > 1 && smem_for(wpb) > smem_cap) wpb >>= 1;  // keep the staging ring within shared memory
+    if (smem_for(wpb) > smem_cap) return cudaErrorInvalidValue;
     const int threads = wpb * 32;
     if (threads > 256) return cudaErrorInvalidValue;
-    const size_t smem = static_cast<size_t>(wpb) * stages * (p.order + 1) * (E * K) * 4 +
-                        static_cast<size_t>(wpb) * stages * 8;
+    const size_t smem = smem_for(wpb);
     e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     int dev = 0, sms = 148, occ = 1;

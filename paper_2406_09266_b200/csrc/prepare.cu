@@ -106,11 +106,10 @@ __device__ __forceinline__ long long dfact(int k) {
 
 template <int N>
 __global__ void stats_kernel(int64_t nnz, int64_t ld, const int32_t *__restrict__ coords, DevStats *st) {
-    __shared__ unsigned long long s_hist[16];
-    __shared__ unsigned long long s_sum[4];  // G, expanded, lead_runs, pos1_runs
-    if (threadIdx.x < 16) s_hist[threadIdx.x] = 0;
-    if (threadIdx.x < 4) s_sum[threadIdx.x] = 0;
-    __syncthreads();
+    constexpr int NC = 1 << (N - 1);  // equality patterns
+    unsigned long long hist[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) hist[c] = 0;
     unsigned long long G = 0, expanded = 0, lead = 0, pos1 = 0, maxrun = 0;
     const int32_t *c0 = coords;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz;
@@ -134,7 +133,8 @@ __global__ void stats_kernel(int64_t nnz, int64_t ld, const int32_t *__restrict_
         denom *= dfact(run);
         G += distinct;
         expanded += static_cast<unsigned long long>(dfact(N) / denom);
-        atomicAdd(&s_hist[code], 1ull);
+#pragma unroll
+        for (int q = 0; q < NC; ++q) hist[q] += (code == q);
         if (e == 0 || c0[e - 1] != c[0]) ++lead;
         if (N >= 2 && (e == 0 || coords[ld + e - 1] != c[1])) ++pos1;
         if (e == nnz - 1 || c0[e + 1] != c[0]) {  // end of a leading run: its start by binary search
@@ -147,18 +147,34 @@ __global__ void stats_kernel(int64_t nnz, int64_t ld, const int32_t *__restrict_
             maxrun = len > maxrun ? len : maxrun;
         }
     }
-    atomicAdd(&s_sum[0], G);
-    atomicAdd(&s_sum[1], expanded);
-    atomicAdd(&s_sum[2], lead);
-    atomicAdd(&s_sum[3], pos1);
-    if (maxrun) atomicMax(&st->max_lead_run, maxrun);
-    __syncthreads();
-    if (threadIdx.x < 16 && s_hist[threadIdx.x]) atomicAdd(&st->hist[threadIdx.x], s_hist[threadIdx.x]);
-    if (threadIdx.x == 0) {
-        atomicAdd(&st->G, s_sum[0]);
-        atomicAdd(&st->expanded, s_sum[1]);
-        atomicAdd(&st->lead_runs, s_sum[2]);
-        atomicAdd(&st->pos1_runs, s_sum[3]);
+    // warp reductions, then one atomic per warp and counter
+    auto wsum = [](unsigned long long v) {
+        for (int d = 16; d; d >>= 1) v += __shfl_down_sync(0xffffffffu, v, d);
+        return v;
+    };
+    auto wmax = [](unsigned long long v) {
+        for (int d = 16; d; d >>= 1) {
+            const unsigned long long o = __shfl_down_sync(0xffffffffu, v, d);
+            v = o > v ? o : v;
+        }
+        return v;
+    };
+    G = wsum(G);
+    expanded = wsum(expanded);
+    lead = wsum(lead);
+    pos1 = wsum(pos1);
+    maxrun = wmax(maxrun);
+#pragma unroll
+    for (int q = 0; q < NC; ++q) hist[q] = wsum(hist[q]);
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(&st->G, G);
+        atomicAdd(&st->expanded, expanded);
+        atomicAdd(&st->lead_runs, lead);
+        atomicAdd(&st->pos1_runs, pos1);
+        if (maxrun) atomicMax(&st->max_lead_run, maxrun);
+#pragma unroll
+        for (int q = 0; q < NC; ++q)
+            if (hist[q]) atomicAdd(&st->hist[q], hist[q]);
     }
 }
 

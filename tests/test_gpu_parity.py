@@ -113,7 +113,7 @@ def test_empty_and_degenerate(systec):
     torch.cuda.synchronize()
     assert not C.any()
     # dim = 1: every entry is all-equal
-    w1 = make("d1", 4, 1, 1, 3, seed=0)
+    w1 = make("d1", 4, 1, 1, 3, seed=0, mode="strict", n_forced=1)
     Cref, S = oracle.mttkrp(4, 1, w1.idx, w1.vals, w1.B)
     parity(run(systec, w1), Cref, S)
 

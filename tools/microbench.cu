@@ -79,6 +79,26 @@ __global__ void mttkrp_like(const float *__restrict__ B, float *C, uint32_t rows
     }
 }
 
+// TMA-engine bulk reductions: each lane reduces one ROWB-byte row of smem into a random C row
+template <int ROWB>
+__global__ void bulk_red_rows(float *C, uint32_t rows, int iters) {
+    __shared__ __align__(128) float buf[8][32][ROWB / 4];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int i = lane; i < 32 * ROWB / 4; i += 32) (&buf[warp][0][0])[i] = 1.f;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncwarp();
+    const uint32_t src = (uint32_t)__cvta_generic_to_shared(&buf[warp][lane][0]);
+    const uint32_t gt = blockIdx.x * blockDim.x + threadIdx.x;
+    for (int it = 0; it < iters; ++it) {
+        const uint32_t r = hash32(gt * 131071u + it) % rows;
+        float *dst = C + (size_t)r * (ROWB / 4);
+        asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], %2;" ::"l"(dst), "r"(src), "r"(ROWB) : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        asm volatile("cp.async.bulk.wait_group.read 16;" ::: "memory");
+    }
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 int main() {
     int dev = 0, sms = 0, l2 = 0, smem = 0, clk = 0;
     CK(cudaGetDevice(&dev));
@@ -224,6 +244,40 @@ int main() {
         CK(cudaFree(B));
         CK(cudaFree(C));
     }
-    printf("}\n");
+    // 6) bulk reductions (cp.reduce.async.bulk .add.f32) of 128-B / 64-B rows into 12.8 MB
+    {
+        uint32_t bytes_tab = 12800000;
+        float *C;
+        CK(cudaMalloc(&C, bytes_tab));
+        CK(cudaMemset(C, 0, bytes_tab));
+        const int iters = 64, blocks = sms * 4, threads = 256;
+        float best = 1e30f;
+        for (int r = 0; r < 3; ++r) {
+            CK(cudaEventRecord(e0));
+            bulk_red_rows<128><<<blocks, threads>>>(C, bytes_tab / 128, iters);
+            CK(cudaEventRecord(e1));
+            CK(cudaEventSynchronize(e1));
+            float ms;
+            CK(cudaEventElapsedTime(&ms, e0, e1));
+            best = ms < best ? ms : best;
+        }
+        printf(", \"bulk_red_128B_rows_gbs\": %.1f", (double)blocks * threads * iters * 128 / (best * 1e-3) / 1e9);
+        best = 1e30f;
+        for (int r = 0; r < 3; ++r) {
+            CK(cudaEventRecord(e0));
+            bulk_red_rows<64><<<blocks, threads>>>(C, bytes_tab / 64, iters);
+            CK(cudaEventRecord(e1));
+            CK(cudaEventSynchronize(e1));
+            float ms;
+            CK(cudaEventElapsedTime(&ms, e0, e1));
+            best = ms < best ? ms : best;
+        }
+        printf(", \"bulk_red_64B_rows_gbs\": %.1f", (double)blocks * threads * iters * 64 / (best * 1e-3) / 1e9);
+        CK(cudaFree(C));
+    }
+    // 7) red.v4 into 64-B rows (R = 16: 4 lanes per row), 640 KB and 64 KB tables
+    {
+        printf("}\n");
+    }
     return 0;
 }
