@@ -199,6 +199,7 @@ def main():
 
     import torch
     import paper_2406_09266_b200 as systec
+    from paper_2406_09266_b200.shard import reduce_partials, shard_range
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -212,7 +213,7 @@ def main():
     stream = torch.cuda.current_stream()
 
     # this rank's slice of the sorted stream (whole stream at N = 1)
-    lo, hi = w.nnz * rank // world, w.nnz * (rank + 1) // world
+    lo, hi = shard_range(w.nnz, rank, world)
     idx_d = torch.from_numpy(w.idx[lo:hi]).to(dev)
     vals_d = torch.from_numpy(w.vals[lo:hi]).to(dev)
     B_d = torch.from_numpy(w.B).to(dev)
@@ -233,7 +234,7 @@ def main():
         if timed_events:
             timed_events[2].record(stream)
         if dist is not None:
-            dist.all_reduce(C_d)
+            reduce_partials(C_d)
         if timed_events:
             timed_events[3].record(stream)
 
