@@ -1,0 +1,326 @@
+// mttkrp_kernel.cuh — the sm_100a symmetric sparse MTTKRP kernel template
+// (SURVEY.md §8(a) a3-a6).  Instantiated per order in mttkrp_n{2,3,4,5}.cu.
+//
+// What one stored canonical entry e = (c_0 <= ... <= c_{n-1}; v) contributes
+// (PAPER.md:859-865 for the MTTKRP, Listings 6/7 PAPER.md:685-729 for the
+// symmetrised form, coef_table.cuh for the factors):
+//
+//     for every run-first position t:   C[c_t, r] += coef[code][t] * v * prod_{s != t} B[c_s, r]
+//
+// i.e. one read of the canonical entry, one gather per B
+// row the entry names (common tensor access elimination),
+// and one update per distinct index position (distributive grouping,
+// PAPER.md:577-591), diagonals included through the coefficient table (no
+// separate loop nest: this departs from Listing 7's diagonal splitting,
+// PAPER.md:616-638).
+//
+// B200 mapping
+//   * persistent grid; each warp owns a contiguous, nnz-balanced range of the
+//     sorted stream (the nonzero-parallel loop with atomic output updates that
+//     PAPER.md:918 names as future work);
+//   * the range is consumed in chunks of CH = E*K entries that one elected lane
+//     stages into shared memory with 1-D bulk async copies (TMA engine,
+//     `cp.async.bulk` + mbarrier, evict-first L2 policy), in a ring of S stages;
+//   * a warp is split into E = 32/LPE lane groups; group g walks entries
+//     [g*K, (g+1)*K) of the chunk (K odd => the E groups hit distinct smem
+//     banks); its LPE lanes spread over the rank dimension, VPL float4 (or one
+//     float) per lane; B rows (rank-contiguous: the concordant B_T of
+//     Listing 7) are gathered with 16-byte loads under an evict-last L2 policy;
+//   * position 0: entries are sorted, so equal leading indices are contiguous;
+//     the group keeps the running sum in registers (the workspace
+//     transformation) and writes it only when c_0 changes;
+//     at the chunk end a segmented shuffle reduction merges the groups'
+//     pending sums and the last segment is carried into the next chunk;
+//   * position 1 optionally accumulates the same way along runs of equal c_1;
+//   * every other run-first position issues a vector `red.global.add.v4.f32`.
+#pragma once
+#include <cstdint>
+
+#include "coef_table.cuh"
+#include "internal.cuh"
+#include "ptx.cuh"
+
+namespace systec {
+
+// one copy per translation unit (no relocatable device code needed)
+static __constant__ CoefTable kCoef = make_coef_table();
+
+struct KParams {
+    const int32_t *coords;  // [N][ld]
+    const float *vals;      // [ld]
+    const float *B;         // [dim][R]
+    float *C;               // [dim][R]
+    int64_t ld;
+    int64_t nnz;
+    int64_t span;           // entries per warp (multiple of 4)
+    uint32_t R;
+    int K;                  // entries per lane group per chunk
+    int stages;             // shared-memory ring depth
+    int hints;              // 1: evict-last policy on B gathers, 0: evict-normal
+};
+
+using KernelFn = void (*)(KParams);
+
+template <int VW> struct VecT;
+template <> struct VecT<4> {
+    using T = float4;
+    static __device__ __forceinline__ T zero() { return make_float4(0.f, 0.f, 0.f, 0.f); }
+    static __device__ __forceinline__ T mul(T a, T b) { return make_float4(a.x * b.x, a.y * b.y, a.z * b.z, a.w * b.w); }
+    static __device__ __forceinline__ T scale(float s, T a) { return make_float4(s * a.x, s * a.y, s * a.z, s * a.w); }
+    static __device__ __forceinline__ T add(T a, T b) { return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w); }
+    static __device__ __forceinline__ T load(const float *p, uint64_t pol) { return ldg4_hint(p, pol); }
+    static __device__ __forceinline__ void red(float *p, T v) { red_add4(p, v); }
+    static __device__ __forceinline__ T shfl_down(T v, int d) {
+        return make_float4(__shfl_down_sync(0xffffffffu, v.x, d), __shfl_down_sync(0xffffffffu, v.y, d),
+                           __shfl_down_sync(0xffffffffu, v.z, d), __shfl_down_sync(0xffffffffu, v.w, d));
+    }
+    static __device__ __forceinline__ T shfl(T v, int src) {
+        return make_float4(__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src),
+                           __shfl_sync(0xffffffffu, v.z, src), __shfl_sync(0xffffffffu, v.w, src));
+    }
+};
+template <> struct VecT<1> {
+    using T = float;
+    static __device__ __forceinline__ T zero() { return 0.f; }
+    static __device__ __forceinline__ T mul(T a, T b) { return a * b; }
+    static __device__ __forceinline__ T scale(float s, T a) { return s * a; }
+    static __device__ __forceinline__ T add(T a, T b) { return a + b; }
+    static __device__ __forceinline__ T load(const float *p, uint64_t pol) { return ldg1_hint(p, pol); }
+    static __device__ __forceinline__ void red(float *p, T v) { red_add1(p, v); }
+    static __device__ __forceinline__ T shfl_down(T v, int d) { return __shfl_down_sync(0xffffffffu, v, d); }
+    static __device__ __forceinline__ T shfl(T v, int src) { return __shfl_sync(0xffffffffu, v, src); }
+};
+
+__device__ __forceinline__ uint64_t policy_evict_normal() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+
+// rank offset of row c: 32x32 -> 64-bit multiply (one IMAD.WIDE.U32)
+__device__ __forceinline__ uint64_t row_off(int32_t c, uint32_t R) {
+    return static_cast<uint64_t>(static_cast<uint32_t>(c)) * R;
+}
+
+template <int N, int LPE, int VPL, int VW, bool POS1>
+__global__ void __launch_bounds__(256) mttkrp_sym_kernel(const KParams p) {
+    using V = VecT<VW>;
+    using T = typename V::T;
+    constexpr int E = 32 / LPE;          // lane groups (entries in flight) per warp
+    constexpr int ARR = N + 1;           // staged arrays: c_0..c_{N-1}, v
+    constexpr int QS = LPE * VW;         // column stride between a lane's vectors
+    constexpr int TILE = LPE * VPL * VW; // rank columns per blockIdx.y
+    const int K = p.K;
+    const int CH = E * K;
+    const int S = p.stages;
+    const int WPB = blockDim.x >> 5;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int g = lane / LPE, j = lane % LPE;
+
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    int32_t *wbuf = reinterpret_cast<int32_t *>(smem_raw) + static_cast<size_t>(warp) * S * ARR * CH;
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw + static_cast<size_t>(WPB) * S * ARR * CH * 4) + warp * S;
+
+    const int64_t gw = static_cast<int64_t>(blockIdx.x) * WPB + warp;
+    const int64_t begin = gw * p.span;
+    const int64_t end = min(begin + p.span, p.nnz);
+    if (begin >= end) return;  // warp-uniform; no block-wide barrier below
+    const int64_t nch = (end - begin + CH - 1) / CH;
+
+    const uint32_t R = p.R;
+    const uint32_t col0 = blockIdx.y * TILE + j * VW;
+    bool act[VPL];
+#pragma unroll
+    for (int q = 0; q < VPL; ++q) act[q] = col0 + q * QS < R;
+    const float *Bc = p.B + col0;
+    float *Cc = p.C + col0;
+    const uint64_t pol_keep = p.hints ? policy_evict_last() : policy_evict_normal();
+    const uint64_t pol_stream = policy_evict_first();
+    const float *coef = kCoef.v[N - 2][0];
+
+    if (lane == 0) {
+        for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
+        fence_mbar_init();
+    }
+    __syncwarp();
+
+    auto issue = [&](int64_t k) {
+        const int s = static_cast<int>(k % S);
+        const int64_t cb = begin + k * CH;
+        const int64_t cnt = min(static_cast<int64_t>(CH), end - cb);
+        const uint32_t bytes = static_cast<uint32_t>(((cnt + 3) & ~3ll) * 4);
+        int32_t *dst = wbuf + static_cast<size_t>(s) * ARR * CH;
+        mbar_arrive_expect_tx(&bars[s], bytes * ARR);
+#pragma unroll
+        for (int a = 0; a < N; ++a) bulk_g2s(dst + a * CH, p.coords + a * p.ld + cb, bytes, &bars[s], pol_stream);
+        bulk_g2s(dst + N * CH, p.vals + cb, bytes, &bars[s], pol_stream);
+    };
+
+    if (lane == 0)
+        for (int64_t k = 0; k < min(static_cast<int64_t>(S - 1), nch); ++k) issue(k);
+
+    // running sums: position 0 (carried across chunks) and position 1
+    int cur0 = -1;
+    T acc0[VPL];
+    int cur1 = -1;
+    bool has1 = false;
+    T acc1[VPL];
+#pragma unroll
+    for (int q = 0; q < VPL; ++q) acc0[q] = acc1[q] = V::zero();
+
+    for (int64_t k = 0; k < nch; ++k) {
+        if (lane == 0 && k + S - 1 < nch) {
+            fence_proxy_async_smem();
+            issue(k + S - 1);
+        }
+        const int s = static_cast<int>(k % S);
+        mbar_wait(&bars[s], static_cast<uint32_t>((k / S) & 1));
+
+        const int32_t *sc = wbuf + static_cast<size_t>(s) * ARR * CH;
+        const float *sv = reinterpret_cast<const float *>(sc + N * CH);
+        const int64_t cb = begin + k * CH;
+        const int cnt = static_cast<int>(min(static_cast<int64_t>(CH), end - cb));
+        const int lo = g * K;
+        const int hi = min(lo + K, cnt);
+
+        for (int i = lo; i < hi; ++i) {
+            int32_t c[N];
+#pragma unroll
+            for (int t = 0; t < N; ++t) c[t] = sc[t * CH + i];
+            const float v = sv[i];
+            int code = 0;
+#pragma unroll
+            for (int t = 0; t + 1 < N; ++t) code |= (c[t] == c[t + 1]) << t;
+            const float *cf = coef + code * kMaxOrder;
+
+            uint64_t off[N];
+#pragma unroll
+            for (int t = 0; t < N; ++t) off[t] = row_off(c[t], R);
+            T b[N][VPL];
+#pragma unroll
+            for (int t = 0; t < N; ++t)
+#pragma unroll
+                for (int q = 0; q < VPL; ++q) b[t][q] = act[q] ? V::load(Bc + off[t] + q * QS, pol_keep) : V::zero();
+
+            // prefix / suffix products: u_t = (coef_t v) prod_{s<t} b_s prod_{s>t} b_s
+            T u[N][VPL];
+#pragma unroll
+            for (int q = 0; q < VPL; ++q) {
+                T pre[N];
+                pre[1 % N] = b[0][q];
+#pragma unroll
+                for (int t = 2; t < N; ++t) pre[t] = V::mul(pre[t - 1], b[t - 1][q]);
+                T suf = b[N - 1][q];
+#pragma unroll
+                for (int t = N - 1; t >= 0; --t) {
+                    const T prod = (t == N - 1) ? pre[t] : (t == 0 ? suf : V::mul(pre[t], suf));
+                    u[t][q] = V::scale(cf[t] * v, prod);
+                    if (t > 0 && t < N - 1) suf = V::mul(suf, b[t][q]);
+                }
+            }
+
+            // position 0: register run accumulation
+            if (c[0] != cur0) {
+                if (cur0 >= 0) {
+                    const uint64_t o = row_off(cur0, R);
+#pragma unroll
+                    for (int q = 0; q < VPL; ++q)
+                        if (act[q]) V::red(Cc + o + q * QS, acc0[q]);
+                }
+                cur0 = c[0];
+#pragma unroll
+                for (int q = 0; q < VPL; ++q) acc0[q] = V::zero();
+            }
+#pragma unroll
+            for (int q = 0; q < VPL; ++q) acc0[q] = V::add(acc0[q], u[0][q]);
+            // position 1
+            if (POS1) {
+                if (c[1] != cur1) {
+                    if (has1) {
+                        const uint64_t o = row_off(cur1, R);
+#pragma unroll
+                        for (int q = 0; q < VPL; ++q)
+                            if (act[q]) V::red(Cc + o + q * QS, acc1[q]);
+                    }
+                    cur1 = c[1];
+                    has1 = false;
+#pragma unroll
+                    for (int q = 0; q < VPL; ++q) acc1[q] = V::zero();
+                }
+                if (cf[1] != 0.f) {
+                    has1 = true;
+#pragma unroll
+                    for (int q = 0; q < VPL; ++q) acc1[q] = V::add(acc1[q], u[1][q]);
+                }
+            }
+#pragma unroll
+            for (int t = POS1 ? 2 : 1; t < N; ++t)
+                if (cf[t] != 0.f) {
+#pragma unroll
+                    for (int q = 0; q < VPL; ++q)
+                        if (act[q]) V::red(Cc + off[t] + q * QS, u[t][q]);
+                }
+        }
+        __syncwarp();
+
+        if (POS1) {
+            if (has1) {
+                const uint64_t o = row_off(cur1, R);
+#pragma unroll
+                for (int q = 0; q < VPL; ++q)
+                    if (act[q]) V::red(Cc + o + q * QS, acc1[q]);
+            }
+            has1 = false;
+            cur1 = -1;
+#pragma unroll
+            for (int q = 0; q < VPL; ++q) acc1[q] = V::zero();
+        }
+
+        // segmented reduction of the groups' pending position-0 sums
+        // (keys are non-decreasing in g; empty tail groups carry key -1)
+        const int key = cur0;
+#pragma unroll
+        for (int d = 1; d < E; d <<= 1) {
+            const int ok = __shfl_down_sync(0xffffffffu, key, d * LPE);
+            const bool take = (g + d < E) && ok == key;
+#pragma unroll
+            for (int q = 0; q < VPL; ++q) {
+                const T o = V::shfl_down(acc0[q], d * LPE);
+                if (take) acc0[q] = V::add(acc0[q], o);
+            }
+        }
+        const int prev_key = __shfl_up_sync(0xffffffffu, key, LPE);
+        const bool head = (g == 0) || (prev_key != key);
+        const int last_key = __shfl_sync(0xffffffffu, key, (E - 1) * LPE);
+        const bool carry = (k + 1 < nch);  // chunk was full: the next chunk continues the stream
+        if (head && key >= 0 && !(carry && key == last_key)) {
+            const uint64_t o = row_off(key, R);
+#pragma unroll
+            for (int q = 0; q < VPL; ++q)
+                if (act[q]) V::red(Cc + o + q * QS, acc0[q]);
+        }
+        if (carry) {
+            const unsigned heads = __ballot_sync(0xffffffffu, head && j == 0 && key == last_key);
+            const int hl = __ffs(heads) - 1;  // lane of the last segment's head (j == 0)
+#pragma unroll
+            for (int q = 0; q < VPL; ++q) {
+                const T carried = V::shfl(acc0[q], hl + j);
+                acc0[q] = (g == 0) ? carried : V::zero();
+            }
+            cur0 = (g == 0) ? last_key : -1;
+        } else {
+            cur0 = -1;
+#pragma unroll
+            for (int q = 0; q < VPL; ++q) acc0[q] = V::zero();
+        }
+    }
+}
+
+// instantiation tables, one translation unit per order (mttkrp_n{2..5}.cu)
+template <int N> KernelFn pick_kernel(int vw, int lpe, int vpl, bool pos1);
+template <> KernelFn pick_kernel<2>(int vw, int lpe, int vpl, bool pos1);
+template <> KernelFn pick_kernel<3>(int vw, int lpe, int vpl, bool pos1);
+template <> KernelFn pick_kernel<4>(int vw, int lpe, int vpl, bool pos1);
+template <> KernelFn pick_kernel<5>(int vw, int lpe, int vpl, bool pos1);
+
+}  // namespace systec

@@ -1,0 +1,46 @@
+// mttkrp_n2.cu — instantiations of mttkrp_sym_kernel for order 2 (split per
+// order so the instantiations compile in parallel).
+#include "mttkrp_kernel.cuh"
+
+namespace systec {
+
+template <int LPE, int VPL, int VW>
+static KernelFn pos1_of(bool pos1) {
+    return pos1 ? mttkrp_sym_kernel<2, LPE, VPL, VW, true> : mttkrp_sym_kernel<2, LPE, VPL, VW, false>;
+}
+
+template <>
+KernelFn pick_kernel<2>(int vw, int lpe, int vpl, bool pos1) {
+    if (vw == 1) {
+        if (vpl != 1) return nullptr;
+        switch (lpe) {
+            case 1: return pos1_of<1, 1, 1>(pos1);
+            case 2: return pos1_of<2, 1, 1>(pos1);
+            case 4: return pos1_of<4, 1, 1>(pos1);
+            case 8: return pos1_of<8, 1, 1>(pos1);
+            case 16: return pos1_of<16, 1, 1>(pos1);
+            case 32: return pos1_of<32, 1, 1>(pos1);
+            default: return nullptr;
+        }
+    }
+    switch (lpe * 8 + vpl) {  // (lanes per entry, float4 per lane)
+        case 1 * 8 + 1: return pos1_of<1, 1, 4>(pos1);
+        case 1 * 8 + 2: return pos1_of<1, 2, 4>(pos1);
+        case 1 * 8 + 4: return pos1_of<1, 4, 4>(pos1);
+        case 2 * 8 + 1: return pos1_of<2, 1, 4>(pos1);
+        case 2 * 8 + 2: return pos1_of<2, 2, 4>(pos1);
+        case 2 * 8 + 4: return pos1_of<2, 4, 4>(pos1);
+        case 4 * 8 + 1: return pos1_of<4, 1, 4>(pos1);
+        case 4 * 8 + 2: return pos1_of<4, 2, 4>(pos1);
+        case 4 * 8 + 4: return pos1_of<4, 4, 4>(pos1);
+        case 8 * 8 + 1: return pos1_of<8, 1, 4>(pos1);
+        case 8 * 8 + 2: return pos1_of<8, 2, 4>(pos1);
+        case 8 * 8 + 4: return pos1_of<8, 4, 4>(pos1);
+        case 16 * 8 + 1: return pos1_of<16, 1, 4>(pos1);
+        case 16 * 8 + 2: return pos1_of<16, 2, 4>(pos1);
+        case 32 * 8 + 1: return pos1_of<32, 1, 4>(pos1);
+        default: return nullptr;
+    }
+}
+
+}  // namespace systec

@@ -117,6 +117,8 @@ def _opts(**kw) -> SystecExecOpts:
             o.reserved[0] = int(v)
         elif k == "stages":
             o.reserved[1] = int(v)
+        elif k == "vpl":
+            o.reserved[2] = int(v)
         else:
             setattr(o, k, int(v))
     return o
@@ -181,7 +183,12 @@ class Plan:
     def last_launch(self) -> dict:
         vals = [ctypes.c_int32() for _ in range(5)]
         _check(load().systec_plan_last_launch(self._h, *[ctypes.byref(v) for v in vals]), "systec_plan_last_launch")
-        return dict(zip(["grid_x", "grid_y", "block", "smem_bytes", "kernel_id"], [v.value for v in vals]))
+        d = dict(zip(["grid_x", "grid_y", "block", "smem_bytes", "kernel_id"], [v.value for v in vals]))
+        kid = d["kernel_id"]
+        if kid >= 0:   # decimal fields: order | vw | lpe (2 digits) | vpl | pos1
+            d.update(order=kid // 100000, vw=kid // 10000 % 10, lpe=kid // 100 % 100, vpl=kid // 10 % 10,
+                     pos1=kid % 10)
+        return d
 
     def destroy(self):
         if getattr(self, "_h", None) is not None and self._h.value:
