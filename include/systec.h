@@ -87,6 +87,12 @@ typedef struct systec_exec_opts {
     int32_t force_scalar;        /* 1 = scalar (non-float4) path even when float4 is possible  */
     int32_t no_zero;             /* 1 = accumulate into C instead of overwriting it            */
     int32_t l2_hints;            /* 0 = default (on), -1 = off                                 */
+    /* reserved[0] K: entries per lane group per chunk (0 = auto)
+     * reserved[1] stages: shared-memory ring depth (0 = 2)
+     * reserved[2] vpl: float4 per lane, 1/2/4 (0 = 1)
+     * reserved[3] prefetch: 1 on, -1 off, 0 = auto (on when B > 32 MB)
+     * reserved[4] copies: replicas of C for L2-slice spreading, 1 = off, 0 = auto
+     *             (outputs < 4 MB and nnz >= 1e5: up to 32 replicas)          */
     int32_t reserved[10];
 } systec_exec_opts;
 
@@ -127,7 +133,9 @@ SYSTEC_API int systec_plan_create(systec_plan *out, int order, int64_t dim, int6
 
 /*
  * Execute: C[dim][R] = MTTKRP(plan, B).  Zeroes C and launches the kernel on
- * `stream`; never allocates, never synchronises (CUDA-graph capturable).
+ * `stream`; never synchronises (CUDA-graph capturable).  Its only allocation
+ * is stream-ordered scratch from the device's default pool (cudaMallocAsync)
+ * for the replicas of a small C (< 4 MB), returned before the call's work ends.
  * Concurrent executions of one plan on different streams are safe when
  * their C buffers differ.  Errors: ARG, ALIAS, CUDA (launch failure).
  */

@@ -10,12 +10,12 @@ namespace systec {
 
 namespace {
 
-KernelFn pick(int order, int vw, int lpe, int vpl, bool pos1) {
+KernelFn pick(int order, int vw, int lpe, int vpl, bool pos1, bool pf) {
     switch (order) {
-        case 2: return pick_kernel<2>(vw, lpe, vpl, pos1);
-        case 3: return pick_kernel<3>(vw, lpe, vpl, pos1);
-        case 4: return pick_kernel<4>(vw, lpe, vpl, pos1);
-        case 5: return pick_kernel<5>(vw, lpe, vpl, pos1);
+        case 2: return pick_kernel<2>(vw, lpe, vpl, pos1, pf);
+        case 3: return pick_kernel<3>(vw, lpe, vpl, pos1, pf);
+        case 4: return pick_kernel<4>(vw, lpe, vpl, pos1, pf);
+        case 5: return pick_kernel<5>(vw, lpe, vpl, pos1, pf);
         default: return nullptr;
     }
 }
@@ -42,15 +42,66 @@ int default_K(int E) {
 
 }  // namespace
 
+__global__ void reduce_copies_kernel(const float *__restrict__ Cp, float *__restrict__ C, int64_t plane, int copies,
+                                     int vec) {
+    const int64_t n4 = vec ? plane / 4 : 0;
+    const float4 *P4 = reinterpret_cast<const float4 *>(Cp);
+    float4 *C4 = reinterpret_cast<float4 *>(C);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+        float4 a = P4[i];
+        for (int c = 1; c < copies; ++c) {
+            const float4 b = P4[c * n4 + i];
+            a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
+        }
+        C4[i] = a;
+    }
+    for (int64_t i = 4 * n4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < plane;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        float a = 0.f;
+        for (int c = 0; c < copies; ++c) a += Cp[c * plane + i];
+        C[i] = a;
+    }
+}
+
 cudaError_t launch_mttkrp(Plan &p, const float *B, int R, float *C, const systec_exec_opts &o, cudaStream_t s) {
     cudaError_t e;
-    if (!o.no_zero) {
-        e = cudaMemsetAsync(C, 0, static_cast<size_t>(p.dim) * R * sizeof(float), s);
+    const int64_t plane = p.dim * static_cast<int64_t>(R);
+    // L2-slice spreading: an output smaller than ~4 MB maps onto a few L2
+    // slices whose atomic units then serialise the reductions (ncu on c5:
+    // atomic-input activity max 57 % vs avg 20 %); spread it over replicas.
+    int copies = o.reserved[4];
+    if (copies <= 0) {
+        const int64_t bytes = plane * 4;
+        copies = bytes >= (4 << 20) ? 1 : static_cast<int>(std::min<int64_t>(32, (4 << 20) / std::max<int64_t>(bytes, 1)));
+        if (p.nnz < 100000) copies = 1;  // latency-bound sizes: not worth the extra pass
+    }
+    if (copies > 64) return cudaErrorInvalidValue;
+    if (o.no_zero && copies > 1) copies = 1;  // accumulate-into-C mode reduces in place
+    float *Cdst = C;
+    float *scratch = nullptr;
+    if (copies > 1) {
+        e = cudaMallocAsync(&scratch, static_cast<size_t>(copies) * plane * 4, s);  // stream-ordered pool
+        if (e != cudaSuccess) return e;
+        e = cudaMemsetAsync(scratch, 0, static_cast<size_t>(copies) * plane * 4, s);
+        if (e != cudaSuccess) return e;
+        Cdst = scratch;
+    } else if (!o.no_zero) {
+        e = cudaMemsetAsync(C, 0, static_cast<size_t>(plane) * sizeof(float), s);
         if (e != cudaSuccess) return e;
     }
-    if (p.nnz == 0) return cudaSuccess;
+    if (p.nnz == 0) {
+        if (scratch) {
+            cudaFreeAsync(scratch, s);
+            return cudaMemsetAsync(C, 0, static_cast<size_t>(plane) * sizeof(float), s);
+        }
+        return cudaSuccess;
+    }
 
     const bool aligned = (reinterpret_cast<uintptr_t>(B) % 16 == 0) && (reinterpret_cast<uintptr_t>(C) % 16 == 0);
+    auto release = [&](cudaError_t err) {
+        if (scratch) cudaFreeAsync(scratch, s);
+        return err;
+    };
     const int vw = (R % 4 == 0 && aligned && !o.force_scalar) ? 4 : 1;
     const int vecs = (R + vw - 1) / vw;              // vectors per B row
     const int tile_vecs = std::min(32, pow2ceil(vecs));
@@ -65,31 +116,35 @@ cudaError_t launch_mttkrp(Plan &p, const float *B, int R, float *C, const systec
     const int tiles = (R + tile_vecs * vw - 1) / (tile_vecs * vw);
     int K = o.reserved[0] > 0 ? o.reserved[0] : default_K(E);
     const int stages = o.reserved[1] > 0 ? o.reserved[1] : 2;
-    if ((E * K) % 4 != 0 || stages > 8) return cudaErrorInvalidValue;
+    if ((E * K) % 4 != 0 || stages > 8) return release(cudaErrorInvalidValue);
 
     bool pos1 = false;
     if (o.pos1_accumulate > 0) pos1 = true;
     else if (o.pos1_accumulate == 0 && p.stats.pos1_runs > 0)
         pos1 = (static_cast<double>(p.nnz) / static_cast<double>(p.stats.pos1_runs)) >= 1.5;
 
-    KernelFn fn = pick(p.order, vw, lpe, vpl, pos1);
-    if (!fn) return cudaErrorInvalidValue;
+    // software-prefetch the next entry's B rows: pays when gathers miss L2
+    // (B footprint well beyond what stays resident: c3 -12 %), neutral or
+    // slightly negative when B is L2-resident (c2 +1 %, more registers)
+    const bool pf = o.reserved[3] > 0 || (o.reserved[3] == 0 && plane * 4 > (32ll << 20));
+    KernelFn fn = pick(p.order, vw, lpe, vpl, pos1, pf);
+    if (!fn) return release(cudaErrorInvalidValue);
     int wpb = o.warps_per_block > 0 ? o.warps_per_block : 8;
     auto smem_for = [&](int w) {
         return static_cast<size_t>(w) * stages * (p.order + 1) * (E * K) * 4 + static_cast<size_t>(w) * stages * 8;
     };
     const size_t smem_cap = 200 * 1024;
     while (wpb > 1 && smem_for(wpb) > smem_cap) wpb >>= 1;  // keep the staging ring within shared memory
-    if (smem_for(wpb) > smem_cap) return cudaErrorInvalidValue;
+    if (smem_for(wpb) > smem_cap) return release(cudaErrorInvalidValue);
     const int threads = wpb * 32;
     const size_t smem = smem_for(wpb);
     e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    if (e != cudaSuccess) return e;
+    if (e != cudaSuccess) return release(e);
     int dev = 0, sms = 148, occ = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, smem);
-    if (e != cudaSuccess) return e;
+    if (e != cudaSuccess) return release(e);
     if (occ < 1) occ = 1;
     if (o.blocks_per_sm > 0) occ = std::min(occ, static_cast<int>(o.blocks_per_sm));
     const int64_t total_warps = static_cast<int64_t>(sms) * occ * wpb;
@@ -102,7 +157,9 @@ cudaError_t launch_mttkrp(Plan &p, const float *B, int R, float *C, const systec
     kp.coords = p.coords;
     kp.vals = p.vals;
     kp.B = B;
-    kp.C = C;
+    kp.C = Cdst;
+    kp.copies = copies;
+    kp.plane = plane;
     kp.ld = p.ld;
     kp.nnz = p.nnz;
     kp.span = span;
@@ -112,12 +169,21 @@ cudaError_t launch_mttkrp(Plan &p, const float *B, int R, float *C, const systec
     kp.hints = o.l2_hints >= 0 ? 1 : 0;
     dim3 grid(static_cast<unsigned>(blocks), static_cast<unsigned>(tiles));
     fn<<<grid, threads, smem, s>>>(kp);
+    if (copies > 1) {
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return release(e);
+        const int64_t work = std::max<int64_t>(1, plane / 4);
+        const int rb = static_cast<int>(std::min<int64_t>((work + 255) / 256, static_cast<int64_t>(sms) * 4));
+        const int vec = (reinterpret_cast<uintptr_t>(C) % 16 == 0) && (plane % 4 == 0);
+        reduce_copies_kernel<<<rb, 256, 0, s>>>(scratch, C, plane, copies, vec);
+        cudaFreeAsync(scratch, s);
+    }
     p.last_grid_x = static_cast<int>(blocks);
     p.last_grid_y = tiles;
     p.last_block = threads;
     p.last_smem = static_cast<int>(smem);
-    // kernel id, decimal fields: order | vw | lpe (2 digits) | vpl | pos1
-    p.last_kernel = p.order * 100000 + vw * 10000 + lpe * 100 + vpl * 10 + (pos1 ? 1 : 0);
+    // kernel id, decimal fields: copies (2 digits) | pf | order | vw | lpe (2 digits) | vpl | pos1
+    p.last_kernel = copies * 10000000 + (pf ? 1000000 : 0) + p.order * 100000 + vw * 10000 + lpe * 100 + vpl * 10 + (pos1 ? 1 : 0);
     return cudaGetLastError();
 }
 

@@ -57,6 +57,8 @@ struct KParams {
     int K;                  // entries per lane group per chunk
     int stages;             // shared-memory ring depth
     int hints;              // 1: evict-last policy on B gathers, 0: evict-normal
+    int copies;             // replicas of C the warps spread their reductions over (>= 1)
+    int64_t plane;          // dim * R (floats per replica)
 };
 
 using KernelFn = void (*)(KParams);
@@ -102,7 +104,7 @@ __device__ __forceinline__ uint64_t row_off(int32_t c, uint32_t R) {
     return static_cast<uint64_t>(static_cast<uint32_t>(c)) * R;
 }
 
-template <int N, int LPE, int VPL, int VW, bool POS1>
+template <int N, int LPE, int VPL, int VW, bool POS1, bool PF>
 __global__ void __launch_bounds__(256) mttkrp_sym_kernel(const KParams p) {
     using V = VecT<VW>;
     using T = typename V::T;
@@ -133,7 +135,9 @@ __global__ void __launch_bounds__(256) mttkrp_sym_kernel(const KParams p) {
 #pragma unroll
     for (int q = 0; q < VPL; ++q) act[q] = col0 + q * QS < R;
     const float *Bc = p.B + col0;
-    float *Cc = p.C + col0;
+    // small outputs are spread over `copies` replicas (L2-slice spreading):
+    // warp gw accumulates into replica gw % copies, summed afterwards
+    float *Cc = p.C + static_cast<size_t>(gw % p.copies) * p.plane + col0;
     const uint64_t pol_keep = p.hints ? policy_evict_last() : policy_evict_normal();
     const uint64_t pol_stream = policy_evict_first();
     const float *coef = kCoef.v[N - 2][0];
@@ -183,51 +187,53 @@ __global__ void __launch_bounds__(256) mttkrp_sym_kernel(const KParams p) {
         const int lo = g * K;
         const int hi = min(lo + K, cnt);
 
-        for (int i = lo; i < hi; ++i) {
+        // one entry's operands: indices, value, and its gathered B rows
+        struct Slot {
             int32_t c[N];
+            float v;
+            T b[N][VPL];
+        };
+        auto fetch = [&](int i, Slot &x) {
 #pragma unroll
-            for (int t = 0; t < N; ++t) c[t] = sc[t * CH + i];
-            const float v = sv[i];
+            for (int t = 0; t < N; ++t) x.c[t] = sc[t * CH + i];
+            x.v = sv[i];
+#pragma unroll
+            for (int t = 0; t < N; ++t) {
+                const uint64_t o = row_off(x.c[t], R);
+#pragma unroll
+                for (int q = 0; q < VPL; ++q) x.b[t][q] = act[q] ? V::load(Bc + o + q * QS, pol_keep) : V::zero();
+            }
+        };
+        auto consume = [&](const Slot &x) {
             int code = 0;
 #pragma unroll
-            for (int t = 0; t + 1 < N; ++t) code |= (c[t] == c[t + 1]) << t;
+            for (int t = 0; t + 1 < N; ++t) code |= (x.c[t] == x.c[t + 1]) << t;
             const float *cf = coef + code * kMaxOrder;
-
-            uint64_t off[N];
-#pragma unroll
-            for (int t = 0; t < N; ++t) off[t] = row_off(c[t], R);
-            T b[N][VPL];
-#pragma unroll
-            for (int t = 0; t < N; ++t)
-#pragma unroll
-                for (int q = 0; q < VPL; ++q) b[t][q] = act[q] ? V::load(Bc + off[t] + q * QS, pol_keep) : V::zero();
-
             // prefix / suffix products: u_t = (coef_t v) prod_{s<t} b_s prod_{s>t} b_s
             T u[N][VPL];
 #pragma unroll
             for (int q = 0; q < VPL; ++q) {
                 T pre[N];
-                pre[1 % N] = b[0][q];
+                pre[1 % N] = x.b[0][q];
 #pragma unroll
-                for (int t = 2; t < N; ++t) pre[t] = V::mul(pre[t - 1], b[t - 1][q]);
-                T suf = b[N - 1][q];
+                for (int t = 2; t < N; ++t) pre[t] = V::mul(pre[t - 1], x.b[t - 1][q]);
+                T suf = x.b[N - 1][q];
 #pragma unroll
                 for (int t = N - 1; t >= 0; --t) {
                     const T prod = (t == N - 1) ? pre[t] : (t == 0 ? suf : V::mul(pre[t], suf));
-                    u[t][q] = V::scale(cf[t] * v, prod);
-                    if (t > 0 && t < N - 1) suf = V::mul(suf, b[t][q]);
+                    u[t][q] = V::scale(cf[t] * x.v, prod);
+                    if (t > 0 && t < N - 1) suf = V::mul(suf, x.b[t][q]);
                 }
             }
-
             // position 0: register run accumulation
-            if (c[0] != cur0) {
+            if (x.c[0] != cur0) {
                 if (cur0 >= 0) {
                     const uint64_t o = row_off(cur0, R);
 #pragma unroll
                     for (int q = 0; q < VPL; ++q)
                         if (act[q]) V::red(Cc + o + q * QS, acc0[q]);
                 }
-                cur0 = c[0];
+                cur0 = x.c[0];
 #pragma unroll
                 for (int q = 0; q < VPL; ++q) acc0[q] = V::zero();
             }
@@ -235,14 +241,14 @@ __global__ void __launch_bounds__(256) mttkrp_sym_kernel(const KParams p) {
             for (int q = 0; q < VPL; ++q) acc0[q] = V::add(acc0[q], u[0][q]);
             // position 1
             if (POS1) {
-                if (c[1] != cur1) {
+                if (x.c[1] != cur1) {
                     if (has1) {
                         const uint64_t o = row_off(cur1, R);
 #pragma unroll
                         for (int q = 0; q < VPL; ++q)
                             if (act[q]) V::red(Cc + o + q * QS, acc1[q]);
                     }
-                    cur1 = c[1];
+                    cur1 = x.c[1];
                     has1 = false;
 #pragma unroll
                     for (int q = 0; q < VPL; ++q) acc1[q] = V::zero();
@@ -256,10 +262,32 @@ __global__ void __launch_bounds__(256) mttkrp_sym_kernel(const KParams p) {
 #pragma unroll
             for (int t = POS1 ? 2 : 1; t < N; ++t)
                 if (cf[t] != 0.f) {
+                    const uint64_t o = row_off(x.c[t], R);
 #pragma unroll
                     for (int q = 0; q < VPL; ++q)
-                        if (act[q]) V::red(Cc + off[t] + q * QS, u[t][q]);
+                        if (act[q]) V::red(Cc + o + q * QS, u[t][q]);
                 }
+        };
+
+        if (PF) {
+            // software pipeline: the next entry's gathers are in flight while
+            // this one is consumed (ping-pong slots, no register copies)
+            Slot xa, xb;
+            int i = lo;
+            if (i < hi) fetch(i, xa);
+            for (; i + 1 < hi; i += 2) {
+                fetch(i + 1, xb);
+                consume(xa);
+                if (i + 2 < hi) fetch(i + 2, xa);
+                consume(xb);
+            }
+            if (i < hi) consume(xa);
+        } else {
+            for (int i = lo; i < hi; ++i) {
+                Slot x;
+                fetch(i, x);
+                consume(x);
+            }
         }
         __syncwarp();
 
@@ -316,11 +344,15 @@ __global__ void __launch_bounds__(256) mttkrp_sym_kernel(const KParams p) {
     }
 }
 
+// Sum `copies` replicas Cp[copies][plane] into C[plane] (float4 when aligned).
+__global__ void reduce_copies_kernel(const float *__restrict__ Cp, float *__restrict__ C, int64_t plane, int copies,
+                                     int vec);
+
 // instantiation tables, one translation unit per order (mttkrp_n{2..5}.cu)
-template <int N> KernelFn pick_kernel(int vw, int lpe, int vpl, bool pos1);
-template <> KernelFn pick_kernel<2>(int vw, int lpe, int vpl, bool pos1);
-template <> KernelFn pick_kernel<3>(int vw, int lpe, int vpl, bool pos1);
-template <> KernelFn pick_kernel<4>(int vw, int lpe, int vpl, bool pos1);
-template <> KernelFn pick_kernel<5>(int vw, int lpe, int vpl, bool pos1);
+template <int N> KernelFn pick_kernel(int vw, int lpe, int vpl, bool pos1, bool pf);
+template <> KernelFn pick_kernel<2>(int vw, int lpe, int vpl, bool pos1, bool pf);
+template <> KernelFn pick_kernel<3>(int vw, int lpe, int vpl, bool pos1, bool pf);
+template <> KernelFn pick_kernel<4>(int vw, int lpe, int vpl, bool pos1, bool pf);
+template <> KernelFn pick_kernel<5>(int vw, int lpe, int vpl, bool pos1, bool pf);
 
 }  // namespace systec

@@ -5,40 +5,41 @@
 namespace systec {
 
 template <int LPE, int VPL, int VW>
-static KernelFn pos1_of(bool pos1) {
-    return pos1 ? mttkrp_sym_kernel<4, LPE, VPL, VW, true> : mttkrp_sym_kernel<4, LPE, VPL, VW, false>;
+static KernelFn pos1_of(bool pos1, bool pf) {
+    if (pf) return pos1 ? mttkrp_sym_kernel<4, LPE, VPL, VW, true, true> : mttkrp_sym_kernel<4, LPE, VPL, VW, false, true>;
+    return pos1 ? mttkrp_sym_kernel<4, LPE, VPL, VW, true, false> : mttkrp_sym_kernel<4, LPE, VPL, VW, false, false>;
 }
 
 template <>
-KernelFn pick_kernel<4>(int vw, int lpe, int vpl, bool pos1) {
+KernelFn pick_kernel<4>(int vw, int lpe, int vpl, bool pos1, bool pf) {
     if (vw == 1) {
         if (vpl != 1) return nullptr;
         switch (lpe) {
-            case 1: return pos1_of<1, 1, 1>(pos1);
-            case 2: return pos1_of<2, 1, 1>(pos1);
-            case 4: return pos1_of<4, 1, 1>(pos1);
-            case 8: return pos1_of<8, 1, 1>(pos1);
-            case 16: return pos1_of<16, 1, 1>(pos1);
-            case 32: return pos1_of<32, 1, 1>(pos1);
+            case 1: return pos1_of<1, 1, 1>(pos1, pf);
+            case 2: return pos1_of<2, 1, 1>(pos1, pf);
+            case 4: return pos1_of<4, 1, 1>(pos1, pf);
+            case 8: return pos1_of<8, 1, 1>(pos1, pf);
+            case 16: return pos1_of<16, 1, 1>(pos1, pf);
+            case 32: return pos1_of<32, 1, 1>(pos1, pf);
             default: return nullptr;
         }
     }
     switch (lpe * 8 + vpl) {  // (lanes per entry, float4 per lane)
-        case 1 * 8 + 1: return pos1_of<1, 1, 4>(pos1);
-        case 1 * 8 + 2: return pos1_of<1, 2, 4>(pos1);
-        case 1 * 8 + 4: return pos1_of<1, 4, 4>(pos1);
-        case 2 * 8 + 1: return pos1_of<2, 1, 4>(pos1);
-        case 2 * 8 + 2: return pos1_of<2, 2, 4>(pos1);
-        case 2 * 8 + 4: return pos1_of<2, 4, 4>(pos1);
-        case 4 * 8 + 1: return pos1_of<4, 1, 4>(pos1);
-        case 4 * 8 + 2: return pos1_of<4, 2, 4>(pos1);
-        case 4 * 8 + 4: return pos1_of<4, 4, 4>(pos1);
-        case 8 * 8 + 1: return pos1_of<8, 1, 4>(pos1);
-        case 8 * 8 + 2: return pos1_of<8, 2, 4>(pos1);
-        case 8 * 8 + 4: return pos1_of<8, 4, 4>(pos1);
-        case 16 * 8 + 1: return pos1_of<16, 1, 4>(pos1);
-        case 16 * 8 + 2: return pos1_of<16, 2, 4>(pos1);
-        case 32 * 8 + 1: return pos1_of<32, 1, 4>(pos1);
+        case 1 * 8 + 1: return pos1_of<1, 1, 4>(pos1, pf);
+        case 1 * 8 + 2: return pos1_of<1, 2, 4>(pos1, pf);
+        case 1 * 8 + 4: return pos1_of<1, 4, 4>(pos1, pf);
+        case 2 * 8 + 1: return pos1_of<2, 1, 4>(pos1, pf);
+        case 2 * 8 + 2: return pos1_of<2, 2, 4>(pos1, pf);
+        case 2 * 8 + 4: return pos1_of<2, 4, 4>(pos1, pf);
+        case 4 * 8 + 1: return pos1_of<4, 1, 4>(pos1, pf);
+        case 4 * 8 + 2: return pos1_of<4, 2, 4>(pos1, pf);
+        case 4 * 8 + 4: return pos1_of<4, 4, 4>(pos1, pf);
+        case 8 * 8 + 1: return pos1_of<8, 1, 4>(pos1, pf);
+        case 8 * 8 + 2: return pos1_of<8, 2, 4>(pos1, pf);
+        case 8 * 8 + 4: return pos1_of<8, 4, 4>(pos1, pf);
+        case 16 * 8 + 1: return pos1_of<16, 1, 4>(pos1, pf);
+        case 16 * 8 + 2: return pos1_of<16, 2, 4>(pos1, pf);
+        case 32 * 8 + 1: return pos1_of<32, 1, 4>(pos1, pf);
         default: return nullptr;
     }
 }

@@ -119,6 +119,10 @@ def _opts(**kw) -> SystecExecOpts:
             o.reserved[1] = int(v)
         elif k == "vpl":
             o.reserved[2] = int(v)
+        elif k == "prefetch":
+            o.reserved[3] = int(v)
+        elif k == "copies":
+            o.reserved[4] = int(v)
         else:
             setattr(o, k, int(v))
     return o
@@ -185,9 +189,9 @@ class Plan:
         _check(load().systec_plan_last_launch(self._h, *[ctypes.byref(v) for v in vals]), "systec_plan_last_launch")
         d = dict(zip(["grid_x", "grid_y", "block", "smem_bytes", "kernel_id"], [v.value for v in vals]))
         kid = d["kernel_id"]
-        if kid >= 0:   # decimal fields: order | vw | lpe (2 digits) | vpl | pos1
-            d.update(order=kid // 100000, vw=kid // 10000 % 10, lpe=kid // 100 % 100, vpl=kid // 10 % 10,
-                     pos1=kid % 10)
+        if kid >= 0:   # decimal fields: copies (2) | pf | order | vw | lpe (2 digits) | vpl | pos1
+            d.update(copies=kid // 10000000, prefetch=kid // 1000000 % 10, order=kid // 100000 % 10,
+                     vw=kid // 10000 % 10, lpe=kid // 100 % 100, vpl=kid // 10 % 10, pos1=kid % 10)
         return d
 
     def destroy(self):

@@ -53,6 +53,8 @@ def test_rank_sweep(systec, R):
     Cref, S = oracle.mttkrp(3, 120, w.idx, w.vals, w.B)
     parity(run(systec, w), Cref, S)
     parity(run(systec, w, force_scalar=1), Cref, S)
+    parity(run(systec, w, copies=3), Cref, S)
+    parity(run(systec, w, copies=4, force_scalar=1), Cref, S)
     if R % 4 == 0 and R >= 8:
         parity(run(systec, w, vpl=2), Cref, S)
     if R % 4 == 0 and R >= 16:
@@ -72,6 +74,9 @@ def test_integer_valued_bit_exact(systec, n):
     assert np.array_equal(Cg2.astype(np.float64), Cref)
     for vpl in (2, 4):
         assert np.array_equal(run(systec, w, vpl=vpl).astype(np.float64), Cref)
+        assert np.array_equal(run(systec, w, vpl=vpl, prefetch=1).astype(np.float64), Cref)
+    assert np.array_equal(run(systec, w, prefetch=1, K=3).astype(np.float64), Cref)
+    assert np.array_equal(run(systec, w, copies=5).astype(np.float64), Cref)
 
 
 def test_unsorted_noncanonical_input(systec):
@@ -95,7 +100,9 @@ def test_option_variants_agree(systec):
     for opts in [dict(), dict(pos1_accumulate=1), dict(pos1_accumulate=-1), dict(l2_hints=-1),
                  dict(warps_per_block=4), dict(warps_per_block=1, blocks_per_sm=1), dict(K=1), dict(K=7),
                  dict(K=64, stages=4), dict(stages=3), dict(vpl=2), dict(vpl=4), dict(vpl=2, K=3),
-                 dict(vpl=4, pos1_accumulate=1)]:
+                 dict(vpl=4, pos1_accumulate=1), dict(prefetch=1), dict(prefetch=1, pos1_accumulate=1, K=4),
+                 dict(prefetch=1, vpl=2, K=3), dict(prefetch=1, K=2), dict(copies=1), dict(copies=7),
+                 dict(copies=32, prefetch=1), dict(copies=3, force_scalar=1)]:
         parity(run(systec, w, **opts), Cref, S)
 
 
@@ -106,6 +113,7 @@ def test_hub_rows_long_runs(systec):
     Cref, S = oracle.mttkrp(3, w.dim, w.idx, w.vals, w.B)
     parity(run(systec, w), Cref, S)
     parity(run(systec, w, pos1_accumulate=1), Cref, S)
+    parity(run(systec, w, prefetch=1), Cref, S)
 
 
 def test_empty_and_degenerate(systec):
