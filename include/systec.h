@@ -132,6 +132,33 @@ SYSTEC_API int systec_plan_create(systec_plan *out, int order, int64_t dim, int6
                        const int32_t *idx, const float *vals, systec_stream_t stream);
 
 /*
+ * The non-symmetric baseline (the paper's "naive"
+ * kernels): a plan over a GENERAL sparse tensor —
+ * tuples are validated and sorted lexicographically but NOT canonicalised —
+ * whose execute computes C[i,r] = sum_{e: idx_e[0] = i} v_e prod_{t>=1} B[idx_e[t], r]
+ * (one update per stored entry, leading-index runs accumulated in registers).
+ * Fed with systec_expand_symmetric's output it computes the same C as the
+ * symmetric plan, doing the work the symmetric method avoids.  Same
+ * arguments, errors and ownership as systec_plan_create.
+ */
+SYSTEC_API int systec_plan_create_general(systec_plan *out, int order, int64_t dim, int64_t nnz,
+                                          const int32_t *idx, const float *vals, systec_stream_t stream);
+
+/*
+ * Expand a symmetric tensor's stored entries (device idx [nnz][order], vals
+ * [nnz]; any tuple order) into every distinct permutation of each tuple — the
+ * non-symmetric tensor it stands for (Def. Symmetry, PAPER.md:141-147;
+ * n!/prod m! members per entry).  *count receives the total.
+ * out_idx == out_vals == NULL: count only.  Otherwise out_idx [capacity][order]
+ * and out_vals [capacity] (device) receive the entries, grouped by input
+ * entry, each group in lexicographic order; capacity < *count -> ERR_ARG.
+ * Synchronises `stream` once.  Errors: ARG, UNSUPPORTED, INDEX, NOMEM, CUDA.
+ */
+SYSTEC_API int systec_expand_symmetric(int order, int64_t dim, int64_t nnz, const int32_t *idx,
+                                       const float *vals, int64_t capacity, int32_t *out_idx,
+                                       float *out_vals, int64_t *count, systec_stream_t stream);
+
+/*
  * Execute: C[dim][R] = MTTKRP(plan, B).  Zeroes C and launches the kernel on
  * `stream`; never synchronises (CUDA-graph capturable).  Its only allocation
  * is stream-ordered scratch from the device's default pool (cudaMallocAsync)

@@ -11,6 +11,8 @@ no code with the CUDA path (``paper_2406_09266_b200``) and never imports it.
   (north_star; PAPER.md:859-865 for the MTTKRP definition
   for "as many assignments as unique permutations").  Also returns S, the sum
   of absolute terms used to normalise the parity error.
+* :func:`mttkrp_general` — the naive kernel on a general (non-symmetric) COO
+  tensor, for the non-symmetric GPU baseline.
 * :mod:`oracle.symmetric_ref` — the per-position multiplicity-coefficient
   formula, written independently in fp64 numpy (pin P4 of SURVEY.md §8(c)).
 
@@ -51,6 +53,8 @@ def _load():
         lib.oracle_mttkrp.restype = i32
         lib.oracle_mttkrp_rows.argtypes = [i32, i64, i64, vp, vp, vp, i32, i64, vp, vp, vp, i32]
         lib.oracle_mttkrp_rows.restype = i32
+        lib.oracle_mttkrp_general.argtypes = [i32, i64, i64, vp, vp, vp, i32, vp, vp]
+        lib.oracle_mttkrp_general.restype = i32
         lib.oracle_count_expanded.argtypes = [i32, i64, vp]
         lib.oracle_count_expanded.restype = i64
         _lib = lib
@@ -112,6 +116,22 @@ def mttkrp_rows(order: int, dim: int, idx, vals, B, rows, threads: int | None = 
         raise IndexError("index outside [0, dim)")
     if rc != 0:
         raise RuntimeError(f"oracle_mttkrp_rows failed with status {rc}")
+    return C, S
+
+
+def mttkrp_general(order: int, dim: int, idx, vals, B):
+    """Naive non-symmetric MTTKRP on a general COO tensor (tuples as given):
+    C[idx_e[0], r] += v_e prod_{t>=1} B[idx_e[t], r].  Returns (C, S) fp64."""
+    idx, vals, B = _prep(order, idx, vals, B)
+    R = B.shape[1]
+    C = np.empty((dim, R), np.float64)
+    S = np.empty((dim, R), np.float64)
+    rc = _load().oracle_mttkrp_general(order, dim, idx.shape[0], _ptr(idx), _ptr(vals), _ptr(B), R,
+                                       _ptr(C), _ptr(S))
+    if rc == 3:
+        raise IndexError("index outside [0, dim)")
+    if rc != 0:
+        raise RuntimeError(f"oracle_mttkrp_general failed with status {rc}")
     return C, S
 
 

@@ -244,3 +244,29 @@ int64_t oracle_count_expanded(int order, int64_t nnz, const int32_t *idx) {
     }
     return count;
 }
+
+/*
+ * General (non-symmetric) sparse MTTKRP, the naive kernel the paper compares
+ * against (MTTKRP definitions):
+ *   C[idx_e[0], r] += v_e * prod_{t>=1} B[idx_e[t], r],   S likewise with |.|.
+ * Tuples are used exactly as given (no canonicalisation, no expansion).
+ * Single-threaded: used on small inputs by the NEXT-1 parity tests.
+ */
+int oracle_mttkrp_general(int order, int64_t dim, int64_t nnz, const int32_t *idx, const float *vals,
+                          const float *B, int R, double *C, double *S) {
+    int rc = check_args(order, dim, nnz, idx, vals, B, R);
+    if (rc) return rc;
+    if (!C || !S) return 1;
+    memset(C, 0, (size_t)dim * R * sizeof(double));
+    memset(S, 0, (size_t)dim * R * sizeof(double));
+    for (int64_t e = 0; e < nnz; e++) {
+        const int32_t *x = idx + e * order;
+        for (int r = 0; r < R; r++) {
+            double term = (double)vals[e];
+            for (int t = 1; t < order; t++) term *= (double)B[(int64_t)x[t] * R + r];
+            C[(int64_t)x[0] * R + r] += term;
+            S[(int64_t)x[0] * R + r] += fabs(term);
+        }
+    }
+    return 0;
+}

@@ -4,7 +4,8 @@ The computation lives in ``libsystec.so`` (hand-written sm_100a CUDA behind the
 C ABI of ``include/systec.h``); this package is the thin ctypes binding with
 the same names.  See DESIGN.md.
 """
-from .systec import (EXPORTS, LIB_PATH, Plan, SystecError, load, mttkrp, mttkrp_host,
-                     plan_create)
+from .systec import (EXPORTS, LIB_PATH, Plan, SystecError, expand_symmetric, load, mttkrp, mttkrp_host,
+                     plan_create, plan_create_general)
 
-__all__ = ["EXPORTS", "LIB_PATH", "Plan", "SystecError", "load", "mttkrp", "mttkrp_host", "plan_create"]
+__all__ = ["EXPORTS", "LIB_PATH", "Plan", "SystecError", "expand_symmetric", "load", "mttkrp", "mttkrp_host",
+           "plan_create", "plan_create_general"]

@@ -58,7 +58,7 @@ int check_shape(int order, int64_t dim, int64_t nnz, int *bits_out) {
 
 // Builds the plan.  `pooled` plans keep their storage in the stream-ordered pool.
 int plan_create_impl(Plan **out, int order, int64_t dim, int64_t nnz, const int32_t *idx, const float *vals,
-                     cudaStream_t s, bool pooled) {
+                     cudaStream_t s, bool pooled, bool general = false) {
     *out = nullptr;
     int bits = 0;
     int rc = check_shape(order, dim, nnz, &bits);
@@ -74,6 +74,7 @@ int plan_create_impl(Plan **out, int order, int64_t dim, int64_t nnz, const int3
     p->ld = ((nnz + 3) & ~int64_t(3)) + 4;
     p->key_bits = bits;
     p->pooled = pooled;
+    p->general = general;
     p->stream = s;
     const size_t bytes = static_cast<size_t>(order + 1) * p->ld * 4;
     cudaError_t e = pooled ? cudaMallocAsync(&p->storage, bytes, s) : cudaMalloc(&p->storage, bytes);
@@ -110,7 +111,8 @@ int plan_create_impl(Plan **out, int order, int64_t dim, int64_t nnz, const int3
     if ((e = cudaMemcpyAsync(dst, &hst, sizeof(hst), cudaMemcpyHostToDevice, s)) != cudaSuccess) return fail(e);
 
     // a1: validate + canonicalise + pack keys
-    if ((e = launch_canonicalize(order, dim, nnz, bits, idx, keys, perm, dst, s)) != cudaSuccess) return fail(e);
+    if ((e = launch_canonicalize(order, dim, nnz, bits, idx, keys, perm, dst, s, !general)) != cudaSuccess)
+        return fail(e);
     if ((e = cudaMemcpyAsync(&hst, dst, sizeof(hst), cudaMemcpyDeviceToHost, s)) != cudaSuccess) return fail(e);
     if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return fail(e);  // sync 1: validation verdict
     if (hst.err) {
@@ -195,6 +197,63 @@ int systec_plan_create(systec_plan *out, int order, int64_t dim, int64_t nnz, co
     int rc = systec::plan_create_impl(&p, order, dim, nnz, idx, vals, reinterpret_cast<cudaStream_t>(stream), false);
     *out = reinterpret_cast<systec_plan>(p);
     return rc;
+}
+
+int systec_plan_create_general(systec_plan *out, int order, int64_t dim, int64_t nnz, const int32_t *idx,
+                               const float *vals, systec_stream_t stream) {
+    if (!out) return SYSTEC_ERR_ARG;
+    Plan *p = nullptr;
+    int rc = systec::plan_create_impl(&p, order, dim, nnz, idx, vals, reinterpret_cast<cudaStream_t>(stream), false,
+                                      true);
+    *out = reinterpret_cast<systec_plan>(p);
+    return rc;
+}
+
+int systec_expand_symmetric(int order, int64_t dim, int64_t nnz, const int32_t *idx, const float *vals,
+                            int64_t capacity, int32_t *out_idx, float *out_vals, int64_t *count,
+                            systec_stream_t stream) {
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    int bits = 0;
+    int rc = systec::check_shape(order, dim, nnz, &bits);
+    if (rc) return rc;
+    if (!count || (nnz > 0 && (!idx || !vals))) return SYSTEC_ERR_ARG;
+    *count = 0;
+    if (nnz == 0) return SYSTEC_OK;
+    systec::DevStats *dst = nullptr;
+    unsigned long long *sizes = nullptr, *offsets = nullptr;
+    systec::DevStats hst;
+    std::memset(&hst, 0, sizeof(hst));
+    hst.bad_entry = ULLONG_MAX;
+    cudaError_t e = cudaSuccess;
+    auto done = [&](int status) {
+        if (dst) cudaFreeAsync(dst, s);
+        if (sizes) cudaFreeAsync(sizes, s);
+        if (offsets) cudaFreeAsync(offsets, s);
+        return status;
+    };
+    if ((e = cudaMallocAsync(&dst, sizeof(hst), s)) != cudaSuccess) return done(systec::cuda_fail(e));
+    if ((e = cudaMallocAsync(&sizes, nnz * 8, s)) != cudaSuccess) return done(systec::cuda_fail(e));
+    if ((e = cudaMallocAsync(&offsets, nnz * 8, s)) != cudaSuccess) return done(systec::cuda_fail(e));
+    if ((e = cudaMemcpyAsync(dst, &hst, sizeof(hst), cudaMemcpyHostToDevice, s)) != cudaSuccess)
+        return done(systec::cuda_fail(e));
+    if ((e = systec::expand_count(order, dim, nnz, idx, sizes, offsets, dst, s)) != cudaSuccess)
+        return done(systec::cuda_fail(e));
+    unsigned long long last[2] = {0, 0};
+    if ((e = cudaMemcpyAsync(&hst, dst, sizeof(hst), cudaMemcpyDeviceToHost, s)) != cudaSuccess ||
+        (e = cudaMemcpyAsync(&last[0], offsets + nnz - 1, 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess ||
+        (e = cudaMemcpyAsync(&last[1], sizes + nnz - 1, 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess ||
+        (e = cudaStreamSynchronize(s)) != cudaSuccess)
+        return done(systec::cuda_fail(e));
+    if (hst.err) {
+        systec::g_last_bad_entry = static_cast<int64_t>(hst.bad_entry);
+        return done(SYSTEC_ERR_INDEX);
+    }
+    *count = static_cast<int64_t>(last[0] + last[1]);
+    if (!out_idx && !out_vals) return done(SYSTEC_OK);  // count-only query
+    if (!out_idx || !out_vals || capacity < *count) return done(SYSTEC_ERR_ARG);
+    if ((e = systec::expand_write(order, nnz, idx, vals, offsets, out_idx, out_vals, s)) != cudaSuccess)
+        return done(systec::cuda_fail(e));
+    return done(SYSTEC_OK);
 }
 
 int systec_plan_execute(systec_plan plan, const float *B, int R, float *C, systec_stream_t stream) {

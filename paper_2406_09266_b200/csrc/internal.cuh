@@ -19,6 +19,7 @@ struct Plan {
     float *vals = nullptr;     // [ld] fp32
     void *storage = nullptr;   // one allocation holding coords + vals
     bool pooled = false;       // storage from the stream-ordered pool (freed async)
+    bool general = false;      // non-symmetric tensor: tuples kept as given, naive kernel
     cudaStream_t stream = nullptr;
     systec_stats stats{};
     // last launch (for reporting)
@@ -41,7 +42,7 @@ struct DevStats {
 // prepare.cu
 cudaError_t launch_canonicalize(int order, int64_t dim, int64_t nnz, int bits, const int32_t *idx,
                                 unsigned long long *keys, uint32_t *perm, DevStats *st,
-                                cudaStream_t s);
+                                cudaStream_t s, bool canonicalise = true);
 cudaError_t sort_keys(int64_t nnz, int end_bit, unsigned long long *keys_in, unsigned long long *keys_out,
                       uint32_t *perm_in, uint32_t *perm_out, cudaStream_t s, bool pooled);
 cudaError_t launch_gather(int order, int64_t nnz, int64_t ld, int bits, const unsigned long long *keys,
@@ -49,6 +50,12 @@ cudaError_t launch_gather(int order, int64_t nnz, int64_t ld, int bits, const un
                           int32_t *coords, float *vals_out, cudaStream_t s);
 cudaError_t launch_stats(int order, int64_t nnz, int64_t ld, const int32_t *coords, DevStats *st,
                          cudaStream_t s);
+
+// expand.cu
+cudaError_t expand_count(int order, int64_t dim, int64_t nnz, const int32_t *idx, unsigned long long *sizes,
+                         unsigned long long *offsets, DevStats *st, cudaStream_t s);
+cudaError_t expand_write(int order, int64_t nnz, const int32_t *idx, const float *vals,
+                         const unsigned long long *offsets, int32_t *out_idx, float *out_vals, cudaStream_t s);
 
 // mttkrp.cu
 cudaError_t launch_mttkrp(Plan &p, const float *B, int R, float *C, const systec_exec_opts &o,

@@ -10,6 +10,16 @@ namespace systec {
 
 namespace {
 
+KernelFn pick_naive(int order, int vw, int lpe, bool pf) {
+    switch (order) {
+        case 2: return pick_naive_kernel<2>(vw, lpe, pf);
+        case 3: return pick_naive_kernel<3>(vw, lpe, pf);
+        case 4: return pick_naive_kernel<4>(vw, lpe, pf);
+        case 5: return pick_naive_kernel<5>(vw, lpe, pf);
+        default: return nullptr;
+    }
+}
+
 KernelFn pick(int order, int vw, int lpe, int vpl, bool pos1, bool pf) {
     switch (order) {
         case 2: return pick_kernel<2>(vw, lpe, vpl, pos1, pf);
@@ -106,7 +116,7 @@ cudaError_t launch_mttkrp(Plan &p, const float *B, int R, float *C, const systec
     const int vecs = (R + vw - 1) / vw;              // vectors per B row
     const int tile_vecs = std::min(32, pow2ceil(vecs));
     int vpl = 1;
-    if (vw == 4) {
+    if (vw == 4 && !p.general) {
         const int want = o.reserved[2] > 0 ? o.reserved[2] : 1;  // float4 per lane
         vpl = std::min(want, tile_vecs);
         if (vpl != 1 && vpl != 2 && vpl != 4) return cudaErrorInvalidValue;
@@ -119,7 +129,8 @@ cudaError_t launch_mttkrp(Plan &p, const float *B, int R, float *C, const systec
     if ((E * K) % 4 != 0 || stages > 8) return release(cudaErrorInvalidValue);
 
     bool pos1 = false;
-    if (o.pos1_accumulate > 0) pos1 = true;
+    if (p.general) pos1 = false;  // the general kernel updates position 0 only
+    else if (o.pos1_accumulate > 0) pos1 = true;
     else if (o.pos1_accumulate == 0 && p.stats.pos1_runs > 0)
         pos1 = (static_cast<double>(p.nnz) / static_cast<double>(p.stats.pos1_runs)) >= 1.5;
 
@@ -127,7 +138,7 @@ cudaError_t launch_mttkrp(Plan &p, const float *B, int R, float *C, const systec
     // (B footprint well beyond what stays resident: c3 -12 %), neutral or
     // slightly negative when B is L2-resident (c2 +1 %, more registers)
     const bool pf = o.reserved[3] > 0 || (o.reserved[3] == 0 && plane * 4 > (32ll << 20));
-    KernelFn fn = pick(p.order, vw, lpe, vpl, pos1, pf);
+    KernelFn fn = p.general ? pick_naive(p.order, vw, lpe, pf) : pick(p.order, vw, lpe, vpl, pos1, pf);
     if (!fn) return release(cudaErrorInvalidValue);
     int wpb = o.warps_per_block > 0 ? o.warps_per_block : 8;
     auto smem_for = [&](int w) {
@@ -182,8 +193,8 @@ cudaError_t launch_mttkrp(Plan &p, const float *B, int R, float *C, const systec
     p.last_grid_y = tiles;
     p.last_block = threads;
     p.last_smem = static_cast<int>(smem);
-    // kernel id, decimal fields: copies (2 digits) | pf | order | vw | lpe (2 digits) | vpl | pos1
-    p.last_kernel = copies * 10000000 + (pf ? 1000000 : 0) + p.order * 100000 + vw * 10000 + lpe * 100 + vpl * 10 + (pos1 ? 1 : 0);
+    // kernel id, decimal fields: general | copies (2 digits) | pf | order | vw | lpe (2 digits) | vpl | pos1
+    p.last_kernel = (p.general ? 1000000000 : 0) + copies * 10000000 + (pf ? 1000000 : 0) + p.order * 100000 + vw * 10000 + lpe * 100 + vpl * 10 + (pos1 ? 1 : 0);
     return cudaGetLastError();
 }
 

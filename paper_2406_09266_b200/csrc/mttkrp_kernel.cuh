@@ -104,7 +104,7 @@ __device__ __forceinline__ uint64_t row_off(int32_t c, uint32_t R) {
     return static_cast<uint64_t>(static_cast<uint32_t>(c)) * R;
 }
 
-template <int N, int LPE, int VPL, int VW, bool POS1, bool PF>
+template <int N, int LPE, int VPL, int VW, bool POS1, bool PF, bool NAIVE = false>
 __global__ void __launch_bounds__(256) mttkrp_sym_kernel(const KParams p) {
     using V = VecT<VW>;
     using T = typename V::T;
@@ -198,7 +198,7 @@ __global__ void __launch_bounds__(256) mttkrp_sym_kernel(const KParams p) {
             for (int t = 0; t < N; ++t) x.c[t] = sc[t * CH + i];
             x.v = sv[i];
 #pragma unroll
-            for (int t = 0; t < N; ++t) {
+            for (int t = NAIVE ? 1 : 0; t < N; ++t) {  // the naive kernel never reads B[c_0]
                 const uint64_t o = row_off(x.c[t], R);
 #pragma unroll
                 for (int q = 0; q < VPL; ++q) x.b[t][q] = act[q] ? V::load(Bc + o + q * QS, pol_keep) : V::zero();
@@ -213,6 +213,13 @@ __global__ void __launch_bounds__(256) mttkrp_sym_kernel(const KParams p) {
             T u[N][VPL];
 #pragma unroll
             for (int q = 0; q < VPL; ++q) {
+                if (NAIVE) {  // general (non-symmetric) entry: only C[c_0] += v prod_{t>=1} B[c_t]
+                    T prod = x.b[1 % N][q];
+#pragma unroll
+                    for (int t = 2; t < N; ++t) prod = V::mul(prod, x.b[t][q]);
+                    u[0][q] = V::scale(x.v, prod);
+                    continue;
+                }
                 T pre[N];
                 pre[1 % N] = x.b[0][q];
 #pragma unroll
@@ -239,6 +246,7 @@ __global__ void __launch_bounds__(256) mttkrp_sym_kernel(const KParams p) {
             }
 #pragma unroll
             for (int q = 0; q < VPL; ++q) acc0[q] = V::add(acc0[q], u[0][q]);
+            if (NAIVE) return;
             // position 1
             if (POS1) {
                 if (x.c[1] != cur1) {
@@ -354,5 +362,12 @@ template <> KernelFn pick_kernel<2>(int vw, int lpe, int vpl, bool pos1, bool pf
 template <> KernelFn pick_kernel<3>(int vw, int lpe, int vpl, bool pos1, bool pf);
 template <> KernelFn pick_kernel<4>(int vw, int lpe, int vpl, bool pos1, bool pf);
 template <> KernelFn pick_kernel<5>(int vw, int lpe, int vpl, bool pos1, bool pf);
+// the non-symmetric (expanded-tensor) baseline: position 0 only, one float4/float per lane
+template <int N> KernelFn pick_naive_kernel(int vw, int lpe, bool pf);
+template <> KernelFn pick_naive_kernel<2>(int vw, int lpe, bool pf);
+template <> KernelFn pick_naive_kernel<3>(int vw, int lpe, bool pf);
+template <> KernelFn pick_naive_kernel<4>(int vw, int lpe, bool pf);
+template <> KernelFn pick_naive_kernel<5>(int vw, int lpe, bool pf);
+
 
 }  // namespace systec

@@ -44,4 +44,33 @@ KernelFn pick_kernel<3>(int vw, int lpe, int vpl, bool pos1, bool pf) {
     }
 }
 
+template <int LPE, int VW>
+static KernelFn naive_of(bool pf) {
+    return pf ? mttkrp_sym_kernel<3, LPE, 1, VW, false, true, true> : mttkrp_sym_kernel<3, LPE, 1, VW, false, false, true>;
+}
+
+template <>
+KernelFn pick_naive_kernel<3>(int vw, int lpe, bool pf) {
+    if (vw == 4) {
+        switch (lpe) {
+            case 1: return naive_of<1, 4>(pf);
+            case 2: return naive_of<2, 4>(pf);
+            case 4: return naive_of<4, 4>(pf);
+            case 8: return naive_of<8, 4>(pf);
+            case 16: return naive_of<16, 4>(pf);
+            case 32: return naive_of<32, 4>(pf);
+            default: return nullptr;
+        }
+    }
+    switch (lpe) {
+        case 1: return naive_of<1, 1>(pf);
+        case 2: return naive_of<2, 1>(pf);
+        case 4: return naive_of<4, 1>(pf);
+        case 8: return naive_of<8, 1>(pf);
+        case 16: return naive_of<16, 1>(pf);
+        case 32: return naive_of<32, 1>(pf);
+        default: return nullptr;
+    }
+}
+
 }  // namespace systec

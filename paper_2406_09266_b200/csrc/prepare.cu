@@ -38,7 +38,7 @@ __device__ __forceinline__ unsigned long long pack_key(const int32_t (&c)[N], in
     return k;
 }
 
-template <int N>
+template <int N, bool CANON>
 __device__ __forceinline__ bool load_canonical(const int32_t *idx, int64_t e, int64_t dim, int32_t (&c)[N]) {
     bool ok = true;
 #pragma unroll
@@ -46,18 +46,18 @@ __device__ __forceinline__ bool load_canonical(const int32_t *idx, int64_t e, in
         c[t] = idx[e * N + t];
         ok &= (c[t] >= 0) & (static_cast<int64_t>(c[t]) < dim);
     }
-    sort_net<N>(c);
+    if (CANON) sort_net<N>(c);  // a general (non-symmetric) tensor keeps its tuples as given
     return ok;
 }
 
-template <int N>
+template <int N, bool CANON>
 __global__ void canonicalize_kernel(const int32_t *__restrict__ idx, int64_t nnz, int64_t dim, int bits,
                                     unsigned long long *__restrict__ keys, uint32_t *__restrict__ perm,
                                     DevStats *st) {
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz;
          e += (int64_t)gridDim.x * blockDim.x) {
         int32_t c[N];
-        const bool ok = load_canonical<N>(idx, e, dim, c);
+        const bool ok = load_canonical<N, CANON>(idx, e, dim, c);
         if (!ok) {
             atomicOr(&st->err, 1ull);
             atomicMin(&st->bad_entry, static_cast<unsigned long long>(e));
@@ -70,7 +70,7 @@ __global__ void canonicalize_kernel(const int32_t *__restrict__ idx, int64_t nnz
         perm[e] = static_cast<uint32_t>(e);
         if (e > 0) {
             int32_t q[N];
-            if (load_canonical<N>(idx, e - 1, dim, q) && pack_key<N>(q, bits) > k) st->unsorted = 1ull;
+            if (load_canonical<N, CANON>(idx, e - 1, dim, q) && pack_key<N>(q, bits) > k) st->unsorted = 1ull;
         }
     }
 }
@@ -199,10 +199,15 @@ int grid_for(int64_t n, int threads) {
     }
 
 cudaError_t launch_canonicalize(int order, int64_t dim, int64_t nnz, int bits, const int32_t *idx,
-                                unsigned long long *keys, uint32_t *perm, DevStats *st, cudaStream_t s) {
+                                unsigned long long *keys, uint32_t *perm, DevStats *st, cudaStream_t s,
+                                bool canonicalise) {
     if (nnz == 0) return cudaSuccess;
     const int th = 256;
-    SYSTEC_ORDER_SWITCH(order, canonicalize_kernel<N><<<grid_for(nnz, th), th, 0, s>>>(idx, nnz, dim, bits, keys, perm, st));
+    if (canonicalise) {
+        SYSTEC_ORDER_SWITCH(order, canonicalize_kernel<N, true><<<grid_for(nnz, th), th, 0, s>>>(idx, nnz, dim, bits, keys, perm, st));
+    } else {
+        SYSTEC_ORDER_SWITCH(order, canonicalize_kernel<N, false><<<grid_for(nnz, th), th, 0, s>>>(idx, nnz, dim, bits, keys, perm, st));
+    }
     return cudaGetLastError();
 }
 

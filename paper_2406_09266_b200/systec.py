@@ -37,7 +37,8 @@ class SystecExecOpts(ctypes.Structure):
 EXPORTS = ["systec_mttkrp", "systec_mttkrp_host", "systec_plan_create", "systec_plan_execute",
            "systec_plan_execute_ex", "systec_plan_stats", "systec_plan_prepared",
            "systec_plan_copy_prepared", "systec_plan_last_launch", "systec_plan_destroy",
-           "systec_status_string", "systec_last_cuda_error", "systec_version", "systec_last_bad_entry"]
+           "systec_status_string", "systec_last_cuda_error", "systec_version", "systec_last_bad_entry",
+           "systec_plan_create_general", "systec_expand_symmetric"]
 
 _lib = None
 
@@ -57,6 +58,8 @@ def load(path: str | None = None):
     lib.systec_mttkrp_host.argtypes = [i32, i64, i64, vp, vp, vp, i32, vp, vp]
     lib.systec_plan_create.argtypes = [ctypes.POINTER(vp), i32, i64, i64, vp, vp, vp]
     lib.systec_plan_execute.argtypes = [vp, vp, i32, vp, vp]
+    lib.systec_plan_create_general.argtypes = [ctypes.POINTER(vp), i32, i64, i64, vp, vp, vp]
+    lib.systec_expand_symmetric.argtypes = [i32, i64, i64, vp, vp, i64, vp, vp, ctypes.POINTER(i64), vp]
     lib.systec_plan_execute_ex.argtypes = [vp, vp, i32, vp, ctypes.POINTER(SystecExecOpts), vp]
     lib.systec_plan_stats.argtypes = [vp, ctypes.POINTER(SystecStats)]
     lib.systec_plan_prepared.argtypes = [vp, ctypes.POINTER(vp), ctypes.POINTER(vp)]
@@ -133,16 +136,18 @@ class Plan:
     ``systec_plan_create``.  ``idx`` [nnz][order] int32 and ``vals`` [nnz] fp32
     are CUDA tensors; they may be freed after construction."""
 
-    def __init__(self, order: int, dim: int, idx, vals, stream=None):
+    def __init__(self, order: int, dim: int, idx, vals, stream=None, general: bool = False):
         import torch
         lib = load()
         nnz = int(vals.shape[0])
         if idx.dim() != 2 or idx.shape[1] != order or idx.shape[0] != nnz:
             raise ValueError("idx must be [nnz][order]")
         h = ctypes.c_void_p()
-        _check(lib.systec_plan_create(ctypes.byref(h), order, dim, nnz, _dev(idx, torch.int32, "idx"),
-                                      _dev(vals, torch.float32, "vals"), _stream_handle(stream)),
-               "systec_plan_create")
+        fn, name = ((lib.systec_plan_create_general, "systec_plan_create_general") if general
+                    else (lib.systec_plan_create, "systec_plan_create"))
+        _check(fn(ctypes.byref(h), order, dim, nnz, _dev(idx, torch.int32, "idx"),
+                  _dev(vals, torch.float32, "vals"), _stream_handle(stream)), name)
+        self.general = general
         self._h = h
         self.order, self.dim, self.nnz = order, dim, nnz
 
@@ -189,8 +194,9 @@ class Plan:
         _check(load().systec_plan_last_launch(self._h, *[ctypes.byref(v) for v in vals]), "systec_plan_last_launch")
         d = dict(zip(["grid_x", "grid_y", "block", "smem_bytes", "kernel_id"], [v.value for v in vals]))
         kid = d["kernel_id"]
-        if kid >= 0:   # decimal fields: copies (2) | pf | order | vw | lpe (2 digits) | vpl | pos1
-            d.update(copies=kid // 10000000, prefetch=kid // 1000000 % 10, order=kid // 100000 % 10,
+        if kid >= 0:   # decimal fields: general | copies (2) | pf | order | vw | lpe (2 digits) | vpl | pos1
+            d.update(general=kid // 1000000000, copies=kid // 10000000 % 100, prefetch=kid // 1000000 % 10,
+                     order=kid // 100000 % 10,
                      vw=kid // 10000 % 10, lpe=kid // 100 % 100, vpl=kid // 10 % 10, pos1=kid % 10)
         return d
 
@@ -208,6 +214,31 @@ class Plan:
 
 def plan_create(order, dim, idx, vals, stream=None) -> Plan:
     return Plan(order, dim, idx, vals, stream)
+
+
+def plan_create_general(order, dim, idx, vals, stream=None) -> Plan:
+    """``systec_plan_create_general``: the non-symmetric baseline plan."""
+    return Plan(order, dim, idx, vals, stream, general=True)
+
+
+def expand_symmetric(order: int, dim: int, idx, vals, stream=None):
+    """``systec_expand_symmetric``: (idx_exp [m][order] int32, vals_exp [m] fp32) CUDA tensors."""
+    import torch
+    lib = load()
+    nnz = int(vals.shape[0])
+    cnt = ctypes.c_int64()
+    ip, vp_ = _dev(idx, torch.int32, "idx"), _dev(vals, torch.float32, "vals")
+    s = _stream_handle(stream)
+    _check(lib.systec_expand_symmetric(order, dim, nnz, ip, vp_, 0, None, None, ctypes.byref(cnt), s),
+           "systec_expand_symmetric")
+    m = cnt.value
+    out_i = torch.empty((m, order), dtype=torch.int32, device=idx.device)
+    out_v = torch.empty(m, dtype=torch.float32, device=idx.device)
+    if m:
+        _check(lib.systec_expand_symmetric(order, dim, nnz, ip, vp_, m, ctypes.c_void_p(out_i.data_ptr()),
+                                           ctypes.c_void_p(out_v.data_ptr()), ctypes.byref(cnt), s),
+               "systec_expand_symmetric")
+    return out_i, out_v
 
 
 def mttkrp(order: int, dim: int, idx, vals, B, C=None, stream=None):

@@ -1,5 +1,7 @@
 """Parity of the CUDA path (through the C ABI) with the CPU oracle.
 GPU tests: run with `pytest -m gpu` on a B200."""
+import itertools
+
 import numpy as np
 import pytest
 
@@ -229,3 +231,61 @@ def test_config_full_size_sampled(systec, name):
     inv = contraction_invariant(w, Cg)
     assert inv <= TOL, inv
     print(f"{name}: rows={len(rows)} max_rel_err={err:.3e} P7={inv:.3e}")
+
+
+# ---------------------------------------------------------------- NEXT-1: non-symmetric baseline
+def expand_py(idx, vals):
+    out = []
+    for c, v in zip(idx, vals):
+        for p in sorted(set(itertools.permutations(sorted(c.tolist())))):
+            out.append((p, float(v)))
+    return out
+
+
+@pytest.mark.parametrize("n,dim,nnz", [(3, 20, 500), (4, 12, 700), (5, 9, 600), (2, 30, 200)])
+def test_expand_symmetric_matches_itertools(systec, n, dim, nnz):
+    import torch
+    w = small_random(n, dim, nnz, 2, seed=n + 40, diag_frac=0.3)
+    si, sv = scramble(w.idx, w.vals, seed=3)
+    di, dv = to_dev(si, sv)
+    ei, ev = systec.expand_symmetric(n, dim, di, dv)
+    torch.cuda.synchronize()
+    got = sorted(zip(map(tuple, ei.cpu().numpy().tolist()), ev.cpu().numpy().tolist()))
+    want = sorted(expand_py(si, sv))
+    assert len(got) == oracle.count_expanded(n, w.idx)
+    assert got == want
+
+
+@pytest.mark.parametrize("n,dim,nnz,R", [(3, 50, 3000, 32), (4, 20, 2500, 16), (5, 11, 2000, 16), (3, 40, 999, 7)])
+def test_general_plan_vs_general_oracle(systec, n, dim, nnz, R):
+    import torch
+    rng = np.random.default_rng(n + nnz)
+    idx = rng.integers(0, dim, (nnz, n)).astype(np.int32)       # a general tensor: no symmetry
+    vals = rng.uniform(-1, 1, nnz).astype(np.float32)
+    B = rng.uniform(-1, 1, (dim, R)).astype(np.float32)
+    Cref, S = oracle.mttkrp_general(n, dim, idx, vals, B)
+    di, dv, dB = to_dev(idx, vals, B)
+    plan = systec.plan_create_general(n, dim, di, dv)
+    C = plan.execute(dB)
+    torch.cuda.synchronize()
+    parity(C.cpu().numpy(), Cref, S)
+    assert plan.last_launch()["general"] == 1
+    for opts in (dict(prefetch=1), dict(copies=4), dict(force_scalar=1)):
+        C = plan.execute(dB, **opts)
+        torch.cuda.synchronize()
+        parity(C.cpu().numpy(), Cref, S)
+
+
+@pytest.mark.parametrize("n,dim,nnz,R", [(3, 60, 4000, 32), (4, 20, 3000, 16), (5, 12, 2000, 16)])
+def test_general_plan_on_expansion_equals_symmetric(systec, n, dim, nnz, R):
+    """The paper's comparison, on the GPU: the naive kernel over the expanded
+    tensor and the symmetric kernel over the canonical one agree."""
+    import torch
+    w = small_random(n, dim, nnz, R, seed=n + 5, diag_frac=0.2)
+    Cref, S = oracle.mttkrp(n, dim, w.idx, w.vals, w.B)
+    di, dv, dB = to_dev(w.idx, w.vals, w.B)
+    ei, ev = systec.expand_symmetric(n, dim, di, dv)
+    plan = systec.plan_create_general(n, dim, ei, ev)
+    C = plan.execute(dB)
+    torch.cuda.synchronize()
+    parity(C.cpu().numpy(), Cref, S)

@@ -290,3 +290,31 @@ def test_oracle_errors():
         oracle.mttkrp(3, 4, np.array([[0, 1, 4]], np.int32), np.ones(1, np.float32), np.ones((4, 2), np.float32))
     C, S = oracle.mttkrp(3, 4, np.zeros((0, 3), np.int32), np.zeros(0, np.float32), np.ones((4, 2), np.float32))
     assert not C.any() and not S.any()
+
+
+# ---------------------------------------------------------------- general (non-symmetric) oracle
+@pytest.mark.parametrize("n,dim,nnz", [(3, 9, 200), (4, 6, 300), (5, 5, 400), (2, 12, 50)])
+def test_general_oracle_vs_dense_einsum(n, dim, nnz):
+    rng = np.random.default_rng(n * 7 + dim)
+    idx = rng.integers(0, dim, (nnz, n)).astype(np.int32)          # arbitrary tuples, repeats allowed
+    vals = rng.uniform(-1, 1, nnz).astype(np.float32)
+    B = rng.uniform(-1, 1, (dim, 3)).astype(np.float32)
+    A = np.zeros((dim,) * n)
+    np.add.at(A, tuple(idx.T), vals.astype(np.float64))
+    C, S = oracle.mttkrp_general(n, dim, idx, vals, B)
+    assert rel_err(C, dense_mttkrp(A, B), S) < 1e-12
+
+
+@pytest.mark.parametrize("n,dim,nnz", [(3, 10, 150), (4, 7, 200), (5, 6, 150)])
+def test_general_oracle_on_expanded_equals_symmetric(n, dim, nnz):
+    """The naive kernel over the expanded tensor (every distinct permutation
+    listed, via itertools) equals the symmetric oracle: the paper's premise."""
+    w = small_random(n, dim, nnz, 4, seed=n, diag_frac=0.3)
+    ex_i, ex_v = [], []
+    for c, v in zip(w.idx, w.vals):
+        for p in sorted(set(itertools.permutations(c.tolist()))):
+            ex_i.append(p)
+            ex_v.append(v)
+    C1, S1 = oracle.mttkrp(n, dim, w.idx, w.vals, w.B)
+    C2, _ = oracle.mttkrp_general(n, dim, np.array(ex_i, np.int32), np.array(ex_v, np.float32), w.B)
+    assert rel_err(C2, C1, S1) < 1e-13

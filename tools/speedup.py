@@ -1,0 +1,86 @@
+"""The paper's own experiment on the B200: the
+symmetric kernel over the canonical tensor vs the naive kernel over the
+expanded (non-symmetric) tensor, same output.  The paper expects 2x/6x/24x
+for 3/4/5-D and measured up to 3.38x/7.35x/29.8x on one Haswell core
+(PAPER.md:886).  Prints one JSON line per config.
+
+    python tools/speedup.py --configs c2,c3,c4,c5
+"""
+import argparse
+import json
+import math
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def time_exec(plan, B, C, reps, flush, **opts):
+    import numpy as np
+    import torch
+    for _ in range(3):
+        plan.execute(B, C, **opts)
+    ts = []
+    for _ in range(reps):
+        flush.fill_(1.0)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        plan.execute(B, C, **opts)
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    return float(np.median(ts))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--configs", default="c2,c3,c4,c5")
+    ap.add_argument("--reps", type=int, default=20)
+    a = ap.parse_args()
+    import torch
+
+    import paper_2406_09266_b200 as systec
+    from synth import generate
+    flush = torch.empty(64 << 20, device="cuda")
+    for name in a.configs.split(","):
+        w = generate(name)
+        di, dv = torch.from_numpy(w.idx).cuda(), torch.from_numpy(w.vals).cuda()
+        B = torch.from_numpy(w.B).cuda()
+        C1 = torch.empty((w.dim, w.R), device="cuda")
+        C2 = torch.empty((w.dim, w.R), device="cuda")
+        sym = systec.Plan(w.order, w.dim, di, dv)
+        t_sym = time_exec(sym, B, C1, a.reps, flush)
+        st = sym.stats()
+        sym.destroy()
+        ei, ev = systec.expand_symmetric(w.order, w.dim, di, dv)
+        del di, dv
+        torch.cuda.synchronize()
+        m = int(ev.shape[0])
+        gen = systec.plan_create_general(w.order, w.dim, ei, ev)
+        del ei, ev
+        torch.cuda.empty_cache()
+        t_naive = time_exec(gen, B, C2, a.reps, flush)
+        t_naive_pf = time_exec(gen, B, C2, a.reps, flush, prefetch=1)
+        gen.execute(B, C2)
+        sym = systec.Plan(w.order, w.dim, torch.from_numpy(w.idx).cuda(), torch.from_numpy(w.vals).cuda())
+        sym.execute(B, C1)
+        torch.cuda.synchronize()
+        rel = float(((C1 - C2).abs().max() / C1.abs().max()).item())
+        n = w.order
+        best_naive = min(t_naive, t_naive_pf)
+        print(json.dumps({
+            "config": name, "order": n, "nnz": w.nnz, "expanded_nnz": m, "G": st["G"],
+            "t_sym_ms": t_sym, "t_naive_ms": t_naive, "t_naive_prefetch_ms": t_naive_pf,
+            "speedup": best_naive / t_sym,
+            "expected_compute_ratio": math.factorial(n - 1), "expected_read_ratio": math.factorial(n),
+            "paper_max_speedup_cpu": {3: 3.38, 4: 7.35, 5: 29.8}.get(n),
+            "updates_ratio_measured": m / st["G"], "reads_ratio_measured": m / w.nnz,
+            "max_rel_diff_sym_vs_naive": rel}), flush=True)
+        sym.destroy()
+        gen.destroy()
+        torch.cuda.empty_cache()
+
+
+if __name__ == "__main__":
+    main()
