@@ -10,6 +10,8 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libsystec.so")
+# experiment builds only: extra nvcc flags (e.g. -DSYSTEC_L1_NOALLOC) into another file
+EXTRA = os.environ.get("SYSTEC_NVCC_EXTRA", "").split()
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 NVCC_FLAGS = [
@@ -34,13 +36,14 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, out: str | None = None) -> str:
+    lib = out or LIB
+    if out is None and not force and not _stale():
         return LIB
     objs, procs = [], []
     for src in sources():      # one nvcc per translation unit, in parallel
-        obj = os.path.join(CSRC, os.path.basename(src)[:-3] + ".o")
-        cmd = [NVCC, *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-c", src, "-o", obj]
+        obj = os.path.join(CSRC, os.path.basename(src)[:-3] + (".x.o" if out else ".o"))
+        cmd = [NVCC, *NVCC_FLAGS, *EXTRA, "-I", os.path.join(ROOT, "include"), "-c", src, "-o", obj]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
         procs.append((subprocess.Popen(cmd), cmd))
@@ -48,19 +51,22 @@ def build(force: bool = False, verbose: bool = False) -> str:
     for pr, cmd in procs:
         if pr.wait() != 0:
             raise subprocess.CalledProcessError(pr.returncode, cmd)
-    tmp = LIB + f".{os.getpid()}.tmp"
+    tmp = lib + f".{os.getpid()}.tmp"
     # exported symbols: only the extern "C" ABI (visibility default via the macro below)
     cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-cudart", "static",
            "-Xcompiler", "-fPIC", "-o", tmp, *objs]
     subprocess.check_call(cmd)
-    os.replace(tmp, LIB)
+    os.replace(tmp, lib)
     for o in objs:
         try:
             os.remove(o)
         except OSError:
             pass
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    outp = None
+    if "--out" in sys.argv:
+        outp = sys.argv[sys.argv.index("--out") + 1]
+    print(build(force="--force" in sys.argv, verbose=True, out=outp))

@@ -134,10 +134,11 @@ cudaError_t launch_mttkrp(Plan &p, const float *B, int R, float *C, const systec
     else if (o.pos1_accumulate == 0 && p.stats.pos1_runs > 0)
         pos1 = (static_cast<double>(p.nnz) / static_cast<double>(p.stats.pos1_runs)) >= 1.5;
 
-    // software-prefetch the next entry's B rows: pays when gathers miss L2
-    // (B footprint well beyond what stays resident: c3 -12 %), neutral or
-    // slightly negative when B is L2-resident (c2 +1 %, more registers)
-    const bool pf = o.reserved[3] > 0 || (o.reserved[3] == 0 && plane * 4 > (32ll << 20));
+    // software-prefetch the next entry's B rows: opt-in.  Measured (profiles/
+    // r01_sweep_v3.jsonl): c2 -1 %, c3 +12 %, c4/c5 +1 % time with the
+    // branch-free kernel — the extra registers cost more occupancy than the
+    // in-flight gathers gain.
+    const bool pf = o.reserved[3] > 0;
     KernelFn fn = p.general ? pick_naive(p.order, vw, lpe, pf) : pick(p.order, vw, lpe, vpl, pos1, pf);
     if (!fn) return release(cudaErrorInvalidValue);
     int wpb = o.warps_per_block > 0 ? o.warps_per_block : 8;

@@ -72,6 +72,7 @@ template <> struct VecT<4> {
     static __device__ __forceinline__ T add(T a, T b) { return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w); }
     static __device__ __forceinline__ T load(const float *p, uint64_t pol) { return ldg4_hint(p, pol); }
     static __device__ __forceinline__ void red(float *p, T v) { red_add4(p, v); }
+    static __device__ __forceinline__ void red_if(float *p, T v, bool pred) { red_add4_if(p, v, pred); }
     static __device__ __forceinline__ T shfl_down(T v, int d) {
         return make_float4(__shfl_down_sync(0xffffffffu, v.x, d), __shfl_down_sync(0xffffffffu, v.y, d),
                            __shfl_down_sync(0xffffffffu, v.z, d), __shfl_down_sync(0xffffffffu, v.w, d));
@@ -89,6 +90,7 @@ template <> struct VecT<1> {
     static __device__ __forceinline__ T add(T a, T b) { return a + b; }
     static __device__ __forceinline__ T load(const float *p, uint64_t pol) { return ldg1_hint(p, pol); }
     static __device__ __forceinline__ void red(float *p, T v) { red_add1(p, v); }
+    static __device__ __forceinline__ void red_if(float *p, T v, bool pred) { red_add1_if(p, v, pred); }
     static __device__ __forceinline__ T shfl_down(T v, int d) { return __shfl_down_sync(0xffffffffu, v, d); }
     static __device__ __forceinline__ T shfl(T v, int src) { return __shfl_sync(0xffffffffu, v, src); }
 };
@@ -130,17 +132,28 @@ __global__ void __launch_bounds__(256) mttkrp_sym_kernel(const KParams p) {
     const int64_t nch = (end - begin + CH - 1) / CH;
 
     const uint32_t R = p.R;
+    const uint32_t Rb = R * 4u;  // row stride in bytes
     const uint32_t col0 = blockIdx.y * TILE + j * VW;
+    // per-lane column byte offsets; inactive lanes (col >= R) read column 0 of
+    // the same row (valid memory) and never write
     bool act[VPL];
-#pragma unroll
-    for (int q = 0; q < VPL; ++q) act[q] = col0 + q * QS < R;
-    const float *Bc = p.B + col0;
+    const char *Bq[VPL];
+    char *Cq[VPL];
     // small outputs are spread over `copies` replicas (L2-slice spreading):
     // warp gw accumulates into replica gw % copies, summed afterwards
-    float *Cc = p.C + static_cast<size_t>(gw % p.copies) * p.plane + col0;
+    char *Cbase = reinterpret_cast<char *>(p.C + static_cast<size_t>(gw % p.copies) * p.plane);
+#pragma unroll
+    for (int q = 0; q < VPL; ++q) {
+        const uint32_t col = col0 + q * QS;
+        act[q] = col < R;
+        const uint32_t ofs = act[q] ? col * 4u : 0u;
+        Bq[q] = reinterpret_cast<const char *>(p.B) + ofs;
+        Cq[q] = Cbase + ofs;
+    }
     const uint64_t pol_keep = p.hints ? policy_evict_last() : policy_evict_normal();
     const uint64_t pol_stream = policy_evict_first();
     const float *coef = kCoef.v[N - 2][0];
+    constexpr float kFact = static_cast<float>(cfact(N - 1));  // (n-1)!: every coefficient of a strict entry
 
     if (lane == 0) {
         for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
@@ -162,6 +175,10 @@ __global__ void __launch_bounds__(256) mttkrp_sym_kernel(const KParams p) {
 
     if (lane == 0)
         for (int64_t k = 0; k < min(static_cast<int64_t>(S - 1), nch); ++k) issue(k);
+
+    // row address of row c for the lane's vector q: one IMAD.WIDE.U32
+    auto rowB = [&](int32_t c, int q) { return reinterpret_cast<const float *>(Bq[q] + static_cast<uint64_t>(static_cast<uint32_t>(c)) * Rb); };
+    auto rowC = [&](int32_t c, int q) { return reinterpret_cast<float *>(Cq[q] + static_cast<uint64_t>(static_cast<uint32_t>(c)) * Rb); };
 
     // running sums: position 0 (carried across chunks) and position 1
     int cur0 = -1;
@@ -198,83 +215,89 @@ __global__ void __launch_bounds__(256) mttkrp_sym_kernel(const KParams p) {
             for (int t = 0; t < N; ++t) x.c[t] = sc[t * CH + i];
             x.v = sv[i];
 #pragma unroll
-            for (int t = NAIVE ? 1 : 0; t < N; ++t) {  // the naive kernel never reads B[c_0]
-                const uint64_t o = row_off(x.c[t], R);
+            for (int t = NAIVE ? 1 : 0; t < N; ++t)  // the naive kernel never reads B[c_0]
 #pragma unroll
-                for (int q = 0; q < VPL; ++q) x.b[t][q] = act[q] ? V::load(Bc + o + q * QS, pol_keep) : V::zero();
-            }
+                for (int q = 0; q < VPL; ++q) x.b[t][q] = V::load(rowB(x.c[t], q), pol_keep);
         };
         auto consume = [&](const Slot &x) {
-            int code = 0;
-#pragma unroll
-            for (int t = 0; t + 1 < N; ++t) code |= (x.c[t] == x.c[t + 1]) << t;
-            const float *cf = coef + code * kMaxOrder;
-            // prefix / suffix products: u_t = (coef_t v) prod_{s<t} b_s prod_{s>t} b_s
             T u[N][VPL];
+            // run-first flags: position t updates C iff it starts a run of equal indices
+            bool first[N];
+            int code = 0;
+            first[0] = true;
 #pragma unroll
-            for (int q = 0; q < VPL; ++q) {
-                if (NAIVE) {  // general (non-symmetric) entry: only C[c_0] += v prod_{t>=1} B[c_t]
+            for (int t = 1; t < N; ++t) {
+                first[t] = x.c[t] != x.c[t - 1];
+                code |= (!first[t]) << (t - 1);
+            }
+            if (NAIVE) {  // general (non-symmetric) entry: only C[c_0] += v prod_{t>=1} B[c_t]
+#pragma unroll
+                for (int q = 0; q < VPL; ++q) {
                     T prod = x.b[1 % N][q];
 #pragma unroll
                     for (int t = 2; t < N; ++t) prod = V::mul(prod, x.b[t][q]);
                     u[0][q] = V::scale(x.v, prod);
-                    continue;
                 }
-                T pre[N];
-                pre[1 % N] = x.b[0][q];
+            } else {
+                // u_t = coef_t v prod_{j != t} b_j.  A strict entry (code 0) has every
+                // coef = (n-1)!, folded into the scalar; a diagonal entry rescales by its
+                // table row below.  P_t = s prod_{j<t} b_j, Q_t = prod_{j>t} b_j.
+                const bool strict = code == 0;
+                const float sc0 = strict ? x.v * kFact : x.v;
 #pragma unroll
-                for (int t = 2; t < N; ++t) pre[t] = V::mul(pre[t - 1], x.b[t - 1][q]);
-                T suf = x.b[N - 1][q];
+                for (int q = 0; q < VPL; ++q) {
+                    T P[N];
+                    P[1 % N] = V::scale(sc0, x.b[0][q]);
 #pragma unroll
-                for (int t = N - 1; t >= 0; --t) {
-                    const T prod = (t == N - 1) ? pre[t] : (t == 0 ? suf : V::mul(pre[t], suf));
-                    u[t][q] = V::scale(cf[t] * x.v, prod);
-                    if (t > 0 && t < N - 1) suf = V::mul(suf, x.b[t][q]);
+                    for (int t = 2; t < N; ++t) P[t] = V::mul(P[t - 1], x.b[t - 1][q]);
+                    T Q = x.b[N - 1][q];
+                    u[N - 1][q] = P[N - 1];
+#pragma unroll
+                    for (int t = N - 2; t >= 1; --t) {
+                        u[t][q] = V::mul(P[t], Q);
+                        Q = V::mul(Q, x.b[t][q]);
+                    }
+                    u[0][q] = V::scale(sc0, Q);
+                }
+                if (__any_sync(__activemask(), !strict) && !strict) {  // warp-uniform skip when all strict
+                    const float *cf = coef + code * kMaxOrder;
+#pragma unroll
+                    for (int t = 0; t < N; ++t) {
+                        const float f = cf[t];
+#pragma unroll
+                        for (int q = 0; q < VPL; ++q) u[t][q] = V::scale(f, u[t][q]);
+                    }
                 }
             }
-            // position 0: register run accumulation
-            if (x.c[0] != cur0) {
-                if (cur0 >= 0) {
-                    const uint64_t o = row_off(cur0, R);
+            // position 0: register run accumulation; the finished run is written
+            // with one (predicated) vector reduction when c_0 changes
+            {
+                const bool flush = x.c[0] != cur0;
 #pragma unroll
-                    for (int q = 0; q < VPL; ++q)
-                        if (act[q]) V::red(Cc + o + q * QS, acc0[q]);
+                for (int q = 0; q < VPL; ++q) {
+                    V::red_if(rowC(cur0, q), acc0[q], flush && cur0 >= 0 && act[q]);
+                    acc0[q] = flush ? u[0][q] : V::add(acc0[q], u[0][q]);
                 }
                 cur0 = x.c[0];
-#pragma unroll
-                for (int q = 0; q < VPL; ++q) acc0[q] = V::zero();
             }
-#pragma unroll
-            for (int q = 0; q < VPL; ++q) acc0[q] = V::add(acc0[q], u[0][q]);
             if (NAIVE) return;
-            // position 1
+            // position 1 (POS1): the same along runs of equal c_1
             if (POS1) {
-                if (x.c[1] != cur1) {
-                    if (has1) {
-                        const uint64_t o = row_off(cur1, R);
+                const bool flush = x.c[1] != cur1;
+                const bool take = first[1];
 #pragma unroll
-                        for (int q = 0; q < VPL; ++q)
-                            if (act[q]) V::red(Cc + o + q * QS, acc1[q]);
-                    }
-                    cur1 = x.c[1];
-                    has1 = false;
-#pragma unroll
-                    for (int q = 0; q < VPL; ++q) acc1[q] = V::zero();
+                for (int q = 0; q < VPL; ++q) {
+                    V::red_if(rowC(cur1, q), acc1[q], flush && has1 && act[q]);
+                    const T base = flush ? V::zero() : acc1[q];
+                    acc1[q] = take ? V::add(base, u[1][q]) : base;
                 }
-                if (cf[1] != 0.f) {
-                    has1 = true;
-#pragma unroll
-                    for (int q = 0; q < VPL; ++q) acc1[q] = V::add(acc1[q], u[1][q]);
-                }
+                has1 = flush ? take : (has1 || take);
+                cur1 = x.c[1];
             }
 #pragma unroll
             for (int t = POS1 ? 2 : 1; t < N; ++t)
-                if (cf[t] != 0.f) {
-                    const uint64_t o = row_off(x.c[t], R);
 #pragma unroll
-                    for (int q = 0; q < VPL; ++q)
-                        if (act[q]) V::red(Cc + o + q * QS, u[t][q]);
-                }
+                for (int q = 0; q < VPL; ++q) V::red_if(rowC(x.c[t], q), u[t][q], first[t] && act[q]);
         };
 
         if (PF) {
@@ -300,16 +323,13 @@ __global__ void __launch_bounds__(256) mttkrp_sym_kernel(const KParams p) {
         __syncwarp();
 
         if (POS1) {
-            if (has1) {
-                const uint64_t o = row_off(cur1, R);
 #pragma unroll
-                for (int q = 0; q < VPL; ++q)
-                    if (act[q]) V::red(Cc + o + q * QS, acc1[q]);
+            for (int q = 0; q < VPL; ++q) {
+                V::red_if(rowC(cur1, q), acc1[q], has1 && act[q]);
+                acc1[q] = V::zero();
             }
             has1 = false;
             cur1 = -1;
-#pragma unroll
-            for (int q = 0; q < VPL; ++q) acc1[q] = V::zero();
         }
 
         // segmented reduction of the groups' pending position-0 sums
@@ -329,12 +349,9 @@ __global__ void __launch_bounds__(256) mttkrp_sym_kernel(const KParams p) {
         const bool head = (g == 0) || (prev_key != key);
         const int last_key = __shfl_sync(0xffffffffu, key, (E - 1) * LPE);
         const bool carry = (k + 1 < nch);  // chunk was full: the next chunk continues the stream
-        if (head && key >= 0 && !(carry && key == last_key)) {
-            const uint64_t o = row_off(key, R);
+        const bool write = head && key >= 0 && !(carry && key == last_key);
 #pragma unroll
-            for (int q = 0; q < VPL; ++q)
-                if (act[q]) V::red(Cc + o + q * QS, acc0[q]);
-        }
+        for (int q = 0; q < VPL; ++q) V::red_if(rowC(key, q), acc0[q], write && act[q]);
         if (carry) {
             const unsigned heads = __ballot_sync(0xffffffffu, head && j == 0 && key == last_key);
             const int hl = __ffs(heads) - 1;  // lane of the last segment's head (j == 0)

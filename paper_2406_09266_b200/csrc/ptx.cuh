@@ -65,16 +65,21 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
 }
 
 // ---- gathers ------------------------------------------------------------------
+#ifdef SYSTEC_L1_NOALLOC
+#define SYSTEC_LD_L1 ".L1::no_allocate"
+#else
+#define SYSTEC_LD_L1 ""
+#endif
 __device__ __forceinline__ float4 ldg4_hint(const float *p, uint64_t policy) {
     float4 v;
-    asm volatile("ld.global.nc.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+    asm volatile("ld.global.nc" SYSTEC_LD_L1 ".L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
                  : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
                  : "l"(p), "l"(policy));
     return v;
 }
 __device__ __forceinline__ float ldg1_hint(const float *p, uint64_t policy) {
     float v;
-    asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(policy));
+    asm volatile("ld.global.nc" SYSTEC_LD_L1 ".L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(policy));
     return v;
 }
 __device__ __forceinline__ float4 ldg4(const float *p) {
@@ -90,6 +95,22 @@ __device__ __forceinline__ void red_add4(float *p, float4 v) {
 }
 __device__ __forceinline__ void red_add1(float *p, float v) {
     asm volatile("red.global.add.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
+}
+
+// predicated forms: one REDG issued under a predicate, no branch
+__device__ __forceinline__ void red_add4_if(float *p, float4 v, bool pred) {
+    asm volatile(
+        "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %5, 0;\n\t"
+        "@q red.global.add.v4.f32 [%0], {%1,%2,%3,%4};\n\t}" ::"l"(p),
+        "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "r"(static_cast<int>(pred))
+        : "memory");
+}
+__device__ __forceinline__ void red_add1_if(float *p, float v, bool pred) {
+    asm volatile(
+        "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t"
+        "@q red.global.add.f32 [%0], %1;\n\t}" ::"l"(p),
+        "f"(v), "r"(static_cast<int>(pred))
+        : "memory");
 }
 
 }  // namespace systec

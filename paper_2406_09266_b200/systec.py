@@ -48,7 +48,7 @@ def load(path: str | None = None):
     global _lib
     if _lib is not None:
         return _lib
-    p = path or LIB_PATH
+    p = path or os.environ.get("SYSTEC_LIB") or LIB_PATH   # SYSTEC_LIB: experiment builds
     if not os.path.exists(p):
         raise ImportError(f"libsystec.so not built at {p}; run __graft_entry__.build() "
                           "(there is no CPU fallback)")
