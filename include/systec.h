@@ -92,7 +92,9 @@ typedef struct systec_exec_opts {
      * reserved[2] vpl: float4 per lane, 1/2/4 (0 = 1)
      * reserved[3] prefetch: 1 on, -1 off, 0 = auto (on when B > 32 MB)
      * reserved[4] copies: replicas of C for L2-slice spreading, 1 = off, 0 = auto
-     *             (outputs < 4 MB and nnz >= 1e5: up to 32 replicas)          */
+     *             (outputs < 4 MB and nnz >= 1e5: up to 32 replicas)
+     * reserved[5] ablation bits (evidence study; c2/c5 kernel shapes only):
+     *             1 = no shared-memory staging, 2 = no position-0 accumulation */
     int32_t reserved[10];
 } systec_exec_opts;
 

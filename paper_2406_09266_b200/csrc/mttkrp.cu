@@ -52,6 +52,12 @@ int default_K(int E) {
 
 }  // namespace
 
+KernelFn ablation3(int abl);
+KernelFn ablation5(int abl);
+KernelFn pick_ablation_kernel(int order, int abl) {
+    return order == 3 ? ablation3(abl) : order == 5 ? ablation5(abl) : nullptr;
+}
+
 __global__ void reduce_copies_kernel(const float *__restrict__ Cp, float *__restrict__ C, int64_t plane, int copies,
                                      int vec) {
     const int64_t n4 = vec ? plane / 4 : 0;
@@ -140,6 +146,12 @@ cudaError_t launch_mttkrp(Plan &p, const float *B, int R, float *C, const systec
     // in-flight gathers gain.
     const bool pf = o.reserved[3] > 0;
     KernelFn fn = p.general ? pick_naive(p.order, vw, lpe, pf) : pick(p.order, vw, lpe, vpl, pos1, pf);
+    const int abl = o.reserved[5];
+    if (abl > 0) {  // ablation study: only the c2 / c5 kernel shapes exist
+        const bool shape3 = p.order == 3 && vw == 4 && lpe == 8 && vpl == 1 && !pos1 && !pf && !p.general;
+        const bool shape5 = p.order == 5 && vw == 4 && lpe == 4 && vpl == 1 && pos1 && !pf && !p.general;
+        fn = (shape3 || shape5) ? pick_ablation_kernel(p.order, abl) : nullptr;
+    }
     if (!fn) return release(cudaErrorInvalidValue);
     int wpb = o.warps_per_block > 0 ? o.warps_per_block : 8;
     auto smem_for = [&](int w) {

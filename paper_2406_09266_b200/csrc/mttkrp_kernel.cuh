@@ -106,7 +106,10 @@ __device__ __forceinline__ uint64_t row_off(int32_t c, uint32_t R) {
     return static_cast<uint64_t>(static_cast<uint32_t>(c)) * R;
 }
 
-template <int N, int LPE, int VPL, int VW, bool POS1, bool PF, bool NAIVE = false>
+// ABL (ablations for the evidence table, instantiated for the c2/c5 shapes only):
+//   bit 0: no shared-memory staging (indices and values read with plain loads)
+//   bit 1: no position-0 run accumulation (one reduction per entry)
+template <int N, int LPE, int VPL, int VW, bool POS1, bool PF, bool NAIVE = false, int ABL = 0>
 __global__ void __launch_bounds__(256) mttkrp_sym_kernel(const KParams p) {
     using V = VecT<VW>;
     using T = typename V::T;
@@ -173,7 +176,8 @@ __global__ void __launch_bounds__(256) mttkrp_sym_kernel(const KParams p) {
         bulk_g2s(dst + N * CH, p.vals + cb, bytes, &bars[s], pol_stream);
     };
 
-    if (lane == 0)
+    constexpr bool kStage = (ABL & 1) == 0;
+    if (kStage && lane == 0)
         for (int64_t k = 0; k < min(static_cast<int64_t>(S - 1), nch); ++k) issue(k);
 
     // row address of row c for the lane's vector q: one IMAD.WIDE.U32
@@ -190,12 +194,14 @@ __global__ void __launch_bounds__(256) mttkrp_sym_kernel(const KParams p) {
     for (int q = 0; q < VPL; ++q) acc0[q] = acc1[q] = V::zero();
 
     for (int64_t k = 0; k < nch; ++k) {
-        if (lane == 0 && k + S - 1 < nch) {
-            fence_proxy_async_smem();
-            issue(k + S - 1);
-        }
         const int s = static_cast<int>(k % S);
-        mbar_wait(&bars[s], static_cast<uint32_t>((k / S) & 1));
+        if (kStage) {
+            if (lane == 0 && k + S - 1 < nch) {
+                fence_proxy_async_smem();
+                issue(k + S - 1);
+            }
+            mbar_wait(&bars[s], static_cast<uint32_t>((k / S) & 1));
+        }
 
         const int32_t *sc = wbuf + static_cast<size_t>(s) * ARR * CH;
         const float *sv = reinterpret_cast<const float *>(sc + N * CH);
@@ -211,9 +217,15 @@ __global__ void __launch_bounds__(256) mttkrp_sym_kernel(const KParams p) {
             T b[N][VPL];
         };
         auto fetch = [&](int i, Slot &x) {
+            if (kStage) {
 #pragma unroll
-            for (int t = 0; t < N; ++t) x.c[t] = sc[t * CH + i];
-            x.v = sv[i];
+                for (int t = 0; t < N; ++t) x.c[t] = sc[t * CH + i];
+                x.v = sv[i];
+            } else {  // ablation: plain (cached) global loads of the stream
+#pragma unroll
+                for (int t = 0; t < N; ++t) x.c[t] = __ldg(p.coords + t * p.ld + cb + i);
+                x.v = __ldg(p.vals + cb + i);
+            }
 #pragma unroll
             for (int t = NAIVE ? 1 : 0; t < N; ++t)  // the naive kernel never reads B[c_0]
 #pragma unroll
@@ -272,7 +284,7 @@ __global__ void __launch_bounds__(256) mttkrp_sym_kernel(const KParams p) {
             // position 0: register run accumulation; the finished run is written
             // with one (predicated) vector reduction when c_0 changes
             {
-                const bool flush = x.c[0] != cur0;
+                const bool flush = (ABL & 2) || x.c[0] != cur0;
 #pragma unroll
                 for (int q = 0; q < VPL; ++q) {
                     V::red_if(rowC(cur0, q), acc0[q], flush && cur0 >= 0 && act[q]);
@@ -379,6 +391,8 @@ template <> KernelFn pick_kernel<2>(int vw, int lpe, int vpl, bool pos1, bool pf
 template <> KernelFn pick_kernel<3>(int vw, int lpe, int vpl, bool pos1, bool pf);
 template <> KernelFn pick_kernel<4>(int vw, int lpe, int vpl, bool pos1, bool pf);
 template <> KernelFn pick_kernel<5>(int vw, int lpe, int vpl, bool pos1, bool pf);
+// ablation variants (abl bits above) of the c2 kernel <3,8,1,4,false,false> and c5 kernel <5,4,1,4,true,false>
+KernelFn pick_ablation_kernel(int order, int abl);
 // the non-symmetric (expanded-tensor) baseline: position 0 only, one float4/float per lane
 template <int N> KernelFn pick_naive_kernel(int vw, int lpe, bool pf);
 template <> KernelFn pick_naive_kernel<2>(int vw, int lpe, bool pf);

@@ -73,4 +73,13 @@ KernelFn pick_naive_kernel<3>(int vw, int lpe, bool pf) {
     }
 }
 
+KernelFn ablation3(int abl) {
+    switch (abl) {
+        case 1: return mttkrp_sym_kernel<3, 8, 1, 4, false, false, false, 1>;
+        case 2: return mttkrp_sym_kernel<3, 8, 1, 4, false, false, false, 2>;
+        case 3: return mttkrp_sym_kernel<3, 8, 1, 4, false, false, false, 3>;
+        default: return nullptr;
+    }
+}
+
 }  // namespace systec

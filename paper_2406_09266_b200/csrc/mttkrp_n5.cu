@@ -73,4 +73,13 @@ KernelFn pick_naive_kernel<5>(int vw, int lpe, bool pf) {
     }
 }
 
+KernelFn ablation5(int abl) {
+    switch (abl) {
+        case 1: return mttkrp_sym_kernel<5, 4, 1, 4, true, false, false, 1>;
+        case 2: return mttkrp_sym_kernel<5, 4, 1, 4, true, false, false, 2>;
+        case 3: return mttkrp_sym_kernel<5, 4, 1, 4, true, false, false, 3>;
+        default: return nullptr;
+    }
+}
+
 }  // namespace systec

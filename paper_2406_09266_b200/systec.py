@@ -126,6 +126,8 @@ def _opts(**kw) -> SystecExecOpts:
             o.reserved[3] = int(v)
         elif k == "copies":
             o.reserved[4] = int(v)
+        elif k == "ablation":
+            o.reserved[5] = int(v)
         else:
             setattr(o, k, int(v))
     return o

@@ -289,3 +289,41 @@ def test_general_plan_on_expansion_equals_symmetric(systec, n, dim, nnz, R):
     C = plan.execute(dB)
     torch.cuda.synchronize()
     parity(C.cpu().numpy(), Cref, S)
+
+
+# ---------------------------------------------------------------- ablation variants + graph capture
+@pytest.mark.parametrize("n,R", [(3, 32), (5, 16)])
+def test_ablation_variants_are_correct(systec, n, R):
+    """The evidence-study variants (no smem staging / no pos-0 accumulation)
+    compute the same C."""
+    w = small_random(n, {3: 300, 5: 25}[n], 30000, R, seed=77, diag_frac=0.05)
+    Cref, S = oracle.mttkrp(n, w.dim, w.idx, w.vals, w.B)
+    pos1 = 1 if n == 5 else -1
+    for abl in (1, 2, 3):
+        parity(run(systec, w, ablation=abl, pos1_accumulate=pos1, copies=1), Cref, S)
+    with pytest.raises(ValueError):
+        run(systec, w, ablation=1, vpl=2)           # no such ablation shape
+
+
+def test_execute_is_cuda_graph_capturable(systec):
+    import torch
+    for n, dim, nnz, R in ((3, 2000, 200000, 32), (5, 60, 200000, 16)):   # copies = 1 and copies > 1
+        w = small_random(n, dim, nnz, R, seed=5, diag_frac=0.05)
+        Cref, S = oracle.mttkrp(n, dim, w.idx, w.vals, w.B)
+        di, dv, dB = to_dev(w.idx, w.vals, w.B)
+        plan = systec.Plan(n, dim, di, dv)
+        C = torch.empty((dim, R), device="cuda")
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            plan.execute(dB, C)                       # warm-up outside capture
+        torch.cuda.current_stream().wait_stream(s)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            plan.execute(dB, C)
+        C.fill_(123.0)
+        g.replay()
+        g.replay()
+        torch.cuda.synchronize()
+        parity(C.cpu().numpy(), Cref, S)
