@@ -184,6 +184,7 @@ cudaError_t launch_mttkrp(Plan &p, const float *B, int R, float *C, const systec
     kp.C = Cdst;
     kp.copies = copies;
     kp.plane = plane;
+    kp.dim = p.dim;
     kp.ld = p.ld;
     kp.nnz = p.nnz;
     kp.span = span;

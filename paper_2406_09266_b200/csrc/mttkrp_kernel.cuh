@@ -34,6 +34,7 @@
 //   * position 1 optionally accumulates the same way along runs of equal c_1;
 //   * every other run-first position issues a vector `red.global.add.v4.f32`.
 #pragma once
+#include <cassert>
 #include <cstdint>
 
 #include "coef_table.cuh"
@@ -59,6 +60,7 @@ struct KParams {
     int hints;              // 1: evict-last policy on B gathers, 0: evict-normal
     int copies;             // replicas of C the warps spread their reductions over (>= 1)
     int64_t plane;          // dim * R (floats per replica)
+    int64_t dim;            // rows of B and C (bounds checks in SYSTEC_DEBUG builds)
 };
 
 using KernelFn = void (*)(KParams);
@@ -226,6 +228,11 @@ __global__ void __launch_bounds__(256) mttkrp_sym_kernel(const KParams p) {
                 for (int t = 0; t < N; ++t) x.c[t] = __ldg(p.coords + t * p.ld + cb + i);
                 x.v = __ldg(p.vals + cb + i);
             }
+#ifdef SYSTEC_DEBUG
+#pragma unroll
+            for (int t = 0; t < N; ++t) assert(x.c[t] >= 0 && x.c[t] < p.dim);
+            assert(cb + i < p.nnz && i < CH);
+#endif
 #pragma unroll
             for (int t = NAIVE ? 1 : 0; t < N; ++t)  // the naive kernel never reads B[c_0]
 #pragma unroll
