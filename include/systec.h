@@ -147,6 +147,18 @@ SYSTEC_API int systec_plan_create_general(systec_plan *out, int order, int64_t d
                                           const int32_t *idx, const float *vals, systec_stream_t stream);
 
 /*
+ * One Bellman-Ford relaxation in the (min, +) semiring over a symmetric sparse
+ * MATRIX (an order-2 plan, the paper's Bellman-Ford
+ * kernel `y[i] min= A[i,j] + d[j]`):
+ *     y[i] = min(d[i], min over stored (i,j,v) or (j,i,v) of v + d[j])
+ * d [dim] and y [dim] are device fp32 vectors (must not overlap).  Each
+ * candidate is one fp32 add and the min is exact, so the result does not
+ * depend on the update order.  Async on `stream`.
+ * Errors: ARG, UNSUPPORTED (plan order != 2 or a general plan), ALIAS, CUDA.
+ */
+SYSTEC_API int systec_plan_minplus(systec_plan plan, const float *d, float *y, systec_stream_t stream);
+
+/*
  * Expand a symmetric tensor's stored entries (device idx [nnz][order], vals
  * [nnz]; any tuple order) into every distinct permutation of each tuple — the
  * non-symmetric tensor it stands for (Def. Symmetry, PAPER.md:141-147;

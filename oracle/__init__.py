@@ -13,6 +13,8 @@ no code with the CUDA path (``paper_2406_09266_b200``) and never imports it.
   of absolute terms used to normalise the parity error.
 * :func:`mttkrp_general` — the naive kernel on a general (non-symmetric) COO
   tensor, for the non-symmetric GPU baseline.
+* :func:`minplus_sym2` — one Bellman-Ford (min, +) relaxation over a
+  symmetric matrix.
 * :mod:`oracle.symmetric_ref` — the per-position multiplicity-coefficient
   formula, written independently in fp64 numpy (pin P4 of SURVEY.md §8(c)).
 
@@ -55,6 +57,8 @@ def _load():
         lib.oracle_mttkrp_rows.restype = i32
         lib.oracle_mttkrp_general.argtypes = [i32, i64, i64, vp, vp, vp, i32, vp, vp]
         lib.oracle_mttkrp_general.restype = i32
+        lib.oracle_minplus_sym2.argtypes = [i64, i64, vp, vp, vp, vp]
+        lib.oracle_minplus_sym2.restype = i32
         lib.oracle_count_expanded.argtypes = [i32, i64, vp]
         lib.oracle_count_expanded.restype = i64
         _lib = lib
@@ -133,6 +137,21 @@ def mttkrp_general(order: int, dim: int, idx, vals, B):
     if rc != 0:
         raise RuntimeError(f"oracle_mttkrp_general failed with status {rc}")
     return C, S
+
+
+def minplus_sym2(dim: int, idx, vals, d):
+    """One (min,+) relaxation over a symmetric matrix given by its stored
+    entries (either orientation): y = min(d, min_j A[i,j] + d[j]), fp32 adds."""
+    idx = np.ascontiguousarray(idx, dtype=np.int32).reshape(-1, 2)
+    vals = np.ascontiguousarray(vals, dtype=np.float32)
+    d = np.ascontiguousarray(d, dtype=np.float32)
+    y = np.empty(dim, np.float32)
+    rc = _load().oracle_minplus_sym2(dim, idx.shape[0], _ptr(idx), _ptr(vals), _ptr(d), _ptr(y))
+    if rc == 3:
+        raise IndexError("index outside [0, dim)")
+    if rc != 0:
+        raise RuntimeError(f"oracle_minplus_sym2 failed with status {rc}")
+    return y
 
 
 def count_expanded(order: int, idx) -> int:

@@ -270,3 +270,30 @@ int oracle_mttkrp_general(int order, int64_t dim, int64_t nnz, const int32_t *id
     }
     return 0;
 }
+
+/*
+ * One Bellman-Ford relaxation over a symmetric sparse matrix in the (min, +)
+ * semiring: every stored entry (a, b, v) stands for both
+ * A[a,b] and A[b,a] (Def. Symmetry); the naive kernel visits
+ * both orientations (once when a == b):
+ *     y[i] = min(d[i], min over expanded (i, j, v) of v + d[j]),
+ * each candidate computed as ONE fp32 addition (the precision the GPU path
+ * uses, so the min takes the same decision), the min exact.
+ */
+int oracle_minplus_sym2(int64_t dim, int64_t nnz, const int32_t *idx, const float *vals,
+                        const float *d, float *y) {
+    if (dim < 1 || nnz < 0 || !d || !y || (nnz > 0 && (!idx || !vals))) return 1;
+    for (int64_t k = 0; k < 2 * nnz; k++)
+        if (idx[k] < 0 || idx[k] >= dim) return 3;
+    for (int64_t i = 0; i < dim; i++) y[i] = d[i];
+    for (int64_t e = 0; e < nnz; e++) {
+        const int32_t a = idx[2 * e], b = idx[2 * e + 1];
+        volatile float cand = vals[e] + d[b];           /* (a, b) orientation */
+        if (cand < y[a]) y[a] = cand;
+        if (a != b) {                                    /* (b, a) orientation */
+            volatile float cand2 = vals[e] + d[a];
+            if (cand2 < y[b]) y[b] = cand2;
+        }
+    }
+    return 0;
+}

@@ -256,6 +256,16 @@ int systec_expand_symmetric(int order, int64_t dim, int64_t nnz, const int32_t *
     return done(SYSTEC_OK);
 }
 
+int systec_plan_minplus(systec_plan plan, const float *d, float *y, systec_stream_t stream) {
+    Plan *p = reinterpret_cast<Plan *>(plan);
+    if (!p || !d || !y) return SYSTEC_ERR_ARG;
+    if (p->order != 2 || p->general) return SYSTEC_ERR_UNSUPPORTED;
+    const size_t bytes = static_cast<size_t>(p->dim) * 4;
+    if (systec::overlap(d, bytes, y, bytes)) return SYSTEC_ERR_ALIAS;
+    cudaError_t e = systec::launch_minplus(*p, d, y, reinterpret_cast<int *>(y), reinterpret_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? SYSTEC_OK : systec::cuda_fail(e);
+}
+
 int systec_plan_execute(systec_plan plan, const float *B, int R, float *C, systec_stream_t stream) {
     return systec::execute_impl(reinterpret_cast<Plan *>(plan), B, R, C, nullptr,
                                 reinterpret_cast<cudaStream_t>(stream));

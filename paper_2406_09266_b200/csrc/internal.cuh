@@ -57,6 +57,9 @@ cudaError_t expand_count(int order, int64_t dim, int64_t nnz, const int32_t *idx
 cudaError_t expand_write(int order, int64_t nnz, const int32_t *idx, const float *vals,
                          const unsigned long long *offsets, int32_t *out_idx, float *out_vals, cudaStream_t s);
 
+// minplus.cu — keys may alias y (in-place order-preserving integer keys)
+cudaError_t launch_minplus(const Plan &p, const float *d, float *y, int *scratch_keys, cudaStream_t s);
+
 // mttkrp.cu
 cudaError_t launch_mttkrp(Plan &p, const float *B, int R, float *C, const systec_exec_opts &o,
                           cudaStream_t s);

@@ -38,7 +38,7 @@ EXPORTS = ["systec_mttkrp", "systec_mttkrp_host", "systec_plan_create", "systec_
            "systec_plan_execute_ex", "systec_plan_stats", "systec_plan_prepared",
            "systec_plan_copy_prepared", "systec_plan_last_launch", "systec_plan_destroy",
            "systec_status_string", "systec_last_cuda_error", "systec_version", "systec_last_bad_entry",
-           "systec_plan_create_general", "systec_expand_symmetric"]
+           "systec_plan_create_general", "systec_expand_symmetric", "systec_plan_minplus"]
 
 _lib = None
 
@@ -59,6 +59,7 @@ def load(path: str | None = None):
     lib.systec_plan_create.argtypes = [ctypes.POINTER(vp), i32, i64, i64, vp, vp, vp]
     lib.systec_plan_execute.argtypes = [vp, vp, i32, vp, vp]
     lib.systec_plan_create_general.argtypes = [ctypes.POINTER(vp), i32, i64, i64, vp, vp, vp]
+    lib.systec_plan_minplus.argtypes = [vp, vp, vp, vp]
     lib.systec_expand_symmetric.argtypes = [i32, i64, i64, vp, vp, i64, vp, vp, ctypes.POINTER(i64), vp]
     lib.systec_plan_execute_ex.argtypes = [vp, vp, i32, vp, ctypes.POINTER(SystecExecOpts), vp]
     lib.systec_plan_stats.argtypes = [vp, ctypes.POINTER(SystecStats)]
@@ -172,6 +173,17 @@ class Plan:
         else:
             _check(lib.systec_plan_execute(self._h, bp, R, cp, s), "systec_plan_execute")
         return C
+
+    def minplus(self, d, y=None, stream=None):
+        """``systec_plan_minplus`` (order-2 plans): y[i] = min(d[i], min_j A[i,j] + d[j])."""
+        import torch
+        if d.dim() != 1 or d.shape[0] != self.dim:
+            raise ValueError("d must be [dim]")
+        if y is None:
+            y = torch.empty_like(d)
+        _check(load().systec_plan_minplus(self._h, _dev(d, torch.float32, "d"), _dev(y, torch.float32, "y"),
+                                          _stream_handle(stream)), "systec_plan_minplus")
+        return y
 
     def stats(self) -> dict:
         st = SystecStats()

@@ -42,6 +42,7 @@ def run(systec, w, idx=None, vals=None, **opts):
 @pytest.mark.parametrize("n,dim,nnz,R", [
     (3, 64, 2000, 8), (3, 300, 5003, 32), (3, 97, 777, 16),
     (4, 40, 6001, 16), (4, 25, 1234, 4), (5, 18, 4099, 16), (5, 12, 999, 32), (2, 500, 3001, 32),
+    (2, 3000, 20000, 1), (2, 700, 9001, 4),
 ])
 def test_parity_small(systec, n, dim, nnz, R):
     w = small_random(n, dim, nnz, R, seed=nnz + n, diag_frac=0.15)
@@ -327,3 +328,23 @@ def test_execute_is_cuda_graph_capturable(systec):
         g.replay()
         torch.cuda.synchronize()
         parity(C.cpu().numpy(), Cref, S)
+
+
+# ---------------------------------------------------------------- NEXT-3: (min,+) relaxation
+@pytest.mark.parametrize("dim,nnz", [(50, 400), (3000, 40000), (100000, 1000000)])
+def test_minplus_bit_exact(systec, dim, nnz):
+    import torch
+    rng = np.random.default_rng(dim)
+    w = make(f"mp{dim}", 2, dim, nnz, 1, seed=dim, mode="uniform")
+    vals = rng.uniform(-1, 5, nnz).astype(np.float32)
+    d = rng.uniform(0, 100, dim).astype(np.float32)
+    want = oracle.minplus_sym2(dim, w.idx, vals, d)
+    si, sv = scramble(w.idx, vals, seed=2)
+    for idx, vv in ((w.idx, vals), (si, sv)):
+        di, dv, dd = to_dev(idx, vv, d)
+        plan = systec.Plan(2, dim, di, dv)
+        y = plan.minplus(dd)
+        torch.cuda.synchronize()
+        assert np.array_equal(y.cpu().numpy(), want)
+    with pytest.raises(NotImplementedError):
+        systec.Plan(3, 10, *to_dev(np.zeros((1, 3), np.int32), np.ones(1, np.float32))).minplus(dd[:10])

@@ -318,3 +318,19 @@ def test_general_oracle_on_expanded_equals_symmetric(n, dim, nnz):
     C1, S1 = oracle.mttkrp(n, dim, w.idx, w.vals, w.B)
     C2, _ = oracle.mttkrp_general(n, dim, np.array(ex_i, np.int32), np.array(ex_v, np.float32), w.B)
     assert rel_err(C2, C1, S1) < 1e-13
+
+
+# ---------------------------------------------------------------- (min,+) relaxation oracle (NEXT-3)
+def test_minplus_oracle_vs_dense():
+    rng = np.random.default_rng(3)
+    dim, nnz = 40, 300
+    w = small_random(2, dim, nnz, 1, seed=3, diag_frac=0.1)
+    vals = rng.uniform(-1, 3, nnz).astype(np.float32)
+    d = rng.uniform(0, 10, dim).astype(np.float32)
+    A = np.full((dim, dim), np.inf, np.float32)
+    for (a, b), v in zip(w.idx, vals):
+        A[a, b] = min(A[a, b], v)
+        A[b, a] = min(A[b, a], v)
+    want = np.minimum(d, np.min(A + d[None, :], axis=1))        # fp32 adds, exact min
+    si, sv = scramble(w.idx, vals, seed=1)                       # either orientation
+    assert np.array_equal(oracle.minplus_sym2(dim, si, sv, d), want)
