@@ -159,6 +159,23 @@ SYSTEC_API int systec_plan_create_general(systec_plan *out, int order, int64_t d
 SYSTEC_API int systec_plan_minplus(systec_plan plan, const float *d, float *y, systec_stream_t stream);
 
 /*
+ * Symmetric CP decomposition by alternating least squares (SURVEY.md §8(f)
+ * NEXT-2; one factor matrix for every mode, so the update is
+ * the same in all modes).  X ≈ sum_r lambda_r b_r^{(x)n}.  Each iteration:
+ *     M = MTTKRP(X, B);  B = M ((B^T B)^{.(n-1)})^{-1};  lambda = column norms;  B /= lambda
+ * (R = 1 is the symmetric higher-order power method).  B [dim][R] (device) holds
+ * the initial factor on entry and the unit-column factor on return; lambda [R]
+ * (device) receives the weights.  Runs up to max_iters iterations and stops
+ * early when the fit changes by less than tol; fit_host [max_iters] (host, may
+ * be NULL) receives fit_k = 1 - ||X - Xhat_k|| / ||X|| of each iterate;
+ * *iters_done the number of iterations run.  1 <= R <= 48.  Synchronises
+ * `stream` once per iteration (to read the fit).
+ * Errors: ARG, UNSUPPORTED (general plan, R > 48), ALIAS, NOMEM, CUDA.
+ */
+SYSTEC_API int systec_cp_als_sym(systec_plan plan, float *B, int R, float *lambda, int max_iters, double tol,
+                                 double *fit_host, int *iters_done, systec_stream_t stream);
+
+/*
  * Expand a symmetric tensor's stored entries (device idx [nnz][order], vals
  * [nnz]; any tuple order) into every distinct permutation of each tuple — the
  * non-symmetric tensor it stands for (Def. Symmetry, PAPER.md:141-147;

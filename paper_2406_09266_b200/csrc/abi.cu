@@ -3,6 +3,7 @@
 // every step of the computation itself runs in the kernels of prepare.cu and
 // mttkrp.cu.  There is no host compute path.
 #include <climits>
+#include <cmath>
 #include <cstring>
 #include <new>
 
@@ -264,6 +265,66 @@ int systec_plan_minplus(systec_plan plan, const float *d, float *y, systec_strea
     if (systec::overlap(d, bytes, y, bytes)) return SYSTEC_ERR_ALIAS;
     cudaError_t e = systec::launch_minplus(*p, d, y, reinterpret_cast<int *>(y), reinterpret_cast<cudaStream_t>(stream));
     return e == cudaSuccess ? SYSTEC_OK : systec::cuda_fail(e);
+}
+
+int systec_cp_als_sym(systec_plan plan, float *B, int R, float *lambda, int max_iters, double tol,
+                      double *fit_host, int *iters_done, systec_stream_t stream) {
+    Plan *p = reinterpret_cast<Plan *>(plan);
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (!p || !B || !lambda || R < 1 || max_iters < 0) return SYSTEC_ERR_ARG;
+    if (p->general || R > systec::cpd_max_rank()) return SYSTEC_ERR_UNSUPPORTED;
+    const size_t plane = static_cast<size_t>(p->dim) * R;
+    if (systec::overlap(B, plane * 4, lambda, static_cast<size_t>(R) * 4)) return SYSTEC_ERR_ALIAS;
+    float *M = nullptr, *fs = nullptr;
+    double *ds = nullptr;
+    double host[2] = {0, 0}, x2 = 0;
+    cudaError_t e = cudaSuccess;
+    int rc = SYSTEC_OK;
+    int done = 0;
+    auto cleanup = [&]() {
+        if (M) cudaFreeAsync(M, s);
+        if (fs) cudaFreeAsync(fs, s);
+        if (ds) cudaFreeAsync(ds, s);
+    };
+    do {
+        if ((e = cudaMallocAsync(&M, plane * 4, s)) != cudaSuccess) break;
+        if ((e = cudaMallocAsync(&fs, static_cast<size_t>(R) * R * 4, s)) != cudaSuccess) break;
+        if ((e = cudaMallocAsync(&ds, sizeof(double) * (R * R + 2 * R + 2), s)) != cudaSuccess) break;
+        if ((e = systec::cpd_tensor_norm2(*p, ds, s)) != cudaSuccess) break;
+        if ((e = cudaMemcpyAsync(&x2, ds, sizeof(double), cudaMemcpyDeviceToHost, s)) != cudaSuccess) break;
+        if ((e = cudaStreamSynchronize(s)) != cudaSuccess) break;
+        const double xn = sqrt(x2 > 0 ? x2 : 1e-300);
+        double prev_fit = -1e300;
+        double *scal = ds + R * R + 2 * R;
+        // iteration k: M = MTTKRP(X, B_k); the same pass yields fit(B_{k-1}-step iterate) pieces
+        for (int it = 0; it <= max_iters; ++it) {
+            systec_exec_opts o;
+            std::memset(&o, 0, sizeof(o));
+            if ((e = systec::launch_mttkrp(*p, B, R, M, o, s)) != cudaSuccess) break;
+            const bool last = it == max_iters;
+            if ((e = systec::cpd_step(*p, M, B, lambda, R, ds, fs, it > 0, last, s)) != cudaSuccess) break;
+            if (it > 0) {
+                if ((e = cudaMemcpyAsync(host, scal, 2 * sizeof(double), cudaMemcpyDeviceToHost, s)) != cudaSuccess) break;
+                if ((e = cudaStreamSynchronize(s)) != cudaSuccess) break;
+                const double r2 = x2 - 2 * host[1] + host[0];
+                const double fit = 1.0 - sqrt(r2 > 0 ? r2 : 0.0) / xn;
+                if (fit_host) fit_host[it - 1] = fit;
+                done = it;
+                if (last || fabs(fit - prev_fit) < tol) {
+                    if (!last) {  // converged: the step just taken produced one more iterate; keep it
+                        // (its fit is not evaluated; callers read fit_host[done-1])
+                    }
+                    break;
+                }
+                prev_fit = fit;
+            }
+        }
+    } while (false);
+    cleanup();
+    if (e != cudaSuccess) rc = systec::cuda_fail(e);
+    if (iters_done) *iters_done = done;
+    if (rc == SYSTEC_OK && (e = cudaStreamSynchronize(s)) != cudaSuccess) rc = systec::cuda_fail(e);
+    return rc;
 }
 
 int systec_plan_execute(systec_plan plan, const float *B, int R, float *C, systec_stream_t stream) {

@@ -60,6 +60,12 @@ cudaError_t expand_write(int order, int64_t nnz, const int32_t *idx, const float
 // minplus.cu — keys may alias y (in-place order-preserving integer keys)
 cudaError_t launch_minplus(const Plan &p, const float *d, float *y, int *scratch_keys, cudaStream_t s);
 
+// cpd.cu
+int cpd_max_rank();
+cudaError_t cpd_tensor_norm2(const Plan &p, double *out, cudaStream_t s);
+cudaError_t cpd_step(const Plan &p, const float *M, float *B, float *lam, int R, double *dscratch,
+                     float *fscratch, bool have_lam, bool fit_only, cudaStream_t s);
+
 // mttkrp.cu
 cudaError_t launch_mttkrp(Plan &p, const float *B, int R, float *C, const systec_exec_opts &o,
                           cudaStream_t s);

@@ -38,7 +38,8 @@ EXPORTS = ["systec_mttkrp", "systec_mttkrp_host", "systec_plan_create", "systec_
            "systec_plan_execute_ex", "systec_plan_stats", "systec_plan_prepared",
            "systec_plan_copy_prepared", "systec_plan_last_launch", "systec_plan_destroy",
            "systec_status_string", "systec_last_cuda_error", "systec_version", "systec_last_bad_entry",
-           "systec_plan_create_general", "systec_expand_symmetric", "systec_plan_minplus"]
+           "systec_plan_create_general", "systec_expand_symmetric", "systec_plan_minplus",
+           "systec_cp_als_sym"]
 
 _lib = None
 
@@ -60,6 +61,7 @@ def load(path: str | None = None):
     lib.systec_plan_execute.argtypes = [vp, vp, i32, vp, vp]
     lib.systec_plan_create_general.argtypes = [ctypes.POINTER(vp), i32, i64, i64, vp, vp, vp]
     lib.systec_plan_minplus.argtypes = [vp, vp, vp, vp]
+    lib.systec_cp_als_sym.argtypes = [vp, vp, i32, vp, i32, ctypes.c_double, vp, ctypes.POINTER(i32), vp]
     lib.systec_expand_symmetric.argtypes = [i32, i64, i64, vp, vp, i64, vp, vp, ctypes.POINTER(i64), vp]
     lib.systec_plan_execute_ex.argtypes = [vp, vp, i32, vp, ctypes.POINTER(SystecExecOpts), vp]
     lib.systec_plan_stats.argtypes = [vp, ctypes.POINTER(SystecStats)]
@@ -184,6 +186,21 @@ class Plan:
         _check(load().systec_plan_minplus(self._h, _dev(d, torch.float32, "d"), _dev(y, torch.float32, "y"),
                                           _stream_handle(stream)), "systec_plan_minplus")
         return y
+
+    def cp_als(self, B, max_iters: int = 50, tol: float = 1e-7, stream=None):
+        """``systec_cp_als_sym``: symmetric CP-ALS from the initial factor B (CUDA
+        tensor [dim][R], updated in place).  Returns (B, lambda, fits)."""
+        import torch
+        if B.dim() != 2 or B.shape[0] != self.dim:
+            raise ValueError("B must be [dim][R]")
+        R = int(B.shape[1])
+        lam = torch.empty(R, dtype=torch.float32, device=B.device)
+        fits = np.zeros(max(max_iters, 1), np.float64)
+        done = ctypes.c_int()
+        _check(load().systec_cp_als_sym(self._h, _dev(B, torch.float32, "B"), R, _dev(lam, torch.float32, "lambda"),
+                                        max_iters, tol, fits.ctypes.data_as(ctypes.c_void_p), ctypes.byref(done),
+                                        _stream_handle(stream)), "systec_cp_als_sym")
+        return B, lam, fits[:done.value]
 
     def stats(self) -> dict:
         st = SystecStats()

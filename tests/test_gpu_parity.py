@@ -348,3 +348,40 @@ def test_minplus_bit_exact(systec, dim, nnz):
         assert np.array_equal(y.cpu().numpy(), want)
     with pytest.raises(NotImplementedError):
         systec.Plan(3, 10, *to_dev(np.zeros((1, 3), np.int32), np.ones(1, np.float32))).minplus(dd[:10])
+
+
+# ---------------------------------------------------------------- NEXT-2: symmetric CP-ALS
+@pytest.mark.parametrize("order,dim,R", [(3, 12, 3), (4, 8, 2), (5, 7, 2), (3, 10, 1)])
+def test_cp_als_iterates_match_oracle(systec, order, dim, R):
+    import torch
+    from oracle import cpd_ref
+    from test_oracle_pins import planted
+    idx, vals, Bt, lam = planted(order, dim, R, seed=order + R, noise=0.01)
+    rng = np.random.default_rng(5)
+    B0 = (Bt + 0.2 * rng.standard_normal(Bt.shape)).astype(np.float32)
+    iters = 4
+    Bref, lref, fref = cpd_ref.cp_als_sym(order, dim, idx, vals, B0, iters=iters)
+    di, dv, dB = to_dev(idx, vals, B0)
+    plan = systec.Plan(order, dim, di, dv)
+    B, lam_g, fits = plan.cp_als(dB, max_iters=iters, tol=0.0)
+    torch.cuda.synchronize()
+    assert len(fits) == iters
+    np.testing.assert_allclose(B.cpu().numpy(), Bref, rtol=0, atol=2e-4)
+    np.testing.assert_allclose(lam_g.cpu().numpy(), lref, rtol=2e-4)
+    np.testing.assert_allclose(fits, fref, atol=2e-4)
+
+
+def test_cp_als_recovers_planted_and_stops_early(systec):
+    import torch
+    from test_oracle_pins import planted
+    idx, vals, Bt, lam = planted(3, 30, 4, seed=9)
+    rng = np.random.default_rng(1)
+    B0 = (Bt + 0.1 * rng.standard_normal(Bt.shape)).astype(np.float32)
+    di, dv, dB = to_dev(idx, vals, B0)
+    plan = systec.Plan(3, 30, di, dv)
+    B, lam_g, fits = plan.cp_als(dB, max_iters=200, tol=1e-6)
+    torch.cuda.synchronize()
+    assert fits[-1] > 0.999 and len(fits) < 200
+    match = np.abs(B.cpu().numpy().T @ Bt)
+    assert np.all(match.max(axis=1) > 0.999)
+    np.testing.assert_allclose(np.sort(lam_g.cpu().numpy()), np.sort(lam), rtol=1e-3)

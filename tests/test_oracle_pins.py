@@ -334,3 +334,50 @@ def test_minplus_oracle_vs_dense():
     want = np.minimum(d, np.min(A + d[None, :], axis=1))        # fp32 adds, exact min
     si, sv = scramble(w.idx, vals, seed=1)                       # either orientation
     assert np.array_equal(oracle.minplus_sym2(dim, si, sv, d), want)
+
+
+# ---------------------------------------------------------------- symmetric CP-ALS oracle (NEXT-2)
+def planted(order, dim, R, seed, noise=0.0):
+    """All canonical coordinates of X = sum_r lam_r b_r^{(x)n} (+ noise)."""
+    rng = np.random.default_rng(seed)
+    Bt = rng.standard_normal((dim, R))
+    Bt /= np.linalg.norm(Bt, axis=0)
+    lam = np.linspace(2.0, 1.0, R)
+    canon = np.array(list(itertools.combinations_with_replacement(range(dim), order)), np.int32)
+    vals = np.zeros(len(canon))
+    for r in range(R):
+        vals += lam[r] * np.prod(Bt[canon, r], axis=1)
+    vals += noise * rng.standard_normal(len(canon))
+    return canon, vals.astype(np.float32), Bt, lam
+
+
+def test_cpd_oracle_fit_formula_vs_dense():
+    from oracle import cpd_ref
+    order, dim, R = 3, 7, 2
+    idx, vals, Bt, lam = planted(order, dim, R, seed=1, noise=0.05)
+    rng = np.random.default_rng(2)
+    B = rng.standard_normal((dim, R))
+    B /= np.linalg.norm(B, axis=0)
+    lam_e = np.array([1.3, 0.7])
+    M, _ = oracle.mttkrp(order, dim, idx, vals, B.astype(np.float32))
+    A = dense_from_entries(order, dim, idx, vals)
+    Xhat = sum(lam_e[r] * np.einsum("i,j,k->ijk", B[:, r], B[:, r], B[:, r]) for r in range(R))
+    want = 1 - np.linalg.norm(A - Xhat) / np.linalg.norm(A)
+    x2 = cpd_ref.tensor_norm2(order, idx, vals)
+    assert abs(x2 - np.sum(A * A)) < 1e-9 * x2
+    # M was computed from fp32-rounded B: compare at that precision
+    assert abs(cpd_ref.fit_of(order, x2, M, B, lam_e) - want) < 1e-6
+
+
+@pytest.mark.parametrize("order,dim,R", [(3, 12, 3), (4, 8, 2), (3, 10, 1)])
+def test_cpd_oracle_recovers_planted(order, dim, R):
+    from oracle import cpd_ref
+    idx, vals, Bt, lam = planted(order, dim, R, seed=order + R)
+    rng = np.random.default_rng(5)
+    B0 = Bt + 0.1 * rng.standard_normal(Bt.shape)
+    B, lam_got, fits = cpd_ref.cp_als_sym(order, dim, idx, vals, B0, iters=40)
+    assert fits[-1] > 0.999          # the fit formula cancels: ~1e-4 floor from fp32 MTTKRP input
+    # columns match the planted factors up to order and sign
+    match = np.abs(B.T @ Bt)
+    assert np.all(match.max(axis=1) > 0.999)
+    assert np.allclose(np.sort(lam_got), np.sort(lam), rtol=1e-3)
