@@ -176,6 +176,27 @@ SYSTEC_API int systec_cp_als_sym(systec_plan plan, float *B, int R, float *lambd
                                  double *fit_host, int *iters_done, systec_stream_t stream);
 
 /*
+ * Symmetric TTM with visible output symmetry (the
+ * paper's TTM, Listings 1-3 PAPER.md:262-325), order-3 plans:
+ *     C[i, j, l] = sum_k A[k, j, l] B[k, i],    C[i,j,l] = C[i,l,j]
+ * Only the canonical half j <= l is computed, packed as
+ * C_packed [dim(dim+1)/2][R] (device; row pair(j,l) = l(l+1)/2 + j, rank
+ * innermost), OVERWRITTEN.  B [dim][R] device.  Async on `stream`.
+ * On a GENERAL order-3 plan (the naive baseline, e.g. over the expanded
+ * tensor) every entry updates the full output and C_packed must hold the full
+ * [dim][dim][R] tensor instead.
+ * Errors: ARG, UNSUPPORTED (order != 3), ALIAS, CUDA.
+ */
+SYSTEC_API int systec_plan_ttm(systec_plan plan, const float *B, int R, float *C_packed, systec_stream_t stream);
+
+/*
+ * Replicate the packed TTM output to the full tensor C_full [dim][dim][R]
+ * (device; C_full[j][l][i] = C[i,j,l]) — the output replication the paper
+ * excludes from its timings.  Async.  Errors: ARG, ALIAS, CUDA.
+ */
+SYSTEC_API int systec_ttm_unpack(int64_t dim, int R, const float *C_packed, float *C_full, systec_stream_t stream);
+
+/*
  * Expand a symmetric tensor's stored entries (device idx [nnz][order], vals
  * [nnz]; any tuple order) into every distinct permutation of each tuple — the
  * non-symmetric tensor it stands for (Def. Symmetry, PAPER.md:141-147;

@@ -15,6 +15,7 @@ no code with the CUDA path (``paper_2406_09266_b200``) and never imports it.
   tensor, for the non-symmetric GPU baseline.
 * :func:`minplus_sym2` — one Bellman-Ford (min, +) relaxation over a
   symmetric matrix.
+* :func:`ttm_sym3` — naive TTM over the expanded order-3 tensor (NEXT-4).
 * :mod:`oracle.symmetric_ref` — the per-position multiplicity-coefficient
   formula, written independently in fp64 numpy (pin P4 of SURVEY.md §8(c)).
 
@@ -59,6 +60,8 @@ def _load():
         lib.oracle_mttkrp_general.restype = i32
         lib.oracle_minplus_sym2.argtypes = [i64, i64, vp, vp, vp, vp]
         lib.oracle_minplus_sym2.restype = i32
+        lib.oracle_ttm_sym3.argtypes = [i64, i64, vp, vp, vp, i32, vp]
+        lib.oracle_ttm_sym3.restype = i32
         lib.oracle_count_expanded.argtypes = [i32, i64, vp]
         lib.oracle_count_expanded.restype = i64
         _lib = lib
@@ -152,6 +155,20 @@ def minplus_sym2(dim: int, idx, vals, d):
     if rc != 0:
         raise RuntimeError(f"oracle_minplus_sym2 failed with status {rc}")
     return y
+
+
+def ttm_sym3(dim: int, idx, vals, B):
+    """Naive TTM over the expanded order-3 tensor: full C [dim][dim][R] fp64
+    with C[j][l][r] = sum_k A[k,j,l] B[k,r]."""
+    idx, vals, B = _prep(3, idx, vals, B)
+    R = B.shape[1]
+    C = np.empty((dim, dim, R), np.float64)
+    rc = _load().oracle_ttm_sym3(dim, idx.shape[0], _ptr(idx), _ptr(vals), _ptr(B), R, _ptr(C))
+    if rc == 3:
+        raise IndexError("index outside [0, dim)")
+    if rc != 0:
+        raise RuntimeError(f"oracle_ttm_sym3 failed with status {rc}")
+    return C
 
 
 def count_expanded(order: int, idx) -> int:

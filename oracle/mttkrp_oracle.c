@@ -297,3 +297,29 @@ int oracle_minplus_sym2(int64_t dim, int64_t nnz, const int32_t *idx, const floa
     }
     return 0;
 }
+
+/*
+ * Naive TTM on the expanded order-3 tensor:
+ *   C[i, j, l] = sum_k A[k, j, l] B[k, i]
+ * every distinct permutation (p0, p1, p2) of every stored canonical entry
+ * adds v * B[p0, r] to C[p1][p2][r].  C is the FULL output [dim][dim][R] fp64.
+ */
+int oracle_ttm_sym3(int64_t dim, int64_t nnz, const int32_t *idx, const float *vals, const float *B, int R,
+                    double *C) {
+    int rc = check_args(3, dim, nnz, idx, vals, B, R);
+    if (rc) return rc;
+    if (!C) return 1;
+    memset(C, 0, (size_t)dim * dim * R * sizeof(double));
+    int32_t p[3];
+    for (int64_t e = 0; e < nnz; e++) {
+        for (int t = 0; t < 3; t++) p[t] = idx[e * 3 + t];
+        sort_small(p, 3);
+        const double v = (double)vals[e];
+        do {
+            double *c = C + ((int64_t)p[1] * dim + p[2]) * R;
+            const float *b = B + (int64_t)p[0] * R;
+            for (int r = 0; r < R; r++) c[r] += v * (double)b[r];
+        } while (next_perm(p, 3));
+    }
+    return 0;
+}

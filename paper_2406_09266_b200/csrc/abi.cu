@@ -327,6 +327,26 @@ int systec_cp_als_sym(systec_plan plan, float *B, int R, float *lambda, int max_
     return rc;
 }
 
+int systec_plan_ttm(systec_plan plan, const float *B, int R, float *C_packed, systec_stream_t stream) {
+    Plan *p = reinterpret_cast<Plan *>(plan);
+    if (!p || !B || !C_packed || R < 1) return SYSTEC_ERR_ARG;
+    if (p->order != 3) return SYSTEC_ERR_UNSUPPORTED;
+    const size_t rows = p->general ? static_cast<size_t>(p->dim) * p->dim : static_cast<size_t>(systec::ttm_packed_rows(p->dim));
+    const size_t cb = rows * R * 4;
+    if (systec::overlap(B, static_cast<size_t>(p->dim) * R * 4, C_packed, cb)) return SYSTEC_ERR_ALIAS;
+    cudaError_t e = systec::launch_ttm(*p, B, R, C_packed, reinterpret_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? SYSTEC_OK : systec::cuda_fail(e);
+}
+
+int systec_ttm_unpack(int64_t dim, int R, const float *C_packed, float *C_full, systec_stream_t stream) {
+    if (dim < 1 || R < 1 || !C_packed || !C_full) return SYSTEC_ERR_ARG;
+    if (systec::overlap(C_packed, static_cast<size_t>(systec::ttm_packed_rows(dim)) * R * 4, C_full,
+                        static_cast<size_t>(dim) * dim * R * 4))
+        return SYSTEC_ERR_ALIAS;
+    cudaError_t e = systec::launch_ttm_unpack(dim, R, C_packed, C_full, reinterpret_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? SYSTEC_OK : systec::cuda_fail(e);
+}
+
 int systec_plan_execute(systec_plan plan, const float *B, int R, float *C, systec_stream_t stream) {
     return systec::execute_impl(reinterpret_cast<Plan *>(plan), B, R, C, nullptr,
                                 reinterpret_cast<cudaStream_t>(stream));

@@ -66,6 +66,11 @@ cudaError_t cpd_tensor_norm2(const Plan &p, double *out, cudaStream_t s);
 cudaError_t cpd_step(const Plan &p, const float *M, float *B, float *lam, int R, double *dscratch,
                      float *fscratch, bool have_lam, bool fit_only, cudaStream_t s);
 
+// ttm.cu
+int64_t ttm_packed_rows(int64_t dim);
+cudaError_t launch_ttm(const Plan &p, const float *B, int R, float *Cp, cudaStream_t s);
+cudaError_t launch_ttm_unpack(int64_t dim, int R, const float *Cp, float *C, cudaStream_t s);
+
 // mttkrp.cu
 cudaError_t launch_mttkrp(Plan &p, const float *B, int R, float *C, const systec_exec_opts &o,
                           cudaStream_t s);

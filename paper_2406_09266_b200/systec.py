@@ -39,7 +39,7 @@ EXPORTS = ["systec_mttkrp", "systec_mttkrp_host", "systec_plan_create", "systec_
            "systec_plan_copy_prepared", "systec_plan_last_launch", "systec_plan_destroy",
            "systec_status_string", "systec_last_cuda_error", "systec_version", "systec_last_bad_entry",
            "systec_plan_create_general", "systec_expand_symmetric", "systec_plan_minplus",
-           "systec_cp_als_sym"]
+           "systec_cp_als_sym", "systec_plan_ttm", "systec_ttm_unpack"]
 
 _lib = None
 
@@ -61,6 +61,8 @@ def load(path: str | None = None):
     lib.systec_plan_execute.argtypes = [vp, vp, i32, vp, vp]
     lib.systec_plan_create_general.argtypes = [ctypes.POINTER(vp), i32, i64, i64, vp, vp, vp]
     lib.systec_plan_minplus.argtypes = [vp, vp, vp, vp]
+    lib.systec_plan_ttm.argtypes = [vp, vp, i32, vp, vp]
+    lib.systec_ttm_unpack.argtypes = [i64, i32, vp, vp, vp]
     lib.systec_cp_als_sym.argtypes = [vp, vp, i32, vp, i32, ctypes.c_double, vp, ctypes.POINTER(i32), vp]
     lib.systec_expand_symmetric.argtypes = [i32, i64, i64, vp, vp, i64, vp, vp, ctypes.POINTER(i64), vp]
     lib.systec_plan_execute_ex.argtypes = [vp, vp, i32, vp, ctypes.POINTER(SystecExecOpts), vp]
@@ -201,6 +203,24 @@ class Plan:
                                         max_iters, tol, fits.ctypes.data_as(ctypes.c_void_p), ctypes.byref(done),
                                         _stream_handle(stream)), "systec_cp_als_sym")
         return B, lam, fits[:done.value]
+
+    def ttm(self, B, packed=None, full: bool = False, stream=None):
+        """``systec_plan_ttm`` (order-3 plans): packed canonical half
+        [dim(dim+1)/2][R]; with full=True also ``systec_ttm_unpack`` -> [dim][dim][R]."""
+        import torch
+        R = int(B.shape[1])
+        rows = self.dim * self.dim if getattr(self, "general", False) else self.dim * (self.dim + 1) // 2
+        if packed is None:
+            packed = torch.empty((rows, R), dtype=torch.float32, device=B.device)
+        s = _stream_handle(stream)
+        _check(load().systec_plan_ttm(self._h, _dev(B, torch.float32, "B"), R, _dev(packed, torch.float32, "C"), s),
+               "systec_plan_ttm")
+        if not full or getattr(self, "general", False):
+            return packed
+        Cf = torch.empty((self.dim, self.dim, R), dtype=torch.float32, device=B.device)
+        _check(load().systec_ttm_unpack(self.dim, R, ctypes.c_void_p(packed.data_ptr()),
+                                        ctypes.c_void_p(Cf.data_ptr()), s), "systec_ttm_unpack")
+        return Cf
 
     def stats(self) -> dict:
         st = SystecStats()

@@ -385,3 +385,30 @@ def test_cp_als_recovers_planted_and_stops_early(systec):
     match = np.abs(B.cpu().numpy().T @ Bt)
     assert np.all(match.max(axis=1) > 0.999)
     np.testing.assert_allclose(np.sort(lam_g.cpu().numpy()), np.sort(lam), rtol=1e-3)
+
+
+# ---------------------------------------------------------------- NEXT-4: symmetric TTM
+@pytest.mark.parametrize("dim,nnz,R", [(30, 2000, 16), (64, 20000, 8), (20, 500, 3), (100, 50000, 32)])
+def test_ttm_matches_oracle(systec, dim, nnz, R):
+    import torch
+    w = small_random(3, dim, nnz, R, seed=dim, diag_frac=0.2)
+    want = oracle.ttm_sym3(dim, w.idx, w.vals, w.B)
+    S = oracle.ttm_sym3(dim, w.idx, np.abs(w.vals), np.abs(w.B))   # sum of |terms|
+    di, dv, dB = to_dev(w.idx, w.vals, w.B)
+    plan = systec.Plan(3, dim, di, dv)
+    Cf = plan.ttm(dB, full=True)
+    torch.cuda.synchronize()
+    parity(Cf.cpu().numpy(), want, S)
+
+
+def test_ttm_general_plan_on_expansion(systec):
+    import torch
+    w = small_random(3, 40, 5000, 8, seed=4, diag_frac=0.2)
+    want = oracle.ttm_sym3(40, w.idx, w.vals, w.B)
+    S = oracle.ttm_sym3(40, w.idx, np.abs(w.vals), np.abs(w.B))
+    di, dv, dB = to_dev(w.idx, w.vals, w.B)
+    ei, ev = systec.expand_symmetric(3, 40, di, dv)
+    gplan = systec.plan_create_general(3, 40, ei, ev)
+    Cf = gplan.ttm(dB).view(40, 40, 8)
+    torch.cuda.synchronize()
+    parity(Cf.cpu().numpy(), want, S)

@@ -381,3 +381,14 @@ def test_cpd_oracle_recovers_planted(order, dim, R):
     match = np.abs(B.T @ Bt)
     assert np.all(match.max(axis=1) > 0.999)
     assert np.allclose(np.sort(lam_got), np.sort(lam), rtol=1e-3)
+
+
+# ---------------------------------------------------------------- TTM oracle (NEXT-4)
+def test_ttm_oracle_vs_einsum():
+    w = small_random(3, 9, 120, 4, seed=31, diag_frac=0.3)
+    si, sv = scramble(w.idx, w.vals, seed=3)
+    A = dense_from_entries(3, 9, si, sv)
+    want = np.einsum("kjl,ki->jli", A, w.B.astype(np.float64))     # C[j][l][i]
+    got = oracle.ttm_sym3(9, si, sv, w.B)
+    np.testing.assert_allclose(got, want, rtol=1e-12, atol=1e-12)
+    assert np.allclose(got, got.transpose(1, 0, 2))                   # visible output symmetry
