@@ -6,6 +6,8 @@
 #include <cmath>
 #include <cstring>
 #include <new>
+#include <vector>
+#include <algorithm>
 
 #include "internal.cuh"
 
@@ -421,6 +423,123 @@ int systec_mttkrp(int order, int64_t dim, int64_t nnz, const int32_t *idx, const
     return rc;
 }
 
+namespace systec {
+namespace {
+
+cudaStream_t copy_stream() {
+    static cudaStream_t cs = nullptr;  // one non-blocking stream for host->device copies
+    if (!cs) cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
+    return cs;
+}
+
+// Pipelined end-to-end call: chunk k's host->device copy (copy stream) overlaps
+// chunk k-1's validate/canonicalise/gather/execute (caller's stream).  Chunks
+// are contiguous and independent (MTTKRP is linear in A), so each one is
+// executed into C as it lands; the sort is skipped (lexicographic input stays
+// sorted per chunk; any other order is still correct, only with shorter runs).
+// Position-1 accumulation is decided from chunk 0's statistics (one sync).
+int mttkrp_host_pipelined(int order, int64_t dim, int64_t nnz, int bits, const int32_t *idx_host,
+                          const float *vals_host, const float *B_host, int R, float *C_host, cudaStream_t s) {
+    const int64_t per = std::max<int64_t>(4, ((nnz + 7) / 8 + 3) & ~int64_t(3));  // 8 chunks, 16-byte aligned
+    const int nch = static_cast<int>((nnz + per - 1) / per);
+    const int64_t ld = ((nnz + 3) & ~int64_t(3)) + 4;
+    const size_t ib = static_cast<size_t>(nnz) * order * 4, vb = static_cast<size_t>(nnz) * 4;
+    const size_t bb = static_cast<size_t>(dim) * R * 4;
+    auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+    const size_t soa = static_cast<size_t>(order + 1) * ld * 4;
+    const size_t kb = static_cast<size_t>(per) * 8, pb = static_cast<size_t>(per) * 4;
+    const size_t total = al(ib) + al(vb) + 2 * al(bb) + al(soa) + al(kb) + al(pb) + al(sizeof(DevStats));
+    char *buf = nullptr;
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void **>(&buf), total, s);
+    if (e != cudaSuccess) return cuda_fail(e);
+    char *q = buf;
+    auto take = [&](size_t x) { char *r = q; q += al(x); return r; };
+    int32_t *d_idx = reinterpret_cast<int32_t *>(take(ib));
+    float *d_vals = reinterpret_cast<float *>(take(vb));
+    float *d_B = reinterpret_cast<float *>(take(bb));
+    float *d_C = reinterpret_cast<float *>(take(bb));
+    int32_t *coords = reinterpret_cast<int32_t *>(take(soa));
+    float *svals = reinterpret_cast<float *>(coords + static_cast<size_t>(order) * ld);
+    unsigned long long *keys = reinterpret_cast<unsigned long long *>(take(kb));
+    uint32_t *perm = reinterpret_cast<uint32_t *>(take(pb));
+    DevStats *dst = reinterpret_cast<DevStats *>(take(sizeof(DevStats)));
+    DevStats hst;
+    std::memset(&hst, 0, sizeof(hst));
+    hst.bad_entry = ULLONG_MAX;
+    cudaStream_t cs = copy_stream();
+    std::vector<cudaEvent_t> ev(nch + 2, nullptr);
+    int rc = SYSTEC_OK;
+    do {
+        for (auto &x : ev)
+            if ((e = cudaEventCreateWithFlags(&x, cudaEventDisableTiming)) != cudaSuccess) break;
+        if (e != cudaSuccess) break;
+        if ((e = cudaMemcpyAsync(dst, &hst, sizeof(hst), cudaMemcpyHostToDevice, s)) != cudaSuccess) break;
+        if ((e = cudaMemsetAsync(d_C, 0, bb, s)) != cudaSuccess) break;
+        if ((e = cudaEventRecord(ev[nch + 1], s)) != cudaSuccess) break;          // buffers exist
+        if ((e = cudaStreamWaitEvent(cs, ev[nch + 1], 0)) != cudaSuccess) break;
+        if ((e = cudaMemcpyAsync(d_B, B_host, bb, cudaMemcpyHostToDevice, cs)) != cudaSuccess) break;
+        if ((e = cudaEventRecord(ev[nch], cs)) != cudaSuccess) break;
+        for (int k = 0; k < nch && e == cudaSuccess; ++k) {
+            const int64_t lo = k * per, n = std::min(per, nnz - lo);
+            if ((e = cudaMemcpyAsync(d_idx + lo * order, idx_host + lo * order, n * order * 4, cudaMemcpyHostToDevice, cs)) != cudaSuccess) break;
+            if ((e = cudaMemcpyAsync(d_vals + lo, vals_host + lo, n * 4, cudaMemcpyHostToDevice, cs)) != cudaSuccess) break;
+            e = cudaEventRecord(ev[k], cs);
+        }
+        if (e != cudaSuccess) break;
+        if ((e = cudaStreamWaitEvent(s, ev[nch], 0)) != cudaSuccess) break;        // B landed
+        systec_exec_opts o;
+        std::memset(&o, 0, sizeof(o));
+        o.no_zero = 1;
+        for (int k = 0; k < nch; ++k) {
+            const int64_t lo = k * per, n = std::min(per, nnz - lo);
+            if ((e = cudaStreamWaitEvent(s, ev[k], 0)) != cudaSuccess) break;
+            if ((e = launch_canonicalize(order, dim, n, bits, d_idx + lo * order, keys, perm, dst, s, true, lo)) != cudaSuccess)
+                break;
+            if ((e = launch_gather_range(order, n, ld, bits, keys, d_vals + lo, coords + lo, svals + lo, s)) != cudaSuccess) break;
+            if (k == 0) {  // chunk-0 statistics decide position-1 accumulation (one sync)
+                if ((e = launch_stats(order, n, ld, coords, dst, s)) != cudaSuccess) break;
+                if ((e = cudaMemcpyAsync(&hst, dst, sizeof(hst), cudaMemcpyDeviceToHost, s)) != cudaSuccess) break;
+                if ((e = cudaStreamSynchronize(s)) != cudaSuccess) break;
+                if (hst.err) break;
+                o.pos1_accumulate = (hst.pos1_runs > 0 && static_cast<double>(n) / hst.pos1_runs >= 1.5) ? 1 : -1;
+            }
+            Plan pk;
+            pk.order = order;
+            pk.dim = dim;
+            pk.nnz = n;
+            pk.ld = ld;
+            pk.key_bits = bits;
+            pk.coords = coords + lo;
+            pk.vals = svals + lo;
+            pk.stream = s;
+            if ((e = launch_mttkrp(pk, d_B, R, d_C, o, s)) != cudaSuccess) break;
+        }
+        if (e != cudaSuccess) break;
+        if (hst.err) {
+            g_last_bad_entry = static_cast<int64_t>(hst.bad_entry);
+            rc = SYSTEC_ERR_INDEX;
+            break;
+        }
+        if ((e = cudaMemcpyAsync(&hst, dst, sizeof(hst), cudaMemcpyDeviceToHost, s)) != cudaSuccess) break;
+        if ((e = cudaMemcpyAsync(C_host, d_C, bb, cudaMemcpyDeviceToHost, s)) != cudaSuccess) break;
+        if ((e = cudaStreamSynchronize(s)) != cudaSuccess) break;
+        if (hst.err) {  // a later chunk held a bad index: C is not valid
+            g_last_bad_entry = static_cast<int64_t>(hst.bad_entry);
+            rc = SYSTEC_ERR_INDEX;
+        }
+    } while (false);
+    cudaStreamSynchronize(cs);
+    cudaFreeAsync(buf, s);
+    for (auto &x : ev)
+        if (x) cudaEventDestroy(x);
+    if (e != cudaSuccess) return cuda_fail(e);
+    if (rc == SYSTEC_OK && (e = cudaStreamSynchronize(s)) != cudaSuccess) return cuda_fail(e);
+    return rc;
+}
+
+}  // namespace
+}  // namespace systec
+
 int systec_mttkrp_host(int order, int64_t dim, int64_t nnz, const int32_t *idx_host, const float *vals_host,
                        const float *B_host, int R, float *C_host, systec_stream_t stream) {
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
@@ -429,6 +548,7 @@ int systec_mttkrp_host(int order, int64_t dim, int64_t nnz, const int32_t *idx_h
     if (rc) return rc;
     if (!B_host || !C_host || R < 1 || (nnz > 0 && (!idx_host || !vals_host))) return SYSTEC_ERR_ARG;
     systec::ensure_pool_keeps_memory();
+    if (nnz >= (1 << 20)) return systec::mttkrp_host_pipelined(order, dim, nnz, bits, idx_host, vals_host, B_host, R, C_host, s);
     const size_t ib = static_cast<size_t>(nnz) * order * 4, vb = static_cast<size_t>(nnz) * 4;
     const size_t bb = static_cast<size_t>(dim) * R * 4;
     char *buf = nullptr;

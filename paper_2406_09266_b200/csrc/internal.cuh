@@ -42,7 +42,7 @@ struct DevStats {
 // prepare.cu
 cudaError_t launch_canonicalize(int order, int64_t dim, int64_t nnz, int bits, const int32_t *idx,
                                 unsigned long long *keys, uint32_t *perm, DevStats *st,
-                                cudaStream_t s, bool canonicalise = true);
+                                cudaStream_t s, bool canonicalise = true, int64_t e_offset = 0);
 cudaError_t sort_keys(int64_t nnz, int end_bit, unsigned long long *keys_in, unsigned long long *keys_out,
                       uint32_t *perm_in, uint32_t *perm_out, cudaStream_t s, bool pooled);
 cudaError_t launch_gather(int order, int64_t nnz, int64_t ld, int bits, const unsigned long long *keys,
@@ -50,6 +50,8 @@ cudaError_t launch_gather(int order, int64_t nnz, int64_t ld, int bits, const un
                           int32_t *coords, float *vals_out, cudaStream_t s);
 cudaError_t launch_stats(int order, int64_t nnz, int64_t ld, const int32_t *coords, DevStats *st,
                          cudaStream_t s);
+cudaError_t launch_gather_range(int order, int64_t n, int64_t ld, int bits, const unsigned long long *keys,
+                                const float *vals_in, int32_t *coords, float *vals_out, cudaStream_t s);
 
 // expand.cu
 cudaError_t expand_count(int order, int64_t dim, int64_t nnz, const int32_t *idx, unsigned long long *sizes,

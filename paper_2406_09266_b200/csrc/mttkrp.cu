@@ -59,7 +59,7 @@ KernelFn pick_ablation_kernel(int order, int abl) {
 }
 
 __global__ void reduce_copies_kernel(const float *__restrict__ Cp, float *__restrict__ C, int64_t plane, int copies,
-                                     int vec) {
+                                     int vec, int accumulate) {
     const int64_t n4 = vec ? plane / 4 : 0;
     const float4 *P4 = reinterpret_cast<const float4 *>(Cp);
     float4 *C4 = reinterpret_cast<float4 *>(C);
@@ -69,11 +69,15 @@ __global__ void reduce_copies_kernel(const float *__restrict__ Cp, float *__rest
             const float4 b = P4[c * n4 + i];
             a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
         }
+        if (accumulate) {
+            const float4 c = C4[i];
+            a.x += c.x; a.y += c.y; a.z += c.z; a.w += c.w;
+        }
         C4[i] = a;
     }
     for (int64_t i = 4 * n4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < plane;
          i += (int64_t)gridDim.x * blockDim.x) {
-        float a = 0.f;
+        float a = accumulate ? C[i] : 0.f;
         for (int c = 0; c < copies; ++c) a += Cp[c * plane + i];
         C[i] = a;
     }
@@ -92,7 +96,6 @@ cudaError_t launch_mttkrp(Plan &p, const float *B, int R, float *C, const systec
         if (p.nnz < 100000) copies = 1;  // latency-bound sizes: not worth the extra pass
     }
     if (copies > 64) return cudaErrorInvalidValue;
-    if (o.no_zero && copies > 1) copies = 1;  // accumulate-into-C mode reduces in place
     float *Cdst = C;
     float *scratch = nullptr;
     if (copies > 1) {
@@ -108,7 +111,7 @@ cudaError_t launch_mttkrp(Plan &p, const float *B, int R, float *C, const systec
     if (p.nnz == 0) {
         if (scratch) {
             cudaFreeAsync(scratch, s);
-            return cudaMemsetAsync(C, 0, static_cast<size_t>(plane) * sizeof(float), s);
+            return o.no_zero ? cudaSuccess : cudaMemsetAsync(C, 0, static_cast<size_t>(plane) * sizeof(float), s);
         }
         return cudaSuccess;
     }
@@ -200,7 +203,7 @@ cudaError_t launch_mttkrp(Plan &p, const float *B, int R, float *C, const systec
         const int64_t work = std::max<int64_t>(1, plane / 4);
         const int rb = static_cast<int>(std::min<int64_t>((work + 255) / 256, static_cast<int64_t>(sms) * 4));
         const int vec = (reinterpret_cast<uintptr_t>(C) % 16 == 0) && (plane % 4 == 0);
-        reduce_copies_kernel<<<rb, 256, 0, s>>>(scratch, C, plane, copies, vec);
+        reduce_copies_kernel<<<rb, 256, 0, s>>>(scratch, C, plane, copies, vec, o.no_zero ? 1 : 0);
         cudaFreeAsync(scratch, s);
     }
     p.last_grid_x = static_cast<int>(blocks);

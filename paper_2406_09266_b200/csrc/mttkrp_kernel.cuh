@@ -351,29 +351,35 @@ __global__ void __launch_bounds__(256) mttkrp_sym_kernel(const KParams p) {
             cur1 = -1;
         }
 
-        // segmented reduction of the groups' pending position-0 sums
-        // (keys are non-decreasing in g; empty tail groups carry key -1)
+        // segmented suffix reduction of the groups' pending position-0 sums over
+        // maximal runs of equal keys (sorted input: keys non-decreasing in g;
+        // any order stays correct because a segment stops at every key change);
+        // empty tail groups carry key -1
         const int key = cur0;
+        const int next_key = __shfl_down_sync(0xffffffffu, key, LPE);
+        bool ends = (g == E - 1) || next_key != key;  // my segment ends within [g, g + covered)
 #pragma unroll
         for (int d = 1; d < E; d <<= 1) {
-            const int ok = __shfl_down_sync(0xffffffffu, key, d * LPE);
-            const bool take = (g + d < E) && ok == key;
+            const bool o_ends = __shfl_down_sync(0xffffffffu, ends, d * LPE);
+            const bool take = (g + d < E) && !ends;
 #pragma unroll
             for (int q = 0; q < VPL; ++q) {
                 const T o = V::shfl_down(acc0[q], d * LPE);
                 if (take) acc0[q] = V::add(acc0[q], o);
             }
+            if (take) ends = o_ends;
         }
         const int prev_key = __shfl_up_sync(0xffffffffu, key, LPE);
         const bool head = (g == 0) || (prev_key != key);
         const int last_key = __shfl_sync(0xffffffffu, key, (E - 1) * LPE);
+        // the last segment (the one containing group E-1) starts at the highest head
+        const unsigned heads = __ballot_sync(0xffffffffu, head && j == 0);
+        const int hl = 31 - __clz(heads);  // lane (j == 0) of the last segment's head
         const bool carry = (k + 1 < nch);  // chunk was full: the next chunk continues the stream
-        const bool write = head && key >= 0 && !(carry && key == last_key);
+        const bool write = head && key >= 0 && !(carry && lane - j == hl);
 #pragma unroll
         for (int q = 0; q < VPL; ++q) V::red_if(rowC(key, q), acc0[q], write && act[q]);
         if (carry) {
-            const unsigned heads = __ballot_sync(0xffffffffu, head && j == 0 && key == last_key);
-            const int hl = __ffs(heads) - 1;  // lane of the last segment's head (j == 0)
 #pragma unroll
             for (int q = 0; q < VPL; ++q) {
                 const T carried = V::shfl(acc0[q], hl + j);
@@ -388,9 +394,10 @@ __global__ void __launch_bounds__(256) mttkrp_sym_kernel(const KParams p) {
     }
 }
 
-// Sum `copies` replicas Cp[copies][plane] into C[plane] (float4 when aligned).
+// Sum `copies` replicas Cp[copies][plane] into C[plane] (float4 when aligned);
+// accumulate != 0 adds them to C's current contents (no_zero executes).
 __global__ void reduce_copies_kernel(const float *__restrict__ Cp, float *__restrict__ C, int64_t plane, int copies,
-                                     int vec);
+                                     int vec, int accumulate);
 
 // instantiation tables, one translation unit per order (mttkrp_n{2..5}.cu)
 template <int N> KernelFn pick_kernel(int vw, int lpe, int vpl, bool pos1, bool pf);

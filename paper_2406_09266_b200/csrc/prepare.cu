@@ -53,14 +53,14 @@ __device__ __forceinline__ bool load_canonical(const int32_t *idx, int64_t e, in
 template <int N, bool CANON>
 __global__ void canonicalize_kernel(const int32_t *__restrict__ idx, int64_t nnz, int64_t dim, int bits,
                                     unsigned long long *__restrict__ keys, uint32_t *__restrict__ perm,
-                                    DevStats *st) {
+                                    DevStats *st, int64_t e_offset) {
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz;
          e += (int64_t)gridDim.x * blockDim.x) {
         int32_t c[N];
         const bool ok = load_canonical<N, CANON>(idx, e, dim, c);
         if (!ok) {
             atomicOr(&st->err, 1ull);
-            atomicMin(&st->bad_entry, static_cast<unsigned long long>(e));
+            atomicMin(&st->bad_entry, static_cast<unsigned long long>(e + e_offset));
             keys[e] = 0;
             perm[e] = static_cast<uint32_t>(e);
             continue;
@@ -95,6 +95,23 @@ __global__ void gather_kernel(int64_t nnz, int64_t ld, int bits, const unsigned 
             for (int t = 0; t < N; ++t) coords[t * ld + e] = 0;
             vals_out[e] = 0.0f;
         }
+    }
+}
+
+// chunk form for the pipelined host path: n entries, no permutation, no padding
+template <int N>
+__global__ void gather_range_kernel(int64_t n, int64_t ld, int bits, const unsigned long long *__restrict__ keys,
+                                    const float *__restrict__ vals_in, int32_t *__restrict__ coords,
+                                    float *__restrict__ vals_out) {
+    const unsigned long long mask = (bits >= 64) ? ~0ull : ((1ull << bits) - 1ull);
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+        unsigned long long k = keys[e];
+#pragma unroll
+        for (int t = N - 1; t >= 0; --t) {
+            coords[t * ld + e] = static_cast<int32_t>(k & mask);
+            k >>= bits;
+        }
+        vals_out[e] = vals_in[e];
     }
 }
 
@@ -200,13 +217,13 @@ int grid_for(int64_t n, int threads) {
 
 cudaError_t launch_canonicalize(int order, int64_t dim, int64_t nnz, int bits, const int32_t *idx,
                                 unsigned long long *keys, uint32_t *perm, DevStats *st, cudaStream_t s,
-                                bool canonicalise) {
+                                bool canonicalise, int64_t e_offset) {
     if (nnz == 0) return cudaSuccess;
     const int th = 256;
     if (canonicalise) {
-        SYSTEC_ORDER_SWITCH(order, canonicalize_kernel<N, true><<<grid_for(nnz, th), th, 0, s>>>(idx, nnz, dim, bits, keys, perm, st));
+        SYSTEC_ORDER_SWITCH(order, canonicalize_kernel<N, true><<<grid_for(nnz, th), th, 0, s>>>(idx, nnz, dim, bits, keys, perm, st, e_offset));
     } else {
-        SYSTEC_ORDER_SWITCH(order, canonicalize_kernel<N, false><<<grid_for(nnz, th), th, 0, s>>>(idx, nnz, dim, bits, keys, perm, st));
+        SYSTEC_ORDER_SWITCH(order, canonicalize_kernel<N, false><<<grid_for(nnz, th), th, 0, s>>>(idx, nnz, dim, bits, keys, perm, st, e_offset));
     }
     return cudaGetLastError();
 }
@@ -233,6 +250,14 @@ cudaError_t launch_gather(int order, int64_t nnz, int64_t ld, int bits, const un
     if (ld == 0) return cudaSuccess;
     const int th = 256;
     SYSTEC_ORDER_SWITCH(order, gather_kernel<N><<<grid_for(ld, th), th, 0, s>>>(nnz, ld, bits, keys, perm, vals_in, coords, vals_out));
+    return cudaGetLastError();
+}
+
+cudaError_t launch_gather_range(int order, int64_t n, int64_t ld, int bits, const unsigned long long *keys,
+                                const float *vals_in, int32_t *coords, float *vals_out, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    const int th = 256;
+    SYSTEC_ORDER_SWITCH(order, gather_range_kernel<N><<<grid_for(n, th), th, 0, s>>>(n, ld, bits, keys, vals_in, coords, vals_out));
     return cudaGetLastError();
 }
 

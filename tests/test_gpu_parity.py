@@ -412,3 +412,25 @@ def test_ttm_general_plan_on_expansion(systec):
     Cf = gplan.ttm(dB).view(40, 40, 8)
     torch.cuda.synchronize()
     parity(Cf.cpu().numpy(), want, S)
+
+
+# ---------------------------------------------------------------- pipelined host-buffer path (nnz >= 2^20)
+@pytest.mark.parametrize("n,dim,nnz,R,shuffle", [(3, 20000, 1_300_001, 16, False), (5, 60, 1_100_000, 16, False),
+                                                 (4, 200, 1_050_000, 8, True)])
+def test_host_call_pipelined(systec, n, dim, nnz, R, shuffle):
+    import torch
+    w = make(f"pipe{n}", n, dim, nnz, R, seed=n, mode="uniform")
+    idx, vals = (scramble(w.idx, w.vals, seed=1) if shuffle else (w.idx, w.vals))
+    rows = np.unique(np.concatenate([w.idx[:50, 0], w.idx[-50:, -1], np.arange(0, dim, max(1, dim // 40))]))
+    Cref, S = oracle.mttkrp_rows(n, dim, w.idx, w.vals, w.B, rows)
+    pin = [torch.from_numpy(np.ascontiguousarray(a)).pin_memory() for a in (idx, vals, w.B)]
+    Cp = torch.empty((dim, R), dtype=torch.float32).pin_memory()
+    systec.mttkrp_host(n, dim, *pin, C=Cp)
+    parity(Cp.numpy()[rows], Cref, S)
+    # same result through the device plan
+    parity(run(systec, w)[rows], Cref, S)
+    # a bad index in the last chunk is reported
+    bad = np.ascontiguousarray(idx).copy()
+    bad[nnz - 3, 0] = dim
+    with pytest.raises(IndexError, match=f"first bad entry {nnz - 3}"):
+        systec.mttkrp_host(n, dim, bad, vals, w.B)
