@@ -94,7 +94,9 @@ typedef struct systec_exec_opts {
      * reserved[4] copies: replicas of C for L2-slice spreading, 1 = off, 0 = auto
      *             (outputs < 4 MB and nnz >= 1e5: up to 32 replicas)
      * reserved[5] ablation bits (evidence study; c2/c5 kernel shapes only):
-     *             1 = no shared-memory staging, 2 = no position-0 accumulation */
+     *             1 = no shared-memory staging, 2 = no position-0 accumulation
+     * reserved[7] occupancy: order-3 R=32 kernel compiled for 5 blocks/SM;
+     *             1 on, -1 off, 0 auto (on when B > 64 MB)                  */
     int32_t reserved[10];
 } systec_exec_opts;
 

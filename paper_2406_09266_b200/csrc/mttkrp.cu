@@ -149,6 +149,14 @@ cudaError_t launch_mttkrp(Plan &p, const float *B, int R, float *C, const systec
     // in-flight gathers gain.
     const bool pf = o.reserved[3] > 0;
     KernelFn fn = p.general ? pick_naive(p.order, vw, lpe, pf) : pick(p.order, vw, lpe, vpl, pos1, pf);
+    // occupancy variant: 5 resident blocks (48 registers) for the order-3 R=32
+    // kernel when B is too large to stay L2-resident, so gathers wait on DRAM
+    // and more warps in flight pay (c3: 2.65 -> 2.40 ms; c2 with its 12.8 MB
+    // B is L2-resident and loses 2 %).  reserved[7]: 1 on, -1 off, 0 auto.
+    const bool occ_shape = vw == 4 && vpl == 1 && !pf && !p.general &&
+                           ((p.order == 3 && lpe == 8) || (p.order >= 4 && lpe == 4));
+    const bool occ5 = occ_shape && (o.reserved[7] > 0 || (o.reserved[7] == 0 && p.order == 3 && plane * 4 > (64ll << 20)));
+    if (occ5) fn = p.order == 3 ? occupancy3(pos1) : p.order == 4 ? occupancy4(pos1) : occupancy5(pos1);
     const int abl = o.reserved[5];
     if (abl > 0) {  // ablation study: only the c2 / c5 kernel shapes exist
         const bool shape3 = p.order == 3 && vw == 4 && lpe == 8 && vpl == 1 && !pos1 && !pf && !p.general;
@@ -210,8 +218,9 @@ cudaError_t launch_mttkrp(Plan &p, const float *B, int R, float *C, const systec
     p.last_grid_y = tiles;
     p.last_block = threads;
     p.last_smem = static_cast<int>(smem);
-    // kernel id, decimal fields: general | copies (2 digits) | pf | order | vw | lpe (2 digits) | vpl | pos1
-    p.last_kernel = (p.general ? 1000000000 : 0) + copies * 10000000 + (pf ? 1000000 : 0) + p.order * 100000 + vw * 10000 + lpe * 100 + vpl * 10 + (pos1 ? 1 : 0);
+    // kernel id, decimal fields: general | copies (2 digits) | pf | order | vw | lpe (2 digits) | vpl | pos1;
+    // the occupancy variant sets vpl's digit to 5 (vpl itself is 1 there)
+    p.last_kernel = (p.general ? 1000000000 : 0) + copies * 10000000 + (pf ? 1000000 : 0) + p.order * 100000 + vw * 10000 + lpe * 100 + (occ5 ? 5 : vpl) * 10 + (pos1 ? 1 : 0);
     return cudaGetLastError();
 }
 

@@ -111,8 +111,8 @@ __device__ __forceinline__ uint64_t row_off(int32_t c, uint32_t R) {
 // ABL (ablations for the evidence table, instantiated for the c2/c5 shapes only):
 //   bit 0: no shared-memory staging (indices and values read with plain loads)
 //   bit 1: no position-0 run accumulation (one reduction per entry)
-template <int N, int LPE, int VPL, int VW, bool POS1, bool PF, bool NAIVE = false, int ABL = 0>
-__global__ void __launch_bounds__(256) mttkrp_sym_kernel(const KParams p) {
+template <int N, int LPE, int VPL, int VW, bool POS1, bool PF, bool NAIVE, int ABL>
+__device__ __forceinline__ void mttkrp_sym_body(const KParams &p) {
     using V = VecT<VW>;
     using T = typename V::T;
     constexpr int E = 32 / LPE;          // lane groups (entries in flight) per warp
@@ -394,6 +394,20 @@ __global__ void __launch_bounds__(256) mttkrp_sym_kernel(const KParams p) {
     }
 }
 
+template <int N, int LPE, int VPL, int VW, bool POS1, bool PF, bool NAIVE = false, int ABL = 0>
+__global__ void __launch_bounds__(256) mttkrp_sym_kernel(const KParams p) {
+    mttkrp_sym_body<N, LPE, VPL, VW, POS1, PF, NAIVE, ABL>(p);
+}
+
+// occupancy variant: ask ptxas for MINB resident 256-thread blocks per SM
+// (<= 65536 / (MINB*256) registers) — for gather-latency-bound inputs.  A
+// separate kernel because __launch_bounds__(256, 1) is not the same request
+// as __launch_bounds__(256) (ptxas then spends registers more freely).
+template <int N, int LPE, int VPL, int VW, bool POS1, int MINB>
+__global__ void __launch_bounds__(256, MINB) mttkrp_sym_kernel_occ(const KParams p) {
+    mttkrp_sym_body<N, LPE, VPL, VW, POS1, false, false, 0>(p);
+}
+
 // Sum `copies` replicas Cp[copies][plane] into C[plane] (float4 when aligned);
 // accumulate != 0 adds them to C's current contents (no_zero executes).
 __global__ void reduce_copies_kernel(const float *__restrict__ Cp, float *__restrict__ C, int64_t plane, int copies,
@@ -407,6 +421,11 @@ template <> KernelFn pick_kernel<4>(int vw, int lpe, int vpl, bool pos1, bool pf
 template <> KernelFn pick_kernel<5>(int vw, int lpe, int vpl, bool pos1, bool pf);
 // ablation variants (abl bits above) of the c2 kernel <3,8,1,4,false,false> and c5 kernel <5,4,1,4,true,false>
 KernelFn pick_ablation_kernel(int order, int abl);
+// occupancy variants (more resident blocks, fewer registers): order 3 at R=32
+// (<3,8,1,4,pos1>, 5 blocks/SM), orders 4 and 5 at R=16 (<n,4,1,4,pos1>, 4 blocks/SM)
+KernelFn occupancy3(bool pos1);
+KernelFn occupancy4(bool pos1);
+KernelFn occupancy5(bool pos1);
 // the non-symmetric (expanded-tensor) baseline: position 0 only, one float4/float per lane
 template <int N> KernelFn pick_naive_kernel(int vw, int lpe, bool pf);
 template <> KernelFn pick_naive_kernel<2>(int vw, int lpe, bool pf);

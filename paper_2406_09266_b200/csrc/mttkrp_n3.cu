@@ -73,6 +73,10 @@ KernelFn pick_naive_kernel<3>(int vw, int lpe, bool pf) {
     }
 }
 
+KernelFn occupancy3(bool pos1) {
+    return pos1 ? mttkrp_sym_kernel_occ<3, 8, 1, 4, true, 5> : mttkrp_sym_kernel_occ<3, 8, 1, 4, false, 5>;
+}
+
 KernelFn ablation3(int abl) {
     switch (abl) {
         case 1: return mttkrp_sym_kernel<3, 8, 1, 4, false, false, false, 1>;

@@ -73,4 +73,8 @@ KernelFn pick_naive_kernel<4>(int vw, int lpe, bool pf) {
     }
 }
 
+KernelFn occupancy4(bool pos1) {
+    return pos1 ? mttkrp_sym_kernel_occ<4, 4, 1, 4, true, 4> : mttkrp_sym_kernel_occ<4, 4, 1, 4, false, 4>;
+}
+
 }  // namespace systec

@@ -82,4 +82,8 @@ KernelFn ablation5(int abl) {
     }
 }
 
+KernelFn occupancy5(bool pos1) {
+    return pos1 ? mttkrp_sym_kernel_occ<5, 4, 1, 4, true, 4> : mttkrp_sym_kernel_occ<5, 4, 1, 4, false, 4>;
+}
+
 }  // namespace systec

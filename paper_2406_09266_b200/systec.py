@@ -133,6 +133,8 @@ def _opts(**kw) -> SystecExecOpts:
             o.reserved[4] = int(v)
         elif k == "ablation":
             o.reserved[5] = int(v)
+        elif k == "occupancy":
+            o.reserved[7] = int(v)
         else:
             setattr(o, k, int(v))
     return o

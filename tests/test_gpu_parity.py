@@ -105,7 +105,8 @@ def test_option_variants_agree(systec):
                  dict(K=64, stages=4), dict(stages=3), dict(vpl=2), dict(vpl=4), dict(vpl=2, K=3),
                  dict(vpl=4, pos1_accumulate=1), dict(prefetch=1), dict(prefetch=1, pos1_accumulate=1, K=4),
                  dict(prefetch=1, vpl=2, K=3), dict(prefetch=1, K=2), dict(copies=1), dict(copies=7),
-                 dict(copies=32, prefetch=1), dict(copies=3, force_scalar=1)]:
+                 dict(copies=32, prefetch=1), dict(copies=3, force_scalar=1), dict(occupancy=1),
+                 dict(occupancy=1, pos1_accumulate=1), dict(occupancy=-1)]:
         parity(run(systec, w, **opts), Cref, S)
 
 
@@ -117,6 +118,7 @@ def test_hub_rows_long_runs(systec):
     parity(run(systec, w), Cref, S)
     parity(run(systec, w, pos1_accumulate=1), Cref, S)
     parity(run(systec, w, prefetch=1), Cref, S)
+    parity(run(systec, w, occupancy=1), Cref, S)
 
 
 def test_empty_and_degenerate(systec):
