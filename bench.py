@@ -361,6 +361,43 @@ def main():
                        "h2d_bytes_per_step": w.idx.nbytes + w.vals.nbytes + w.B.nbytes,
                        "d2h_bytes_per_step": pin_C.numel() * 4, "ms_per_step": e2e_ms,
                        "includes": "H2D + validate/canonicalise/sort-check/gather/stats + execute + D2H"}
+    # N > 1: every rank, every step: H2D of its slice + B from pinned memory,
+    # plan creation (validate/canonicalise/sort-check/gather/stats), execute,
+    # one all-reduce of C, D2H of C; time = max over ranks
+    if world > 1 and not args.no_e2e:
+        pin_idx = torch.from_numpy(np.ascontiguousarray(w.idx[lo:hi])).pin_memory()
+        pin_vals = torch.from_numpy(np.ascontiguousarray(w.vals[lo:hi])).pin_memory()
+        pin_B = torch.from_numpy(w.B).pin_memory()
+        pin_C = torch.empty((w.dim, w.R), dtype=torch.float32).pin_memory()
+
+        def e2e_step():
+            di = pin_idx.to(dev, non_blocking=True)
+            dv = pin_vals.to(dev, non_blocking=True)
+            dB = pin_B.to(dev, non_blocking=True)
+            pl = systec.Plan(w.order, w.dim, di, dv)
+            Cd = pl.execute(dB)
+            reduce_partials(Cd)
+            pin_C.copy_(Cd, non_blocking=True)
+            torch.cuda.synchronize()
+            pl.destroy()
+
+        e2e_step()
+        ts = []
+        for _ in range(args.e2e_steps):
+            dist.barrier()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            e2e_step()
+            ts.append(time.perf_counter() - t0)
+        t = torch.tensor([float(np.mean(ts))], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        if rank == 0:
+            e2e_ms = t.item() * 1e3
+            line["e2e"] = {"value": w.nnz / (e2e_ms * 1e-3), "unit": UNIT,
+                           "h2d_bytes_per_step": (w.idx.nbytes + w.vals.nbytes) + world * w.B.nbytes,
+                           "d2h_bytes_per_step": world * pin_C.numel() * 4, "ms_per_step": e2e_ms,
+                           "includes": "per rank: H2D slice + plan creation + execute + all-reduce(C) + D2H; "
+                                       "max over ranks (host clock around synchronised steps)"}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(w)
     if rank == 0:
