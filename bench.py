@@ -43,6 +43,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--opts", default="", help="kernel options, e.g. K=33,stages=2,pos1_accumulate=1")
+    ap.add_argument("--dist-backend", default="nccl", help="collective backend for N>1 (gloo: code-path tests)")
+    ap.add_argument("--same-device", action="store_true",
+                    help="test mode: every rank on cuda:0 (with --dist-backend gloo; no kernel waits on another)")
     return ap.parse_args()
 
 
@@ -230,11 +233,16 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.same_device:
+        local = 0
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(args.dist_backend)
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream()
 
