@@ -3,6 +3,7 @@
 // every step of the computation itself runs in the kernels of prepare.cu and
 // mttkrp.cu.  There is no host compute path.
 #include <climits>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <new>
@@ -440,7 +441,12 @@ cudaStream_t copy_stream() {
 // Position-1 accumulation is decided from chunk 0's statistics (one sync).
 int mttkrp_host_pipelined(int order, int64_t dim, int64_t nnz, int bits, const int32_t *idx_host,
                           const float *vals_host, const float *B_host, int R, float *C_host, cudaStream_t s) {
-    const int64_t per = std::max<int64_t>(4, ((nnz + 7) / 8 + 3) & ~int64_t(3));  // 8 chunks, 16-byte aligned
+    static const int kChunks = [] {  // SYSTEC_HOST_CHUNKS: tuning knob for the pipeline depth (default 16)
+        const char *e = std::getenv("SYSTEC_HOST_CHUNKS");
+        const int v = e ? std::atoi(e) : 16;
+        return v < 1 ? 1 : (v > 256 ? 256 : v);
+    }();
+    const int64_t per = std::max<int64_t>(4, ((nnz + kChunks - 1) / kChunks + 3) & ~int64_t(3));  // 16-byte aligned
     const int nch = static_cast<int>((nnz + per - 1) / per);
     const int64_t ld = ((nnz + 3) & ~int64_t(3)) + 4;
     const size_t ib = static_cast<size_t>(nnz) * order * 4, vb = static_cast<size_t>(nnz) * 4;
