@@ -292,7 +292,7 @@ int systec_cp_als_sym(systec_plan plan, float *B, int R, float *lambda, int max_
     do {
         if ((e = cudaMallocAsync(&M, plane * 4, s)) != cudaSuccess) break;
         if ((e = cudaMallocAsync(&fs, static_cast<size_t>(R) * R * 4, s)) != cudaSuccess) break;
-        if ((e = cudaMallocAsync(&ds, sizeof(double) * (R * R + 2 * R + 2), s)) != cudaSuccess) break;
+        if ((e = cudaMallocAsync(&ds, sizeof(double) * systec::cpd_scratch_doubles(R), s)) != cudaSuccess) break;
         if ((e = systec::cpd_tensor_norm2(*p, ds, s)) != cudaSuccess) break;
         if ((e = cudaMemcpyAsync(&x2, ds, sizeof(double), cudaMemcpyDeviceToHost, s)) != cudaSuccess) break;
         if ((e = cudaStreamSynchronize(s)) != cudaSuccess) break;

@@ -28,29 +28,78 @@ namespace systec {
 
 namespace {
 
-constexpr int kMaxCpR = 48;  // two fp64 R x R tiles in static shared memory
+constexpr int kMaxCpR = 48;  // two fp64 R x R tiles + a 256-double scratch in static shared memory
 
-// G[a][b] += sum over this block's rows of B[i][a] * B[i][b]   (fp64 accumulation)
-__global__ void gram_kernel(const float *__restrict__ B, int64_t dim, int R, double *__restrict__ G) {
-    const int pairs = R * R;
-    for (int pidx = threadIdx.x; pidx < pairs; pidx += blockDim.x) {
-        const int a = pidx / R, b = pidx % R;
-        double acc = 0.0;
-        for (int64_t i = blockIdx.x; i < dim; i += gridDim.x)
-            acc += static_cast<double>(B[i * R + a]) * static_cast<double>(B[i * R + b]);
-        atomicAdd(&G[pidx], acc);
+// Two-stage column reductions (no global atomics): each block owns a contiguous
+// row range and writes its partial sums; sum_partials_kernel adds the blocks.
+//   gram:   part[blk][a*R+b] = sum_{i in blk} B[i][a] B[i][b]       (fp64)
+//   coldot: part[blk][r]     = sum_{i in blk} X[i][r] Y[i][r]
+__global__ void gram_partial_kernel(const float *__restrict__ B, int64_t dim, int R, double *__restrict__ part) {
+    // rows of this block staged in shared memory in tiles, pairs accumulated in fp64
+    constexpr int kTileRows = 64;
+    __shared__ float tile[kTileRows * kMaxCpR];
+    const int64_t rows = (dim + gridDim.x - 1) / gridDim.x;
+    const int64_t lo = blockIdx.x * rows, hi = min(dim, lo + rows);
+    constexpr int kPairsPerThread = (kMaxCpR * kMaxCpR + 255) / 256;
+    double acc[kPairsPerThread];
+#pragma unroll
+    for (int k = 0; k < kPairsPerThread; ++k) acc[k] = 0.0;
+    for (int64_t r0 = lo; r0 < hi; r0 += kTileRows) {
+        const int nr = static_cast<int>(min(static_cast<int64_t>(kTileRows), hi - r0));
+        __syncthreads();
+        for (int q = threadIdx.x; q < nr * R; q += blockDim.x) tile[q] = B[r0 * R + q];
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < kPairsPerThread; ++k) {
+            const int pidx = threadIdx.x + k * blockDim.x;
+            if (pidx < R * R) {
+                const int a = pidx / R, b = pidx % R;
+                double s0 = 0.0, s1 = 0.0;
+                int i = 0;
+                for (; i + 1 < nr; i += 2) {
+                    s0 += static_cast<double>(tile[i * R + a]) * tile[i * R + b];
+                    s1 += static_cast<double>(tile[(i + 1) * R + a]) * tile[(i + 1) * R + b];
+                }
+                if (i < nr) s0 += static_cast<double>(tile[i * R + a]) * tile[i * R + b];
+                acc[k] += s0 + s1;
+            }
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < kPairsPerThread; ++k) {
+        const int pidx = threadIdx.x + k * blockDim.x;
+        if (pidx < R * R) part[static_cast<int64_t>(blockIdx.x) * R * R + pidx] = acc[k];
     }
 }
 
-// w[r] += sum_i X[i][r] * Y[i][r]
-__global__ void coldot_kernel(const float *__restrict__ X, const float *__restrict__ Y, int64_t dim, int R,
-                              double *__restrict__ w) {
-    for (int r = threadIdx.x; r < R; r += blockDim.x) {
-        double acc = 0.0;
-        for (int64_t i = blockIdx.x; i < dim; i += gridDim.x)
+__global__ void coldot_partial_kernel(const float *__restrict__ X, const float *__restrict__ Y, int64_t dim, int R,
+                                      double *__restrict__ part) {
+    const int64_t rows = (dim + gridDim.x - 1) / gridDim.x;
+    const int64_t lo = blockIdx.x * rows, hi = min(dim, lo + rows);
+    // blockDim = 256: 256/R row lanes x R columns
+    const int lanes = blockDim.x / R;
+    const int r = threadIdx.x % R, li = threadIdx.x / R;
+    __shared__ double red[256];
+    double acc = 0.0;
+    if (li < lanes)
+        for (int64_t i = lo + li; i < hi; i += lanes)
             acc += static_cast<double>(X[i * R + r]) * static_cast<double>(Y[i * R + r]);
-        atomicAdd(&w[r], acc);
+    red[threadIdx.x] = (li < lanes) ? acc : 0.0;
+    __syncthreads();
+    if (threadIdx.x < R) {
+        double s = 0.0;
+        for (int k = 0; k < lanes; ++k) s += red[k * R + threadIdx.x];
+        part[static_cast<int64_t>(blockIdx.x) * R + threadIdx.x] = s;
     }
+}
+
+// out[q] = sum_blk part[blk][q], q < width
+__global__ void sum_partials_kernel(const double *__restrict__ part, int blocks, int width, double *__restrict__ out) {
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= width) return;
+    double s = 0.0;
+    for (int b = 0; b < blocks; ++b) s += part[static_cast<int64_t>(b) * width + q];
+    out[q] = s;
 }
 
 // ||X||^2 = sum_e v_e^2 orbit_e over the plan's canonical stream
@@ -84,68 +133,67 @@ __global__ void tensor_norm_kernel(const int32_t *__restrict__ coords, int64_t l
     if ((threadIdx.x & 31) == 0) atomicAdd(out, acc);
 }
 
-// One block: H = G^{.(n-1)}, Cholesky H = L L^T (with a tiny relative ridge
-// for safety), Hinv = H^{-1}; also ||Xhat||^2 = lam^T G^{.n} lam when lam given.
+// One block (blockDim = 256): H = G^{.(n-1)}, Cholesky H = L L^T (tiny relative
+// ridge for safety), Hinv = H^{-1}; with lam: ||Xhat||^2 = lam^T G^{.n} lam and
+// <X,Xhat> = lam . dots.  Right-looking Cholesky, one column step per barrier.
 __global__ void small_solve_kernel(const double *__restrict__ G, int R, int n, float *__restrict__ Hinv,
                                    const float *__restrict__ lam, const double *__restrict__ dots,
                                    double *__restrict__ xhat2) {
     __shared__ double L[kMaxCpR * kMaxCpR];
     __shared__ double Inv[kMaxCpR * kMaxCpR];
-    const int tid = threadIdx.x;
-    for (int p = tid; p < R * R; p += blockDim.x) {
+    __shared__ double red[256];
+    const int tid = threadIdx.x, nt = blockDim.x;
+    double fit_part = 0.0;
+    for (int p = tid; p < R * R; p += nt) {
         double h = 1.0;
         for (int k = 0; k < n - 1; ++k) h *= G[p];
         L[p] = h;
+        if (lam) fit_part += static_cast<double>(lam[p / R]) * lam[p % R] * h * G[p];
     }
+    red[tid] = fit_part;
     __syncthreads();
+    if (lam && xhat2 && tid == 0) {
+        double s = 0.0, ip = 0.0;
+        for (int k = 0; k < nt; ++k) s += red[k];
+        for (int a = 0; a < R; ++a) ip += static_cast<double>(lam[a]) * dots[a];
+        xhat2[0] = s;
+        xhat2[1] = ip;
+    }
     if (tid == 0) {
-        if (lam && xhat2) {  // fit pieces of the current iterate: ||Xhat||^2 and <X, Xhat>
-            double s = 0.0;
-            for (int a = 0; a < R; ++a)
-                for (int b = 0; b < R; ++b) {
-                    double g = 1.0;
-                    for (int k = 0; k < n; ++k) g *= G[a * R + b];
-                    s += static_cast<double>(lam[a]) * lam[b] * g;
-                }
-            xhat2[0] = s;
-            double ip = 0.0;
-            for (int a = 0; a < R; ++a) ip += static_cast<double>(lam[a]) * dots[a];
-            xhat2[1] = ip;
-        }
         double tr = 0.0;
         for (int a = 0; a < R; ++a) tr += L[a * R + a];
         const double ridge = 1e-12 * (tr / R + 1e-300);
         for (int a = 0; a < R; ++a) L[a * R + a] += ridge;
-        // in-place Cholesky (lower)
-        for (int j = 0; j < R; ++j) {
-            double d = L[j * R + j];
-            for (int k = 0; k < j; ++k) d -= L[j * R + k] * L[j * R + k];
-            d = sqrt(fmax(d, 1e-300));
-            L[j * R + j] = d;
-            for (int i = j + 1; i < R; ++i) {
-                double s = L[i * R + j];
-                for (int k = 0; k < j; ++k) s -= L[i * R + k] * L[j * R + k];
-                L[i * R + j] = s / d;
-            }
-        }
     }
     __syncthreads();
+    for (int j = 0; j < R; ++j) {  // right-looking Cholesky (lower triangle of L)
+        if (tid == 0) L[j * R + j] = sqrt(fmax(L[j * R + j], 1e-300));
+        __syncthreads();
+        const double d = L[j * R + j];
+        for (int i = j + 1 + tid; i < R; i += nt) L[i * R + j] /= d;
+        __syncthreads();
+        for (int p = tid; p < (R - j - 1) * (R - j - 1); p += nt) {
+            const int i = j + 1 + p / (R - j - 1), k = j + 1 + p % (R - j - 1);
+            if (k <= i) L[i * R + k] -= L[i * R + j] * L[k * R + j];
+        }
+        __syncthreads();
+    }
     // columns of the inverse: solve L L^T x = e_c, one column per thread
-    for (int c = tid; c < R; c += blockDim.x) {
+    for (int c = tid; c < R; c += nt) {
         double y[kMaxCpR];
         for (int i = 0; i < R; ++i) {
-            double s = (i == c) ? 1.0 : 0.0;
-            for (int k = 0; k < i; ++k) s -= L[i * R + k] * y[k];
-            y[i] = s / L[i * R + i];
+            double sacc = (i == c) ? 1.0 : 0.0;
+            for (int k = 0; k < i; ++k) sacc -= L[i * R + k] * y[k];
+            y[i] = sacc / L[i * R + i];
         }
         for (int i = R - 1; i >= 0; --i) {
-            double s = y[i];
-            for (int k = i + 1; k < R; ++k) s -= L[k * R + i] * Inv[k * R + c];
-            Inv[i * R + c] = s / L[i * R + i];
+            double sacc = y[i];
+            for (int k = i + 1; k < R; ++k) sacc -= L[k * R + i] * Inv[k * R + c];
+            Inv[i * R + c] = sacc / L[i * R + i];
         }
     }
     __syncthreads();
-    for (int p = tid; p < R * R; p += blockDim.x) Hinv[p] = static_cast<float>(Inv[p]);
+    for (int p = tid; p < R * R; p += nt) Hinv[p] = static_cast<float>(Inv[p]);
 }
 
 // Bout[i][b] = sum_a M[i][a] Hinv[a][b]
@@ -202,22 +250,30 @@ cudaError_t cpd_tensor_norm2(const Plan &p, double *out, cudaStream_t s) {
     return cudaGetLastError();
 }
 
-// scratch layout (doubles): G[R*R], dots[R], norms[R], scalars[2] = {||Xhat||^2, <X,Xhat>} | floats: Hinv[R*R]
+int cpd_partial_blocks() { return sm_count() * 4; }
+
+// scratch (doubles): G[R*R], dots[R], norms[R], scalars[2] = {||Xhat||^2, <X,Xhat>},
+// then partials[PB][R*R] | floats: Hinv[R*R]
+int64_t cpd_scratch_doubles(int R) { return static_cast<int64_t>(R) * R + 2 * R + 2 + static_cast<int64_t>(cpd_partial_blocks()) * R * R; }
+
 cudaError_t cpd_step(const Plan &p, const float *M, float *B, float *lam, int R, double *dscratch,
                      float *fscratch, bool have_lam, bool fit_only, cudaStream_t s) {
-    double *G = dscratch, *dots = G + R * R, *norms = dots + R, *xhat2 = norms + R;
+    double *G = dscratch, *dots = G + R * R, *norms = dots + R, *xhat2 = norms + R, *part = xhat2 + 2;
     float *Hinv = fscratch;
-    cudaError_t e = cudaMemsetAsync(dscratch, 0, sizeof(double) * (R * R + 2 * R + 2), s);
-    if (e != cudaSuccess) return e;
-    const int blocks = std::max(1, std::min(sm_count() * 4, static_cast<int>((p.dim + 63) / 64)));
-    gram_kernel<<<blocks, 256, 0, s>>>(B, p.dim, R, G);
-    coldot_kernel<<<blocks, 64, 0, s>>>(M, B, p.dim, R, dots);     // <X,Xhat> pieces for the current iterate
-    small_solve_kernel<<<1, 64, 0, s>>>(G, R, p.order, Hinv, have_lam ? lam : nullptr, dots, xhat2);
+    // partial blocks: ~128 rows each, at most 4 per SM
+    const int PB = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(cpd_partial_blocks(), (p.dim + 127) / 128)));
+    const int rr = R * R;
+    gram_partial_kernel<<<PB, 256, 0, s>>>(B, p.dim, R, part);
+    sum_partials_kernel<<<(rr + 255) / 256, 256, 0, s>>>(part, PB, rr, G);
+    coldot_partial_kernel<<<PB, 256, 0, s>>>(M, B, p.dim, R, part);   // <X,Xhat> pieces of the current iterate
+    sum_partials_kernel<<<1, 64, 0, s>>>(part, PB, R, dots);
+    small_solve_kernel<<<1, 256, 0, s>>>(G, R, p.order, Hinv, have_lam ? lam : nullptr, dots, xhat2);
     if (fit_only) return cudaGetLastError();
     const int64_t total = p.dim * R;
     const int ab = static_cast<int>(std::min<int64_t>((total + 255) / 256, static_cast<int64_t>(sm_count()) * 8));
     apply_inverse_kernel<<<ab, 256, 0, s>>>(M, Hinv, p.dim, R, B);
-    coldot_kernel<<<blocks, 64, 0, s>>>(B, B, p.dim, R, norms);     // squared column norms of B_new
+    coldot_partial_kernel<<<PB, 256, 0, s>>>(B, B, p.dim, R, part);   // squared column norms of B_new
+    sum_partials_kernel<<<1, 64, 0, s>>>(part, PB, R, norms);
     normalize_kernel<<<ab, 256, 0, s>>>(B, p.dim, R, norms, lam);
     return cudaGetLastError();
 }

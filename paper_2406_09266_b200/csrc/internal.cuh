@@ -64,6 +64,7 @@ cudaError_t launch_minplus(const Plan &p, const float *d, float *y, int *scratch
 
 // cpd.cu
 int cpd_max_rank();
+int64_t cpd_scratch_doubles(int R);
 cudaError_t cpd_tensor_norm2(const Plan &p, double *out, cudaStream_t s);
 cudaError_t cpd_step(const Plan &p, const float *M, float *B, float *lam, int R, double *dscratch,
                      float *fscratch, bool have_lam, bool fit_only, cudaStream_t s);
