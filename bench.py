@@ -40,6 +40,9 @@ def parse():
     ap.add_argument("--config", default="c2")
     ap.add_argument("--impl", default="systec", choices=["systec", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-baseline-only", action="store_true",
+                    help="print only the cpu_baseline leg (the oracle on the host), e.g. with --oracle-threads 1")
+    ap.add_argument("--oracle-threads", type=int, default=0, help="threads for the cpu_baseline leg (0 = all)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--opts", default="", help="kernel options, e.g. K=33,stages=2,pos1_accumulate=1")
@@ -149,11 +152,11 @@ def l2_model(w, st, nnz_local, kern_ms, launch):
             "source": "profiles/r01_microbench.json (tools/microbench.cu, 128-B rows, 12.8 MB tables)"}
 
 
-def cpu_baseline(w, target_wall=4.0, max_entries=None):
+def cpu_baseline(w, target_wall=4.0, max_entries=None, threads=0):
     """The oracle as it stands on the host cores, on a bounded sample (the
     first m stored entries), scaled up until one run takes ~target_wall s."""
     import oracle
-    T = oracle.default_threads()
+    T = threads if threads > 0 else oracle.default_threads()
     m = min(w.nnz, 50_000)
     while True:
         t0 = time.perf_counter()
@@ -224,6 +227,10 @@ def main():
     w = generate(args.config)
     if args.impl == "reference":
         run_reference(args, w)
+        return
+    if args.cpu_baseline_only:
+        print(json.dumps({"config": config_dict(w, args),
+                          "cpu_baseline": cpu_baseline(w, threads=args.oracle_threads)}), flush=True)
         return
 
     import torch
@@ -407,7 +414,7 @@ def main():
                            "includes": "per rank: H2D slice + plan creation + execute + all-reduce(C) + D2H; "
                                        "max over ranks (host clock around synchronised steps)"}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(w)
+        line["cpu_baseline"] = cpu_baseline(w, threads=args.oracle_threads)
     if rank == 0:
         print(json.dumps(line), flush=True)
     plan.destroy()
