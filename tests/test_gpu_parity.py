@@ -226,8 +226,33 @@ def test_config_full_size_sampled(systec, name):
     """BASELINE.json full sizes, default launch configuration (the one bench.py
     times): sampled output rows checked against the oracle row by row, and the
     full-contraction invariant P7 over all of C."""
+    import torch
     w = generate(name)
     Cg = run(systec, w)
+    # prepare at full size: statistics equal numpy counts on the canonical stream
+    plan = systec.Plan(w.order, w.dim, *to_dev(w.idx, w.vals))
+    st = plan.stats()
+    c = w.idx
+    neq = c[:, 1:] != c[:, :-1]
+    assert st["G"] == int(w.nnz + neq.sum())
+    code = np.zeros(w.nnz, np.int64)
+    for t in range(w.order - 1):
+        code |= (~neq[:, t]).astype(np.int64) << t
+    assert st["pattern_hist"][:1 << (w.order - 1)] == np.bincount(code, minlength=1 << (w.order - 1)).tolist()
+    lead = np.bincount(c[:, 0])
+    assert st["lead_runs"] == int((lead > 0).sum()) and st["max_lead_run"] == int(lead.max())
+    assert st["pos1_runs"] == int(1 + (c[1:, 1] != c[:-1, 1]).sum())
+    assert st["input_was_sorted"] == 1
+    plan.destroy()
+    if name == "c2":  # the CUB sort path at full size: a shuffled, non-canonical spelling
+        si, sv = scramble(w.idx, w.vals, seed=5)
+        plan = systec.Plan(w.order, w.dim, *to_dev(si, sv))
+        coords, pv = plan.prepared()
+        torch.cuda.synchronize()
+        assert plan.stats()["input_was_sorted"] == 0
+        assert np.array_equal(coords.cpu().numpy().T, w.idx)
+        assert np.array_equal(pv.cpu().numpy(), w.vals)
+        plan.destroy()
     rows = sample_rows(w)
     Cref, S = oracle.mttkrp_rows(w.order, w.dim, w.idx, w.vals, w.B, rows)
     err = parity(Cg[rows], Cref, S)
