@@ -46,6 +46,21 @@ def build(force: bool = False) -> str:
     return _LIB
 
 
+def _bind(lib):
+    i64, i32, vp = ctypes.c_int64, ctypes.c_int, ctypes.c_void_p
+    lib.oracle_mttkrp.argtypes = [i32, i64, i64, vp, vp, vp, i32, vp, vp, i32, i64]
+    lib.oracle_mttkrp.restype = i32
+    lib.oracle_count_expanded.argtypes = [i32, i64, vp]
+    lib.oracle_count_expanded.restype = i64
+    return lib
+
+
+def load_variant(path: str):
+    """A separately compiled oracle (the mutation tests build deliberately
+    broken variants with -DORACLE_MUTATION=k to show the pins catch them)."""
+    return _bind(ctypes.CDLL(path))
+
+
 def _load():
     global _lib
     if _lib is None:
@@ -91,7 +106,7 @@ def _ptr(a):
 
 
 def mttkrp(order: int, dim: int, idx, vals, B, threads: int | None = None,
-           mem_budget_bytes: int = 0):
+           mem_budget_bytes: int = 0, lib=None):
     """Expansion oracle.  Returns (C, S), fp64 [dim][R]."""
     idx, vals, B = _prep(order, idx, vals, B)
     if B.shape[0] != dim:
@@ -100,8 +115,8 @@ def mttkrp(order: int, dim: int, idx, vals, B, threads: int | None = None,
     C = np.empty((dim, R), np.float64)
     S = np.empty((dim, R), np.float64)
     T = threads if threads else default_threads()
-    rc = _load().oracle_mttkrp(order, dim, idx.shape[0], _ptr(idx), _ptr(vals), _ptr(B), R,
-                               _ptr(C), _ptr(S), T, mem_budget_bytes)
+    rc = (lib or _load()).oracle_mttkrp(order, dim, idx.shape[0], _ptr(idx), _ptr(vals), _ptr(B), R,
+                                        _ptr(C), _ptr(S), T, mem_budget_bytes)
     if rc == 3:
         raise IndexError("index outside [0, dim)")
     if rc != 0:
@@ -171,7 +186,7 @@ def ttm_sym3(dim: int, idx, vals, B):
     return C
 
 
-def count_expanded(order: int, idx) -> int:
+def count_expanded(order: int, idx, lib=None) -> int:
     """Σ over entries of the number of distinct permutations (expanded nnz)."""
     idx = np.ascontiguousarray(idx, dtype=np.int32).reshape(-1, order)
-    return int(_load().oracle_count_expanded(order, idx.shape[0], _ptr(idx)))
+    return int((lib or _load()).oracle_count_expanded(order, idx.shape[0], _ptr(idx)))
