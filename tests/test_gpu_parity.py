@@ -461,3 +461,19 @@ def test_host_call_pipelined(systec, n, dim, nnz, R, shuffle):
     bad[nnz - 3, 0] = dim
     with pytest.raises(IndexError, match=f"first bad entry {nnz - 3}"):
         systec.mttkrp_host(n, dim, bad, vals, w.B)
+
+
+def test_fault_injection_is_detected_and_located(systec):
+    """A single corrupted stored value must fail the parity check, and exactly
+    the output rows its (distinct) indices name must be the ones that differ."""
+    w = small_random(4, 30, 5000, 16, seed=17, diag_frac=0.0)
+    Cref, S = oracle.mttkrp(4, 30, w.idx, w.vals, w.B)
+    bad = w.vals.copy()
+    k = 1234
+    bad[k] += 0.5
+    Cg = run(systec, w, vals=bad)
+    with pytest.raises(AssertionError):
+        parity(Cg, Cref, S)
+    err = np.abs(Cg - Cref).max(axis=1) / np.maximum(S.max(axis=1), 1e-30)
+    flagged = set(np.nonzero(err > 1e-4)[0].tolist())
+    assert flagged == set(w.idx[k].tolist())
