@@ -313,12 +313,9 @@ int systec_cp_als_sym(systec_plan plan, float *B, int R, float *lambda, int max_
                 const double fit = 1.0 - sqrt(r2 > 0 ? r2 : 0.0) / xn;
                 if (fit_host) fit_host[it - 1] = fit;
                 done = it;
-                if (last || fabs(fit - prev_fit) < tol) {
-                    if (!last) {  // converged: the step just taken produced one more iterate; keep it
-                        // (its fit is not evaluated; callers read fit_host[done-1])
-                    }
-                    break;
-                }
+                // converged (or out of iterations): when converged early, B already holds
+                // one more update than the last evaluated fit describes — it is kept
+                if (last || fabs(fit - prev_fit) < tol) break;
                 prev_fit = fit;
             }
         }
