@@ -102,3 +102,20 @@ def test_sass_shows_bulk_async_copies_and_vector_reductions(lib):
     assert "REDG.E.ADD.F32x4" in sass
     assert "LDG.E.128" in sass
     assert "SYNCS" in sass          # mbarrier waits
+
+
+def test_header_is_plain_c_and_example_builds(lib):
+    """include/systec.h is valid C11 and a plain C program links against the
+    library (run on the GPU box by tests/test_gpu_parity.py)."""
+    import shutil
+    import subprocess
+    import tempfile
+    if not shutil.which("gcc"):
+        pytest.skip("gcc not available")
+    out = os.path.join(tempfile.mkdtemp(), "mttkrp_c")
+    subprocess.check_call(["gcc", "-std=c11", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"),
+                           os.path.join(ROOT, "examples", "mttkrp_c.c"), "-o", out,
+                           "-L", os.path.join(ROOT, "paper_2406_09266_b200"), "-lsystec",
+                           "-L", "/usr/local/cuda/lib64", "-lcudart",
+                           "-Wl,-rpath," + os.path.join(ROOT, "paper_2406_09266_b200")])
+    assert os.path.exists(out)

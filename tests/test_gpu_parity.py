@@ -1,6 +1,7 @@
 """Parity of the CUDA path (through the C ABI) with the CPU oracle.
 GPU tests: run with `pytest -m gpu` on a B200."""
 import itertools
+import os
 
 import numpy as np
 import pytest
@@ -477,3 +478,18 @@ def test_fault_injection_is_detected_and_located(systec):
     err = np.abs(Cg - Cref).max(axis=1) / np.maximum(S.max(axis=1), 1e-30)
     flagged = set(np.nonzero(err > 1e-4)[0].tolist())
     assert flagged == set(w.idx[k].tolist())
+
+
+def test_plain_c_example_runs(systec, tmp_path):
+    """The C ABI used from a plain C program (examples/mttkrp_c.c)."""
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = str(tmp_path / "mttkrp_c")
+    subprocess.check_call(["gcc", "-std=c11", "-I", os.path.join(root, "include"),
+                           os.path.join(root, "examples", "mttkrp_c.c"), "-o", exe,
+                           "-L", os.path.join(root, "paper_2406_09266_b200"), "-lsystec",
+                           "-L", "/usr/local/cuda/lib64", "-lcudart",
+                           "-Wl,-rpath," + os.path.join(root, "paper_2406_09266_b200")])
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0, out.stderr
+    assert out.stdout.startswith("ok")
