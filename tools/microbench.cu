@@ -132,6 +132,23 @@ __global__ void mttkrp_like_tma(const float *__restrict__ B, float *C, uint32_t 
     if (lane % 8 == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
+// shared-memory fp32 atomicAdd (a CAS loop on sm_100a) into a 64 KB private
+// copy of C — the smem-privatisation alternative for small outputs (c5)
+__global__ void smem_atomic_rows(float *out, int iters) {
+    extern __shared__ float Cs[];  // 64 KB (dynamic): c5's C (1000 x 16)
+    for (int i = threadIdx.x; i < 16384; i += blockDim.x) Cs[i] = 0.f;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, j = lane & 3;
+    const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    for (int it = 0; it < iters; ++it) {
+        const uint32_t r = hash32(gw * 131071u + it * 8u + (lane >> 2)) % 1000;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) atomicAdd(&Cs[r * 16 + j * 4 + q], 1.f);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) out[blockIdx.x] = Cs[0];
+}
+
 int main() {
     int dev = 0, sms = 0, l2 = 0, smem = 0, clk = 0;
     CK(cudaGetDevice(&dev));
@@ -319,9 +336,26 @@ int main() {
         printf(", \"bulk_red_64B_rows_gbs\": %.1f", (double)blocks * threads * iters * 64 / (best * 1e-3) / 1e9);
         CK(cudaFree(C));
     }
-    // 7) red.v4 into 64-B rows (R = 16: 4 lanes per row), 640 KB and 64 KB tables
+    // 7) smem fp32 atomics (CAS loop) vs L2 red.v4: 64-B rows of a 64 KB C
     {
-        printf("}\n");
+        float *o;
+        CK(cudaMalloc(&o, sms * 4 * sizeof(float)));
+        const int iters = 64, blocks = sms, threads = 1024;
+        CK(cudaFuncSetAttribute(smem_atomic_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536));
+        float best = 1e30f;
+        for (int r = 0; r < 3; ++r) {
+            CK(cudaEventRecord(e0));
+            smem_atomic_rows<<<blocks, threads, 65536>>>(o, iters);
+            CK(cudaEventRecord(e1));
+            CK(cudaEventSynchronize(e1));
+            float ms;
+            CK(cudaEventElapsedTime(&ms, e0, e1));
+            best = ms < best ? ms : best;
+        }
+        double bytes = (double)blocks * threads / 4 * iters * 64;   // 64-B row updates
+        printf(", \"smem_cas_atomic_64B_rows_gbs\": %.1f", bytes / (best * 1e-3) / 1e9);
+        CK(cudaFree(o));
     }
+    printf("}\n");
     return 0;
 }
