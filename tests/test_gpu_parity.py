@@ -493,3 +493,26 @@ def test_plain_c_example_runs(systec, tmp_path):
     out = subprocess.run([exe], capture_output=True, text=True, timeout=120)
     assert out.returncode == 0, out.stderr
     assert out.stdout.startswith("ok")
+
+
+@pytest.mark.parametrize("R", [32, 16, 3])
+def test_single_giant_run_and_all_singleton_runs(systec, R):
+    """Every entry shares c_0 = 0 (one run crossing every chunk and warp range),
+    then every entry has its own c_0 (runs of length 1)."""
+    dim = 700
+    j, k = np.triu_indices(dim)
+    idx = np.stack([np.zeros_like(j), j, k], axis=1).astype(np.int32)       # (0, j, k), j <= k
+    rng = np.random.default_rng(R)
+    vals = rng.uniform(-1, 1, len(idx)).astype(np.float32)
+    B = rng.uniform(-1, 1, (dim, R)).astype(np.float32)
+    from synth.workloads import Workload
+    w = Workload("giant", 3, dim, R, idx, vals, B)
+    Cref, S = oracle.mttkrp(3, dim, idx, vals, B)
+    parity(run(systec, w), Cref, S)
+    parity(run(systec, w, pos1_accumulate=1), Cref, S)
+    c = np.arange(dim, dtype=np.int32)
+    idx2 = np.stack([c, c, (c + 1) % dim], axis=1)
+    idx2.sort(axis=1)
+    w2 = Workload("singles", 3, dim, R, np.ascontiguousarray(idx2), vals[:dim].copy(), B)
+    Cref2, S2 = oracle.mttkrp(3, dim, w2.idx, w2.vals, B)
+    parity(run(systec, w2), Cref2, S2)
