@@ -87,17 +87,18 @@ typedef struct systec_exec_opts {
     int32_t force_scalar;        /* 1 = scalar (non-float4) path even when float4 is possible  */
     int32_t no_zero;             /* 1 = accumulate into C instead of overwriting it            */
     int32_t l2_hints;            /* 0 = default (on), -1 = off                                 */
-    /* reserved[0] K: entries per lane group per chunk (0 = auto)
-     * reserved[1] stages: shared-memory ring depth (0 = 2)
-     * reserved[2] vpl: float4 per lane, 1/2/4 (0 = 1)
-     * reserved[3] prefetch: 1 on, -1 off, 0 = auto (on when B > 32 MB)
-     * reserved[4] copies: replicas of C for L2-slice spreading, 1 = off, 0 = auto
-     *             (outputs < 4 MB and nnz >= 1e5: up to 32 replicas)
-     * reserved[5] ablation bits (evidence study; c2/c5 kernel shapes only):
-     *             1 = no shared-memory staging, 2 = no position-0 accumulation
-     * reserved[7] occupancy: order-3 R=32 kernel compiled for 5 blocks/SM;
-     *             1 on, -1 off, 0 auto (on when B > 64 MB)                  */
-    int32_t reserved[10];
+    int32_t chunk_k;             /* entries per lane group per staged chunk (0 = auto)         */
+    int32_t stages;              /* shared-memory ring depth of the stream staging (0 = 2)     */
+    int32_t vpl;                 /* float4 per lane: 1, 2 or 4 (0 = 1)                          */
+    int32_t prefetch;            /* next entry's B rows in flight: 1 on, 0/-1 off              */
+    int32_t copies;              /* replicas of C for L2-slice spreading: 1 = off, 0 = auto     */
+                                 /* (auto: C < 4 MB and nnz >= 1e5 -> up to 32 replicas)        */
+    int32_t ablation;            /* evidence study, c2/c5 kernel shapes only: bit 0 = no smem  */
+                                 /* staging of the stream, bit 1 = no position-0 accumulation  */
+    int32_t unused6;
+    int32_t occupancy;           /* order-3 R=32 kernel built for 5 blocks/SM: 1 on, -1 off,    */
+                                 /* 0 auto (on when B > 64 MB)                                  */
+    int32_t reserved[2];
 } systec_exec_opts;
 
 typedef struct systec_plan_s *systec_plan;

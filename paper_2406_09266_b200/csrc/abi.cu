@@ -12,6 +12,9 @@
 
 #include "internal.cuh"
 
+static_assert(sizeof(systec_exec_opts) == 64, "systec_exec_opts layout is part of the ABI");
+static_assert(sizeof(systec_stats) == 208, "systec_stats layout is part of the ABI");
+
 namespace systec {
 
 static thread_local int g_last_cuda_error = 0;

@@ -89,7 +89,7 @@ cudaError_t launch_mttkrp(Plan &p, const float *B, int R, float *C, const systec
     // L2-slice spreading: an output smaller than ~4 MB maps onto a few L2
     // slices whose atomic units then serialise the reductions (ncu on c5:
     // atomic-input activity max 57 % vs avg 20 %); spread it over replicas.
-    int copies = o.reserved[4];
+    int copies = o.copies;
     if (copies <= 0) {
         const int64_t bytes = plane * 4;
         copies = bytes >= (4 << 20) ? 1 : static_cast<int>(std::min<int64_t>(32, (4 << 20) / std::max<int64_t>(bytes, 1)));
@@ -126,15 +126,15 @@ cudaError_t launch_mttkrp(Plan &p, const float *B, int R, float *C, const systec
     const int tile_vecs = std::min(32, pow2ceil(vecs));
     int vpl = 1;
     if (vw == 4 && !p.general) {
-        const int want = o.reserved[2] > 0 ? o.reserved[2] : 1;  // float4 per lane
+        const int want = o.vpl > 0 ? o.vpl : 1;  // float4 per lane
         vpl = std::min(want, tile_vecs);
         if (vpl != 1 && vpl != 2 && vpl != 4) return cudaErrorInvalidValue;
     }
     const int lpe = tile_vecs / vpl;
     const int E = 32 / lpe;
     const int tiles = (R + tile_vecs * vw - 1) / (tile_vecs * vw);
-    int K = o.reserved[0] > 0 ? o.reserved[0] : default_K(E);
-    const int stages = o.reserved[1] > 0 ? o.reserved[1] : 2;
+    int K = o.chunk_k > 0 ? o.chunk_k : default_K(E);
+    const int stages = o.stages > 0 ? o.stages : 2;
     if ((E * K) % 4 != 0 || stages > 8) return release(cudaErrorInvalidValue);
 
     bool pos1 = false;
@@ -147,17 +147,17 @@ cudaError_t launch_mttkrp(Plan &p, const float *B, int R, float *C, const systec
     // r01_sweep_v3.jsonl): c2 -1 %, c3 +12 %, c4/c5 +1 % time with the
     // branch-free kernel — the extra registers cost more occupancy than the
     // in-flight gathers gain.
-    const bool pf = o.reserved[3] > 0;
+    const bool pf = o.prefetch > 0;
     KernelFn fn = p.general ? pick_naive(p.order, vw, lpe, pf) : pick(p.order, vw, lpe, vpl, pos1, pf);
     // occupancy variant: 5 resident blocks (48 registers) for the order-3 R=32
     // kernel when B is too large to stay L2-resident, so gathers wait on DRAM
     // and more warps in flight pay (c3: 2.65 -> 2.40 ms; c2 with its 12.8 MB
-    // B is L2-resident and loses 2 %).  reserved[7]: 1 on, -1 off, 0 auto.
+    // B is L2-resident and loses 2 %).  opts.occupancy: 1 on, -1 off, 0 auto.
     const bool occ_shape = vw == 4 && vpl == 1 && !pf && !p.general &&
                            ((p.order == 3 && lpe == 8) || (p.order >= 4 && lpe == 4));
-    const bool occ5 = occ_shape && (o.reserved[7] > 0 || (o.reserved[7] == 0 && p.order == 3 && plane * 4 > (64ll << 20)));
+    const bool occ5 = occ_shape && (o.occupancy > 0 || (o.occupancy == 0 && p.order == 3 && plane * 4 > (64ll << 20)));
     if (occ5) fn = p.order == 3 ? occupancy3(pos1) : p.order == 4 ? occupancy4(pos1) : occupancy5(pos1);
-    const int abl = o.reserved[5];
+    const int abl = o.ablation;
     if (abl > 0) {  // ablation study: only the c2 / c5 kernel shapes exist
         const bool shape3 = p.order == 3 && vw == 4 && lpe == 8 && vpl == 1 && !pos1 && !pf && !p.general;
         const bool shape5 = p.order == 5 && vw == 4 && lpe == 4 && vpl == 1 && pos1 && !pf && !p.general;

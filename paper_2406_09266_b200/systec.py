@@ -31,7 +31,9 @@ class SystecExecOpts(ctypes.Structure):
     _fields_ = [("warps_per_block", ctypes.c_int32), ("blocks_per_sm", ctypes.c_int32),
                 ("pos1_accumulate", ctypes.c_int32), ("force_scalar", ctypes.c_int32),
                 ("no_zero", ctypes.c_int32), ("l2_hints", ctypes.c_int32),
-                ("reserved", ctypes.c_int32 * 10)]
+                ("chunk_k", ctypes.c_int32), ("stages", ctypes.c_int32), ("vpl", ctypes.c_int32),
+                ("prefetch", ctypes.c_int32), ("copies", ctypes.c_int32), ("ablation", ctypes.c_int32),
+                ("unused6", ctypes.c_int32), ("occupancy", ctypes.c_int32), ("reserved", ctypes.c_int32 * 2)]
 
 
 EXPORTS = ["systec_mttkrp", "systec_mttkrp_host", "systec_plan_create", "systec_plan_execute",
@@ -120,23 +122,13 @@ def _dev(t, dtype, name):
 
 def _opts(**kw) -> SystecExecOpts:
     o = SystecExecOpts()
+    alias = {"K": "chunk_k"}
+    names = {f for f, _ in SystecExecOpts._fields_}
     for k, v in kw.items():
-        if k == "K":
-            o.reserved[0] = int(v)
-        elif k == "stages":
-            o.reserved[1] = int(v)
-        elif k == "vpl":
-            o.reserved[2] = int(v)
-        elif k == "prefetch":
-            o.reserved[3] = int(v)
-        elif k == "copies":
-            o.reserved[4] = int(v)
-        elif k == "ablation":
-            o.reserved[5] = int(v)
-        elif k == "occupancy":
-            o.reserved[7] = int(v)
-        else:
-            setattr(o, k, int(v))
+        k = alias.get(k, k)
+        if k not in names or k in ("reserved", "unused6"):
+            raise TypeError(f"unknown execute option {k!r}")
+        setattr(o, k, int(v))
     return o
 
 
