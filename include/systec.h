@@ -127,7 +127,8 @@ SYSTEC_API int systec_mttkrp_host(int order, int64_t dim, int64_t nnz, const int
  * tuple (ascending sort), sort entries lexicographically (skipped when the
  * input already is), and store the prepared structure-of-arrays copy
  * (order x int32 + 1 x fp32 per entry, owned by the plan).  idx and vals may
- * be freed once this returns.  Synchronises `stream` twice: once to read the
+ * be freed once this returns.  The plan belongs to the device current at
+ * creation; execute it there.  Synchronises `stream` twice: once to read the
  * device validation verdict (which also decides whether the sort can be
  * skipped) and once to read the statistics.
  * Errors: ARG, UNSUPPORTED, INDEX (plan not created, *out = NULL, and
