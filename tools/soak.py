@@ -1,0 +1,54 @@
+"""Soak / race test: thousands of executes of the BASELINE configs with
+integer-valued values and B (small integers, so every partial sum is an exactly
+representable fp32 integer): every run must produce a bit-identical C whatever
+the order of the atomic reductions.  A lost or doubled update anywhere — a
+race in the staging ring, the run carry, the chunk-end merge, the replicas —
+shows up as a mismatch.  Prints one JSON line per config.
+
+    python tools/soak.py --configs c2,c3,c4,c5 --runs 1000
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--configs", default="c2,c3,c4,c5")
+    ap.add_argument("--runs", type=int, default=1000)
+    a = ap.parse_args()
+    import numpy as np
+    import torch
+
+    import paper_2406_09266_b200 as systec
+    from synth import generate
+    for name in a.configs.split(","):
+        w = generate(name)
+        rng = np.random.default_rng(7)
+        lo, hi = (-1, 1)  # |partial sums| stay far below 2^24 on every config
+        vals = rng.integers(lo, hi + 1, w.nnz).astype(np.float32)
+        B = torch.from_numpy(rng.integers(lo, hi + 1, w.B.shape).astype(np.float32)).cuda()
+        plan = systec.Plan(w.order, w.dim, torch.from_numpy(w.idx).cuda(), torch.from_numpy(vals).cuda())
+        C0 = plan.execute(B).clone()
+        torch.cuda.synchronize()
+        assert float(C0.abs().max()) < 2 ** 24
+        C = torch.empty_like(C0)
+        mism = 0
+        t0 = time.perf_counter()
+        for k in range(a.runs):
+            plan.execute(B, C)
+            if not torch.equal(C, C0):
+                mism += 1
+        torch.cuda.synchronize()
+        print(json.dumps({"config": name, "runs": a.runs, "mismatches": mism, "max_abs_C": float(C0.abs().max()),
+                          "seconds": time.perf_counter() - t0, "launch": plan.last_launch()}), flush=True)
+        plan.destroy()
+
+
+if __name__ == "__main__":
+    main()
