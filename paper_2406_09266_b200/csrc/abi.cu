@@ -136,7 +136,7 @@ int plan_create_impl(Plan **out, int order, int64_t dim, int64_t nnz, const int3
     if (!sorted && nnz > 1) {
         if ((e = cudaMallocAsync(&keys2, nk * 8, s)) != cudaSuccess) return fail(e);
         if ((e = cudaMallocAsync(&perm2, nk * 4, s)) != cudaSuccess) return fail(e);
-        if ((e = sort_keys(nnz, bits * order, keys, keys2, perm, perm2, s, pooled)) != cudaSuccess) return fail(e);
+        if ((e = sort_keys(nnz, bits * order, keys, keys2, perm, perm2, s)) != cudaSuccess) return fail(e);
         skeys = keys2;
         sperm = perm2;
     }

@@ -44,7 +44,7 @@ cudaError_t launch_canonicalize(int order, int64_t dim, int64_t nnz, int bits, c
                                 unsigned long long *keys, uint32_t *perm, DevStats *st,
                                 cudaStream_t s, bool canonicalise = true, int64_t e_offset = 0);
 cudaError_t sort_keys(int64_t nnz, int end_bit, unsigned long long *keys_in, unsigned long long *keys_out,
-                      uint32_t *perm_in, uint32_t *perm_out, cudaStream_t s, bool pooled);
+                      uint32_t *perm_in, uint32_t *perm_out, cudaStream_t s);
 cudaError_t launch_gather(int order, int64_t nnz, int64_t ld, int bits, const unsigned long long *keys,
                           const uint32_t *perm /* null = identity */, const float *vals_in,
                           int32_t *coords, float *vals_out, cudaStream_t s);

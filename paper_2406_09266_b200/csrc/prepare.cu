@@ -229,7 +229,7 @@ cudaError_t launch_canonicalize(int order, int64_t dim, int64_t nnz, int bits, c
 }
 
 cudaError_t sort_keys(int64_t nnz, int end_bit, unsigned long long *keys_in, unsigned long long *keys_out,
-                      uint32_t *perm_in, uint32_t *perm_out, cudaStream_t s, bool pooled) {
+                      uint32_t *perm_in, uint32_t *perm_out, cudaStream_t s) {
     size_t temp = 0;
     cudaError_t e = cub::DeviceRadixSort::SortPairs(nullptr, temp, keys_in, keys_out, perm_in, perm_out,
                                                     static_cast<int>(nnz), 0, end_bit, s);
@@ -240,7 +240,6 @@ cudaError_t sort_keys(int64_t nnz, int end_bit, unsigned long long *keys_in, uns
     e = cub::DeviceRadixSort::SortPairs(tmp, temp, keys_in, keys_out, perm_in, perm_out,
                                         static_cast<int>(nnz), 0, end_bit, s);
     cudaError_t f = cudaFreeAsync(tmp, s);
-    (void)pooled;
     return e != cudaSuccess ? e : f;
 }
 

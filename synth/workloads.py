@@ -93,8 +93,6 @@ def _distinct_first(draw, target: int, bits: int, batch: int) -> np.ndarray:
     """Draw sorted tuples with ``draw(m)`` until ``target`` distinct ones exist;
     keep first occurrences in draw order."""
     parts = []
-    total = 0
-    have = None
     rounds = 0
     while True:
         rounds += 1

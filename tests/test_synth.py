@@ -1,10 +1,8 @@
 """The seeded input generators (synth/): deterministic, canonical, distinct,
 and with the structure BASELINE.json asks for.  CPU only."""
 import hashlib
-import math
 
 import numpy as np
-import pytest
 
 from synth import CONFIGS, generate, scramble, small_random
 from synth.workloads import make, run_lengths
