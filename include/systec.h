@@ -180,6 +180,19 @@ SYSTEC_API int systec_cp_als_sym(systec_plan plan, float *B, int R, float *lambd
                                  double *fit_host, int *iters_done, systec_stream_t stream);
 
 /*
+ * Single-source shortest paths by Bellman-Ford over a symmetric sparse matrix
+ * of edge weights (an order-2 plan: stored (i, j, w) is the undirected edge
+ * i-j): dist [dim] (device, out) starts at +inf except dist[source] = 0 and is
+ * relaxed with systec_plan_minplus until no entry changes or max_iters
+ * relaxations ran; *iters_done (may be NULL) receives the relaxations done,
+ * counting the last one that changed nothing.  Weights must not create
+ * negative cycles (an undirected negative edge is one).  Synchronises `stream`
+ * once per iteration.  Errors: ARG, UNSUPPORTED (order != 2), NOMEM, CUDA.
+ */
+SYSTEC_API int systec_plan_sssp(systec_plan plan, int64_t source, float *dist, int max_iters, int *iters_done,
+                                systec_stream_t stream);
+
+/*
  * Symmetric TTM with visible output symmetry (the
  * paper's TTM, Listings 1-3 PAPER.md:262-325), order-3 plans:
  *     C[i, j, l] = sum_k A[k, j, l] B[k, i],    C[i,j,l] = C[i,l,j]

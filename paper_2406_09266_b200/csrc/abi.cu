@@ -330,6 +330,38 @@ int systec_cp_als_sym(systec_plan plan, float *B, int R, float *lambda, int max_
     return rc;
 }
 
+int systec_plan_sssp(systec_plan plan, int64_t source, float *dist, int max_iters, int *iters_done,
+                     systec_stream_t stream) {
+    Plan *p = reinterpret_cast<Plan *>(plan);
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (!p || !dist || max_iters < 0 || source < 0 || source >= p->dim) return SYSTEC_ERR_ARG;
+    if (p->order != 2 || p->general) return SYSTEC_ERR_UNSUPPORTED;
+    float *y = nullptr;
+    int *flag = nullptr;
+    int done = 0, h_flag = 0;
+    cudaError_t e;
+    do {
+        if ((e = cudaMallocAsync(&y, static_cast<size_t>(p->dim) * 4, s)) != cudaSuccess) break;
+        if ((e = cudaMallocAsync(&flag, sizeof(int), s)) != cudaSuccess) break;
+        if ((e = systec::launch_sssp_init(dist, p->dim, source, s)) != cudaSuccess) break;
+        // one (min,+) relaxation per iteration until nothing changes (Bellman-Ford)
+        for (; done < max_iters; ++done) {
+            if ((e = systec::launch_minplus(*p, dist, y, reinterpret_cast<int *>(y), s)) != cudaSuccess) break;
+            if ((e = systec::launch_changed(y, dist, p->dim, flag, s)) != cudaSuccess) break;
+            if ((e = cudaMemcpyAsync(dist, y, static_cast<size_t>(p->dim) * 4, cudaMemcpyDeviceToDevice, s)) != cudaSuccess) break;
+            if ((e = cudaMemcpyAsync(&h_flag, flag, sizeof(int), cudaMemcpyDeviceToHost, s)) != cudaSuccess) break;
+            if ((e = cudaStreamSynchronize(s)) != cudaSuccess) break;
+            if (!h_flag) break;
+        }
+    } while (false);
+    if (y) cudaFreeAsync(y, s);
+    if (flag) cudaFreeAsync(flag, s);
+    if (iters_done) *iters_done = done + (h_flag == 0 && done < max_iters ? 1 : 0);
+    if (e != cudaSuccess) return systec::cuda_fail(e);
+    e = cudaStreamSynchronize(s);
+    return e == cudaSuccess ? SYSTEC_OK : systec::cuda_fail(e);
+}
+
 int systec_plan_ttm(systec_plan plan, const float *B, int R, float *C_packed, systec_stream_t stream) {
     Plan *p = reinterpret_cast<Plan *>(plan);
     if (!p || !B || !C_packed || R < 1) return SYSTEC_ERR_ARG;

@@ -41,7 +41,7 @@ EXPORTS = ["systec_mttkrp", "systec_mttkrp_host", "systec_plan_create", "systec_
            "systec_plan_copy_prepared", "systec_plan_last_launch", "systec_plan_destroy",
            "systec_status_string", "systec_last_cuda_error", "systec_version", "systec_last_bad_entry",
            "systec_plan_create_general", "systec_expand_symmetric", "systec_plan_minplus",
-           "systec_cp_als_sym", "systec_plan_ttm", "systec_ttm_unpack"]
+           "systec_cp_als_sym", "systec_plan_ttm", "systec_ttm_unpack", "systec_plan_sssp"]
 
 _lib = None
 
@@ -64,6 +64,7 @@ def load(path: str | None = None):
     lib.systec_plan_create_general.argtypes = [ctypes.POINTER(vp), i32, i64, i64, vp, vp, vp]
     lib.systec_plan_minplus.argtypes = [vp, vp, vp, vp]
     lib.systec_plan_ttm.argtypes = [vp, vp, i32, vp, vp]
+    lib.systec_plan_sssp.argtypes = [vp, i64, vp, i32, ctypes.POINTER(i32), vp]
     lib.systec_ttm_unpack.argtypes = [i64, i32, vp, vp, vp]
     lib.systec_cp_als_sym.argtypes = [vp, vp, i32, vp, i32, ctypes.c_double, vp, ctypes.POINTER(i32), vp]
     lib.systec_expand_symmetric.argtypes = [i32, i64, i64, vp, vp, i64, vp, vp, ctypes.POINTER(i64), vp]
@@ -197,6 +198,17 @@ class Plan:
                                         max_iters, tol, fits.ctypes.data_as(ctypes.c_void_p), ctypes.byref(done),
                                         _stream_handle(stream)), "systec_cp_als_sym")
         return B, lam, fits[:done.value]
+
+    def sssp(self, source: int, max_iters: int | None = None, stream=None):
+        """``systec_plan_sssp`` (order-2 plans): Bellman-Ford distances from
+        ``source``; returns (dist CUDA tensor [dim], relaxations done)."""
+        import torch
+        dist = torch.empty(self.dim, dtype=torch.float32, device="cuda")
+        done = ctypes.c_int()
+        it = self.dim if max_iters is None else max_iters
+        _check(load().systec_plan_sssp(self._h, source, ctypes.c_void_p(dist.data_ptr()), it, ctypes.byref(done),
+                                       _stream_handle(stream)), "systec_plan_sssp")
+        return dist, done.value
 
     def ttm(self, B, packed=None, full: bool = False, stream=None):
         """``systec_plan_ttm`` (order-3 plans): packed canonical half

@@ -516,3 +516,19 @@ def test_single_giant_run_and_all_singleton_runs(systec, R):
     w2 = Workload("singles", 3, dim, R, np.ascontiguousarray(idx2), vals[:dim].copy(), B)
     Cref2, S2 = oracle.mttkrp(3, dim, w2.idx, w2.vals, B)
     parity(run(systec, w2), Cref2, S2)
+
+
+@pytest.mark.parametrize("dim,nnz", [(300, 2000), (20000, 200000)])
+def test_sssp_bit_exact_vs_iterated_oracle(systec, dim, nnz):
+    import torch
+    from test_oracle_pins import oracle_sssp
+    w = make(f"g{dim}", 2, dim, nnz, 1, seed=dim, mode="uniform")
+    vals = np.random.default_rng(dim).uniform(0.1, 5.0, nnz).astype(np.float32)
+    want, iters = oracle_sssp(dim, w.idx, vals, 3)
+    plan = systec.Plan(2, dim, *to_dev(w.idx, vals))
+    dist, done = plan.sssp(3)
+    torch.cuda.synchronize()
+    assert np.array_equal(dist.cpu().numpy(), want) and done == iters
+    dist2, done2 = plan.sssp(3, max_iters=2)
+    torch.cuda.synchronize()
+    assert done2 == 2

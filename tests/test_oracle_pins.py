@@ -392,3 +392,32 @@ def test_ttm_oracle_vs_einsum():
     got = oracle.ttm_sym3(9, si, sv, w.B)
     np.testing.assert_allclose(got, want, rtol=1e-12, atol=1e-12)
     assert np.allclose(got, got.transpose(1, 0, 2))                   # visible output symmetry
+
+
+def oracle_sssp(dim, idx, vals, source, max_iters=None):
+    """Bellman-Ford by iterating the (min,+) relaxation oracle until no change."""
+    d = np.full(dim, np.inf, np.float32)
+    d[source] = 0
+    it = 0
+    for it in range(1, (max_iters or dim) + 1):
+        y = oracle.minplus_sym2(dim, idx, vals, d)
+        if np.array_equal(y, d):
+            return y, it
+        d = y
+    return d, it
+
+
+def test_sssp_oracle_vs_scipy_shortest_path():
+    """Pin of the iterated relaxation against scipy's Dijkstra on the same
+    undirected graph (fp32 sums vs fp64: 1e-5 relative)."""
+    from scipy.sparse import coo_matrix
+    from scipy.sparse.csgraph import shortest_path
+    w = small_random(2, 300, 2000, 1, seed=4, diag_frac=0.0)
+    vals = np.random.default_rng(2).uniform(0.1, 5.0, w.nnz).astype(np.float32)
+    A = coo_matrix((vals.astype(np.float64), (w.idx[:, 0], w.idx[:, 1])), shape=(300, 300)).tocsr()
+    want = shortest_path(A, method="D", directed=False, indices=7)
+    got, iters = oracle_sssp(300, w.idx, vals, 7)
+    finite = np.isfinite(want)
+    assert np.array_equal(np.isfinite(got), finite)
+    np.testing.assert_allclose(got[finite], want[finite], rtol=1e-5)
+    assert iters > 1
