@@ -532,3 +532,22 @@ def test_sssp_bit_exact_vs_iterated_oracle(systec, dim, nnz):
     dist2, done2 = plan.sssp(3, max_iters=2)
     torch.cuda.synchronize()
     assert done2 == 2
+
+
+def test_execute_argument_errors(systec):
+    import torch
+    w = small_random(3, 50, 500, 64, seed=1)
+    di, dv, dB = to_dev(w.idx, w.vals, w.B)
+    plan = systec.Plan(3, 50, di, dv)
+    with pytest.raises(ValueError, match="aliases"):          # C overlapping B
+        plan.execute(dB, dB)
+    with pytest.raises(ValueError, match="invalid argument"):  # E*K not a multiple of 4 (R=64: 2 groups)
+        plan.execute(dB, K=3)
+    with pytest.raises(ValueError, match="invalid argument"):
+        plan.execute(dB, vpl=3)
+    with pytest.raises(TypeError):
+        plan.execute(dB, no_such_option=1)
+    C = plan.execute(dB)                                         # the plan is still usable
+    torch.cuda.synchronize()
+    Cref, S = oracle.mttkrp(3, 50, w.idx, w.vals, w.B)
+    parity(C.cpu().numpy(), Cref, S)
