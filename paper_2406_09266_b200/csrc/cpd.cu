@@ -28,78 +28,134 @@ namespace systec {
 
 namespace {
 
-constexpr int kMaxCpR = 48;  // two fp64 R x R tiles + a 256-double scratch in static shared memory
+constexpr int kMaxCpR = 48;  // [R][2R] fp64 Gauss-Jordan tableau (36 KB) in static shared memory
 
-// Two-stage column reductions (no global atomics): each block owns a contiguous
-// row range and writes its partial sums; sum_partials_kernel adds the blocks.
-//   gram:   part[blk][a*R+b] = sum_{i in blk} B[i][a] B[i][b]       (fp64)
-//   coldot: part[blk][r]     = sum_{i in blk} X[i][r] Y[i][r]
-__global__ void gram_partial_kernel(const float *__restrict__ B, int64_t dim, int R, double *__restrict__ part) {
-    // rows of this block staged in shared memory in tiles, pairs accumulated in fp64
-    constexpr int kTileRows = 64;
-    __shared__ float tile[kTileRows * kMaxCpR];
+// Two-stage reductions (no global atomics): every block owns a contiguous row
+// range and writes fp64 partial sums; reduce_partials_kernel adds the blocks.
+//
+// gram_dots_partial_kernel: part[blk][a*R+b] = sum_{i in blk} B[i][a] B[i][b]
+//                           part[blk][R*R+r] = sum_{i in blk} M[i][r] B[i][r]
+// Rows are staged in shared memory in tiles of kTileRows; each thread owns a
+// 4x4 register tile of (a, b) pairs for one row group (rows i = g mod RG) and
+// accumulates a tile in fp32 before adding it to fp64; the row groups are
+// summed in shared memory.  (Reading the rows straight from L1 instead, no
+// staging, measured 3x slower.)
+constexpr int kTileRows = 128;
+constexpr int kRp = (kMaxCpR + 3) / 4 * 4;  // padded column count (multiple of 4)
+
+// rows [r0, r0+nr) of X[.][R] -> dst[nr][Rp] (zero-padded columns; 16-byte
+// loads, all of a thread's loads issued before its stores)
+__device__ __forceinline__ void stage_rows(float *__restrict__ dst, const float *__restrict__ X, int64_t r0, int nr,
+                                           int R, int Rp) {
+    const int tid = threadIdx.x, nt = blockDim.x;
+    if (Rp == R) {  // contiguous rows: a 16-byte copy (R % 4 == 0 keeps every row aligned)
+        const int n4 = nr * R / 4;
+        const float4 *s4 = reinterpret_cast<const float4 *>(X + r0 * R);
+        float4 *d4 = reinterpret_cast<float4 *>(dst);
+        for (int q = tid; q < n4; q += 4 * nt) {
+            float4 v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (q + u * nt < n4) v[u] = __ldg(s4 + q + u * nt);
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (q + u * nt < n4) d4[q + u * nt] = v[u];
+        }
+    } else {
+        for (int q = tid; q < nr * Rp; q += nt) {
+            const int i = q / Rp, c = q % Rp;
+            dst[q] = c < R ? __ldg(X + (r0 + i) * R + c) : 0.f;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) gram_dots_partial_kernel(const float *__restrict__ B, const float *__restrict__ M,
+                                                                int64_t dim, int R, double *__restrict__ part) {
+    extern __shared__ __align__(16) unsigned char cpd_smem[];
+    float *tb = reinterpret_cast<float *>(cpd_smem);  // [kTileRows][Rp] of B
+    float *tm = tb + kTileRows * kRp;                 // [kTileRows][Rp] of M
+    double *red = reinterpret_cast<double *>(cpd_smem);  // reused after the row loop
+    const int Rp = (R + 3) & ~3;
+    const int T4 = Rp / 4;           // 4-wide column blocks
+    const int MT = T4 * T4;          // micro-tiles
+    const int RG = blockDim.x / MT;  // row groups
+    const int tid = threadIdx.x;
+    const int mt = tid % MT, g = tid / MT;
+    const int a0 = (mt / T4) * 4, b0 = (mt % T4) * 4;
+    const bool active = g < RG;
     const int64_t rows = (dim + gridDim.x - 1) / gridDim.x;
     const int64_t lo = blockIdx.x * rows, hi = min(dim, lo + rows);
-    constexpr int kPairsPerThread = (kMaxCpR * kMaxCpR + 255) / 256;
-    double acc[kPairsPerThread];
+    double acc[16];
 #pragma unroll
-    for (int k = 0; k < kPairsPerThread; ++k) acc[k] = 0.0;
+    for (int k = 0; k < 16; ++k) acc[k] = 0.0;
+    double dacc = 0.0;  // column dot: thread (column tid % R, row lane tid / R)
+    const int dl = tid / R, dn = blockDim.x / R;
     for (int64_t r0 = lo; r0 < hi; r0 += kTileRows) {
         const int nr = static_cast<int>(min(static_cast<int64_t>(kTileRows), hi - r0));
         __syncthreads();
-        for (int q = threadIdx.x; q < nr * R; q += blockDim.x) tile[q] = B[r0 * R + q];
+        stage_rows(tb, B, r0, nr, R, Rp);
+        stage_rows(tm, M, r0, nr, R, Rp);
         __syncthreads();
+        if (active) {
+            float f[16];
 #pragma unroll
-        for (int k = 0; k < kPairsPerThread; ++k) {
-            const int pidx = threadIdx.x + k * blockDim.x;
-            if (pidx < R * R) {
-                const int a = pidx / R, b = pidx % R;
-                double s0 = 0.0, s1 = 0.0;
-                int i = 0;
-                for (; i + 1 < nr; i += 2) {
-                    s0 += static_cast<double>(tile[i * R + a]) * tile[i * R + b];
-                    s1 += static_cast<double>(tile[(i + 1) * R + a]) * tile[(i + 1) * R + b];
-                }
-                if (i < nr) s0 += static_cast<double>(tile[i * R + a]) * tile[i * R + b];
-                acc[k] += s0 + s1;
+            for (int k = 0; k < 16; ++k) f[k] = 0.f;
+#pragma unroll 2
+            for (int i = g; i < nr; i += RG) {
+                const float4 x = *reinterpret_cast<const float4 *>(tb + i * Rp + a0);
+                const float4 y = *reinterpret_cast<const float4 *>(tb + i * Rp + b0);
+                const float xa[4] = {x.x, x.y, x.z, x.w}, yb[4] = {y.x, y.y, y.z, y.w};
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+#pragma unroll
+                    for (int v = 0; v < 4; ++v) f[u * 4 + v] = fmaf(xa[u], yb[v], f[u * 4 + v]);
             }
+#pragma unroll
+            for (int k = 0; k < 16; ++k) acc[k] += f[k];
+        }
+        if (dl < dn) {
+            const int c = tid % R;
+            float d = 0.f;
+            for (int i = dl; i < nr; i += dn) d = fmaf(tm[i * Rp + c], tb[i * Rp + c], d);
+            dacc += d;
         }
     }
+    __syncthreads();  // tiles no longer needed: sum the row groups in shared memory
+    double *dred = red + kRp / 4 * (kRp / 4) * 16;  // [256] after the pair sums
+    dred[tid] = dl < dn ? dacc : 0.0;
+    const int W = R * R + R;
+    double *out = part + static_cast<int64_t>(blockIdx.x) * W;
+    for (int grp = 0; grp < RG; ++grp) {
+        if (active && g == grp) {
 #pragma unroll
-    for (int k = 0; k < kPairsPerThread; ++k) {
-        const int pidx = threadIdx.x + k * blockDim.x;
-        if (pidx < R * R) part[static_cast<int64_t>(blockIdx.x) * R * R + pidx] = acc[k];
+            for (int k = 0; k < 16; ++k) red[mt * 16 + k] = (grp == 0 ? 0.0 : red[mt * 16 + k]) + acc[k];
+        }
+        __syncthreads();
+    }
+    for (int q = tid; q < MT * 16; q += blockDim.x) {
+        const int m = q / 16, k = q % 16;
+        const int a = (m / T4) * 4 + k / 4, b = (m % T4) * 4 + k % 4;
+        if (a < R && b < R) out[a * R + b] = red[q];
+    }
+    if (tid < R) {
+        double d = 0.0;
+        for (int l = 0; l < dn; ++l) d += dred[l * R + tid];
+        out[R * R + tid] = d;
     }
 }
 
-__global__ void coldot_partial_kernel(const float *__restrict__ X, const float *__restrict__ Y, int64_t dim, int R,
-                                      double *__restrict__ part) {
-    const int64_t rows = (dim + gridDim.x - 1) / gridDim.x;
-    const int64_t lo = blockIdx.x * rows, hi = min(dim, lo + rows);
-    // blockDim = 256: 256/R row lanes x R columns
-    const int lanes = blockDim.x / R;
-    const int r = threadIdx.x % R, li = threadIdx.x / R;
-    __shared__ double red[256];
-    double acc = 0.0;
-    if (li < lanes)
-        for (int64_t i = lo + li; i < hi; i += lanes)
-            acc += static_cast<double>(X[i * R + r]) * static_cast<double>(Y[i * R + r]);
-    red[threadIdx.x] = (li < lanes) ? acc : 0.0;
-    __syncthreads();
-    if (threadIdx.x < R) {
-        double s = 0.0;
-        for (int k = 0; k < lanes; ++k) s += red[k * R + threadIdx.x];
-        part[static_cast<int64_t>(blockIdx.x) * R + threadIdx.x] = s;
-    }
-}
-
-// out[q] = sum_blk part[blk][q], q < width
-__global__ void sum_partials_kernel(const double *__restrict__ part, int blocks, int width, double *__restrict__ out) {
-    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+// out[q] = sum_blk part[blk][q], q < width: one warp per output, lanes stride
+// over the blocks, shuffle-reduced (fixed order: deterministic)
+__global__ void reduce_partials_kernel(const double *__restrict__ part, int blocks, int width,
+                                       double *__restrict__ out) {
+    const int q = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
     if (q >= width) return;
     double s = 0.0;
-    for (int b = 0; b < blocks; ++b) s += part[static_cast<int64_t>(b) * width + q];
-    out[q] = s;
+    for (int b = lane; b < blocks; b += 32) s += part[static_cast<int64_t>(b) * width + q];
+#pragma unroll
+    for (int d = 16; d; d >>= 1) s += __shfl_down_sync(0xffffffffu, s, d);
+    if (lane == 0) out[q] = s;
 }
 
 // ||X||^2 = sum_e v_e^2 orbit_e over the plan's canonical stream
@@ -133,96 +189,187 @@ __global__ void tensor_norm_kernel(const int32_t *__restrict__ coords, int64_t l
     if ((threadIdx.x & 31) == 0) atomicAdd(out, acc);
 }
 
-// One block (blockDim = 256): H = G^{.(n-1)}, Cholesky H = L L^T (tiny relative
-// ridge for safety), Hinv = H^{-1}; with lam: ||Xhat||^2 = lam^T G^{.n} lam and
-// <X,Xhat> = lam . dots.  Right-looking Cholesky, one column step per barrier.
-__global__ void small_solve_kernel(const double *__restrict__ G, int R, int n, float *__restrict__ Hinv,
-                                   const float *__restrict__ lam, const double *__restrict__ dots,
-                                   double *__restrict__ xhat2) {
-    __shared__ double L[kMaxCpR * kMaxCpR];
-    __shared__ double Inv[kMaxCpR * kMaxCpR];
-    __shared__ double red[256];
+// One block of 1024 threads: H = G^{.(n-1)} (+ a tiny relative ridge for
+// safety), Hinv = H^{-1} by Gauss-Jordan elimination on the tableau [H | I] (H
+// is SPD: no pivoting).  The tableau lives in registers: thread t owns row
+// t / TPR and the CW columns [k*CW, (k+1)*CW), k = t % TPR (TPR = 64, 32, 16
+// for R <= 16, 32, 48; CW = 1, 2, 6); each step publishes the pivot row and
+// the pivot column through shared memory (double-buffered: two barriers per
+// step).  With lam also the fit pieces ||Xhat||^2 = lam^T G^{.n} lam and
+// <X,Xhat> = lam . dots.
+template <int CW>
+__global__ void __launch_bounds__(1024) small_solve_kernel(const double *__restrict__ G, int R, int n,
+                                                           float *__restrict__ Hinv, const float *__restrict__ lam,
+                                                           const double *__restrict__ dots,
+                                                           double *__restrict__ xhat2) {
+    constexpr int TPR = CW == 1 ? 64 : CW == 2 ? 32 : 16;
+    __shared__ double piv[2][2 * kMaxCpR];
+    __shared__ double fcol[2][kMaxCpR];
+    __shared__ double red[1024];
+    __shared__ double ridge_s;
     const int tid = threadIdx.x, nt = blockDim.x;
+    const int W2 = 2 * R;
+    const int row = tid / TPR, k = tid % TPR;
+    const bool own = row < R;
+    const int c0 = k * CW;
+    if (tid < 32) {  // trace of H (one warp)
+        double tr = 0.0;
+        for (int a = tid; a < R; a += 32) {
+            double h = 1.0;
+            for (int q = 0; q < n - 1; ++q) h *= G[a * R + a];
+            tr += h;
+        }
+#pragma unroll
+        for (int d = 16; d; d >>= 1) tr += __shfl_down_sync(0xffffffffu, tr, d);
+        if (tid == 0) ridge_s = 1e-12 * (tr / R + 1e-300);
+    }
+    __syncthreads();
+    double A[CW];
     double fit_part = 0.0;
-    for (int p = tid; p < R * R; p += nt) {
-        double h = 1.0;
-        for (int k = 0; k < n - 1; ++k) h *= G[p];
-        L[p] = h;
-        if (lam) fit_part += static_cast<double>(lam[p / R]) * lam[p % R] * h * G[p];
+#pragma unroll
+    for (int u = 0; u < CW; ++u) {
+        const int c = c0 + u;
+        double v = 0.0;
+        if (own && c < W2) {
+            if (c < R) {
+                const double gp = G[row * R + c];
+                double h = 1.0;
+                for (int q = 0; q < n - 1; ++q) h *= gp;
+                if (lam) fit_part += static_cast<double>(lam[row]) * lam[c] * h * gp;
+                v = h + (c == row ? ridge_s : 0.0);
+            } else {
+                v = (c - R == row) ? 1.0 : 0.0;
+            }
+        }
+        A[u] = v;
     }
     red[tid] = fit_part;
     __syncthreads();
-    if (lam && xhat2 && tid == 0) {
-        double s = 0.0, ip = 0.0;
-        for (int k = 0; k < nt; ++k) s += red[k];
+    for (int w = nt / 2; w > 0; w >>= 1) {  // block reduction (fixed order)
+        if (tid < w) red[tid] += red[tid + w];
+        __syncthreads();
+    }
+    if (tid == 0 && lam && xhat2) {
+        double ip = 0.0;
         for (int a = 0; a < R; ++a) ip += static_cast<double>(lam[a]) * dots[a];
-        xhat2[0] = s;
+        xhat2[0] = red[0];
         xhat2[1] = ip;
     }
-    if (tid == 0) {
-        double tr = 0.0;
-        for (int a = 0; a < R; ++a) tr += L[a * R + a];
-        const double ridge = 1e-12 * (tr / R + 1e-300);
-        for (int a = 0; a < R; ++a) L[a * R + a] += ridge;
-    }
-    __syncthreads();
-    for (int j = 0; j < R; ++j) {  // right-looking Cholesky (lower triangle of L)
-        if (tid == 0) L[j * R + j] = sqrt(fmax(L[j * R + j], 1e-300));
-        __syncthreads();
-        const double d = L[j * R + j];
-        for (int i = j + 1 + tid; i < R; i += nt) L[i * R + j] /= d;
-        __syncthreads();
-        for (int p = tid; p < (R - j - 1) * (R - j - 1); p += nt) {
-            const int i = j + 1 + p / (R - j - 1), k = j + 1 + p % (R - j - 1);
-            if (k <= i) L[i * R + k] -= L[i * R + j] * L[k * R + j];
+    for (int j = 0; j < R; ++j) {
+        const int bsel = j & 1;
+        // publish column j (every row) and row j's raw values
+#pragma unroll
+        for (int u = 0; u < CW; ++u) {
+            const int c = c0 + u;
+            if (own && c < W2) {
+                if (c == j) fcol[bsel][row] = A[u];
+                if (row == j) piv[bsel][c] = A[u];
+            }
         }
         __syncthreads();
-    }
-    // columns of the inverse: solve L L^T x = e_c, one column per thread
-    for (int c = tid; c < R; c += nt) {
-        double y[kMaxCpR];
-        for (int i = 0; i < R; ++i) {
-            double sacc = (i == c) ? 1.0 : 0.0;
-            for (int k = 0; k < i; ++k) sacc -= L[i * R + k] * y[k];
-            y[i] = sacc / L[i * R + i];
+        if (own) {
+            const double inv = 1.0 / piv[bsel][j];
+            const double f = fcol[bsel][row];
+#pragma unroll
+            for (int u = 0; u < CW; ++u) {
+                const int c = c0 + u;
+                if (c < W2) {
+                    const double pj = piv[bsel][c] * inv;
+                    A[u] = (row == j) ? pj : fma(-f, pj, A[u]);
+                }
+            }
         }
-        for (int i = R - 1; i >= 0; --i) {
-            double sacc = y[i];
-            for (int k = i + 1; k < R; ++k) sacc -= L[k * R + i] * Inv[k * R + c];
-            Inv[i * R + c] = sacc / L[i * R + i];
-        }
+        __syncthreads();  // buffers of step j free for step j + 2
     }
-    __syncthreads();
-    for (int p = tid; p < R * R; p += nt) Hinv[p] = static_cast<float>(Inv[p]);
-}
-
-// Bout[i][b] = sum_a M[i][a] Hinv[a][b]
-__global__ void apply_inverse_kernel(const float *__restrict__ M, const float *__restrict__ Hinv, int64_t dim, int R,
-                                     float *__restrict__ Bout) {
-    __shared__ float Hs[kMaxCpR * kMaxCpR];
-    for (int p = threadIdx.x; p < R * R; p += blockDim.x) Hs[p] = Hinv[p];
-    __syncthreads();
-    const int64_t total = dim * R;
-    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t i = q / R;
-        const int b = static_cast<int>(q % R);
-        float s = 0.f;
-        for (int a = 0; a < R; ++a) s += M[i * R + a] * Hs[a * R + b];
-        Bout[q] = s;
+#pragma unroll
+    for (int u = 0; u < CW; ++u) {
+        const int c = c0 + u;
+        if (own && c >= R && c < W2) Hinv[row * R + (c - R)] = static_cast<float>(A[u]);
     }
 }
 
-// lam[b] = sqrt(norms[b]); B[i][b] /= lam[b]
+// Bout = M Hinv and per-block column sums of squares of Bout (the norms of the
+// new factor) into part[blk][R].  RT = R rounded up to a multiple of 8: thread
+// (column b, row group) keeps Hinv[:, b] in registers and reads each staged M
+// row as 16-byte broadcasts.
+template <int RT>
+__global__ void __launch_bounds__(256) apply_inverse_kernel(const float *__restrict__ M, const float *__restrict__ Hinv,
+                                                            int64_t dim, int R, float *__restrict__ Bout,
+                                                            double *__restrict__ part) {
+    __shared__ __align__(16) float Ms[kTileRows * RT];
+    __shared__ double sq[256];
+    const int tid = threadIdx.x;
+    const int b = tid % RT, rg = tid / RT;
+    constexpr int RGN = 256 / RT;
+    const bool active = rg < RGN && b < R;
+    float h[RT];
+#pragma unroll
+    for (int a = 0; a < RT; ++a) h[a] = (active && a < R) ? Hinv[a * R + b] : 0.f;
+    const int64_t rows = (dim + gridDim.x - 1) / gridDim.x;
+    const int64_t lo = blockIdx.x * rows, hi = min(dim, lo + rows);
+    double acc = 0.0;
+    for (int64_t r0 = lo; r0 < hi; r0 += kTileRows) {
+        const int nr = static_cast<int>(min(static_cast<int64_t>(kTileRows), hi - r0));
+        __syncthreads();
+        stage_rows(Ms, M, r0, nr, R, RT);
+        __syncthreads();
+        if (active) {
+            float t = 0.f;
+            for (int i = rg; i < nr; i += RGN) {
+                const float4 *m4 = reinterpret_cast<const float4 *>(Ms + i * RT);
+                float s = 0.f;
+#pragma unroll
+                for (int a4 = 0; a4 < RT / 4; ++a4) {
+                    const float4 x = m4[a4];
+                    s = fmaf(x.x, h[4 * a4 + 0], s);
+                    s = fmaf(x.y, h[4 * a4 + 1], s);
+                    s = fmaf(x.z, h[4 * a4 + 2], s);
+                    s = fmaf(x.w, h[4 * a4 + 3], s);
+                }
+                Bout[(r0 + i) * R + b] = s;
+                t = fmaf(s, s, t);
+            }
+            acc += t;
+        }
+    }
+    sq[tid] = active ? acc : 0.0;
+    __syncthreads();
+    if (tid < R) {
+        double s2 = 0.0;
+        for (int g2 = 0; g2 < RGN; ++g2) s2 += sq[g2 * RT + tid];
+        part[static_cast<int64_t>(blockIdx.x) * R + tid] = s2;
+    }
+}
+
+// lam[b] = sqrt(norms[b]); B[i][b] /= lam[b] (fp32 division by the fp32 norm;
+// 16-byte accesses when R % 4 == 0)
 __global__ void normalize_kernel(float *__restrict__ B, int64_t dim, int R, const double *__restrict__ norms,
                                  float *__restrict__ lam) {
-    const int64_t total = dim * R;
-    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
-        const int b = static_cast<int>(q % R);
-        const double nb = sqrt(norms[b]);
-        B[q] = nb > 0 ? static_cast<float>(B[q] / nb) : B[q];
+    __shared__ float nb[kMaxCpR];
+    for (int b = threadIdx.x; b < R; b += blockDim.x) {
+        nb[b] = static_cast<float>(sqrt(norms[b]));
+        if (blockIdx.x == 0) lam[b] = nb[b];
     }
-    if (blockIdx.x == 0)
-        for (int b = threadIdx.x; b < R; b += blockDim.x) lam[b] = static_cast<float>(sqrt(norms[b]));
+    __syncthreads();
+    const int64_t total = dim * R;
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    if ((R & 3) == 0) {
+        float4 *B4 = reinterpret_cast<float4 *>(B);
+        for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total / 4; q += stride) {
+            const int b = static_cast<int>((q * 4) % R);
+            float4 v = B4[q];
+            if (nb[b + 0] > 0.f) v.x /= nb[b + 0];
+            if (nb[b + 1] > 0.f) v.y /= nb[b + 1];
+            if (nb[b + 2] > 0.f) v.z /= nb[b + 2];
+            if (nb[b + 3] > 0.f) v.w /= nb[b + 3];
+            B4[q] = v;
+        }
+    } else {
+        for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total; q += stride) {
+            const int b = static_cast<int>(q % R);
+            if (nb[b] > 0.f) B[q] /= nb[b];
+        }
+    }
 }
 
 int sm_count() {
@@ -250,30 +397,46 @@ cudaError_t cpd_tensor_norm2(const Plan &p, double *out, cudaStream_t s) {
     return cudaGetLastError();
 }
 
-int cpd_partial_blocks() { return sm_count() * 4; }
+// partial blocks: >= 256 rows each, at most 2 per SM
+int cpd_partial_blocks() { return sm_count() * 2; }
 
-// scratch (doubles): G[R*R], dots[R], norms[R], scalars[2] = {||Xhat||^2, <X,Xhat>},
-// then partials[PB][R*R] | floats: Hinv[R*R]
-int64_t cpd_scratch_doubles(int R) { return static_cast<int64_t>(R) * R + 2 * R + 2 + static_cast<int64_t>(cpd_partial_blocks()) * R * R; }
+size_t gram_smem_bytes() {
+    const size_t tiles = 2ull * kTileRows * kRp * sizeof(float);
+    const size_t redb = (static_cast<size_t>(kRp / 4) * (kRp / 4) * 16 + 256) * sizeof(double);  // row-group sums
+    return std::max(tiles, redb);  // 48 KB: within the default dynamic shared-memory limit
+}
+
+// scratch (doubles): G[R*R], dots[R] (contiguous: one reduction), norms[R],
+// scalars[2] = {||Xhat||^2, <X,Xhat>}, then partials[PB][R*R+R] | floats: Hinv[R*R]
+int64_t cpd_scratch_doubles(int R) {
+    return static_cast<int64_t>(R) * R + 2 * R + 2 + static_cast<int64_t>(cpd_partial_blocks()) * (R * R + R);
+}
 
 cudaError_t cpd_step(const Plan &p, const float *M, float *B, float *lam, int R, double *dscratch,
                      float *fscratch, bool have_lam, bool fit_only, cudaStream_t s) {
     double *G = dscratch, *dots = G + R * R, *norms = dots + R, *xhat2 = norms + R, *part = xhat2 + 2;
     float *Hinv = fscratch;
-    // partial blocks: ~128 rows each, at most 4 per SM
-    const int PB = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(cpd_partial_blocks(), (p.dim + 127) / 128)));
-    const int rr = R * R;
-    gram_partial_kernel<<<PB, 256, 0, s>>>(B, p.dim, R, part);
-    sum_partials_kernel<<<(rr + 255) / 256, 256, 0, s>>>(part, PB, rr, G);
-    coldot_partial_kernel<<<PB, 256, 0, s>>>(M, B, p.dim, R, part);   // <X,Xhat> pieces of the current iterate
-    sum_partials_kernel<<<1, 64, 0, s>>>(part, PB, R, dots);
-    small_solve_kernel<<<1, 256, 0, s>>>(G, R, p.order, Hinv, have_lam ? lam : nullptr, dots, xhat2);
+    const int PB = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(cpd_partial_blocks(), (p.dim + 255) / 256)));
+    const int W = R * R + R;
+    const size_t gsm = gram_smem_bytes();
+    gram_dots_partial_kernel<<<PB, 256, gsm, s>>>(B, M, p.dim, R, part);
+    reduce_partials_kernel<<<(W + 7) / 8, 256, 0, s>>>(part, PB, W, G);  // G and dots (contiguous)
+    const float *lam_in = have_lam ? lam : nullptr;
+    if (R <= 16) small_solve_kernel<1><<<1, 1024, 0, s>>>(G, R, p.order, Hinv, lam_in, dots, xhat2);
+    else if (R <= 32) small_solve_kernel<2><<<1, 1024, 0, s>>>(G, R, p.order, Hinv, lam_in, dots, xhat2);
+    else small_solve_kernel<6><<<1, 1024, 0, s>>>(G, R, p.order, Hinv, lam_in, dots, xhat2);
     if (fit_only) return cudaGetLastError();
+    switch ((R + 7) / 8) {
+        case 1: apply_inverse_kernel<8><<<PB, 256, 0, s>>>(M, Hinv, p.dim, R, B, part); break;
+        case 2: apply_inverse_kernel<16><<<PB, 256, 0, s>>>(M, Hinv, p.dim, R, B, part); break;
+        case 3: apply_inverse_kernel<24><<<PB, 256, 0, s>>>(M, Hinv, p.dim, R, B, part); break;
+        case 4: apply_inverse_kernel<32><<<PB, 256, 0, s>>>(M, Hinv, p.dim, R, B, part); break;
+        case 5: apply_inverse_kernel<40><<<PB, 256, 0, s>>>(M, Hinv, p.dim, R, B, part); break;
+        default: apply_inverse_kernel<48><<<PB, 256, 0, s>>>(M, Hinv, p.dim, R, B, part); break;
+    }
+    reduce_partials_kernel<<<(R + 7) / 8, 256, 0, s>>>(part, PB, R, norms);
     const int64_t total = p.dim * R;
-    const int ab = static_cast<int>(std::min<int64_t>((total + 255) / 256, static_cast<int64_t>(sm_count()) * 8));
-    apply_inverse_kernel<<<ab, 256, 0, s>>>(M, Hinv, p.dim, R, B);
-    coldot_partial_kernel<<<PB, 256, 0, s>>>(B, B, p.dim, R, part);   // squared column norms of B_new
-    sum_partials_kernel<<<1, 64, 0, s>>>(part, PB, R, norms);
+    const int ab = static_cast<int>(std::min<int64_t>((total / 4 + 255) / 256 + 1, static_cast<int64_t>(sm_count()) * 8));
     normalize_kernel<<<ab, 256, 0, s>>>(B, p.dim, R, norms, lam);
     return cudaGetLastError();
 }
