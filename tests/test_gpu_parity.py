@@ -399,6 +399,30 @@ def test_cp_als_iterates_match_oracle(systec, order, dim, R):
     np.testing.assert_allclose(fits, fref, atol=2e-4)
 
 
+@pytest.mark.parametrize("order,dim,nnz,R", [(3, 600, 20000, 8), (3, 700, 30000, 13), (4, 300, 20000, 32),
+                                             (3, 1000, 40000, 37), (5, 60, 20000, 48), (3, 40000, 100000, 16)])
+def test_cp_als_ranks_and_tiles(systec, order, dim, nnz, R):
+    """CP-ALS kernels at every rank template (R padded to 8..48, R % 4 != 0
+    staging, register-tableau widths 1/2/6) and row ranges spanning several
+    blocks and staging tiles with a ragged tail, vs the fp64 reference."""
+    import torch
+    from oracle import cpd_ref
+    w = small_random(order, dim, nnz, R, seed=R + order, diag_frac=0.1)
+    iters = 2
+    Bref, lref, fref = cpd_ref.cp_als_sym(order, dim, w.idx, w.vals, w.B, iters=iters)
+    di, dv, dB = to_dev(w.idx, w.vals, w.B)
+    plan = systec.Plan(order, dim, di, dv)
+    B, lam_g, fits = plan.cp_als(dB, max_iters=iters, tol=0.0)
+    torch.cuda.synchronize()
+    Bg = B.cpu().numpy()
+    scale = np.abs(Bref).max()
+    print(f"cp_als n={order} R={R}: max|dB|/max|B| = {np.max(np.abs(Bg - Bref)) / scale:.2e}")
+    # fp32 MTTKRP / M*Hinv around fp64 reductions and solve: observed <= 1.3e-6
+    assert np.max(np.abs(Bg - Bref)) <= 2e-5 * scale, np.max(np.abs(Bg - Bref)) / scale
+    np.testing.assert_allclose(lam_g.cpu().numpy(), lref, rtol=2e-5)
+    np.testing.assert_allclose(fits, fref, atol=1e-5)
+
+
 def test_cp_als_recovers_planted_and_stops_early(systec):
     import torch
     from test_oracle_pins import planted
