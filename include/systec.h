@@ -200,8 +200,10 @@ SYSTEC_API int systec_plan_sssp(systec_plan plan, int64_t source, float *dist, i
  * C_packed [dim(dim+1)/2][R] (device; row pair(j,l) = l(l+1)/2 + j, rank
  * innermost), OVERWRITTEN.  B [dim][R] device.  Async on `stream`.
  * On a GENERAL order-3 plan (the naive baseline, e.g. over the expanded
- * tensor) every entry updates the full output and C_packed must hold the full
- * [dim][dim][R] tensor instead.
+ * tensor) the LAST mode is contracted — C[p0][p1][:] += v B[p2][:], the mode
+ * innermost in the sorted stream, so runs of equal (p0, p1) accumulate in
+ * registers — and C_packed must hold the full [dim][dim][R] tensor instead
+ * (for the expansion of a symmetric tensor: the same C as above).
  * Errors: ARG, UNSUPPORTED (order != 3), ALIAS, CUDA.
  */
 SYSTEC_API int systec_plan_ttm(systec_plan plan, const float *B, int R, float *C_packed, systec_stream_t stream);

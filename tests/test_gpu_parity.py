@@ -440,7 +440,8 @@ def test_cp_als_recovers_planted_and_stops_early(systec):
 
 
 # ---------------------------------------------------------------- NEXT-4: symmetric TTM
-@pytest.mark.parametrize("dim,nnz,R", [(30, 2000, 16), (64, 20000, 8), (20, 500, 3), (100, 50000, 32)])
+@pytest.mark.parametrize("dim,nnz,R", [(30, 2000, 16), (64, 20000, 8), (20, 500, 3), (100, 50000, 32),
+                                       (50, 5000, 160), (12, 300, 4), (200, 150000, 64)])
 def test_ttm_matches_oracle(systec, dim, nnz, R):
     import torch
     w = small_random(3, dim, nnz, R, seed=dim, diag_frac=0.2)
@@ -451,17 +452,24 @@ def test_ttm_matches_oracle(systec, dim, nnz, R):
     Cf = plan.ttm(dB, full=True)
     torch.cuda.synchronize()
     parity(Cf.cpu().numpy(), want, S)
+    # shuffled, non-canonical spelling: the same plan after prepare
+    si, sv = scramble(w.idx, w.vals, seed=dim)
+    plan2 = systec.Plan(3, dim, *to_dev(si, sv))
+    Cf2 = plan2.ttm(dB, full=True)
+    torch.cuda.synchronize()
+    parity(Cf2.cpu().numpy(), want, S)
 
 
-def test_ttm_general_plan_on_expansion(systec):
+@pytest.mark.parametrize("R", [8, 3, 160])
+def test_ttm_general_plan_on_expansion(systec, R):
     import torch
-    w = small_random(3, 40, 5000, 8, seed=4, diag_frac=0.2)
+    w = small_random(3, 40, 5000, R, seed=4, diag_frac=0.2)
     want = oracle.ttm_sym3(40, w.idx, w.vals, w.B)
     S = oracle.ttm_sym3(40, w.idx, np.abs(w.vals), np.abs(w.B))
     di, dv, dB = to_dev(w.idx, w.vals, w.B)
     ei, ev = systec.expand_symmetric(3, 40, di, dv)
     gplan = systec.plan_create_general(3, 40, ei, ev)
-    Cf = gplan.ttm(dB).view(40, 40, 8)
+    Cf = gplan.ttm(dB).view(40, 40, R)
     torch.cuda.synchronize()
     parity(Cf.cpu().numpy(), want, S)
 
