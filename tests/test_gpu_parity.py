@@ -358,6 +358,51 @@ def test_execute_is_cuda_graph_capturable(systec):
         parity(C.cpu().numpy(), Cref, S)
 
 
+def test_concurrent_executes_on_streams_and_threads(systec):
+    """include/systec.h: a plan is immutable; concurrent executes on different
+    streams (from different host threads too) are safe when their C differ."""
+    import threading
+
+    import torch
+    for n, dim, nnz, R in ((3, 3000, 300000, 32), (5, 60, 200000, 16)):   # copies = 1 and copies > 1
+        w = small_random(n, dim, nnz, R, seed=11, diag_frac=0.05)
+        rng = np.random.default_rng(3)
+        B2 = rng.uniform(-1, 1, w.B.shape).astype(np.float32)
+        want = [oracle.mttkrp(n, dim, w.idx, w.vals, b) for b in (w.B, B2)]
+        di, dv = to_dev(w.idx, w.vals)
+        plan = systec.Plan(n, dim, di, dv)
+        Bs = [torch.from_numpy(b).cuda() for b in (w.B, B2)]
+        streams = [torch.cuda.Stream() for _ in range(4)]
+        Cs = [torch.empty((dim, R), device="cuda") for _ in range(4)]
+        torch.cuda.synchronize()
+        for _ in range(10):                            # interleaved on 4 streams, one host thread
+            for k in range(4):
+                with torch.cuda.stream(streams[k]):
+                    plan.execute(Bs[k % 2], Cs[k])
+        torch.cuda.synchronize()
+        for k in range(4):
+            parity(Cs[k].cpu().numpy(), *want[k % 2])
+        errors = []
+
+        def worker(k):
+            try:
+                with torch.cuda.stream(streams[k]):
+                    for _ in range(10):
+                        plan.execute(Bs[k % 2], Cs[k])
+                streams[k].synchronize()
+            except Exception as e:  # pragma: no cover - reported below
+                errors.append(e)
+        ts = [threading.Thread(target=worker, args=(k,)) for k in range(4)]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
+        assert not errors, errors
+        for k in range(4):
+            parity(Cs[k].cpu().numpy(), *want[k % 2])
+        plan.destroy()
+
+
 # ---------------------------------------------------------------- NEXT-3: (min,+) relaxation
 @pytest.mark.parametrize("dim,nnz", [(50, 400), (3000, 40000), (100000, 1000000)])
 def test_minplus_bit_exact(systec, dim, nnz):
