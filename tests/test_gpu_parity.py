@@ -358,6 +358,39 @@ def test_execute_is_cuda_graph_capturable(systec):
         parity(C.cpu().numpy(), Cref, S)
 
 
+@pytest.mark.parametrize("order,bits,R", [(2, 24, 1), (3, 21, 4), (4, 16, 4), (5, 12, 8)])
+def test_key_width_limits(systec, order, bits, R):
+    """dim = 2^bits at the widest sort key each order allows (order*bits = 48..64;
+    order 4 reaches the all-ones 64-bit key at (dim-1)^4), indices crowded at
+    both ends of [0, dim), shuffled and non-canonical: touched rows vs the
+    oracle row by row, every untouched row exactly zero."""
+    import torch
+    dim = 1 << bits
+    rng = np.random.default_rng(bits)
+    nnz = 20000
+    top = rng.integers(dim - 8, dim, (nnz // 2, order))
+    low = rng.integers(0, 8, (nnz // 4, order))
+    mid = rng.integers(0, dim, (nnz - nnz // 2 - nnz // 4, order))
+    idx = np.concatenate([top, low, mid]).astype(np.int32)
+    idx[0] = dim - 1                                  # the all-equal top entry
+    idx = idx[rng.permutation(nnz)]
+    vals = rng.uniform(-1, 1, nnz).astype(np.float32)
+    B = rng.uniform(-1, 1, (dim, R)).astype(np.float32)
+    di, dv, dB = to_dev(idx, vals, B)
+    plan = systec.Plan(order, dim, di, dv)
+    C = plan.execute(dB)
+    torch.cuda.synchronize()
+    Cg = C.cpu().numpy()
+    touched = np.unique(idx)
+    rows = np.unique(np.concatenate([touched[:150], touched[-150:], rng.choice(touched, 100)]))
+    Cref, S = oracle.mttkrp_rows(order, dim, idx, vals, B, rows)
+    parity(Cg[rows], Cref, S)
+    mask = np.ones(dim, bool)
+    mask[touched] = False
+    assert not np.any(Cg[mask]), "row with no stored index is not zero"
+    plan.destroy()
+
+
 def test_concurrent_executes_on_streams_and_threads(systec):
     """include/systec.h: a plan is immutable; concurrent executes on different
     streams (from different host threads too) are safe when their C differ."""
