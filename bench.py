@@ -165,9 +165,32 @@ def cpu_baseline(w, target_wall=4.0, max_entries=None, threads=0):
         if dt >= target_wall or m >= w.nnz or (max_entries and m >= max_entries):
             break
         m = min(w.nnz, int(m * max(2.0, min(8.0, target_wall / max(dt, 1e-3)))))
-    return {"value": m / dt, "unit": UNIT, "cores": T, "kind": "oracle",
-            "sample": f"first {m} of {w.nnz} stored entries of {w.name} (sorted order), "
-                      f"full expansion + fp64 accumulation into [dim][R], {dt:.2f} s wall on {T} threads"}
+    out = {"value": m / dt, "unit": UNIT, "cores": T, "kind": "oracle",
+           "sample": f"first {m} of {w.nnz} stored entries of {w.name} (sorted order), "
+                     f"full expansion + fp64 accumulation into [dim][R], {dt:.2f} s wall on {T} threads"}
+    out["one_core_context"] = one_core_context(w)
+    return out
+
+
+def one_core_context(w, target_wall=1.0):
+    """The paper's own experiment is symmetric vs naive on ONE core
+    (PAPER.md:740, 886): the expansion oracle and the symmetric method, both
+    plain C in fp64 on one thread, on the same bounded sample.  Context only."""
+    import oracle
+    m = min(w.nnz, 20_000)
+    while True:
+        t0 = time.perf_counter()
+        oracle.mttkrp(w.order, w.dim, w.idx[:m], w.vals[:m], w.B, threads=1)
+        t_exp = time.perf_counter() - t0
+        if t_exp >= target_wall or m >= w.nnz:
+            break
+        m = min(w.nnz, int(m * max(2.0, min(8.0, target_wall / max(t_exp, 1e-3)))))
+    t0 = time.perf_counter()
+    oracle.mttkrp_symmetric(w.order, w.dim, w.idx[:m], w.vals[:m], w.B)
+    t_sym = time.perf_counter() - t0
+    return {"sample_entries": m, "expansion_nnz_s": m / t_exp, "symmetric_nnz_s": m / t_sym,
+            "speedup": t_exp / t_sym, "paper_one_core_speedup_max": {"3": 3.38, "4": 7.35, "5": 29.8}[str(w.order)]
+            if w.order in (3, 4, 5) else None}
 
 
 def run_reference(args, w):

@@ -79,6 +79,8 @@ def _load():
         lib.oracle_ttm_sym3.restype = i32
         lib.oracle_count_expanded.argtypes = [i32, i64, vp]
         lib.oracle_count_expanded.restype = i64
+        lib.oracle_mttkrp_symmetric.argtypes = [i32, i64, i64, vp, vp, vp, i32, vp]
+        lib.oracle_mttkrp_symmetric.restype = i32
         _lib = lib
     return _lib
 
@@ -122,6 +124,23 @@ def mttkrp(order: int, dim: int, idx, vals, B, threads: int | None = None,
     if rc != 0:
         raise RuntimeError(f"oracle_mttkrp failed with status {rc}")
     return C, S
+
+
+def mttkrp_symmetric(order: int, dim: int, idx, vals, B):
+    """The symmetric method (coefficient per run-first position) in plain C,
+    one thread, fp64: pin P4 against the expansion and the one-core CPU
+    analogue of the paper's experiment.  Returns C, fp64 [dim][R]."""
+    idx, vals, B = _prep(order, idx, vals, B)
+    if B.shape[0] != dim:
+        raise ValueError("B must have dim rows")
+    C = np.empty((dim, B.shape[1]), np.float64)
+    rc = _load().oracle_mttkrp_symmetric(order, dim, idx.shape[0], _ptr(idx), _ptr(vals), _ptr(B), B.shape[1],
+                                         _ptr(C))
+    if rc == 3:
+        raise IndexError("index outside [0, dim)")
+    if rc != 0:
+        raise RuntimeError(f"oracle_mttkrp_symmetric failed with status {rc}")
+    return C
 
 
 def mttkrp_rows(order: int, dim: int, idx, vals, B, rows, threads: int | None = None):

@@ -215,6 +215,60 @@ int oracle_mttkrp(int order, int64_t dim, int64_t nnz, const int32_t *idx,
 }
 
 /*
+ * The symmetric METHOD on the CPU, single thread, fp64 — not the oracle's
+ * definition but the paper's algorithm written out plainly, for pin P4 (vs
+ * the expansion above) and for the one-core CPU analogue of the paper's own
+ * experiment (symmetric vs naive on one core; SURVEY.md
+ * §8(d)).  For every stored entry: p = sort(idx_e), v = vals_e; the runs of
+ * equal values have multiplicities m_w; for every run-first position u,
+ *   coef_u = (n-1)! * m_u / prod_w m_w!            (distinct permutations of
+ *            the multiset that put p_u first)
+ *   C[p_u, r] += coef_u * v * prod_{s != u} B[p_s, r]
+ * (fig:mttkrp_symmetrization_3 / Listing 6, after
+ * distributive grouping).  C is [dim][R], overwritten.
+ */
+int oracle_mttkrp_symmetric(int order, int64_t dim, int64_t nnz, const int32_t *idx, const float *vals,
+                            const float *B, int R, double *C) {
+    int rc = check_args(order, dim, nnz, idx, vals, B, R);
+    if (rc) return rc;
+    if (!C) return 1;
+    memset(C, 0, (size_t)(dim * (int64_t)R) * sizeof(double));
+    double fact[ORACLE_MAX_ORDER + 1];
+    fact[0] = 1.0;
+    for (int k = 1; k <= ORACLE_MAX_ORDER; k++) fact[k] = fact[k - 1] * k;
+    for (int64_t e = 0; e < nnz; e++) {
+        int32_t p[ORACLE_MAX_ORDER];
+        for (int t = 0; t < order; t++) {
+            p[t] = idx[e * order + t];
+            if (p[t] < 0 || p[t] >= dim) return 3;
+        }
+        sort_small(p, order);
+        int mult[ORACLE_MAX_ORDER];            /* run length of the run starting at t (0 elsewhere) */
+        double denom = 1.0;
+        for (int t = 0; t < order;) {
+            int u = t;
+            while (u < order && p[u] == p[t]) u++;
+            for (int q = t; q < u; q++) mult[q] = 0;
+            mult[t] = u - t;
+            denom *= fact[u - t];
+            t = u;
+        }
+        const double v = (double)vals[e];
+        for (int u = 0; u < order; u++) {
+            if (mult[u] == 0) continue;
+            const double coef = fact[order - 1] * mult[u] / denom;
+            for (int r = 0; r < R; r++) {
+                double prod = coef * v;
+                for (int s = 0; s < order; s++)
+                    if (s != u) prod *= (double)B[(int64_t)p[s] * R + r];
+                C[(int64_t)p[u] * R + r] += prod;
+            }
+        }
+    }
+    return 0;
+}
+
+/*
  * Sampled-row oracle: the same expansion, keeping only the permutations whose
  * p_0 is one of rows[0..nrows) (distinct, each in [0,dim)).  C and S are
  * [nrows][R] fp64, overwritten.  Used to check full-size runs row by row.

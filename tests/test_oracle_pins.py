@@ -158,6 +158,10 @@ def test_p4_symmetric_formula_equals_expansion(n, dim, nnz):
     C, S = oracle.mttkrp(n, dim, w.idx, w.vals, w.B)
     Csym = symmetric_ref.mttkrp(n, dim, w.idx, w.vals, w.B)
     assert rel_err(Csym, C, S) < 1e-12
+    # the same method in plain C (oracle_mttkrp_symmetric: the one-core CPU
+    # analogue bench.py times), written separately from the numpy one
+    Cc = oracle.mttkrp_symmetric(n, dim, w.idx, w.vals, w.B)
+    assert rel_err(Cc, C, S) < 1e-12
 
 
 # ---------------------------------------------------------------- P5
@@ -185,6 +189,7 @@ def test_p5_hand_worked_example(golden_dir):
     A = dense_from_entries(3, 3, idx, vals)
     assert np.array_equal(dense_mttkrp(A, B), np.array(d["C"]))
     assert np.array_equal(symmetric_ref.mttkrp(3, 3, idx, vals, B), np.array(d["C"]))
+    assert np.array_equal(oracle.mttkrp_symmetric(3, 3, idx, vals, B), np.array(d["C"]))
 
 
 # ---------------------------------------------------------------- P6
