@@ -147,7 +147,8 @@ __global__ void __launch_bounds__(256) gram_dots_partial_kernel(const float *__r
 // out[q] = sum_blk part[blk][q], q < width: one warp per output, lanes stride
 // over the blocks, shuffle-reduced (fixed order: deterministic)
 __global__ void reduce_partials_kernel(const double *__restrict__ part, int blocks, int width,
-                                       double *__restrict__ out) {
+                                       double *__restrict__ out, const int *skip) {
+    if (skip && *skip) return;
     const int q = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
     if (q >= width) return;
@@ -295,7 +296,8 @@ __global__ void __launch_bounds__(1024) small_solve_kernel(const double *__restr
 template <int RT>
 __global__ void __launch_bounds__(256) apply_inverse_kernel(const float *__restrict__ M, const float *__restrict__ Hinv,
                                                             int64_t dim, int R, float *__restrict__ Bout,
-                                                            double *__restrict__ part) {
+                                                            double *__restrict__ part, const int *skip) {
+    if (skip && *skip) return;  // device-side loop: last iteration evaluates the fit only
     __shared__ __align__(16) float Ms[kTileRows * RT];
     __shared__ double sq[256];
     const int tid = threadIdx.x;
@@ -344,7 +346,8 @@ __global__ void __launch_bounds__(256) apply_inverse_kernel(const float *__restr
 // lam[b] = sqrt(norms[b]); B[i][b] /= lam[b] (fp32 division by the fp32 norm;
 // 16-byte accesses when R % 4 == 0)
 __global__ void normalize_kernel(float *__restrict__ B, int64_t dim, int R, const double *__restrict__ norms,
-                                 float *__restrict__ lam) {
+                                 float *__restrict__ lam, const int *skip) {
+    if (skip && *skip) return;
     __shared__ float nb[kMaxCpR];
     for (int b = threadIdx.x; b < R; b += blockDim.x) {
         nb[b] = static_cast<float>(sqrt(norms[b]));
@@ -370,6 +373,35 @@ __global__ void normalize_kernel(float *__restrict__ B, int64_t dim, int R, cons
             if (nb[b] > 0.f) B[q] /= nb[b];
         }
     }
+}
+
+// Device-side convergence test of the CP-ALS loop (one thread): the fit of
+// the current iterate from the pieces small_solve_kernel wrote, stored in
+// fits[it-1]; the loop continues (conditional WHILE node of the iteration
+// graph) unless this was the last iteration or |fit - previous| < tol; on the
+// last iteration the factor update that follows is skipped, as in the host
+// loop.
+__global__ void cpd_fit_check_kernel(const double *__restrict__ xhat2, CpdLoopState *st, double *__restrict__ fits,
+                                     double tol, int max_iters, cudaGraphConditionalHandle handle) {
+    const int it = ++st->it;
+    const double x2 = st->x2;
+    const double r2 = x2 - 2.0 * xhat2[1] + xhat2[0];
+    const double fit = 1.0 - sqrt(r2 > 0.0 ? r2 : 0.0) / sqrt(x2 > 0.0 ? x2 : 1e-300);
+    fits[it - 1] = fit;
+    st->iters_done = it;
+    const bool last = it >= max_iters;
+    const bool conv = fabs(fit - st->prev_fit) < tol;
+    st->prev_fit = fit;
+    st->skip_update = last ? 1 : 0;
+    cudaGraphSetConditional(handle, (last || conv) ? 0u : 1u);
+}
+
+__global__ void cpd_state_init_kernel(CpdLoopState *st, const double *x2) {
+    st->x2 = *x2;
+    st->prev_fit = -1e300;
+    st->it = 0;
+    st->skip_update = 0;
+    st->iters_done = 0;
 }
 
 int sm_count() {
@@ -412,32 +444,57 @@ int64_t cpd_scratch_doubles(int R) {
     return static_cast<int64_t>(R) * R + 2 * R + 2 + static_cast<int64_t>(cpd_partial_blocks()) * (R * R + R);
 }
 
-cudaError_t cpd_step(const Plan &p, const float *M, float *B, float *lam, int R, double *dscratch,
-                     float *fscratch, bool have_lam, bool fit_only, cudaStream_t s) {
+cudaError_t cpd_fit_pieces(const Plan &p, const float *M, const float *B, const float *lam, int R, double *dscratch,
+                           float *fscratch, cudaStream_t s) {
     double *G = dscratch, *dots = G + R * R, *norms = dots + R, *xhat2 = norms + R, *part = xhat2 + 2;
     float *Hinv = fscratch;
     const int PB = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(cpd_partial_blocks(), (p.dim + 255) / 256)));
     const int W = R * R + R;
     const size_t gsm = gram_smem_bytes();
     gram_dots_partial_kernel<<<PB, 256, gsm, s>>>(B, M, p.dim, R, part);
-    reduce_partials_kernel<<<(W + 7) / 8, 256, 0, s>>>(part, PB, W, G);  // G and dots (contiguous)
-    const float *lam_in = have_lam ? lam : nullptr;
-    if (R <= 16) small_solve_kernel<1><<<1, 1024, 0, s>>>(G, R, p.order, Hinv, lam_in, dots, xhat2);
-    else if (R <= 32) small_solve_kernel<2><<<1, 1024, 0, s>>>(G, R, p.order, Hinv, lam_in, dots, xhat2);
-    else small_solve_kernel<6><<<1, 1024, 0, s>>>(G, R, p.order, Hinv, lam_in, dots, xhat2);
-    if (fit_only) return cudaGetLastError();
+    reduce_partials_kernel<<<(W + 7) / 8, 256, 0, s>>>(part, PB, W, G, nullptr);  // G and dots (contiguous)
+    if (R <= 16) small_solve_kernel<1><<<1, 1024, 0, s>>>(G, R, p.order, Hinv, lam, dots, xhat2);
+    else if (R <= 32) small_solve_kernel<2><<<1, 1024, 0, s>>>(G, R, p.order, Hinv, lam, dots, xhat2);
+    else small_solve_kernel<6><<<1, 1024, 0, s>>>(G, R, p.order, Hinv, lam, dots, xhat2);
+    return cudaGetLastError();
+}
+
+cudaError_t cpd_update(const Plan &p, const float *M, float *B, float *lam, int R, double *dscratch,
+                       float *fscratch, const int *skip, cudaStream_t s) {
+    double *G = dscratch, *dots = G + R * R, *norms = dots + R, *xhat2 = norms + R, *part = xhat2 + 2;
+    float *Hinv = fscratch;
+    const int PB = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(cpd_partial_blocks(), (p.dim + 255) / 256)));
     switch ((R + 7) / 8) {
-        case 1: apply_inverse_kernel<8><<<PB, 256, 0, s>>>(M, Hinv, p.dim, R, B, part); break;
-        case 2: apply_inverse_kernel<16><<<PB, 256, 0, s>>>(M, Hinv, p.dim, R, B, part); break;
-        case 3: apply_inverse_kernel<24><<<PB, 256, 0, s>>>(M, Hinv, p.dim, R, B, part); break;
-        case 4: apply_inverse_kernel<32><<<PB, 256, 0, s>>>(M, Hinv, p.dim, R, B, part); break;
-        case 5: apply_inverse_kernel<40><<<PB, 256, 0, s>>>(M, Hinv, p.dim, R, B, part); break;
-        default: apply_inverse_kernel<48><<<PB, 256, 0, s>>>(M, Hinv, p.dim, R, B, part); break;
+        case 1: apply_inverse_kernel<8><<<PB, 256, 0, s>>>(M, Hinv, p.dim, R, B, part, skip); break;
+        case 2: apply_inverse_kernel<16><<<PB, 256, 0, s>>>(M, Hinv, p.dim, R, B, part, skip); break;
+        case 3: apply_inverse_kernel<24><<<PB, 256, 0, s>>>(M, Hinv, p.dim, R, B, part, skip); break;
+        case 4: apply_inverse_kernel<32><<<PB, 256, 0, s>>>(M, Hinv, p.dim, R, B, part, skip); break;
+        case 5: apply_inverse_kernel<40><<<PB, 256, 0, s>>>(M, Hinv, p.dim, R, B, part, skip); break;
+        default: apply_inverse_kernel<48><<<PB, 256, 0, s>>>(M, Hinv, p.dim, R, B, part, skip); break;
     }
-    reduce_partials_kernel<<<(R + 7) / 8, 256, 0, s>>>(part, PB, R, norms);
+    reduce_partials_kernel<<<(R + 7) / 8, 256, 0, s>>>(part, PB, R, norms, skip);
     const int64_t total = p.dim * R;
     const int ab = static_cast<int>(std::min<int64_t>((total / 4 + 255) / 256 + 1, static_cast<int64_t>(sm_count()) * 8));
-    normalize_kernel<<<ab, 256, 0, s>>>(B, p.dim, R, norms, lam);
+    normalize_kernel<<<ab, 256, 0, s>>>(B, p.dim, R, norms, lam, skip);
+    return cudaGetLastError();
+}
+
+cudaError_t cpd_step(const Plan &p, const float *M, float *B, float *lam, int R, double *dscratch,
+                     float *fscratch, bool have_lam, bool fit_only, cudaStream_t s) {
+    cudaError_t e = cpd_fit_pieces(p, M, B, have_lam ? lam : nullptr, R, dscratch, fscratch, s);
+    if (e != cudaSuccess || fit_only) return e;
+    return cpd_update(p, M, B, lam, R, dscratch, fscratch, nullptr, s);
+}
+
+cudaError_t cpd_state_init(CpdLoopState *st, const double *x2, cudaStream_t s) {
+    cpd_state_init_kernel<<<1, 1, 0, s>>>(st, x2);
+    return cudaGetLastError();
+}
+
+cudaError_t cpd_fit_check(const double *dscratch, int R, CpdLoopState *st, double *fits, double tol, int max_iters,
+                          cudaGraphConditionalHandle h, cudaStream_t s) {
+    const double *xhat2 = dscratch + R * R + 2 * R;
+    cpd_fit_check_kernel<<<1, 1, 0, s>>>(xhat2, st, fits, tol, max_iters, h);
     return cudaGetLastError();
 }
 

@@ -70,6 +70,22 @@ int64_t cpd_scratch_doubles(int R);
 cudaError_t cpd_tensor_norm2(const Plan &p, double *out, cudaStream_t s);
 cudaError_t cpd_step(const Plan &p, const float *M, float *B, float *lam, int R, double *dscratch,
                      float *fscratch, bool have_lam, bool fit_only, cudaStream_t s);
+// device-resident CP-ALS loop (one conditional-WHILE graph): state + pieces
+struct CpdLoopState {
+    double x2;         // ||X||^2
+    double prev_fit;
+    int it;            // iterations evaluated
+    int skip_update;   // 1 on the last iteration: fit only
+    int iters_done;
+    int pad;
+};
+cudaError_t cpd_fit_pieces(const Plan &p, const float *M, const float *B, const float *lam, int R, double *dscratch,
+                           float *fscratch, cudaStream_t s);
+cudaError_t cpd_update(const Plan &p, const float *M, float *B, float *lam, int R, double *dscratch,
+                       float *fscratch, const int *skip, cudaStream_t s);
+cudaError_t cpd_state_init(CpdLoopState *st, const double *x2, cudaStream_t s);
+cudaError_t cpd_fit_check(const double *dscratch, int R, CpdLoopState *st, double *fits, double tol, int max_iters,
+                          cudaGraphConditionalHandle h, cudaStream_t s);
 
 // ttm.cu
 int64_t ttm_packed_rows(int64_t dim);
@@ -78,7 +94,10 @@ cudaError_t launch_ttm_unpack(int64_t dim, int R, const float *Cp, float *C, cud
 
 // mttkrp.cu
 cudaError_t launch_mttkrp(Plan &p, const float *B, int R, float *C, const systec_exec_opts &o,
-                          cudaStream_t s);
+                          cudaStream_t s, float *scratch = nullptr);
+// floats of replica scratch launch_mttkrp needs for (plan, R, opts); 0 = none.
+// Passing that much as `scratch` makes the launch allocation-free (graph bodies).
+int64_t mttkrp_scratch_floats(const Plan &p, int R, const systec_exec_opts &o);
 
 void set_last_cuda_error(cudaError_t e);
 

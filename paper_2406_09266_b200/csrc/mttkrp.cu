@@ -83,24 +83,41 @@ __global__ void reduce_copies_kernel(const float *__restrict__ Cp, float *__rest
     }
 }
 
-cudaError_t launch_mttkrp(Plan &p, const float *B, int R, float *C, const systec_exec_opts &o, cudaStream_t s) {
-    cudaError_t e;
+// L2-slice spreading: an output smaller than ~4 MB maps onto a few L2 slices
+// whose atomic units then serialise the reductions (ncu on c5: atomic-input
+// activity max 57 % vs avg 20 %); spread it over replicas.
+static int replica_count(const Plan &p, int R, const systec_exec_opts &o) {
     const int64_t plane = p.dim * static_cast<int64_t>(R);
-    // L2-slice spreading: an output smaller than ~4 MB maps onto a few L2
-    // slices whose atomic units then serialise the reductions (ncu on c5:
-    // atomic-input activity max 57 % vs avg 20 %); spread it over replicas.
     int copies = o.copies;
     if (copies <= 0) {
         const int64_t bytes = plane * 4;
         copies = bytes >= (4 << 20) ? 1 : static_cast<int>(std::min<int64_t>(32, (4 << 20) / std::max<int64_t>(bytes, 1)));
         if (p.nnz < 100000) copies = 1;  // latency-bound sizes: not worth the extra pass
     }
+    return copies;
+}
+
+int64_t mttkrp_scratch_floats(const Plan &p, int R, const systec_exec_opts &o) {
+    const int copies = replica_count(p, R, o);
+    return copies > 1 ? static_cast<int64_t>(copies) * p.dim * R : 0;
+}
+
+cudaError_t launch_mttkrp(Plan &p, const float *B, int R, float *C, const systec_exec_opts &o, cudaStream_t s,
+                          float *scratch_in) {
+    cudaError_t e;
+    const int64_t plane = p.dim * static_cast<int64_t>(R);
+    const int copies = replica_count(p, R, o);
     if (copies > 64) return cudaErrorInvalidValue;
     float *Cdst = C;
     float *scratch = nullptr;
+    const bool own_scratch = scratch_in == nullptr;  // else: caller-provided (allocation-free launch)
     if (copies > 1) {
-        e = cudaMallocAsync(&scratch, static_cast<size_t>(copies) * plane * 4, s);  // stream-ordered pool
-        if (e != cudaSuccess) return e;
+        if (own_scratch) {
+            e = cudaMallocAsync(&scratch, static_cast<size_t>(copies) * plane * 4, s);  // stream-ordered pool
+            if (e != cudaSuccess) return e;
+        } else {
+            scratch = scratch_in;
+        }
         e = cudaMemsetAsync(scratch, 0, static_cast<size_t>(copies) * plane * 4, s);
         if (e != cudaSuccess) return e;
         Cdst = scratch;
@@ -110,7 +127,7 @@ cudaError_t launch_mttkrp(Plan &p, const float *B, int R, float *C, const systec
     }
     if (p.nnz == 0) {
         if (scratch) {
-            cudaFreeAsync(scratch, s);
+            if (own_scratch) cudaFreeAsync(scratch, s);
             return o.no_zero ? cudaSuccess : cudaMemsetAsync(C, 0, static_cast<size_t>(plane) * sizeof(float), s);
         }
         return cudaSuccess;
@@ -118,7 +135,7 @@ cudaError_t launch_mttkrp(Plan &p, const float *B, int R, float *C, const systec
 
     const bool aligned = (reinterpret_cast<uintptr_t>(B) % 16 == 0) && (reinterpret_cast<uintptr_t>(C) % 16 == 0);
     auto release = [&](cudaError_t err) {
-        if (scratch) cudaFreeAsync(scratch, s);
+        if (scratch && own_scratch) cudaFreeAsync(scratch, s);
         return err;
     };
     const int vw = (R % 4 == 0 && aligned && !o.force_scalar) ? 4 : 1;
@@ -212,7 +229,7 @@ cudaError_t launch_mttkrp(Plan &p, const float *B, int R, float *C, const systec
         const int rb = static_cast<int>(std::min<int64_t>((work + 255) / 256, static_cast<int64_t>(sms) * 4));
         const int vec = (reinterpret_cast<uintptr_t>(C) % 16 == 0) && (plane % 4 == 0);
         reduce_copies_kernel<<<rb, 256, 0, s>>>(scratch, C, plane, copies, vec, o.no_zero ? 1 : 0);
-        cudaFreeAsync(scratch, s);
+        if (own_scratch) cudaFreeAsync(scratch, s);
     }
     p.last_grid_x = static_cast<int>(blocks);
     p.last_grid_y = tiles;

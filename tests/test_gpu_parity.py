@@ -501,6 +501,34 @@ def test_cp_als_ranks_and_tiles(systec, order, dim, nnz, R):
     np.testing.assert_allclose(fits, fref, atol=1e-5)
 
 
+@pytest.mark.parametrize("order,dim,nnz,R", [(3, 600, 20000, 8), (5, 60, 200000, 16)])   # copies 1 / replicas
+def test_cp_als_graph_loop_equals_host_loop(systec, order, dim, nnz, R, monkeypatch):
+    """The device-resident loop (conditional WHILE graph, device convergence
+    test) and the host loop give the same iterates, fits and iteration count,
+    both run to max_iters and stopped early by tol."""
+    import torch
+    w = small_random(order, dim, nnz, R, seed=order * R, diag_frac=0.1)
+    di, dv, dB = to_dev(w.idx, w.vals, w.B)
+    plan = systec.Plan(order, dim, di, dv)
+    for iters, tol in ((6, 0.0), (50, 1e-4)):
+        out = {}
+        for mode in ("graph", "host"):
+            monkeypatch.setenv("SYSTEC_CPALS_LOOP", mode)
+            B, lam, fits = plan.cp_als(dB.clone(), max_iters=iters, tol=tol)
+            torch.cuda.synchronize()
+            out[mode] = (B.cpu().numpy(), lam.cpu().numpy(), np.asarray(fits))
+        (Bg, lg, fg), (Bh, lh, fh) = out["graph"], out["host"]
+        assert len(fg) == len(fh)
+        if tol == 0.0:
+            assert len(fg) == iters
+        # same kernels in the same order; they differ only by the order of the
+        # atomic reductions (fp32 rounding, amplified over the iterations)
+        np.testing.assert_allclose(Bg, Bh, rtol=0, atol=1e-4 * np.abs(Bh).max())
+        np.testing.assert_allclose(lg, lh, rtol=1e-4)
+        np.testing.assert_allclose(fg, fh, atol=1e-6)
+    plan.destroy()
+
+
 def test_cp_als_recovers_planted_and_stops_early(systec):
     import torch
     from test_oracle_pins import planted
