@@ -9,6 +9,8 @@
 #include <new>
 #include <vector>
 #include <algorithm>
+#include <atomic>
+#include <mutex>
 
 #include "internal.cuh"
 
@@ -40,17 +42,20 @@ bool overlap(const void *a, size_t na, const void *b, size_t nb) {
     return x < y + nb && y < x + na;
 }
 
+// Keep freed stream-ordered allocations in the current device's default pool
+// (plans and replica scratch come from it), once per device, thread-safe.
 void ensure_pool_keeps_memory() {
-    static bool done = false;
-    if (done) return;
+    static std::atomic<uint64_t> done_mask{0};
     int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess) return;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return;
+    const uint64_t bit = 1ull << dev;
+    if (done_mask.load(std::memory_order_acquire) & bit) return;
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
         uint64_t thr = UINT64_MAX;
-        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        if (cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr) == cudaSuccess)
+            done_mask.fetch_or(bit, std::memory_order_acq_rel);
     }
-    done = true;
 }
 
 int check_shape(int order, int64_t dim, int64_t nnz, int *bits_out) {
@@ -574,10 +579,17 @@ int systec_mttkrp(int order, int64_t dim, int64_t nnz, const int32_t *idx, const
 namespace systec {
 namespace {
 
+// One non-blocking stream per device for the pipeline's host->device copies
+// (created on first use, thread-safe, kept for the process lifetime).
 cudaStream_t copy_stream() {
-    static cudaStream_t cs = nullptr;  // one non-blocking stream for host->device copies
-    if (!cs) cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
-    return cs;
+    static std::mutex mu;
+    static cudaStream_t streams[64] = {};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+    std::lock_guard<std::mutex> lock(mu);
+    if (!streams[dev] && cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking) != cudaSuccess)
+        streams[dev] = nullptr;
+    return streams[dev];
 }
 
 // Pipelined end-to-end call: chunk k's host->device copy (copy stream) overlaps
@@ -620,6 +632,7 @@ int mttkrp_host_pipelined(int order, int64_t dim, int64_t nnz, int bits, const i
     std::memset(&hst, 0, sizeof(hst));
     hst.bad_entry = ULLONG_MAX;
     cudaStream_t cs = copy_stream();
+    if (!cs) cs = s;  // no copy stream: copies on the caller's stream (no overlap, same result)
     std::vector<cudaEvent_t> ev(nch + 2, nullptr);
     int rc = SYSTEC_OK;
     do {
