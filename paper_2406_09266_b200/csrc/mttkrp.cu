@@ -58,22 +58,41 @@ KernelFn pick_ablation_kernel(int order, int abl) {
     return order == 3 ? ablation3(abl) : order == 5 ? ablation5(abl) : nullptr;
 }
 
+// Sum `copies` replicas Cp[copies][plane] into C[plane].  Groups of G lanes
+// share one float4 of the plane, lane k adding replicas k, k+G, ... (more
+// loads in flight than one thread per float4), then a shuffle reduction in
+// fixed order; accumulate != 0 adds the result to C's contents.
+template <int G>
 __global__ void reduce_copies_kernel(const float *__restrict__ Cp, float *__restrict__ C, int64_t plane, int copies,
                                      int vec, int accumulate) {
     const int64_t n4 = vec ? plane / 4 : 0;
     const float4 *P4 = reinterpret_cast<const float4 *>(Cp);
     float4 *C4 = reinterpret_cast<float4 *>(C);
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
-        float4 a = P4[i];
-        for (int c = 1; c < copies; ++c) {
+    const int k = threadIdx.x % G;
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * (blockDim.x / G);
+    // block-uniform loop bound: every lane reaches the shuffles
+    for (int64_t base = blockIdx.x * static_cast<int64_t>(blockDim.x / G); base < n4; base += stride) {
+        const int64_t i = base + threadIdx.x / G;
+        const bool valid = i < n4;
+        float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int c = k; valid && c < copies; c += G) {
             const float4 b = P4[c * n4 + i];
             a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
         }
-        if (accumulate) {
-            const float4 c = C4[i];
-            a.x += c.x; a.y += c.y; a.z += c.z; a.w += c.w;
+#pragma unroll
+        for (int d = G / 2; d > 0; d >>= 1) {
+            a.x += __shfl_xor_sync(0xffffffffu, a.x, d, G);
+            a.y += __shfl_xor_sync(0xffffffffu, a.y, d, G);
+            a.z += __shfl_xor_sync(0xffffffffu, a.z, d, G);
+            a.w += __shfl_xor_sync(0xffffffffu, a.w, d, G);
         }
-        C4[i] = a;
+        if (k == 0 && valid) {
+            if (accumulate) {
+                const float4 c = C4[i];
+                a.x += c.x; a.y += c.y; a.z += c.z; a.w += c.w;
+            }
+            C4[i] = a;
+        }
     }
     for (int64_t i = 4 * n4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < plane;
          i += (int64_t)gridDim.x * blockDim.x) {
@@ -225,10 +244,10 @@ cudaError_t launch_mttkrp(Plan &p, const float *B, int R, float *C, const systec
     if (copies > 1) {
         e = cudaGetLastError();
         if (e != cudaSuccess) return release(e);
-        const int64_t work = std::max<int64_t>(1, plane / 4);
-        const int rb = static_cast<int>(std::min<int64_t>((work + 255) / 256, static_cast<int64_t>(sms) * 4));
+        const int64_t work = std::max<int64_t>(1, plane / 4) * 8;  // 8 lanes per float4 of C
+        const int rb = static_cast<int>(std::min<int64_t>((work + 255) / 256, static_cast<int64_t>(sms) * 8));
         const int vec = (reinterpret_cast<uintptr_t>(C) % 16 == 0) && (plane % 4 == 0);
-        reduce_copies_kernel<<<rb, 256, 0, s>>>(scratch, C, plane, copies, vec, o.no_zero ? 1 : 0);
+        reduce_copies_kernel<8><<<rb, 256, 0, s>>>(scratch, C, plane, copies, vec, o.no_zero ? 1 : 0);
         if (own_scratch) cudaFreeAsync(scratch, s);
     }
     p.last_grid_x = static_cast<int>(blocks);

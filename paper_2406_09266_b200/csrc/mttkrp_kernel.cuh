@@ -410,6 +410,7 @@ __global__ void __launch_bounds__(256, MINB) mttkrp_sym_kernel_occ(const KParams
 
 // Sum `copies` replicas Cp[copies][plane] into C[plane] (float4 when aligned);
 // accumulate != 0 adds them to C's current contents (no_zero executes).
+template <int G>
 __global__ void reduce_copies_kernel(const float *__restrict__ Cp, float *__restrict__ C, int64_t plane, int copies,
                                      int vec, int accumulate);
 
