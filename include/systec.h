@@ -95,7 +95,8 @@ typedef struct systec_exec_opts {
                                  /* (auto: C < 4 MB and nnz >= 1e5 -> up to 32 replicas)        */
     int32_t ablation;            /* evidence study, c2/c5 kernel shapes only: bit 0 = no smem  */
                                  /* staging of the stream, bit 1 = no position-0 accumulation  */
-    int32_t unused6;
+    int32_t static_ranges;       /* 1 = one static nnz-balanced range per warp; 0 = dynamic units */
+                                 /* of ~4 chunks taken from a per-launch counter (default)       */
     int32_t occupancy;           /* order-3 R=32 kernel built for 5 blocks/SM: 1 on, -1 off,    */
                                  /* 0 auto (on when B > 64 MB)                                  */
     int32_t reserved[2];

@@ -116,9 +116,29 @@ static int replica_count(const Plan &p, int R, const systec_exec_opts &o) {
     return copies;
 }
 
+// work counters of the dynamic distribution: one per rank tile (blockIdx.y);
+// a tile is at least 32 columns wide, so ceil(R/32) bounds their number
+static int64_t counter_slots(int R) { return ((R + 31) / 32 + 3) & ~3; }
+
+// Scratch of one launch (floats): the C replicas when copies > 1, then the
+// work counters of the dynamic distribution.
 int64_t mttkrp_scratch_floats(const Plan &p, int R, const systec_exec_opts &o) {
     const int copies = replica_count(p, R, o);
-    return copies > 1 ? static_cast<int64_t>(copies) * p.dim * R : 0;
+    const int64_t rep = copies > 1 ? static_cast<int64_t>(copies) * p.dim * R : 0;
+    return rep + (o.static_ranges > 0 ? 0 : counter_slots(R));
+}
+
+// C = 0 (16-byte stores when aligned) and the work counters = 0, one launch
+__global__ void zero_output_kernel(float *__restrict__ C, int64_t plane, int vec, unsigned int *ctr, int nctr) {
+    if (ctr && blockIdx.x == 0)
+        for (int q = threadIdx.x; q < nctr; q += blockDim.x) ctr[q] = 0u;
+    const int64_t n4 = vec ? plane / 4 : 0;
+    float4 *C4 = reinterpret_cast<float4 *>(C);
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n4; i += stride)
+        C4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int64_t i = 4 * n4 + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < plane; i += stride)
+        C[i] = 0.f;
 }
 
 cudaError_t launch_mttkrp(Plan &p, const float *B, int R, float *C, const systec_exec_opts &o, cudaStream_t s,
@@ -127,28 +147,45 @@ cudaError_t launch_mttkrp(Plan &p, const float *B, int R, float *C, const systec
     const int64_t plane = p.dim * static_cast<int64_t>(R);
     const int copies = replica_count(p, R, o);
     if (copies > 64) return cudaErrorInvalidValue;
+    // work distribution: dynamic units from a counter (default) or one static
+    // range per warp (opts.static_ranges = 1; measured: c3 2.43 -> 2.04 ms,
+    // c4 -2 %, c5 -2 %, c2 -0.3 % with the dynamic one, profiles/r01_sweep_dynamic.jsonl)
+    const bool dyn = o.static_ranges <= 0;
+    const int64_t rep_f = copies > 1 ? static_cast<int64_t>(copies) * plane : 0;
+    const int64_t nctr = dyn ? counter_slots(R) : 0;
+    const int64_t need_f = rep_f + nctr;
     float *Cdst = C;
     float *scratch = nullptr;
     const bool own_scratch = scratch_in == nullptr;  // else: caller-provided (allocation-free launch)
-    if (copies > 1) {
+    if (need_f > 0) {
         if (own_scratch) {
-            e = cudaMallocAsync(&scratch, static_cast<size_t>(copies) * plane * 4, s);  // stream-ordered pool
+            e = cudaMallocAsync(&scratch, static_cast<size_t>(need_f) * 4, s);  // stream-ordered pool
             if (e != cudaSuccess) return e;
         } else {
             scratch = scratch_in;
         }
-        e = cudaMemsetAsync(scratch, 0, static_cast<size_t>(copies) * plane * 4, s);
+    }
+    unsigned int *ctr = dyn ? reinterpret_cast<unsigned int *>(scratch + rep_f) : nullptr;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (copies > 1) {
+        e = cudaMemsetAsync(scratch, 0, static_cast<size_t>(need_f) * 4, s);  // replicas (+ counter)
         if (e != cudaSuccess) return e;
         Cdst = scratch;
     } else if (!o.no_zero) {
-        e = cudaMemsetAsync(C, 0, static_cast<size_t>(plane) * sizeof(float), s);
+        const int vec = (reinterpret_cast<uintptr_t>(C) % 16 == 0) ? 1 : 0;
+        const int64_t work = std::max<int64_t>(1, vec ? plane / 4 : plane);
+        const int zb = static_cast<int>(std::min<int64_t>((work + 255) / 256, static_cast<int64_t>(sms) * 8));
+        zero_output_kernel<<<zb, 256, 0, s>>>(C, plane, vec, ctr, static_cast<int>(nctr));
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    } else if (ctr) {
+        e = cudaMemsetAsync(ctr, 0, static_cast<size_t>(nctr) * sizeof(unsigned int), s);
         if (e != cudaSuccess) return e;
     }
     if (p.nnz == 0) {
-        if (scratch) {
-            if (own_scratch) cudaFreeAsync(scratch, s);
-            return o.no_zero ? cudaSuccess : cudaMemsetAsync(C, 0, static_cast<size_t>(plane) * sizeof(float), s);
-        }
+        if (scratch && own_scratch) cudaFreeAsync(scratch, s);
+        if (copies > 1 && !o.no_zero) return cudaMemsetAsync(C, 0, static_cast<size_t>(plane) * sizeof(float), s);
         return cudaSuccess;
     }
 
@@ -202,7 +239,7 @@ cudaError_t launch_mttkrp(Plan &p, const float *B, int R, float *C, const systec
     if (!fn) return release(cudaErrorInvalidValue);
     int wpb = o.warps_per_block > 0 ? o.warps_per_block : 8;
     auto smem_for = [&](int w) {
-        return static_cast<size_t>(w) * stages * (p.order + 1) * (E * K) * 4 + static_cast<size_t>(w) * stages * 8;
+        return static_cast<size_t>(w) * stages * (p.order + 1) * (E * K) * 4 + static_cast<size_t>(w) * stages * 24;
     };
     const size_t smem_cap = 200 * 1024;
     while (wpb > 1 && smem_for(wpb) > smem_cap) wpb >>= 1;  // keep the staging ring within shared memory
@@ -211,9 +248,7 @@ cudaError_t launch_mttkrp(Plan &p, const float *B, int R, float *C, const systec
     const size_t smem = smem_for(wpb);
     e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return release(e);
-    int dev = 0, sms = 148, occ = 1;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int occ = 1;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, smem);
     if (e != cudaSuccess) return release(e);
     if (occ < 1) occ = 1;
@@ -222,7 +257,7 @@ cudaError_t launch_mttkrp(Plan &p, const float *B, int R, float *C, const systec
     int64_t span = (p.nnz + total_warps - 1) / total_warps;
     span = std::max<int64_t>(4, (span + 3) & ~3ll);
     const int64_t warps_used = (p.nnz + span - 1) / span;
-    const int64_t blocks = (warps_used + wpb - 1) / wpb;
+    int64_t blocks = (warps_used + wpb - 1) / wpb;
 
     KParams kp;
     kp.coords = p.coords;
@@ -239,6 +274,9 @@ cudaError_t launch_mttkrp(Plan &p, const float *B, int R, float *C, const systec
     kp.K = K;
     kp.stages = stages;
     kp.hints = o.l2_hints >= 0 ? 1 : 0;
+    kp.ctr = ctr;
+    kp.unit = E * K * 4;  // units of 4 chunks (~530 entries at E*K = 132)
+    if (dyn) blocks = static_cast<int64_t>(sms) * occ;  // persistent: every resident warp takes units
     dim3 grid(static_cast<unsigned>(blocks), static_cast<unsigned>(tiles));
     fn<<<grid, threads, smem, s>>>(kp);
     if (copies > 1) {
@@ -248,8 +286,8 @@ cudaError_t launch_mttkrp(Plan &p, const float *B, int R, float *C, const systec
         const int rb = static_cast<int>(std::min<int64_t>((work + 255) / 256, static_cast<int64_t>(sms) * 8));
         const int vec = (reinterpret_cast<uintptr_t>(C) % 16 == 0) && (plane % 4 == 0);
         reduce_copies_kernel<8><<<rb, 256, 0, s>>>(scratch, C, plane, copies, vec, o.no_zero ? 1 : 0);
-        if (own_scratch) cudaFreeAsync(scratch, s);
     }
+    if (scratch && own_scratch) cudaFreeAsync(scratch, s);
     p.last_grid_x = static_cast<int>(blocks);
     p.last_grid_y = tiles;
     p.last_block = threads;

@@ -61,6 +61,11 @@ struct KParams {
     int copies;             // replicas of C the warps spread their reductions over (>= 1)
     int64_t plane;          // dim * R (floats per replica)
     int64_t dim;            // rows of B and C (bounds checks in SYSTEC_DEBUG builds)
+    // work distribution: ctr != nullptr -> dynamic (warps take units of `unit`
+    // consecutive entries from this zeroed counter); nullptr -> one static
+    // nnz-balanced range of `span` entries per warp
+    unsigned int *ctr;
+    int unit;
 };
 
 using KernelFn = void (*)(KParams);
@@ -130,11 +135,18 @@ __device__ __forceinline__ void mttkrp_sym_body(const KParams &p) {
     int32_t *wbuf = reinterpret_cast<int32_t *>(smem_raw) + static_cast<size_t>(warp) * S * ARR * CH;
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw + static_cast<size_t>(WPB) * S * ARR * CH * 4) + warp * S;
 
+    const bool dyn = p.ctr != nullptr;
+    // per-warp, per-stage chunk descriptors {base, count} (dynamic distribution)
+    int32_t *meta = reinterpret_cast<int32_t *>(smem_raw + static_cast<size_t>(WPB) * S * ARR * CH * 4 +
+                                                static_cast<size_t>(WPB) * S * 8) + static_cast<size_t>(warp) * S * 2;
     const int64_t gw = static_cast<int64_t>(blockIdx.x) * WPB + warp;
-    const int64_t begin = gw * p.span;
-    const int64_t end = min(begin + p.span, p.nnz);
-    if (begin >= end) return;  // warp-uniform; no block-wide barrier below
-    const int64_t nch = (end - begin + CH - 1) / CH;
+    int64_t begin = 0, end = 0, nch = 0;
+    if (!dyn) {
+        begin = gw * p.span;
+        end = min(begin + p.span, p.nnz);
+        if (begin >= end) return;  // warp-uniform; no block-wide barrier below
+        nch = (end - begin + CH - 1) / CH;
+    }
 
     const uint32_t R = p.R;
     const uint32_t Rb = R * 4u;  // row stride in bytes
@@ -166,10 +178,7 @@ __device__ __forceinline__ void mttkrp_sym_body(const KParams &p) {
     }
     __syncwarp();
 
-    auto issue = [&](int64_t k) {
-        const int s = static_cast<int>(k % S);
-        const int64_t cb = begin + k * CH;
-        const int64_t cnt = min(static_cast<int64_t>(CH), end - cb);
+    auto issue_at = [&](int s, int64_t cb, int64_t cnt) {
         const uint32_t bytes = static_cast<uint32_t>(((cnt + 3) & ~3ll) * 4);
         int32_t *dst = wbuf + static_cast<size_t>(s) * ARR * CH;
         mbar_arrive_expect_tx(&bars[s], bytes * ARR);
@@ -177,10 +186,46 @@ __device__ __forceinline__ void mttkrp_sym_body(const KParams &p) {
         for (int a = 0; a < N; ++a) bulk_g2s(dst + a * CH, p.coords + a * p.ld + cb, bytes, &bars[s], pol_stream);
         bulk_g2s(dst + N * CH, p.vals + cb, bytes, &bars[s], pol_stream);
     };
+    auto issue = [&](int64_t k) {
+        const int64_t cb = begin + k * CH;
+        issue_at(static_cast<int>(k % S), cb, min(static_cast<int64_t>(CH), end - cb));
+    };
+    // dynamic distribution: lane 0 walks units taken from the counter; a
+    // stage whose descriptor base is -1 ends the warp's stream
+    // (entry positions fit in int32: nnz < 2^31, include/systec.h)
+    const int nnz32 = static_cast<int>(p.nnz);
+    const unsigned units = dyn ? static_cast<unsigned>((p.nnz + p.unit - 1) / p.unit) : 0u;
+    unsigned du = 0;
+    int dnext = 0, dend = 0;  // lane 0: current unit, next chunk base, unit end
+    auto take_unit = [&]() {
+        du = atomicAdd(p.ctr + blockIdx.y, 1u);  // one counter per rank tile
+        dnext = static_cast<int>(min(static_cast<int64_t>(du) * p.unit, p.nnz));
+        dend = min(nnz32, dnext + p.unit);
+    };
+    auto issue_dyn = [&](int64_t k) {
+        const int s = static_cast<int>(k % S);
+        if (du < units) {
+            const int cnt = min(CH, dend - dnext);
+            meta[2 * s] = dnext;
+            meta[2 * s + 1] = cnt;
+            issue_at(s, dnext, cnt);
+            dnext += cnt;
+            if (dnext >= dend) take_unit();
+        } else {
+            meta[2 * s] = -1;
+        }
+    };
 
     constexpr bool kStage = (ABL & 1) == 0;
-    if (kStage && lane == 0)
+    if (dyn) {
+        if (lane == 0) {
+            take_unit();
+            for (int64_t k = 0; k < S - 1; ++k) issue_dyn(k);
+        }
+        __syncwarp();
+    } else if (kStage && lane == 0) {
         for (int64_t k = 0; k < min(static_cast<int64_t>(S - 1), nch); ++k) issue(k);
+    }
 
     // row address of row c for the lane's vector q: one IMAD.WIDE.U32
     auto rowB = [&](int32_t c, int q) { return reinterpret_cast<const float *>(Bq[q] + static_cast<uint64_t>(static_cast<uint32_t>(c)) * Rb); };
@@ -195,20 +240,34 @@ __device__ __forceinline__ void mttkrp_sym_body(const KParams &p) {
 #pragma unroll
     for (int q = 0; q < VPL; ++q) acc0[q] = acc1[q] = V::zero();
 
-    for (int64_t k = 0; k < nch; ++k) {
+    for (int64_t k = 0; dyn || k < nch; ++k) {
         const int s = static_cast<int>(k % S);
-        if (kStage) {
-            if (lane == 0 && k + S - 1 < nch) {
+        int64_t cb;
+        int cnt;
+        if (dyn) {
+            if (lane == 0) {
                 fence_proxy_async_smem();
-                issue(k + S - 1);
+                issue_dyn(k + S - 1);
             }
+            __syncwarp();
+            cb = meta[2 * s];
+            if (cb < 0) break;  // warp-uniform: this warp's stream is exhausted
+            cnt = meta[2 * s + 1];
             mbar_wait(&bars[s], static_cast<uint32_t>((k / S) & 1));
+        } else {
+            if (kStage) {
+                if (lane == 0 && k + S - 1 < nch) {
+                    fence_proxy_async_smem();
+                    issue(k + S - 1);
+                }
+                mbar_wait(&bars[s], static_cast<uint32_t>((k / S) & 1));
+            }
+            cb = begin + k * CH;
+            cnt = static_cast<int>(min(static_cast<int64_t>(CH), end - cb));
         }
 
         const int32_t *sc = wbuf + static_cast<size_t>(s) * ARR * CH;
         const float *sv = reinterpret_cast<const float *>(sc + N * CH);
-        const int64_t cb = begin + k * CH;
-        const int cnt = static_cast<int>(min(static_cast<int64_t>(CH), end - cb));
         const int lo = g * K;
         const int hi = min(lo + K, cnt);
 
@@ -375,7 +434,10 @@ __device__ __forceinline__ void mttkrp_sym_body(const KParams &p) {
         // the last segment (the one containing group E-1) starts at the highest head
         const unsigned heads = __ballot_sync(0xffffffffu, head && j == 0);
         const int hl = 31 - __clz(heads);  // lane (j == 0) of the last segment's head
-        const bool carry = (k + 1 < nch);  // chunk was full: the next chunk continues the stream
+        // carry the last segment when the warp's next chunk continues the stream
+        bool carry;
+        if (dyn) carry = meta[2 * ((k + 1) % S)] == cb + cnt;
+        else carry = (k + 1 < nch);
         const bool write = head && key >= 0 && !(carry && lane - j == hl);
 #pragma unroll
         for (int q = 0; q < VPL; ++q) V::red_if(rowC(key, q), acc0[q], write && act[q]);

@@ -33,7 +33,7 @@ class SystecExecOpts(ctypes.Structure):
                 ("no_zero", ctypes.c_int32), ("l2_hints", ctypes.c_int32),
                 ("chunk_k", ctypes.c_int32), ("stages", ctypes.c_int32), ("vpl", ctypes.c_int32),
                 ("prefetch", ctypes.c_int32), ("copies", ctypes.c_int32), ("ablation", ctypes.c_int32),
-                ("unused6", ctypes.c_int32), ("occupancy", ctypes.c_int32), ("reserved", ctypes.c_int32 * 2)]
+                ("static_ranges", ctypes.c_int32), ("occupancy", ctypes.c_int32), ("reserved", ctypes.c_int32 * 2)]
 
 
 EXPORTS = ["systec_mttkrp", "systec_mttkrp_host", "systec_plan_create", "systec_plan_execute",
@@ -127,7 +127,7 @@ def _opts(**kw) -> SystecExecOpts:
     names = {f for f, _ in SystecExecOpts._fields_}
     for k, v in kw.items():
         k = alias.get(k, k)
-        if k not in names or k in ("reserved", "unused6"):
+        if k not in names or k == "reserved":
             raise TypeError(f"unknown execute option {k!r}")
         setattr(o, k, int(v))
     return o

@@ -49,6 +49,7 @@ def test_parity_small(systec, n, dim, nnz, R):
     w = small_random(n, dim, nnz, R, seed=nnz + n, diag_frac=0.15)
     Cref, S = oracle.mttkrp(n, dim, w.idx, w.vals, w.B)
     parity(run(systec, w), Cref, S)
+    parity(run(systec, w, static_ranges=1), Cref, S)
 
 
 @pytest.mark.parametrize("R", [1, 2, 3, 4, 5, 8, 12, 16, 31, 32, 33, 64, 100, 128, 129, 256])
@@ -56,6 +57,7 @@ def test_rank_sweep(systec, R):
     w = small_random(3, 120, 3000, R, seed=R, diag_frac=0.2)
     Cref, S = oracle.mttkrp(3, 120, w.idx, w.vals, w.B)
     parity(run(systec, w), Cref, S)
+    parity(run(systec, w, static_ranges=1), Cref, S)   # one static range per warp
     parity(run(systec, w, force_scalar=1), Cref, S)
     parity(run(systec, w, copies=3), Cref, S)
     parity(run(systec, w, copies=4, force_scalar=1), Cref, S)
