@@ -275,7 +275,18 @@ cudaError_t launch_mttkrp(Plan &p, const float *B, int R, float *C, const systec
     kp.stages = stages;
     kp.hints = o.l2_hints >= 0 ? 1 : 0;
     kp.ctr = ctr;
-    kp.unit = E * K * 4;  // units of 4 chunks (~530 entries at E*K = 132)
+    // unit size: one chunk balances best (c2 0.476 vs 0.486 ms with 4), but a
+    // leading run spanning thousands of chunks (c3's hub row: 10M entries) is
+    // then flushed by a different warp at every chunk — tens of thousands of
+    // reductions into one row, serialised at its L2 slice (c3 2.69 vs 2.03 ms
+    // with 4-chunk units).  SYSTEC_UNIT_CHUNKS overrides (measurements).
+    static const int kUnitEnv = [] {
+        const char *v = std::getenv("SYSTEC_UNIT_CHUNKS");
+        const int u = v ? std::atoi(v) : 0;
+        return u < 0 ? 0 : (u > 64 ? 64 : u);
+    }();
+    const int unit_chunks = kUnitEnv > 0 ? kUnitEnv : (p.stats.max_lead_run > 4096ll * E * K ? 4 : 1);
+    kp.unit = E * K * unit_chunks;
     if (dyn) blocks = static_cast<int64_t>(sms) * occ;  // persistent: every resident warp takes units
     dim3 grid(static_cast<unsigned>(blocks), static_cast<unsigned>(tiles));
     fn<<<grid, threads, smem, s>>>(kp);
