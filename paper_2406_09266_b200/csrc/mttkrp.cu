@@ -150,7 +150,11 @@ cudaError_t launch_mttkrp(Plan &p, const float *B, int R, float *C, const systec
     // work distribution: dynamic units from a counter (default) or one static
     // range per warp (opts.static_ranges = 1; measured: c3 2.43 -> 2.04 ms,
     // c4 -2 %, c5 -2 %, c2 -0.3 % with the dynamic one, profiles/r01_sweep_dynamic.jsonl)
-    const bool dyn = o.static_ranges <= 0;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    // (a problem with fewer ~128-entry units than 8 warps per SM never runs dynamic: no counter)
+    const bool dyn = o.static_ranges <= 0 && p.nnz / 128 >= static_cast<int64_t>(sms) * 8;
     const int64_t rep_f = copies > 1 ? static_cast<int64_t>(copies) * plane : 0;
     const int64_t nctr = dyn ? counter_slots(R) : 0;
     const int64_t need_f = rep_f + nctr;
@@ -166,13 +170,13 @@ cudaError_t launch_mttkrp(Plan &p, const float *B, int R, float *C, const systec
         }
     }
     unsigned int *ctr = dyn ? reinterpret_cast<unsigned int *>(scratch + rep_f) : nullptr;
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (copies > 1) {
         e = cudaMemsetAsync(scratch, 0, static_cast<size_t>(need_f) * 4, s);  // replicas (+ counter)
         if (e != cudaSuccess) return e;
         Cdst = scratch;
+    } else if (!o.no_zero && !ctr) {
+        e = cudaMemsetAsync(C, 0, static_cast<size_t>(plane) * sizeof(float), s);
+        if (e != cudaSuccess) return e;
     } else if (!o.no_zero) {
         const int vec = (reinterpret_cast<uintptr_t>(C) % 16 == 0) ? 1 : 0;
         const int64_t work = std::max<int64_t>(1, vec ? plane / 4 : plane);
@@ -287,7 +291,13 @@ cudaError_t launch_mttkrp(Plan &p, const float *B, int R, float *C, const systec
     }();
     const int unit_chunks = kUnitEnv > 0 ? kUnitEnv : (p.stats.max_lead_run > 4096ll * E * K ? 4 : 1);
     kp.unit = E * K * unit_chunks;
-    if (dyn) blocks = static_cast<int64_t>(sms) * occ;  // persistent: every resident warp takes units
+    // problems with fewer units than resident warps (c1: 16 units) keep the
+    // finer static split: more warps in flight beat balance there (c1 kernel
+    // 6.2 vs 9.3 us)
+    const int64_t units = (p.nnz + kp.unit - 1) / kp.unit;
+    if (dyn && units >= total_warps) blocks = static_cast<int64_t>(sms) * occ;  // persistent
+    else kp.ctr = nullptr;
+
     dim3 grid(static_cast<unsigned>(blocks), static_cast<unsigned>(tiles));
     fn<<<grid, threads, smem, s>>>(kp);
     if (copies > 1) {
@@ -303,9 +313,9 @@ cudaError_t launch_mttkrp(Plan &p, const float *B, int R, float *C, const systec
     p.last_grid_y = tiles;
     p.last_block = threads;
     p.last_smem = static_cast<int>(smem);
-    // kernel id, decimal fields: general | copies (2 digits) | pf | order | vw | lpe (2 digits) | vpl | pos1;
+    // kernel id, decimal fields: general | copies (2 digits) | pf + 2*dynamic | order | vw | lpe (2 digits) | vpl | pos1;
     // the occupancy variant sets vpl's digit to 5 (vpl itself is 1 there)
-    p.last_kernel = (p.general ? 1000000000 : 0) + copies * 10000000 + (pf ? 1000000 : 0) + p.order * 100000 + vw * 10000 + lpe * 100 + (occ5 ? 5 : vpl) * 10 + (pos1 ? 1 : 0);
+    p.last_kernel = (p.general ? 1000000000 : 0) + copies * 10000000 + ((pf ? 1 : 0) + (kp.ctr ? 2 : 0)) * 1000000 + p.order * 100000 + vw * 10000 + lpe * 100 + (occ5 ? 5 : vpl) * 10 + (pos1 ? 1 : 0);
     return cudaGetLastError();
 }
 

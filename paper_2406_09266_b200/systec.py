@@ -251,8 +251,9 @@ class Plan:
         _check(load().systec_plan_last_launch(self._h, *[ctypes.byref(v) for v in vals]), "systec_plan_last_launch")
         d = dict(zip(["grid_x", "grid_y", "block", "smem_bytes", "kernel_id"], [v.value for v in vals]))
         kid = d["kernel_id"]
-        if kid >= 0:   # decimal fields: general | copies (2) | pf | order | vw | lpe (2 digits) | vpl | pos1
-            d.update(general=kid // 1000000000, copies=kid // 10000000 % 100, prefetch=kid // 1000000 % 10,
+        if kid >= 0:   # decimal fields: general | copies (2) | pf + 2 dynamic | order | vw | lpe (2 digits) | vpl | pos1
+            d.update(general=kid // 1000000000, copies=kid // 10000000 % 100, prefetch=kid // 1000000 % 2,
+                     dynamic=kid // 1000000 % 10 // 2,
                      order=kid // 100000 % 10,
                      vw=kid // 10000 % 10, lpe=kid // 100 % 100, vpl=kid // 10 % 10, pos1=kid % 10)
         return d

@@ -393,6 +393,28 @@ def test_key_width_limits(systec, order, bits, R):
     plan.destroy()
 
 
+def test_work_distribution_modes(systec):
+    """Dynamic units when the problem has at least one unit per resident warp,
+    the static split otherwise or on request; same result either way."""
+    import torch
+    w = small_random(3, 3000, 1_500_000, 32, seed=21, diag_frac=0.01)
+    Cref, S = oracle.mttkrp(3, 3000, w.idx, w.vals, w.B)
+    di, dv, dB = to_dev(w.idx, w.vals, w.B)
+    plan = systec.Plan(3, 3000, di, dv)
+    for opts, want in (({}, 1), ({"static_ranges": 1}, 0)):
+        C = plan.execute(dB, **opts)
+        torch.cuda.synchronize()
+        assert plan.last_launch()["dynamic"] == want
+        parity(C.cpu().numpy(), Cref, S)
+    plan.destroy()
+    w = small_random(3, 64, 2000, 8, seed=22, diag_frac=0.1)
+    di, dv, dB = to_dev(w.idx, w.vals, w.B)
+    plan = systec.Plan(3, 64, di, dv)
+    plan.execute(dB)
+    assert plan.last_launch()["dynamic"] == 0        # 16 units: the finer static split
+    plan.destroy()
+
+
 def test_concurrent_executes_on_streams_and_threads(systec):
     """include/systec.h: a plan is immutable; concurrent executes on different
     streams (from different host threads too) are safe when their C differ."""
