@@ -192,7 +192,10 @@ SYSTEC_API int systec_cp_als_sym(systec_plan plan, float *B, int R, float *lambd
  * relaxations ran; *iters_done (may be NULL) receives the relaxations done,
  * counting the last one that changed nothing.  Weights must not create
  * negative cycles (an undirected negative edge is one).  Synchronises `stream`
- * once per iteration.  Errors: ARG, UNSUPPORTED (order != 2), NOMEM, CUDA.
+ * once per iteration (environment SYSTEC_SSSP_LOOP=graph: the loop runs on the
+ * device as one CUDA graph with a conditional WHILE node, one synchronisation
+ * at the end — for graphs needing many relaxations).
+ * Errors: ARG, UNSUPPORTED (order != 2), NOMEM, CUDA.
  */
 SYSTEC_API int systec_plan_sssp(systec_plan plan, int64_t source, float *dist, int max_iters, int *iters_done,
                                 systec_stream_t stream);

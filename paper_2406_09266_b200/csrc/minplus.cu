@@ -86,7 +86,45 @@ __global__ void changed_kernel(const float *__restrict__ y, const float *__restr
     if (__any_sync(0xffffffffu, any) && (threadIdx.x & 31) == 0) atomicOr(changed, 1);
 }
 
+// d = y where they differ, *changed |= any difference (one pass: the
+// relaxation's convergence test and the copy back together)
+__global__ void sssp_update_kernel(const float *__restrict__ y, float *__restrict__ d, int64_t dim, int *changed) {
+    bool any = false;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < dim; i += (int64_t)gridDim.x * blockDim.x) {
+        const float v = y[i];
+        if (v != d[i]) {
+            d[i] = v;
+            any = true;
+        }
+    }
+    if (__any_sync(0xffffffffu, any) && (threadIdx.x & 31) == 0) atomicOr(changed, 1);
+}
+
+// device-side loop control of the SSSP graph: one more relaxation while
+// something changed and the iteration budget lasts
+__global__ void sssp_step_kernel(const int *changed, int *iters, int max_iters, cudaGraphConditionalHandle h) {
+    const int it = ++(*iters);
+    cudaGraphSetConditional(h, (*changed != 0 && it < max_iters) ? 1u : 0u);
+}
+
 }  // namespace
+
+cudaError_t launch_sssp_update(const float *y, float *d, int64_t dim, int *changed, cudaStream_t s) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int gb = static_cast<int>(std::min<int64_t>((dim + 255) / 256, static_cast<int64_t>(sms) * 8));
+    cudaError_t e = cudaMemsetAsync(changed, 0, sizeof(int), s);
+    if (e != cudaSuccess) return e;
+    sssp_update_kernel<<<gb, 256, 0, s>>>(y, d, dim, changed);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_sssp_step(const int *changed, int *iters, int max_iters, cudaGraphConditionalHandle h,
+                             cudaStream_t s) {
+    sssp_step_kernel<<<1, 1, 0, s>>>(changed, iters, max_iters, h);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_sssp_init(float *d, int64_t dim, int64_t source, cudaStream_t s) {
     int dev = 0, sms = 148;

@@ -154,7 +154,12 @@ cudaError_t launch_mttkrp(Plan &p, const float *B, int R, float *C, const systec
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     // (a problem with fewer ~128-entry units than 8 warps per SM never runs dynamic: no counter)
-    const bool dyn = o.static_ranges <= 0 && p.nnz / 128 >= static_cast<int64_t>(sms) * 8;
+    // dynamic units pay where the per-chunk work is large and the costs per
+    // entry vary (orders >= 3 with float4 lanes); orders 2 and scalar ranks keep
+    // the static split (order 2, dim 1e6, 10M nnz: R = 1 0.115 vs 0.123 ms,
+    // R = 32 0.558 vs 0.568 ms static vs dynamic)
+    const bool dyn = o.static_ranges <= 0 && p.order >= 3 && R >= 8 && !p.general &&
+                     p.nnz / 128 >= static_cast<int64_t>(sms) * 8;
     const int64_t rep_f = copies > 1 ? static_cast<int64_t>(copies) * plane : 0;
     const int64_t nctr = dyn ? counter_slots(R) : 0;
     const int64_t need_f = rep_f + nctr;
@@ -289,7 +294,8 @@ cudaError_t launch_mttkrp(Plan &p, const float *B, int R, float *C, const systec
         const int u = v ? std::atoi(v) : 0;
         return u < 0 ? 0 : (u > 64 ? 64 : u);
     }();
-    const int unit_chunks = kUnitEnv > 0 ? kUnitEnv : (p.stats.max_lead_run > 4096ll * E * K ? 4 : 1);
+    const bool big_b = p.dim * static_cast<int64_t>(R) * 4 > (64ll << 20);  // B (and C) not L2-resident
+    const int unit_chunks = kUnitEnv > 0 ? kUnitEnv : ((p.stats.max_lead_run > 4096ll * E * K || big_b) ? 4 : 1);
     kp.unit = E * K * unit_chunks;
     // problems with fewer units than resident warps (c1: 16 units) keep the
     // finer static split: more warps in flight beat balance there (c1 kernel

@@ -197,6 +197,8 @@ __device__ __forceinline__ void mttkrp_sym_body(const KParams &p) {
     const unsigned units = dyn ? static_cast<unsigned>((p.nnz + p.unit - 1) / p.unit) : 0u;
     unsigned du = 0;
     int dnext = 0, dend = 0;  // lane 0: current unit, next chunk base, unit end
+    // (requesting the following unit's id one unit ahead, to overlap the
+    // atomic's round trip, measured 0.5-1 % slower on c2/c5: not done)
     auto take_unit = [&]() {
         du = atomicAdd(p.ctr + blockIdx.y, 1u);  // one counter per rank tile
         dnext = static_cast<int>(min(static_cast<int64_t>(du) * p.unit, p.nnz));

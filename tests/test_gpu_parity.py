@@ -681,9 +681,11 @@ def test_single_giant_run_and_all_singleton_runs(systec, R):
 
 
 @pytest.mark.parametrize("dim,nnz", [(300, 2000), (20000, 200000)])
-def test_sssp_bit_exact_vs_iterated_oracle(systec, dim, nnz):
+@pytest.mark.parametrize("loop", ["graph", "host"])
+def test_sssp_bit_exact_vs_iterated_oracle(systec, dim, nnz, loop, monkeypatch):
     import torch
     from test_oracle_pins import oracle_sssp
+    monkeypatch.setenv("SYSTEC_SSSP_LOOP", loop)
     w = make(f"g{dim}", 2, dim, nnz, 1, seed=dim, mode="uniform")
     vals = np.random.default_rng(dim).uniform(0.1, 5.0, nnz).astype(np.float32)
     want, iters = oracle_sssp(dim, w.idx, vals, 3)
@@ -694,6 +696,15 @@ def test_sssp_bit_exact_vs_iterated_oracle(systec, dim, nnz):
     dist2, done2 = plan.sssp(3, max_iters=2)
     torch.cuda.synchronize()
     assert done2 == 2
+    dist1, done1 = plan.sssp(3, max_iters=1)
+    torch.cuda.synchronize()
+    assert done1 == 1
+    want1, _ = oracle_sssp(dim, w.idx, vals, 3, max_iters=1)
+    assert np.array_equal(dist1.cpu().numpy(), want1)
+    dist0, done0 = plan.sssp(3, max_iters=0)
+    torch.cuda.synchronize()
+    d0 = dist0.cpu().numpy()
+    assert done0 == 0 and d0[3] == 0 and np.all(np.isinf(np.delete(d0, 3)))
 
 
 def test_execute_argument_errors(systec):

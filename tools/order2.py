@@ -73,6 +73,21 @@ def main():
             t2 = timed(lambda: gen.execute(B, C1, **o), a.reps, flush)
             print(json.dumps({"kernel": "SSYMV", "opts": o, "t_sym_ms": t1, "t_naive_ms": t2,
                               "launch": sym.last_launch()}), flush=True)
+    # Bellman-Ford to convergence (device-graph loop vs host loop); positive
+    # weights (the uniform(-1, 1) values above would hold negative cycles)
+    sp = systec.Plan(2, a.dim, di, (dv.abs() + 0.1).contiguous())
+    for loop in ("graph", "host"):
+        os.environ["SYSTEC_SSSP_LOOP"] = loop
+        sp.sssp(0)
+        torch.cuda.synchronize()
+        t0 = __import__("time").perf_counter()
+        dist, iters = sp.sssp(0)
+        torch.cuda.synchronize()
+        dt = (__import__("time").perf_counter() - t0) * 1e3
+        print(json.dumps({"kernel": "SSSP (Bellman-Ford to convergence)", "loop": loop, "dim": a.dim,
+                          "stored_nnz": a.nnz, "relaxations": iters, "t_ms": dt, "ms_per_relaxation": dt / iters}),
+              flush=True)
+    os.environ.pop("SYSTEC_SSSP_LOOP", None)
     d = torch.from_numpy(rng.uniform(0, 100, a.dim).astype(np.float32)).cuda()
     y = torch.empty_like(d)
     t_mp = timed(lambda: sym.minplus(d, y), a.reps, flush)
