@@ -158,7 +158,8 @@ cudaError_t launch_mttkrp(Plan &p, const float *B, int R, float *C, const systec
     // entry vary (orders >= 3 with float4 lanes); orders 2 and scalar ranks keep
     // the static split (order 2, dim 1e6, 10M nnz: R = 1 0.115 vs 0.123 ms,
     // R = 32 0.558 vs 0.568 ms static vs dynamic)
-    const bool dyn = o.static_ranges <= 0 && p.order >= 3 && R >= 8 && !p.general &&
+    // (the ablation builds keep the static split they were measured with)
+    const bool dyn = o.static_ranges <= 0 && o.ablation <= 0 && p.order >= 3 && R >= 8 && !p.general &&
                      p.nnz / 128 >= static_cast<int64_t>(sms) * 8;
     const int64_t rep_f = copies > 1 ? static_cast<int64_t>(copies) * plane : 0;
     const int64_t nctr = dyn ? counter_slots(R) : 0;
