@@ -62,7 +62,6 @@ cudaError_t expand_write(int order, int64_t nnz, const int32_t *idx, const float
 // minplus.cu — keys may alias y (in-place order-preserving integer keys)
 cudaError_t launch_minplus(const Plan &p, const float *d, float *y, int *scratch_keys, cudaStream_t s);
 cudaError_t launch_sssp_init(float *d, int64_t dim, int64_t source, cudaStream_t s);
-cudaError_t launch_changed(const float *y, const float *d, int64_t dim, int *changed, cudaStream_t s);
 // d = y where different, *changed = any difference (zeroes *changed first)
 cudaError_t launch_sssp_update(const float *y, float *d, int64_t dim, int *changed, cudaStream_t s);
 cudaError_t launch_sssp_step(const int *changed, int *iters, int max_iters, cudaGraphConditionalHandle h,

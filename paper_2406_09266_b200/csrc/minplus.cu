@@ -78,14 +78,6 @@ __global__ void sssp_init_kernel(float *__restrict__ d, int64_t dim, int64_t sou
         d[i] = (i == source) ? 0.f : __int_as_float(0x7f800000);  // +inf
 }
 
-// *changed |= any(y != d)
-__global__ void changed_kernel(const float *__restrict__ y, const float *__restrict__ d, int64_t dim, int *changed) {
-    bool any = false;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < dim; i += (int64_t)gridDim.x * blockDim.x)
-        any |= (y[i] != d[i]);
-    if (__any_sync(0xffffffffu, any) && (threadIdx.x & 31) == 0) atomicOr(changed, 1);
-}
-
 // d = y where they differ, *changed |= any difference (one pass: the
 // relaxation's convergence test and the copy back together)
 __global__ void sssp_update_kernel(const float *__restrict__ y, float *__restrict__ d, int64_t dim, int *changed) {
@@ -132,17 +124,6 @@ cudaError_t launch_sssp_init(float *d, int64_t dim, int64_t source, cudaStream_t
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int gb = static_cast<int>(std::min<int64_t>((dim + 255) / 256, static_cast<int64_t>(sms) * 8));
     sssp_init_kernel<<<gb, 256, 0, s>>>(d, dim, source);
-    return cudaGetLastError();
-}
-
-cudaError_t launch_changed(const float *y, const float *d, int64_t dim, int *changed, cudaStream_t s) {
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int gb = static_cast<int>(std::min<int64_t>((dim + 255) / 256, static_cast<int64_t>(sms) * 8));
-    cudaError_t e = cudaMemsetAsync(changed, 0, sizeof(int), s);
-    if (e != cudaSuccess) return e;
-    changed_kernel<<<gb, 256, 0, s>>>(y, d, dim, changed);
     return cudaGetLastError();
 }
 
