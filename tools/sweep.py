@@ -21,7 +21,7 @@ def main():
     ap.add_argument("--configs", default="c2")
     ap.add_argument("--variants", default="")
     ap.add_argument("--reps", type=int, default=30)
-    ap.add_argument("--split", type=int, default=-1, help="plan creation: -1 default, 1 split, 0 no split")
+    ap.add_argument("--split", type=int, default=-1, help="plan creation (split-plan experiment builds): -1 default, 1 split, 0 no split")
     a = ap.parse_args()
     import numpy as np
     import torch
@@ -32,8 +32,8 @@ def main():
     variants = [parse_variant(v) for v in a.variants.split(";")] if a.variants else [{}]
     for name in a.configs.split(","):
         w = generate(name)
-        plan = systec.Plan(w.order, w.dim, torch.from_numpy(w.idx).cuda(), torch.from_numpy(w.vals).cuda(),
-                           split=None if a.split < 0 else bool(a.split))
+        kw = {} if a.split < 0 else {"split": bool(a.split)}   # split: experiment builds only
+        plan = systec.Plan(w.order, w.dim, torch.from_numpy(w.idx).cuda(), torch.from_numpy(w.vals).cuda(), **kw)
         st = plan.stats()
         B = torch.from_numpy(w.B).cuda()
         C = torch.empty((w.dim, w.R), device="cuda")
