@@ -339,7 +339,9 @@ __device__ __forceinline__ void mttkrp_sym_body(const KParams &p) {
                     }
                     u[0][q] = V::scale(sc0, Q);
                 }
-                if (__any_sync(__activemask(), !strict) && !strict) {  // warp-uniform skip when all strict
+                // diagonal entry: rescale by its coefficient row (a per-lane branch;
+                // a warp vote in front of it measured 2.6 % slower on c3)
+                if (!strict) {
                     const float *cf = coef + code * kMaxOrder;
 #pragma unroll
                     for (int t = 0; t < N; ++t) {
