@@ -71,11 +71,12 @@ typedef struct systec_stats {
     int64_t G;                   /* sum over entries of the number of distinct indices d_e     */
     int64_t expanded;            /* sum over entries of the orbit size n!/prod m! (naive work) */
     int64_t pattern_hist[16];    /* entries per equality-pattern code (bit t: c_t == c_{t+1})  */
-    int64_t lead_runs;           /* runs of equal leading index c_0 in sorted order            */
+    int64_t lead_runs;           /* runs of equal leading index c_0 in the plan's stream order */
     int64_t max_lead_run;        /* longest such run                                           */
-    int64_t pos1_runs;           /* runs of equal c_1 in sorted order                          */
+    int64_t pos1_runs;           /* runs of equal c_1 in the plan's stream order               */
     int32_t input_was_sorted;    /* 1: input already canonical and lexicographically sorted    */
-    int32_t pad0;
+    int32_t band_shift;          /* -1: stream in lexicographic order; s >= 0: grouped by band */
+                                 /* c_{n-1} >> s, lexicographic within a band (plan options)   */
     int64_t bad_entry;           /* first entry with an index outside [0,dim), else -1         */
 } systec_stats;
 
@@ -103,6 +104,20 @@ typedef struct systec_exec_opts {
 } systec_exec_opts;
 
 typedef struct systec_plan_s *systec_plan;
+
+/* Plan-creation options for systec_plan_create_ex; zero fields = defaults. */
+typedef struct systec_plan_opts {
+    int32_t band_shift;          /* stream order: 0 = auto, -1 = lexicographic, s > 0 = group  */
+                                 /* entries by band c_{n-1} >> s (band-major, lexicographic    */
+                                 /* within a band) when the band number fits the 64-bit sort   */
+                                 /* key beside the indices, else lexicographic.  Auto bands    */
+                                 /* order-3 plans with dim >= 2^19 into up to 16 bands (no     */
+                                 /* fewer than 2^16 rows each; fewer bands when leading runs   */
+                                 /* are short): the rows that positions >= 1 gather and update */
+                                 /* then stay within an L2-sized window while a band runs.     */
+                                 /* Any order gives the same C up to fp32 rounding order.      */
+    int32_t reserved[7];
+} systec_plan_opts;
 
 /*
  * One-shot call with the paper's signature (north_star):
@@ -137,6 +152,17 @@ SYSTEC_API int systec_mttkrp_host(int order, int64_t dim, int64_t nnz, const int
  */
 SYSTEC_API int systec_plan_create(systec_plan *out, int order, int64_t dim, int64_t nnz,
                        const int32_t *idx, const float *vals, systec_stream_t stream);
+
+/*
+ * systec_plan_create with options (NULL = defaults, i.e. systec_plan_create).
+ * A banded plan (systec_plan_opts.band_shift) re-sorts its prepared stream
+ * once more on the device (one more synchronisation of `stream`).
+ * Errors: as systec_plan_create; ARG for band_shift < -1 or a non-zero
+ * reserved field.
+ */
+SYSTEC_API int systec_plan_create_ex(systec_plan *out, int order, int64_t dim, int64_t nnz,
+                                     const int32_t *idx, const float *vals, const systec_plan_opts *opts,
+                                     systec_stream_t stream);
 
 /*
  * The non-symmetric baseline (the paper's "naive"

@@ -16,6 +16,7 @@
 
 static_assert(sizeof(systec_exec_opts) == 64, "systec_exec_opts layout is part of the ABI");
 static_assert(sizeof(systec_stats) == 208, "systec_stats layout is part of the ABI");
+static_assert(sizeof(systec_plan_opts) == 32, "systec_plan_opts layout is part of the ABI");
 
 namespace systec {
 
@@ -68,9 +69,100 @@ int check_shape(int order, int64_t dim, int64_t nnz, int *bits_out) {
     return SYSTEC_OK;
 }
 
+void fill_stats(Plan *p, const DevStats &hst) {
+    systec_stats &st = p->stats;
+    st.G = static_cast<int64_t>(hst.G);
+    st.expanded = static_cast<int64_t>(hst.expanded);
+    for (int c = 0; c < 16; ++c) st.pattern_hist[c] = static_cast<int64_t>(hst.hist[c]);
+    st.lead_runs = static_cast<int64_t>(hst.lead_runs);
+    st.max_lead_run = static_cast<int64_t>(hst.max_lead_run);
+    st.pos1_runs = static_cast<int64_t>(hst.pos1_runs);
+}
+
+// Band shift for a plan's stream order (systec_plan_opts.band_shift; -1 = lexicographic).
+// Auto: order-3 symmetric plans with dim >= 2^19, i.e. B and C of at least
+// 2 x 16 MB at R = 8 — c3 (dim 1e6, Zipf) runs 1.96 -> 1.82 ms with 16 bands,
+// a uniform dim-1e6 order-3 tensor 1.62 -> 1.47 ms with 4; order 2 loses
+// (its only reuse is the leading run, which bands cut) and is never banded
+// automatically.  Bands: the largest power of two <= mean leading run / 5,
+// at most 16 and at least 2^16 rows each (profiles/r01_band_sweep*.jsonl).
+int choose_band_shift(int request, int order, int64_t dim, int bits, int64_t nnz, int64_t lead_runs, bool general) {
+    if (general || request < 0 || nnz < 2) return -1;
+    int shift;
+    if (request > 0) {
+        shift = request;
+    } else {
+        if (order != 3 || dim < (int64_t(1) << 19) || lead_runs < 1) return -1;
+        const double mean_run = static_cast<double>(nnz) / static_cast<double>(lead_runs);
+        int bb = 0;
+        while (bb < 4 && static_cast<double>(int64_t(2) << bb) <= mean_run / 5.0) ++bb;
+        shift = std::max(bits - bb, 16);
+    }
+    if (shift >= 31) return -1;
+    const int64_t bands = ((dim - 1) >> shift) + 1;
+    if (bands < 2) return -1;
+    const int band_bits = ceil_log2(bands);
+    return bits * order + band_bits <= 64 ? shift : -1;
+}
+
+// Re-sorts a plan's prepared stream band-major (key: band of c_{n-1}, then the
+// lexicographic fields) into new storage and refreshes its run statistics.
+int apply_bands(Plan *p, int shift, bool pooled, cudaStream_t s) {
+    const int64_t nnz = p->nnz;
+    const size_t nk = static_cast<size_t>(nnz);
+    const int band_bits = ceil_log2(((p->dim - 1) >> shift) + 1);
+    const size_t bytes = static_cast<size_t>(p->order + 1) * p->ld * 4;
+    void *storage = nullptr;
+    DevStats *dst = nullptr;
+    unsigned long long *keys = nullptr, *keys2 = nullptr;
+    uint32_t *perm = nullptr, *perm2 = nullptr;
+    auto cleanup = [&]() {
+        if (dst) cudaFreeAsync(dst, s);
+        if (keys) cudaFreeAsync(keys, s);
+        if (keys2) cudaFreeAsync(keys2, s);
+        if (perm) cudaFreeAsync(perm, s);
+        if (perm2) cudaFreeAsync(perm2, s);
+    };
+    auto fail = [&](cudaError_t err) {
+        cleanup();
+        if (storage) { if (pooled) cudaFreeAsync(storage, s); else cudaFree(storage); }
+        return cuda_fail(err);
+    };
+    cudaError_t e = pooled ? cudaMallocAsync(&storage, bytes, s) : cudaMalloc(&storage, bytes);
+    if (e != cudaSuccess) { storage = nullptr; return fail(e); }
+    int32_t *coords = static_cast<int32_t *>(storage);
+    float *vals = reinterpret_cast<float *>(coords + static_cast<size_t>(p->order) * p->ld);
+    if ((e = cudaMallocAsync(&dst, sizeof(DevStats), s)) != cudaSuccess) return fail(e);
+    if ((e = cudaMallocAsync(&keys, nk * 8, s)) != cudaSuccess) return fail(e);
+    if ((e = cudaMallocAsync(&keys2, nk * 8, s)) != cudaSuccess) return fail(e);
+    if ((e = cudaMallocAsync(&perm, nk * 4, s)) != cudaSuccess) return fail(e);
+    if ((e = cudaMallocAsync(&perm2, nk * 4, s)) != cudaSuccess) return fail(e);
+    if ((e = cudaMemsetAsync(dst, 0, sizeof(DevStats), s)) != cudaSuccess) return fail(e);
+    if ((e = launch_band_keys(p->order, nnz, p->ld, p->coords, p->key_bits, shift, keys, perm, s)) != cudaSuccess)
+        return fail(e);
+    if ((e = sort_keys(nnz, p->key_bits * p->order + band_bits, keys, keys2, perm, perm2, s)) != cudaSuccess)
+        return fail(e);
+    if ((e = launch_gather(p->order, nnz, p->ld, p->key_bits, keys2, perm2, p->vals, coords, vals, s)) != cudaSuccess)
+        return fail(e);
+    if ((e = launch_stats(p->order, nnz, p->ld, coords, shift, dst, s)) != cudaSuccess) return fail(e);
+    DevStats hst;
+    if ((e = cudaMemcpyAsync(&hst, dst, sizeof(hst), cudaMemcpyDeviceToHost, s)) != cudaSuccess) return fail(e);
+    cleanup();
+    dst = nullptr; keys = nullptr; keys2 = nullptr; perm = nullptr; perm2 = nullptr;
+    if (p->pooled) cudaFreeAsync(p->storage, s); else cudaFree(p->storage);
+    p->storage = storage;
+    p->coords = coords;
+    p->vals = vals;
+    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return cuda_fail(e);  // the band statistics
+    fill_stats(p, hst);
+    p->band_shift = shift;
+    p->stats.band_shift = shift;
+    return SYSTEC_OK;
+}
+
 // Builds the plan.  `pooled` plans keep their storage in the stream-ordered pool.
 int plan_create_impl(Plan **out, int order, int64_t dim, int64_t nnz, const int32_t *idx, const float *vals,
-                     cudaStream_t s, bool pooled, bool general = false) {
+                     cudaStream_t s, bool pooled, bool general = false, int band_request = 0) {
     *out = nullptr;
     int bits = 0;
     int rc = check_shape(order, dim, nnz, &bits);
@@ -123,7 +215,7 @@ int plan_create_impl(Plan **out, int order, int64_t dim, int64_t nnz, const int3
     if ((e = cudaMemcpyAsync(dst, &hst, sizeof(hst), cudaMemcpyHostToDevice, s)) != cudaSuccess) return fail(e);
 
     // a1: validate + canonicalise + pack keys
-    if ((e = launch_canonicalize(order, dim, nnz, bits, idx, keys, perm, dst, s, !general)) != cudaSuccess)
+    if ((e = launch_canonicalize(order, dim, nnz, bits, -1, idx, keys, perm, dst, s, !general)) != cudaSuccess)
         return fail(e);
     if ((e = cudaMemcpyAsync(&hst, dst, sizeof(hst), cudaMemcpyDeviceToHost, s)) != cudaSuccess) return fail(e);
     if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return fail(e);  // sync 1: validation verdict
@@ -147,7 +239,7 @@ int plan_create_impl(Plan **out, int order, int64_t dim, int64_t nnz, const int3
     }
     if ((e = launch_gather(order, nnz, p->ld, bits, skeys, sperm, vals, p->coords, p->vals, s)) != cudaSuccess)
         return fail(e);
-    if ((e = launch_stats(order, nnz, p->ld, p->coords, dst, s)) != cudaSuccess) return fail(e);
+    if ((e = launch_stats(order, nnz, p->ld, p->coords, -1, dst, s)) != cudaSuccess) return fail(e);
     if ((e = cudaMemcpyAsync(&hst, dst, sizeof(hst), cudaMemcpyDeviceToHost, s)) != cudaSuccess) return fail(e);
     cleanup();
     dst = nullptr; keys = nullptr; keys2 = nullptr; perm = nullptr; perm2 = nullptr;
@@ -161,14 +253,17 @@ int plan_create_impl(Plan **out, int order, int64_t dim, int64_t nnz, const int3
     st.dim = dim;
     st.order = order;
     st.key_bits = bits;
-    st.G = static_cast<int64_t>(hst.G);
-    st.expanded = static_cast<int64_t>(hst.expanded);
-    for (int c = 0; c < 16; ++c) st.pattern_hist[c] = static_cast<int64_t>(hst.hist[c]);
-    st.lead_runs = static_cast<int64_t>(hst.lead_runs);
-    st.max_lead_run = static_cast<int64_t>(hst.max_lead_run);
-    st.pos1_runs = static_cast<int64_t>(hst.pos1_runs);
+    fill_stats(p, hst);
     st.input_was_sorted = sorted ? 1 : 0;
+    st.band_shift = -1;
     st.bad_entry = -1;
+    // banded stream order (a second device sort of the prepared stream)
+    const int shift = choose_band_shift(band_request, order, dim, bits, nnz, st.lead_runs, general);
+    if (shift >= 0 && (rc = apply_bands(p, shift, pooled, s)) != SYSTEC_OK) {
+        if (pooled) cudaFreeAsync(p->storage, s); else cudaFree(p->storage);
+        delete p;
+        return rc;
+    }
     *out = p;
     return SYSTEC_OK;
 }
@@ -207,6 +302,24 @@ int systec_plan_create(systec_plan *out, int order, int64_t dim, int64_t nnz, co
     if (!out) return SYSTEC_ERR_ARG;
     Plan *p = nullptr;
     int rc = systec::plan_create_impl(&p, order, dim, nnz, idx, vals, reinterpret_cast<cudaStream_t>(stream), false);
+    *out = reinterpret_cast<systec_plan>(p);
+    return rc;
+}
+
+int systec_plan_create_ex(systec_plan *out, int order, int64_t dim, int64_t nnz, const int32_t *idx,
+                          const float *vals, const systec_plan_opts *opts, systec_stream_t stream) {
+    if (!out) return SYSTEC_ERR_ARG;
+    *out = nullptr;
+    int band = 0;
+    if (opts) {
+        if (opts->band_shift < -1) return SYSTEC_ERR_ARG;
+        for (int r : opts->reserved)
+            if (r) return SYSTEC_ERR_ARG;
+        band = opts->band_shift;
+    }
+    Plan *p = nullptr;
+    int rc = systec::plan_create_impl(&p, order, dim, nnz, idx, vals, reinterpret_cast<cudaStream_t>(stream), false,
+                                      false, band);
     *out = reinterpret_cast<systec_plan>(p);
     return rc;
 }
@@ -734,11 +847,11 @@ int mttkrp_host_pipelined(int order, int64_t dim, int64_t nnz, int bits, const i
         for (int k = 0; k < nch; ++k) {
             const int64_t lo = k * per, n = std::min(per, nnz - lo);
             if ((e = cudaStreamWaitEvent(s, ev[k], 0)) != cudaSuccess) break;
-            if ((e = launch_canonicalize(order, dim, n, bits, d_idx + lo * order, keys, perm, dst, s, true, lo)) != cudaSuccess)
+            if ((e = launch_canonicalize(order, dim, n, bits, -1, d_idx + lo * order, keys, perm, dst, s, true, lo)) != cudaSuccess)
                 break;
             if ((e = launch_gather_range(order, n, ld, bits, keys, d_vals + lo, coords + lo, svals + lo, s)) != cudaSuccess) break;
             if (k == 0) {  // chunk-0 statistics decide position-1 accumulation (one sync)
-                if ((e = launch_stats(order, n, ld, coords, dst, s)) != cudaSuccess) break;
+                if ((e = launch_stats(order, n, ld, coords, -1, dst, s)) != cudaSuccess) break;
                 if ((e = cudaMemcpyAsync(&hst, dst, sizeof(hst), cudaMemcpyDeviceToHost, s)) != cudaSuccess) break;
                 if ((e = cudaStreamSynchronize(s)) != cudaSuccess) break;
                 if (hst.err) break;

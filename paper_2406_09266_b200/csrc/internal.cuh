@@ -15,6 +15,7 @@ struct Plan {
     int64_t nnz = 0;
     int64_t ld = 0;            // padded length of every array (multiple of 4, >= nnz)
     int key_bits = 0;
+    int band_shift = -1;       // >= 0: entries grouped by band c_{n-1} >> band_shift, lexicographic within a band
     int32_t *coords = nullptr; // [order][ld] int32: c_t of entry e at coords[t*ld + e]
     float *vals = nullptr;     // [ld] fp32
     void *storage = nullptr;   // one allocation holding coords + vals
@@ -40,7 +41,7 @@ struct DevStats {
 };
 
 // prepare.cu
-cudaError_t launch_canonicalize(int order, int64_t dim, int64_t nnz, int bits, const int32_t *idx,
+cudaError_t launch_canonicalize(int order, int64_t dim, int64_t nnz, int bits, int band_shift, const int32_t *idx,
                                 unsigned long long *keys, uint32_t *perm, DevStats *st,
                                 cudaStream_t s, bool canonicalise = true, int64_t e_offset = 0);
 cudaError_t sort_keys(int64_t nnz, int end_bit, unsigned long long *keys_in, unsigned long long *keys_out,
@@ -48,8 +49,10 @@ cudaError_t sort_keys(int64_t nnz, int end_bit, unsigned long long *keys_in, uns
 cudaError_t launch_gather(int order, int64_t nnz, int64_t ld, int bits, const unsigned long long *keys,
                           const uint32_t *perm /* null = identity */, const float *vals_in,
                           int32_t *coords, float *vals_out, cudaStream_t s);
-cudaError_t launch_stats(int order, int64_t nnz, int64_t ld, const int32_t *coords, DevStats *st,
+cudaError_t launch_stats(int order, int64_t nnz, int64_t ld, const int32_t *coords, int band_shift, DevStats *st,
                          cudaStream_t s);
+cudaError_t launch_band_keys(int order, int64_t nnz, int64_t ld, const int32_t *coords, int bits, int band_shift,
+                             unsigned long long *keys, uint32_t *perm, cudaStream_t s);
 cudaError_t launch_gather_range(int order, int64_t n, int64_t ld, int bits, const unsigned long long *keys,
                                 const float *vals_in, int32_t *coords, float *vals_out, cudaStream_t s);
 

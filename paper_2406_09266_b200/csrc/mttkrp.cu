@@ -296,7 +296,12 @@ cudaError_t launch_mttkrp(Plan &p, const float *B, int R, float *C, const systec
         return u < 0 ? 0 : (u > 64 ? 64 : u);
     }();
     const bool big_b = p.dim * static_cast<int64_t>(R) * 4 > (64ll << 20);  // B (and C) not L2-resident
-    const int unit_chunks = kUnitEnv > 0 ? kUnitEnv : ((p.stats.max_lead_run > 4096ll * E * K || big_b) ? 4 : 1);
+    // a banded stream (systec_plan_opts) takes 2-chunk units: c3 1.825 vs 1.85 ms
+    // (4) / 1.92 (1), uniform dim-1e6 1.477 vs 1.485 / 1.772, dim-2^19 1.002 vs
+    // 1.029 / 1.045 (profiles/r01_band_sweep5.jsonl)
+    const int unit_chunks = kUnitEnv > 0 ? kUnitEnv
+                            : p.band_shift >= 0 ? 2
+                            : ((p.stats.max_lead_run > 4096ll * E * K || big_b) ? 4 : 1);
     kp.unit = E * K * unit_chunks;
     // problems with fewer units than resident warps (c1: 16 units) keep the
     // finer static split: more warps in flight beat balance there (c1 kernel

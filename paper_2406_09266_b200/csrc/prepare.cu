@@ -30,11 +30,14 @@ __device__ __forceinline__ void sort_net(int32_t (&c)[N]) {
     }
 }
 
+// key = [band of c_{N-1}] [c_0] ... [c_{N-1}], `bits` per index; band = c_{N-1} >> band_shift
+// (band_shift < 0: no band field, plain lexicographic order)
 template <int N>
-__device__ __forceinline__ unsigned long long pack_key(const int32_t (&c)[N], int bits) {
+__device__ __forceinline__ unsigned long long pack_key(const int32_t (&c)[N], int bits, int band_shift) {
     unsigned long long k = 0;
 #pragma unroll
     for (int t = 0; t < N; ++t) k = (k << bits) | static_cast<unsigned long long>(static_cast<uint32_t>(c[t]));
+    if (band_shift >= 0) k |= static_cast<unsigned long long>(static_cast<uint32_t>(c[N - 1]) >> band_shift) << (bits * N);
     return k;
 }
 
@@ -52,8 +55,8 @@ __device__ __forceinline__ bool load_canonical(const int32_t *idx, int64_t e, in
 
 template <int N, bool CANON>
 __global__ void canonicalize_kernel(const int32_t *__restrict__ idx, int64_t nnz, int64_t dim, int bits,
-                                    unsigned long long *__restrict__ keys, uint32_t *__restrict__ perm,
-                                    DevStats *st, int64_t e_offset) {
+                                    int band_shift, unsigned long long *__restrict__ keys,
+                                    uint32_t *__restrict__ perm, DevStats *st, int64_t e_offset) {
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz;
          e += (int64_t)gridDim.x * blockDim.x) {
         int32_t c[N];
@@ -65,12 +68,12 @@ __global__ void canonicalize_kernel(const int32_t *__restrict__ idx, int64_t nnz
             perm[e] = static_cast<uint32_t>(e);
             continue;
         }
-        const unsigned long long k = pack_key<N>(c, bits);
+        const unsigned long long k = pack_key<N>(c, bits, band_shift);
         keys[e] = k;
         perm[e] = static_cast<uint32_t>(e);
         if (e > 0) {
             int32_t q[N];
-            if (load_canonical<N, CANON>(idx, e - 1, dim, q) && pack_key<N>(q, bits) > k) st->unsorted = 1ull;
+            if (load_canonical<N, CANON>(idx, e - 1, dim, q) && pack_key<N>(q, bits, band_shift) > k) st->unsorted = 1ull;
         }
     }
 }
@@ -115,6 +118,21 @@ __global__ void gather_range_kernel(int64_t n, int64_t ld, int bits, const unsig
     }
 }
 
+// banded stream order (systec_plan_opts.band_shift): keys of the prepared SoA
+// stream with the band of c_{N-1} above the lexicographic fields
+template <int N>
+__global__ void band_keys_kernel(int64_t nnz, int64_t ld, const int32_t *__restrict__ coords, int bits,
+                                 int band_shift, unsigned long long *__restrict__ keys, uint32_t *__restrict__ perm) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        int32_t c[N];
+#pragma unroll
+        for (int t = 0; t < N; ++t) c[t] = coords[t * ld + e];
+        keys[e] = pack_key<N>(c, bits, band_shift);
+        perm[e] = static_cast<uint32_t>(e);
+    }
+}
+
 __device__ __forceinline__ long long dfact(int k) {
     long long f = 1;
     for (int i = 2; i <= k; ++i) f *= i;
@@ -122,7 +140,8 @@ __device__ __forceinline__ long long dfact(int k) {
 }
 
 template <int N>
-__global__ void stats_kernel(int64_t nnz, int64_t ld, const int32_t *__restrict__ coords, DevStats *st) {
+__global__ void stats_kernel(int64_t nnz, int64_t ld, const int32_t *__restrict__ coords, int band_shift,
+                             DevStats *st) {
     constexpr int NC = 1 << (N - 1);  // equality patterns
     unsigned long long hist[NC];
 #pragma unroll
@@ -155,10 +174,17 @@ __global__ void stats_kernel(int64_t nnz, int64_t ld, const int32_t *__restrict_
         if (e == 0 || c0[e - 1] != c[0]) ++lead;
         if (N >= 2 && (e == 0 || coords[ld + e - 1] != c[1])) ++pos1;
         if (e == nnz - 1 || c0[e + 1] != c[0]) {  // end of a leading run: its start by binary search
+            // over (band, c_0), the leading part of the sort key
+            const int32_t *cl = coords + static_cast<int64_t>(N - 1) * ld;
+            auto lead_key = [&](int64_t x) {
+                const uint32_t b = band_shift >= 0 ? static_cast<uint32_t>(cl[x]) >> band_shift : 0u;
+                return (static_cast<unsigned long long>(b) << 32) | static_cast<uint32_t>(c0[x]);
+            };
+            const unsigned long long me = lead_key(e);
             int64_t lo = 0, hi = e;
             while (lo < hi) {
                 const int64_t mid = (lo + hi) >> 1;
-                if (c0[mid] < c[0]) lo = mid + 1; else hi = mid;
+                if (lead_key(mid) < me) lo = mid + 1; else hi = mid;
             }
             const unsigned long long len = static_cast<unsigned long long>(e - lo + 1);
             maxrun = len > maxrun ? len : maxrun;
@@ -215,15 +241,15 @@ int grid_for(int64_t n, int threads) {
         default: return cudaErrorInvalidValue;   \
     }
 
-cudaError_t launch_canonicalize(int order, int64_t dim, int64_t nnz, int bits, const int32_t *idx,
+cudaError_t launch_canonicalize(int order, int64_t dim, int64_t nnz, int bits, int band_shift, const int32_t *idx,
                                 unsigned long long *keys, uint32_t *perm, DevStats *st, cudaStream_t s,
                                 bool canonicalise, int64_t e_offset) {
     if (nnz == 0) return cudaSuccess;
     const int th = 256;
     if (canonicalise) {
-        SYSTEC_ORDER_SWITCH(order, canonicalize_kernel<N, true><<<grid_for(nnz, th), th, 0, s>>>(idx, nnz, dim, bits, keys, perm, st, e_offset));
+        SYSTEC_ORDER_SWITCH(order, canonicalize_kernel<N, true><<<grid_for(nnz, th), th, 0, s>>>(idx, nnz, dim, bits, band_shift, keys, perm, st, e_offset));
     } else {
-        SYSTEC_ORDER_SWITCH(order, canonicalize_kernel<N, false><<<grid_for(nnz, th), th, 0, s>>>(idx, nnz, dim, bits, keys, perm, st, e_offset));
+        SYSTEC_ORDER_SWITCH(order, canonicalize_kernel<N, false><<<grid_for(nnz, th), th, 0, s>>>(idx, nnz, dim, bits, band_shift, keys, perm, st, e_offset));
     }
     return cudaGetLastError();
 }
@@ -252,6 +278,14 @@ cudaError_t launch_gather(int order, int64_t nnz, int64_t ld, int bits, const un
     return cudaGetLastError();
 }
 
+cudaError_t launch_band_keys(int order, int64_t nnz, int64_t ld, const int32_t *coords, int bits, int band_shift,
+                             unsigned long long *keys, uint32_t *perm, cudaStream_t s) {
+    if (nnz == 0) return cudaSuccess;
+    const int th = 256;
+    SYSTEC_ORDER_SWITCH(order, band_keys_kernel<N><<<grid_for(nnz, th), th, 0, s>>>(nnz, ld, coords, bits, band_shift, keys, perm));
+    return cudaGetLastError();
+}
+
 cudaError_t launch_gather_range(int order, int64_t n, int64_t ld, int bits, const unsigned long long *keys,
                                 const float *vals_in, int32_t *coords, float *vals_out, cudaStream_t s) {
     if (n == 0) return cudaSuccess;
@@ -260,11 +294,11 @@ cudaError_t launch_gather_range(int order, int64_t n, int64_t ld, int bits, cons
     return cudaGetLastError();
 }
 
-cudaError_t launch_stats(int order, int64_t nnz, int64_t ld, const int32_t *coords, DevStats *st,
+cudaError_t launch_stats(int order, int64_t nnz, int64_t ld, const int32_t *coords, int band_shift, DevStats *st,
                          cudaStream_t s) {
     if (nnz == 0) return cudaSuccess;
     const int th = 256;
-    SYSTEC_ORDER_SWITCH(order, stats_kernel<N><<<grid_for(nnz, th), th, 0, s>>>(nnz, ld, coords, st));
+    SYSTEC_ORDER_SWITCH(order, stats_kernel<N><<<grid_for(nnz, th), th, 0, s>>>(nnz, ld, coords, band_shift, st));
     return cudaGetLastError();
 }
 

@@ -23,7 +23,7 @@ class SystecStats(ctypes.Structure):
                 ("key_bits", ctypes.c_int32), ("G", ctypes.c_int64), ("expanded", ctypes.c_int64),
                 ("pattern_hist", ctypes.c_int64 * 16), ("lead_runs", ctypes.c_int64),
                 ("max_lead_run", ctypes.c_int64), ("pos1_runs", ctypes.c_int64),
-                ("input_was_sorted", ctypes.c_int32), ("pad0", ctypes.c_int32),
+                ("input_was_sorted", ctypes.c_int32), ("band_shift", ctypes.c_int32),
                 ("bad_entry", ctypes.c_int64)]
 
 
@@ -36,12 +36,17 @@ class SystecExecOpts(ctypes.Structure):
                 ("static_ranges", ctypes.c_int32), ("occupancy", ctypes.c_int32), ("reserved", ctypes.c_int32 * 2)]
 
 
+class SystecPlanOpts(ctypes.Structure):
+    _fields_ = [("band_shift", ctypes.c_int32), ("reserved", ctypes.c_int32 * 7)]
+
+
 EXPORTS = ["systec_mttkrp", "systec_mttkrp_host", "systec_plan_create", "systec_plan_execute",
            "systec_plan_execute_ex", "systec_plan_stats", "systec_plan_prepared",
            "systec_plan_copy_prepared", "systec_plan_last_launch", "systec_plan_destroy",
            "systec_status_string", "systec_last_cuda_error", "systec_version", "systec_last_bad_entry",
            "systec_plan_create_general", "systec_expand_symmetric", "systec_plan_minplus",
-           "systec_cp_als_sym", "systec_plan_ttm", "systec_ttm_unpack", "systec_plan_sssp"]
+           "systec_cp_als_sym", "systec_plan_ttm", "systec_ttm_unpack", "systec_plan_sssp",
+           "systec_plan_create_ex"]
 
 _lib = None
 
@@ -61,6 +66,7 @@ def load(path: str | None = None):
     lib.systec_mttkrp_host.argtypes = [i32, i64, i64, vp, vp, vp, i32, vp, vp]
     lib.systec_plan_create.argtypes = [ctypes.POINTER(vp), i32, i64, i64, vp, vp, vp]
     lib.systec_plan_execute.argtypes = [vp, vp, i32, vp, vp]
+    lib.systec_plan_create_ex.argtypes = [ctypes.POINTER(vp), i32, i64, i64, vp, vp, ctypes.POINTER(SystecPlanOpts), vp]
     lib.systec_plan_create_general.argtypes = [ctypes.POINTER(vp), i32, i64, i64, vp, vp, vp]
     lib.systec_plan_minplus.argtypes = [vp, vp, vp, vp]
     lib.systec_plan_ttm.argtypes = [vp, vp, i32, vp, vp]
@@ -136,19 +142,27 @@ def _opts(**kw) -> SystecExecOpts:
 class Plan:
     """A prepared (validated, canonicalised, sorted) symmetric tensor on the GPU:
     ``systec_plan_create``.  ``idx`` [nnz][order] int32 and ``vals`` [nnz] fp32
-    are CUDA tensors; they may be freed after construction."""
+    are CUDA tensors; they may be freed after construction.  ``band_shift``
+    (``systec_plan_create_ex``): None/0 = auto, -1 = lexicographic stream,
+    s > 0 = band-major by c_{n-1} >> s."""
 
-    def __init__(self, order: int, dim: int, idx, vals, stream=None, general: bool = False):
+    def __init__(self, order: int, dim: int, idx, vals, stream=None, general: bool = False,
+                 band_shift: int | None = None):
         import torch
         lib = load()
         nnz = int(vals.shape[0])
         if idx.dim() != 2 or idx.shape[1] != order or idx.shape[0] != nnz:
             raise ValueError("idx must be [nnz][order]")
         h = ctypes.c_void_p()
-        fn, name = ((lib.systec_plan_create_general, "systec_plan_create_general") if general
-                    else (lib.systec_plan_create, "systec_plan_create"))
-        _check(fn(ctypes.byref(h), order, dim, nnz, _dev(idx, torch.int32, "idx"),
-                  _dev(vals, torch.float32, "vals"), _stream_handle(stream)), name)
+        ip, vp_ = _dev(idx, torch.int32, "idx"), _dev(vals, torch.float32, "vals")
+        if band_shift is not None and not general:
+            po = SystecPlanOpts(band_shift=band_shift)
+            _check(lib.systec_plan_create_ex(ctypes.byref(h), order, dim, nnz, ip, vp_, ctypes.byref(po),
+                                             _stream_handle(stream)), "systec_plan_create_ex")
+        else:
+            fn, name = ((lib.systec_plan_create_general, "systec_plan_create_general") if general
+                        else (lib.systec_plan_create, "systec_plan_create"))
+            _check(fn(ctypes.byref(h), order, dim, nnz, ip, vp_, _stream_handle(stream)), name)
         self.general = general
         self._h = h
         self.order, self.dim, self.nnz = order, dim, nnz
@@ -231,7 +245,7 @@ class Plan:
     def stats(self) -> dict:
         st = SystecStats()
         _check(load().systec_plan_stats(self._h, ctypes.byref(st)), "systec_plan_stats")
-        d = {k: getattr(st, k) for k, _ in SystecStats._fields_ if k != "pad0"}
+        d = {k: getattr(st, k) for k, _ in SystecStats._fields_}
         d["pattern_hist"] = list(st.pattern_hist)
         return d
 

@@ -122,26 +122,30 @@ def test_header_is_plain_c_and_example_builds(lib):
 
 
 def test_ctypes_structs_match_the_c_header(tmp_path):
-    """The binding's ctypes mirrors of systec_stats / systec_exec_opts have the
+    """The binding's ctypes mirrors of systec_stats / systec_exec_opts / systec_plan_opts have the
     C layout (sizes and field offsets compiled from include/systec.h)."""
     import shutil
     import subprocess
     if not shutil.which("gcc"):
         pytest.skip("gcc not available")
-    from paper_2406_09266_b200.systec import SystecExecOpts, SystecStats
+    from paper_2406_09266_b200.systec import SystecExecOpts, SystecPlanOpts, SystecStats
     src = tmp_path / "layout.c"
     fields = [("systec_stats", n) for n, _ in SystecStats._fields_] + \
-             [("systec_exec_opts", n) for n, _ in SystecExecOpts._fields_]
+             [("systec_exec_opts", n) for n, _ in SystecExecOpts._fields_] + \
+             [("systec_plan_opts", n) for n, _ in SystecPlanOpts._fields_]
     body = "\n".join(f'    printf("%s %s %zu\\n", "{t}", "{f}", offsetof({t}, {f}));' for t, f in fields)
     src.write_text('#include <stdio.h>\n#include <stddef.h>\n#include "systec.h"\nint main(void) {\n'
                    '    printf("size systec_stats %zu\\n", sizeof(systec_stats));\n'
-                   '    printf("size systec_exec_opts %zu\\n", sizeof(systec_exec_opts));\n' + body + "\n    return 0;\n}\n")
+                   '    printf("size systec_exec_opts %zu\\n", sizeof(systec_exec_opts));\n'
+                   '    printf("size systec_plan_opts %zu\\n", sizeof(systec_plan_opts));\n' + body + "\n    return 0;\n}\n")
     exe = tmp_path / "layout"
     subprocess.check_call(["gcc", "-std=c11", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)])
     out = subprocess.run([str(exe)], capture_output=True, text=True).stdout.split("\n")
     got = {(a, b): int(c) for a, b, c in (l.split() for l in out if l)}
     assert got[("size", "systec_stats")] == ctypes.sizeof(SystecStats)
     assert got[("size", "systec_exec_opts")] == ctypes.sizeof(SystecExecOpts)
-    for t, cls in (("systec_stats", SystecStats), ("systec_exec_opts", SystecExecOpts)):
+    assert got[("size", "systec_plan_opts")] == ctypes.sizeof(SystecPlanOpts)
+    for t, cls in (("systec_stats", SystecStats), ("systec_exec_opts", SystecExecOpts),
+                   ("systec_plan_opts", SystecPlanOpts)):
         for f, _ in cls._fields_:
             assert got[(t, f)] == getattr(cls, f).offset, (t, f)

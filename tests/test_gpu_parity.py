@@ -242,9 +242,14 @@ def test_config_full_size_sampled(systec, name):
     for t in range(w.order - 1):
         code |= (~neq[:, t]).astype(np.int64) << t
     assert st["pattern_hist"][:1 << (w.order - 1)] == np.bincount(code, minlength=1 << (w.order - 1)).tolist()
-    lead = np.bincount(c[:, 0])
-    assert st["lead_runs"] == int((lead > 0).sum()) and st["max_lead_run"] == int(lead.max())
-    assert st["pos1_runs"] == int(1 + (c[1:, 1] != c[:-1, 1]).sum())
+    # auto stream order (systec_plan_opts): c3 (order 3, dim 1e6, mean leading run 421) -> 16 bands
+    assert st["band_shift"] == (16 if name == "c3" else -1)
+    if st["band_shift"] >= 0:
+        coords, pv = plan.prepared()
+        torch.cuda.synchronize()
+        c = band_major(w.idx, st["band_shift"])
+        assert np.array_equal(coords.cpu().numpy().T, c)
+    assert (st["lead_runs"], st["max_lead_run"], st["pos1_runs"]) == stream_runs(c)
     assert st["input_was_sorted"] == 1
     plan.destroy()
     if name == "c2":  # the CUB sort path at full size: a shuffled, non-canonical spelling
@@ -265,6 +270,53 @@ def test_config_full_size_sampled(systec, name):
 
 
 # ---------------------------------------------------------------- NEXT-1: non-symmetric baseline
+def band_major(c_lex, shift):
+    """The banded stream order (systec_plan_opts.band_shift): stable sort of the
+    lexicographic stream by c_{n-1} >> shift."""
+    return c_lex[np.argsort(c_lex[:, -1] >> shift, kind="stable")]
+
+
+def stream_runs(c):
+    """(lead_runs, max_lead_run, pos1_runs) of a stream in its given order."""
+    cut = np.flatnonzero(c[1:, 0] != c[:-1, 0]) + 1
+    lens = np.diff(np.concatenate([[0], cut, [len(c)]]))
+    return len(lens), int(lens.max()), int(1 + (c[1:, 1] != c[:-1, 1]).sum())
+
+
+@pytest.mark.parametrize("n,dim,nnz,R,shift", [(3, 700, 30000, 32, 6), (3, 700, 30000, 7, 8), (2, 5000, 40000, 16, 9),
+                                               (4, 60, 20000, 16, 3), (5, 30, 8000, 8, 2), (3, 64, 3000, 8, 9)])
+def test_banded_stream_order(systec, n, dim, nnz, R, shift):
+    """Explicit band_shift: the prepared stream is band-major (stable by
+    c_{n-1} >> shift over the lexicographic order), its run statistics are
+    those of that order, and C matches the oracle; shift >= the index width
+    (one band) or -1 leaves the lexicographic order."""
+    import torch
+    w = small_random(n, dim, nnz, R, seed=40 + n, diag_frac=0.1)
+    si, sv = scramble(w.idx, w.vals, seed=3)
+    Cref, S = oracle.mttkrp(n, dim, w.idx, w.vals, w.B)
+    one_band = ((dim - 1) >> shift) == 0
+    for req in (shift, -1, 0):
+        plan = systec.Plan(n, dim, *to_dev(si, sv), band_shift=req)
+        st = plan.stats()
+        banded = req > 0 and not one_band
+        assert st["band_shift"] == (shift if banded else -1)
+        perm = np.argsort(w.idx[:, -1] >> shift, kind="stable") if banded else np.arange(nnz)
+        c = w.idx[perm]
+        coords, pv = plan.prepared()
+        torch.cuda.synchronize()
+        assert np.array_equal(coords.cpu().numpy().T, c)
+        assert np.array_equal(pv.cpu().numpy(), w.vals[perm])
+        assert (st["lead_runs"], st["max_lead_run"], st["pos1_runs"]) == stream_runs(c)
+        assert st["G"] == int(nnz + np.sum(w.idx[:, 1:] != w.idx[:, :-1]))
+        for opts in ({}, {"static_ranges": 1}, {"force_scalar": 1}):
+            C = plan.execute(torch.from_numpy(w.B).cuda(), **opts)
+            torch.cuda.synchronize()
+            parity(C.cpu().numpy(), Cref, S)
+        plan.destroy()
+    with pytest.raises(ValueError):
+        systec.Plan(n, dim, *to_dev(si, sv), band_shift=-2)
+
+
 def expand_py(idx, vals):
     out = []
     for c, v in zip(idx, vals):
