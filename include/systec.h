@@ -100,7 +100,9 @@ typedef struct systec_exec_opts {
                                  /* of ~4 chunks taken from a per-launch counter (default)       */
     int32_t occupancy;           /* order-3 R=32 kernel built for 5 blocks/SM: 1 on, -1 off,    */
                                  /* 0 auto (on when B > 64 MB)                                  */
-    int32_t reserved[2];
+    int32_t fixed_rank;          /* kernels built for R = 16 / 32 exactly (one float4 tile):    */
+                                 /* 0 auto (on when R matches), -1 off                          */
+    int32_t reserved[1];
 } systec_exec_opts;
 
 typedef struct systec_plan_s *systec_plan;

@@ -30,6 +30,15 @@ KernelFn pick(int order, int vw, int lpe, int vpl, bool pos1, bool pf) {
     }
 }
 
+KernelFn pick_full(int order, int lpe, bool pos1, bool occ) {
+    switch (order) {
+        case 3: return pick_full_kernel<3>(lpe, pos1, occ);
+        case 4: return pick_full_kernel<4>(lpe, pos1, occ);
+        case 5: return pick_full_kernel<5>(lpe, pos1, occ);
+        default: return nullptr;
+    }
+}
+
 int pow2ceil(int x) {
     int p = 1;
     while (p < x) p <<= 1;
@@ -240,6 +249,16 @@ cudaError_t launch_mttkrp(Plan &p, const float *B, int R, float *C, const systec
                            ((p.order == 3 && lpe == 8) || (p.order >= 4 && lpe == 4));
     const bool occ5 = occ_shape && (o.occupancy > 0 || (o.occupancy == 0 && p.order == 3 && plane * 4 > (64ll << 20)));
     if (occ5) fn = p.order == 3 ? occupancy3(pos1) : p.order == 4 ? occupancy4(pos1) : occupancy5(pos1);
+    // fixed-rank build when R is exactly one float4 tile of 16 or 32 columns
+    // (opts.fixed_rank: 0 auto = on, -1 off)
+    bool full = false;
+    if (o.fixed_rank >= 0 && vw == 4 && vpl == 1 && !pf && !p.general && tiles == 1 && R == lpe * 4 &&
+        o.ablation <= 0 && K == default_K(E)) {
+        if (KernelFn ff = pick_full(p.order, lpe, pos1, occ5)) {
+            fn = ff;
+            full = true;
+        }
+    }
     const int abl = o.ablation;
     if (abl > 0) {  // ablation study: only the c2 / c5 kernel shapes exist
         const bool shape3 = p.order == 3 && vw == 4 && lpe == 8 && vpl == 1 && !pos1 && !pf && !p.general;
@@ -327,7 +346,7 @@ cudaError_t launch_mttkrp(Plan &p, const float *B, int R, float *C, const systec
     p.last_smem = static_cast<int>(smem);
     // kernel id, decimal fields: general | copies (2 digits) | pf + 2*dynamic | order | vw | lpe (2 digits) | vpl | pos1;
     // the occupancy variant sets vpl's digit to 5 (vpl itself is 1 there)
-    p.last_kernel = (p.general ? 1000000000 : 0) + copies * 10000000 + ((pf ? 1 : 0) + (kp.ctr ? 2 : 0)) * 1000000 + p.order * 100000 + vw * 10000 + lpe * 100 + (occ5 ? 5 : vpl) * 10 + (pos1 ? 1 : 0);
+    p.last_kernel = (p.general ? 1000000000 : 0) + copies * 10000000 + ((pf ? 1 : 0) + (kp.ctr ? 2 : 0) + (full ? 4 : 0)) * 1000000 + p.order * 100000 + vw * 10000 + lpe * 100 + (occ5 ? 5 : vpl) * 10 + (pos1 ? 1 : 0);
     return cudaGetLastError();
 }
 

@@ -108,6 +108,13 @@ __device__ __forceinline__ uint64_t policy_evict_normal() {
     return p;
 }
 
+// base + (u32)c * stride, as one PTX mad.wide.u32
+__device__ __forceinline__ char *mad_wide(int32_t c, uint32_t stride, const char *base) {
+    char *r;
+    asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(r) : "r"(c), "r"(stride), "l"(base));
+    return r;
+}
+
 // rank offset of row c: 32x32 -> 64-bit multiply (one IMAD.WIDE.U32)
 __device__ __forceinline__ uint64_t row_off(int32_t c, uint32_t R) {
     return static_cast<uint64_t>(static_cast<uint32_t>(c)) * R;
@@ -116,7 +123,11 @@ __device__ __forceinline__ uint64_t row_off(int32_t c, uint32_t R) {
 // ABL (ablations for the evidence table, instantiated for the c2/c5 shapes only):
 //   bit 0: no shared-memory staging (indices and values read with plain loads)
 //   bit 1: no position-0 run accumulation (one reduction per entry)
-template <int N, int LPE, int VPL, int VW, bool POS1, bool PF, bool NAIVE, int ABL>
+// RF > 0: fixed-rank build for R == RF == the rank tile (one tile, every lane
+// active) and the default chunk K: the lane's columns, row stride, activity and
+// the staged arrays' offsets are compile-time, which takes the per-entry
+// column/bounds bookkeeping out of the loop.
+template <int N, int LPE, int VPL, int VW, bool POS1, bool PF, bool NAIVE, int ABL, int RF = 0>
 __device__ __forceinline__ void mttkrp_sym_body(const KParams &p) {
     using V = VecT<VW>;
     using T = typename V::T;
@@ -124,7 +135,12 @@ __device__ __forceinline__ void mttkrp_sym_body(const KParams &p) {
     constexpr int ARR = N + 1;           // staged arrays: c_0..c_{N-1}, v
     constexpr int QS = LPE * VW;         // column stride between a lane's vectors
     constexpr int TILE = LPE * VPL * VW; // rank columns per blockIdx.y
-    const int K = p.K;
+    static_assert(RF == 0 || RF == TILE, "fixed-rank builds cover exactly one rank tile");
+    constexpr bool kFull = RF > 0;
+    // fixed-rank builds also fix K at the launcher's default (default_K):
+    // constant smem offsets between the staged arrays
+    constexpr int KF = E == 1 ? 128 : E == 2 ? 64 : E == 4 ? 33 : E == 8 ? 17 : E == 16 ? 9 : 5;
+    const int K = kFull ? KF : p.K;
     const int CH = E * K;
     const int S = p.stages;
     const int WPB = blockDim.x >> 5;
@@ -148,9 +164,9 @@ __device__ __forceinline__ void mttkrp_sym_body(const KParams &p) {
         nch = (end - begin + CH - 1) / CH;
     }
 
-    const uint32_t R = p.R;
+    const uint32_t R = kFull ? static_cast<uint32_t>(RF) : p.R;
     const uint32_t Rb = R * 4u;  // row stride in bytes
-    const uint32_t col0 = blockIdx.y * TILE + j * VW;
+    const uint32_t col0 = kFull ? static_cast<uint32_t>(j * VW) : blockIdx.y * TILE + j * VW;
     // per-lane column byte offsets; inactive lanes (col >= R) read column 0 of
     // the same row (valid memory) and never write
     bool act[VPL];
@@ -162,7 +178,7 @@ __device__ __forceinline__ void mttkrp_sym_body(const KParams &p) {
 #pragma unroll
     for (int q = 0; q < VPL; ++q) {
         const uint32_t col = col0 + q * QS;
-        act[q] = col < R;
+        act[q] = kFull || col < R;
         const uint32_t ofs = act[q] ? col * 4u : 0u;
         Bq[q] = reinterpret_cast<const char *>(p.B) + ofs;
         Cq[q] = Cbase + ofs;
@@ -200,7 +216,7 @@ __device__ __forceinline__ void mttkrp_sym_body(const KParams &p) {
     // (requesting the following unit's id one unit ahead, to overlap the
     // atomic's round trip, measured 0.5-1 % slower on c2/c5: not done)
     auto take_unit = [&]() {
-        du = atomicAdd(p.ctr + blockIdx.y, 1u);  // one counter per rank tile
+        du = atomicAdd(p.ctr + (kFull ? 0 : blockIdx.y), 1u);  // one counter per rank tile
         dnext = static_cast<int>(min(static_cast<int64_t>(du) * p.unit, p.nnz));
         dend = min(nnz32, dnext + p.unit);
     };
@@ -229,9 +245,11 @@ __device__ __forceinline__ void mttkrp_sym_body(const KParams &p) {
         for (int64_t k = 0; k < min(static_cast<int64_t>(S - 1), nch); ++k) issue(k);
     }
 
-    // row address of row c for the lane's vector q: one IMAD.WIDE.U32
-    auto rowB = [&](int32_t c, int q) { return reinterpret_cast<const float *>(Bq[q] + static_cast<uint64_t>(static_cast<uint32_t>(c)) * Rb); };
-    auto rowC = [&](int32_t c, int q) { return reinterpret_cast<float *>(Cq[q] + static_cast<uint64_t>(static_cast<uint32_t>(c)) * Rb); };
+    // row address of row c for the lane's vector q: one IMAD.WIDE.U32 on the
+    // lane's 64-bit base (PTX mad.wide; left to itself the compiler splits it
+    // into a wide multiply, an OR of the lane offset and a 64-bit add)
+    auto rowB = [&](int32_t c, int q) { return reinterpret_cast<const float *>(mad_wide(c, Rb, Bq[q])); };
+    auto rowC = [&](int32_t c, int q) { return reinterpret_cast<float *>(mad_wide(c, Rb, Cq[q])); };
 
     // running sums: position 0 (carried across chunks) and position 1
     int cur0 = -1;
@@ -358,7 +376,7 @@ __device__ __forceinline__ void mttkrp_sym_body(const KParams &p) {
 #pragma unroll
                 for (int q = 0; q < VPL; ++q) {
                     V::red_if(rowC(cur0, q), acc0[q], flush && cur0 >= 0 && act[q]);
-                    acc0[q] = flush ? u[0][q] : V::add(acc0[q], u[0][q]);
+                    acc0[q] = V::add(flush ? V::zero() : acc0[q], u[0][q]);  // 0 + u == u exactly
                 }
                 cur0 = x.c[0];
             }
@@ -460,18 +478,18 @@ __device__ __forceinline__ void mttkrp_sym_body(const KParams &p) {
     }
 }
 
-template <int N, int LPE, int VPL, int VW, bool POS1, bool PF, bool NAIVE = false, int ABL = 0>
+template <int N, int LPE, int VPL, int VW, bool POS1, bool PF, bool NAIVE = false, int ABL = 0, int RF = 0>
 __global__ void __launch_bounds__(256) mttkrp_sym_kernel(const KParams p) {
-    mttkrp_sym_body<N, LPE, VPL, VW, POS1, PF, NAIVE, ABL>(p);
+    mttkrp_sym_body<N, LPE, VPL, VW, POS1, PF, NAIVE, ABL, RF>(p);
 }
 
 // occupancy variant: ask ptxas for MINB resident 256-thread blocks per SM
 // (<= 65536 / (MINB*256) registers) — for gather-latency-bound inputs.  A
 // separate kernel because __launch_bounds__(256, 1) is not the same request
 // as __launch_bounds__(256) (ptxas then spends registers more freely).
-template <int N, int LPE, int VPL, int VW, bool POS1, int MINB>
+template <int N, int LPE, int VPL, int VW, bool POS1, int MINB, int RF = 0>
 __global__ void __launch_bounds__(256, MINB) mttkrp_sym_kernel_occ(const KParams p) {
-    mttkrp_sym_body<N, LPE, VPL, VW, POS1, false, false, 0>(p);
+    mttkrp_sym_body<N, LPE, VPL, VW, POS1, false, false, 0, RF>(p);
 }
 
 // Sum `copies` replicas Cp[copies][plane] into C[plane] (float4 when aligned);
@@ -493,6 +511,13 @@ KernelFn pick_ablation_kernel(int order, int abl);
 KernelFn occupancy3(bool pos1);
 KernelFn occupancy4(bool pos1);
 KernelFn occupancy5(bool pos1);
+// fixed-rank builds (R == 4*lpe, float4 lanes, one tile, no prefetch): order 3
+// lpe 4/8, orders 4/5 lpe 4/8, each with pos1 on/off; occ = the occupancy
+// variant of the shape that has one ((3,8), (4,4), (5,4)); nullptr if none
+template <int N> KernelFn pick_full_kernel(int lpe, bool pos1, bool occ);
+template <> KernelFn pick_full_kernel<3>(int lpe, bool pos1, bool occ);
+template <> KernelFn pick_full_kernel<4>(int lpe, bool pos1, bool occ);
+template <> KernelFn pick_full_kernel<5>(int lpe, bool pos1, bool occ);
 // the non-symmetric (expanded-tensor) baseline: position 0 only, one float4/float per lane
 template <int N> KernelFn pick_naive_kernel(int vw, int lpe, bool pf);
 template <> KernelFn pick_naive_kernel<2>(int vw, int lpe, bool pf);

@@ -86,4 +86,17 @@ KernelFn ablation3(int abl) {
     }
 }
 
+template <>
+KernelFn pick_full_kernel<3>(int lpe, bool pos1, bool occ) {
+    if (occ) {
+        if (lpe != 8) return nullptr;
+        return pos1 ? mttkrp_sym_kernel_occ<3, 8, 1, 4, true, 5, 32> : mttkrp_sym_kernel_occ<3, 8, 1, 4, false, 5, 32>;
+    }
+    switch (lpe) {
+        case 4: return pos1 ? mttkrp_sym_kernel<3, 4, 1, 4, true, false, false, 0, 16> : mttkrp_sym_kernel<3, 4, 1, 4, false, false, false, 0, 16>;
+        case 8: return pos1 ? mttkrp_sym_kernel<3, 8, 1, 4, true, false, false, 0, 32> : mttkrp_sym_kernel<3, 8, 1, 4, false, false, false, 0, 32>;
+        default: return nullptr;
+    }
+}
+
 }  // namespace systec

@@ -86,4 +86,17 @@ KernelFn occupancy5(bool pos1) {
     return pos1 ? mttkrp_sym_kernel_occ<5, 4, 1, 4, true, 4> : mttkrp_sym_kernel_occ<5, 4, 1, 4, false, 4>;
 }
 
+template <>
+KernelFn pick_full_kernel<5>(int lpe, bool pos1, bool occ) {
+    if (occ) {
+        if (lpe != 4) return nullptr;
+        return pos1 ? mttkrp_sym_kernel_occ<5, 4, 1, 4, true, 4, 16> : mttkrp_sym_kernel_occ<5, 4, 1, 4, false, 4, 16>;
+    }
+    switch (lpe) {
+        case 4: return pos1 ? mttkrp_sym_kernel<5, 4, 1, 4, true, false, false, 0, 16> : mttkrp_sym_kernel<5, 4, 1, 4, false, false, false, 0, 16>;
+        case 8: return pos1 ? mttkrp_sym_kernel<5, 8, 1, 4, true, false, false, 0, 32> : mttkrp_sym_kernel<5, 8, 1, 4, false, false, false, 0, 32>;
+        default: return nullptr;
+    }
+}
+
 }  // namespace systec

@@ -33,7 +33,8 @@ class SystecExecOpts(ctypes.Structure):
                 ("no_zero", ctypes.c_int32), ("l2_hints", ctypes.c_int32),
                 ("chunk_k", ctypes.c_int32), ("stages", ctypes.c_int32), ("vpl", ctypes.c_int32),
                 ("prefetch", ctypes.c_int32), ("copies", ctypes.c_int32), ("ablation", ctypes.c_int32),
-                ("static_ranges", ctypes.c_int32), ("occupancy", ctypes.c_int32), ("reserved", ctypes.c_int32 * 2)]
+                ("static_ranges", ctypes.c_int32), ("occupancy", ctypes.c_int32), ("fixed_rank", ctypes.c_int32),
+                ("reserved", ctypes.c_int32 * 1)]
 
 
 class SystecPlanOpts(ctypes.Structure):
@@ -265,9 +266,9 @@ class Plan:
         _check(load().systec_plan_last_launch(self._h, *[ctypes.byref(v) for v in vals]), "systec_plan_last_launch")
         d = dict(zip(["grid_x", "grid_y", "block", "smem_bytes", "kernel_id"], [v.value for v in vals]))
         kid = d["kernel_id"]
-        if kid >= 0:   # decimal fields: general | copies (2) | pf + 2 dynamic | order | vw | lpe (2 digits) | vpl | pos1
+        if kid >= 0:   # decimal fields: general | copies (2) | pf + 2 dynamic + 4 fixed-rank | order | vw | lpe (2) | vpl | pos1
             d.update(general=kid // 1000000000, copies=kid // 10000000 % 100, prefetch=kid // 1000000 % 2,
-                     dynamic=kid // 1000000 % 10 // 2,
+                     dynamic=kid // 1000000 % 10 // 2 % 2, fixed_rank=kid // 1000000 % 10 // 4,
                      order=kid // 100000 % 10,
                      vw=kid // 10000 % 10, lpe=kid // 100 % 100, vpl=kid // 10 % 10, pos1=kid % 10)
         return d

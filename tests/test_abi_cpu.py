@@ -86,7 +86,7 @@ def test_product_path_has_no_oracle_dependency():
 
 
 def test_sass_shows_bulk_async_copies_and_vector_reductions(lib):
-    """The sm_100a kernel really uses the TMA engine (UBLKCP) for the stream,
+    """The sm_100a kernel c2 runs (fixed-rank R = 32 build) really uses the TMA engine (UBLKCP) for the stream,
     16-byte gathers and vector fp32 reductions (checked in the cubin, no GPU)."""
     import shutil
     import subprocess
@@ -94,7 +94,7 @@ def test_sass_shows_bulk_async_copies_and_vector_reductions(lib):
         pytest.skip("cuobjdump not available")
     from paper_2406_09266_b200 import LIB_PATH
     sass = subprocess.run(["cuobjdump", "-sass", "-fun",
-                           "_ZN6systec17mttkrp_sym_kernelILi3ELi8ELi1ELi4ELb0ELb0ELb0ELi0EEEvNS_7KParamsE", LIB_PATH],
+                           "_ZN6systec17mttkrp_sym_kernelILi3ELi8ELi1ELi4ELb0ELb0ELb0ELi0ELi32EEEvNS_7KParamsE", LIB_PATH],
                           capture_output=True, text=True).stdout
     elfs = subprocess.run(["cuobjdump", "-lelf", LIB_PATH], capture_output=True, text=True).stdout
     assert "sm_100a" in elfs

@@ -113,6 +113,29 @@ def test_option_variants_agree(systec):
         parity(run(systec, w, **opts), Cref, S)
 
 
+@pytest.mark.parametrize("n,dim,nnz,R", [(3, 300, 40000, 32), (3, 300, 40000, 16), (4, 60, 30000, 16),
+                                       (4, 60, 30000, 32), (5, 30, 20000, 16), (5, 30, 20000, 32)])
+def test_fixed_rank_builds(systec, n, dim, nnz, R):
+    """The fixed-rank kernels (R == one float4 tile of 16 / 32 columns, default
+    K) are the ones that run by default at those ranks, and agree with the
+    oracle with every combination they are built for (pos1, occupancy
+    variant, static/dynamic split); a non-default K falls back to the
+    general-R build."""
+    import torch
+    w = small_random(n, dim, nnz, R, seed=60 + n, diag_frac=0.15)
+    Cref, S = oracle.mttkrp(n, dim, w.idx, w.vals, w.B)
+    di, dv, dB = to_dev(w.idx, w.vals, w.B)
+    plan = systec.Plan(n, dim, di, dv)
+    for opts, full in [({}, 1), (dict(fixed_rank=-1), 0), (dict(pos1_accumulate=1), 1),
+                       (dict(pos1_accumulate=-1), 1), (dict(occupancy=1), 1), (dict(occupancy=1, pos1_accumulate=1), 1),
+                       (dict(static_ranges=1), 1), (dict(K=5), 0), (dict(copies=4), 1), (dict(no_zero=0), 1)]:
+        C = plan.execute(dB, **opts)
+        torch.cuda.synchronize()
+        parity(C.cpu().numpy(), Cref, S)
+        assert plan.last_launch()["fixed_rank"] == full, opts
+    plan.destroy()
+
+
 def test_hub_rows_long_runs(systec):
     """Zipf-skewed input: long equal-leading-index runs cross chunk and warp
     boundaries (the carried position-0 sums)."""
@@ -315,6 +338,13 @@ def test_banded_stream_order(systec, n, dim, nnz, R, shift):
         plan.destroy()
     with pytest.raises(ValueError):
         systec.Plan(n, dim, *to_dev(si, sv), band_shift=-2)
+    if n == 3 and not one_band:   # the other consumers of the stream: TTM (order 3)
+        want = oracle.ttm_sym3(dim, w.idx, w.vals, w.B)
+        S3 = oracle.ttm_sym3(dim, w.idx, np.abs(w.vals), np.abs(w.B))
+        plan = systec.Plan(n, dim, *to_dev(si, sv), band_shift=shift)
+        Cf = plan.ttm(torch.from_numpy(w.B).cuda(), full=True)
+        torch.cuda.synchronize()
+        parity(Cf.cpu().numpy(), want, S3)
 
 
 def expand_py(idx, vals):
