@@ -1,6 +1,7 @@
 """Summarise an ncu report (raw page) into the metrics DESIGN.md cites.
 
-    python tools/ncu_summary.py gpurun_out/prof.ncu-rep [...]
+    python tools/ncu_summary.py gpurun_out/prof.ncu-rep [...]     (or its `--page raw --csv` export)
+    python tools/ncu_summary.py --json profiles/ncu_summary.json c2=raw.csv c3=raw.csv ...
 """
 import csv
 import io
@@ -42,7 +43,11 @@ KEYS = [
 
 
 def summarise(path):
-    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    if path.endswith(".csv"):   # an exported raw page (ncu's log lines first)
+        lines = open(path).read().splitlines()
+        out = "\n".join(lines[next(i for i, l in enumerate(lines) if l.startswith('"ID"')):])
+    else:
+        out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     hdr, units = rows[0], rows[1]
     res = []
@@ -57,7 +62,27 @@ def summarise(path):
     return res
 
 
+def write_json(dst, pairs):
+    """profiles/ncu_summary.json: DRAM bytes per launch of each config's MTTKRP kernel (bench.py `traffic`)."""
+    import json
+    res = {}
+    for cfg, path in pairs:
+        kn, d = next((k, d) for k, d in summarise(path) if "mttkrp_sym" in k)
+        rd, wr = (float(d[k][0].replace(",", "")) for k in ("dram_read", "dram_write"))
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+        rd *= scale[d["dram_read"][1]]
+        wr *= scale[d["dram_write"][1]]
+        res[cfg] = {"dram_bytes_per_launch": int(round(rd + wr)),
+                    "source": f"{path}: dram__bytes_read.sum {rd / 1e6:.6f} MB + dram__bytes_write.sum {wr / 1e6:.6f} MB "
+                              f"({kn.split('(')[0].replace('void ', '').replace('systec::', '')}, ncu --set full --clock-control none)"}
+    with open(dst, "w") as f:
+        json.dump(res, f, indent=1)
+
+
 if __name__ == "__main__":
+    if sys.argv[1:2] == ["--json"]:
+        write_json(sys.argv[2], [a.split("=", 1) for a in sys.argv[3:]])
+        sys.exit(0)
     for p in sys.argv[1:]:
         for kn, d in summarise(p):
             print(f"== {p}: {kn[:90]}")
