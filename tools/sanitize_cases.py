@@ -35,6 +35,18 @@ def main():
         gplan = systec.plan_create_general(n, dim, ei, ev)
         gplan.execute(dB)
         gplan.destroy()
+    # band-major plans (explicit shift) and the fixed-rank builds with every variant they have
+    for n, dim, nnz, R, shift in ((3, 3000, 150000, 32, 8), (3, 3000, 150000, 16, 9), (4, 200, 100000, 16, 5),
+                                  (5, 60, 80000, 32, 3)):
+        w = small_random(n, dim, nnz, R, seed=n + 10, diag_frac=0.1)
+        di, dv, dB = dev(w.idx, w.vals, w.B)
+        plan = systec.Plan(n, dim, di, dv, band_shift=shift)
+        for opts in ({}, {"occupancy": 1}, {"occupancy": 1, "pos1_accumulate": 1}, {"static_ranges": 1},
+                     {"fixed_rank": -1}, {"copies": 3}):
+            plan.execute(dB, **opts)
+        if n == 3:
+            plan.ttm(dB)
+        plan.destroy()
     systec.mttkrp_host(3, 64, *[a for a in (generate("c1", cache=False).idx, generate("c1", cache=False).vals,
                                              generate("c1", cache=False).B)])
     torch.cuda.synchronize()
