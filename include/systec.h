@@ -118,7 +118,10 @@ typedef struct systec_plan_opts {
                                  /* are short): the rows that positions >= 1 gather and update */
                                  /* then stay within an L2-sized window while a band runs.     */
                                  /* Any order gives the same C up to fp32 rounding order.      */
-    int32_t reserved[7];
+                                 /* General plans are banded only on request (explicit s).     */
+    int32_t general;             /* 1 = a general (non-symmetric) tensor, as                   */
+                                 /* systec_plan_create_general; 0 = symmetric                  */
+    int32_t reserved[6];
 } systec_plan_opts;
 
 /*
@@ -159,8 +162,8 @@ SYSTEC_API int systec_plan_create(systec_plan *out, int order, int64_t dim, int6
  * systec_plan_create with options (NULL = defaults, i.e. systec_plan_create).
  * A banded plan (systec_plan_opts.band_shift) re-sorts its prepared stream
  * once more on the device (one more synchronisation of `stream`).
- * Errors: as systec_plan_create; ARG for band_shift < -1 or a non-zero
- * reserved field.
+ * Errors: as systec_plan_create; ARG for band_shift < -1, general not 0/1 or
+ * a non-zero reserved field.
  */
 SYSTEC_API int systec_plan_create_ex(systec_plan *out, int order, int64_t dim, int64_t nnz,
                                      const int32_t *idx, const float *vals, const systec_plan_opts *opts,

@@ -87,7 +87,7 @@ void fill_stats(Plan *p, const DevStats &hst) {
 // automatically.  Bands: the largest power of two <= mean leading run / 5,
 // at most 16 and at least 2^16 rows each (profiles/r01_band_sweep*.jsonl).
 int choose_band_shift(int request, int order, int64_t dim, int bits, int64_t nnz, int64_t lead_runs, bool general) {
-    if (general || request < 0 || nnz < 2) return -1;
+    if (request < 0 || nnz < 2 || (general && request == 0)) return -1;
     int shift;
     if (request > 0) {
         shift = request;
@@ -311,15 +311,17 @@ int systec_plan_create_ex(systec_plan *out, int order, int64_t dim, int64_t nnz,
     if (!out) return SYSTEC_ERR_ARG;
     *out = nullptr;
     int band = 0;
+    bool general = false;
     if (opts) {
-        if (opts->band_shift < -1) return SYSTEC_ERR_ARG;
+        if (opts->band_shift < -1 || opts->general < 0 || opts->general > 1) return SYSTEC_ERR_ARG;
         for (int r : opts->reserved)
             if (r) return SYSTEC_ERR_ARG;
         band = opts->band_shift;
+        general = opts->general == 1;
     }
     Plan *p = nullptr;
     int rc = systec::plan_create_impl(&p, order, dim, nnz, idx, vals, reinterpret_cast<cudaStream_t>(stream), false,
-                                      false, band);
+                                      general, band);
     *out = reinterpret_cast<systec_plan>(p);
     return rc;
 }

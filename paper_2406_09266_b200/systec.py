@@ -38,7 +38,7 @@ class SystecExecOpts(ctypes.Structure):
 
 
 class SystecPlanOpts(ctypes.Structure):
-    _fields_ = [("band_shift", ctypes.c_int32), ("reserved", ctypes.c_int32 * 7)]
+    _fields_ = [("band_shift", ctypes.c_int32), ("general", ctypes.c_int32), ("reserved", ctypes.c_int32 * 6)]
 
 
 EXPORTS = ["systec_mttkrp", "systec_mttkrp_host", "systec_plan_create", "systec_plan_execute",
@@ -156,8 +156,8 @@ class Plan:
             raise ValueError("idx must be [nnz][order]")
         h = ctypes.c_void_p()
         ip, vp_ = _dev(idx, torch.int32, "idx"), _dev(vals, torch.float32, "vals")
-        if band_shift is not None and not general:
-            po = SystecPlanOpts(band_shift=band_shift)
+        if band_shift is not None:
+            po = SystecPlanOpts(band_shift=band_shift, general=int(general))
             _check(lib.systec_plan_create_ex(ctypes.byref(h), order, dim, nnz, ip, vp_, ctypes.byref(po),
                                              _stream_handle(stream)), "systec_plan_create_ex")
         else:

@@ -387,6 +387,15 @@ def test_general_plan_vs_general_oracle(systec, n, dim, nnz, R):
         C = plan.execute(dB, **opts)
         torch.cuda.synchronize()
         parity(C.cpu().numpy(), Cref, S)
+    # band-major general plan (explicit only; auto keeps general plans lexicographic)
+    assert systec.Plan(n, dim, di, dv, general=True, band_shift=0).stats()["band_shift"] == -1
+    bplan = systec.Plan(n, dim, di, dv, general=True, band_shift=2)
+    assert bplan.stats()["band_shift"] == 2 and bplan.last_launch()["kernel_id"] == -1
+    for opts in ({}, dict(prefetch=1)):
+        C = bplan.execute(dB, **opts)
+        torch.cuda.synchronize()
+        parity(C.cpu().numpy(), Cref, S)
+        assert bplan.last_launch()["general"] == 1
 
 
 @pytest.mark.parametrize("n,dim,nnz,R", [(3, 60, 4000, 32), (4, 20, 3000, 16), (5, 12, 2000, 16)])
