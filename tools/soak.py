@@ -37,6 +37,11 @@ def main():
         C0 = plan.execute(B).clone()
         torch.cuda.synchronize()
         assert float(C0.abs().max()) < 2 ** 24
+        # exact integers: every other stream order / build must give the same bits
+        alt = systec.Plan(w.order, w.dim, torch.from_numpy(w.idx).cuda(), torch.from_numpy(vals).cuda(), band_shift=-1)
+        same_lex = bool(torch.equal(alt.execute(B), C0))
+        same_general_build = bool(torch.equal(alt.execute(B, fixed_rank=-1, static_ranges=1), C0))
+        alt.destroy()
         C = torch.empty_like(C0)
         mism = 0
         t0 = time.perf_counter()
@@ -46,7 +51,9 @@ def main():
                 mism += 1
         torch.cuda.synchronize()
         print(json.dumps({"config": name, "runs": a.runs, "mismatches": mism, "max_abs_C": float(C0.abs().max()),
-                          "seconds": time.perf_counter() - t0, "launch": plan.last_launch()}), flush=True)
+                          "seconds": time.perf_counter() - t0, "launch": plan.last_launch(),
+                          "band_shift": plan.stats()["band_shift"], "equals_lexicographic_plan": same_lex,
+                          "equals_general_rank_static_build": same_general_build}), flush=True)
         plan.destroy()
 
 
