@@ -1,9 +1,11 @@
 """Band study: plans whose stream is grouped by bands of the last (largest)
-index, c_{n-1} >> shift, lexicographic within a band (at plan
-creation, systec_plan_opts.band_shift: -1 lexicographic, 0 auto).  Times execute (CUDA events, L2 flushed between runs) per shift and
-compares each result with the unbanded plan's.  Tuning aid only.
+index, c_{n-1} >> shift, lexicographic within a band (chosen at plan creation:
+systec_plan_opts.band_shift, -1 lexicographic, 0 auto).  Times execute (CUDA
+events, L2 flushed between runs) per shift and compares each result with the
+first shift's.  Tuning aid only.
 
-    python tools/band_sweep.py --configs c3 --shifts=-1,19,18,17,16
+    python tools/band_sweep.py --configs c3 --shifts=-1,0,18,17,16 [--R 8] [--opts occupancy=1]
+    python tools/band_sweep.py --configs "" --make "3:1000000:20000000:32:uniform" --shifts=-1,0
 """
 import argparse
 import json
