@@ -372,7 +372,11 @@ def main():
             "l2_model": l2_model(w, st, hi - lo, kern_avg_ms, launch),
             "warm_ms_per_step": warm_ms,
             "step_ms_min": float(np.min(step_ms)), "step_ms_median": float(np.median(step_ms)),
-            "gpu_launches": args.steps * (2 if launch.get("copies", 1) > 1 else 1),
+            # our kernels per execute: the MTTKRP kernel, + the replica sum (copies > 1; the
+            # replicas are zeroed by cudaMemsetAsync), + zero_output_kernel when a single C
+            # is zeroed together with the dynamic-distribution counter
+            "gpu_launches": args.steps * (1 + (launch.get("copies", 1) > 1)
+                                          + (launch.get("copies", 1) == 1 and launch.get("dynamic", 0) == 1)),
             "launch": launch,
             "plan_stats": {k: st[k] for k in ("G", "expanded", "lead_runs", "max_lead_run", "pos1_runs")},
         }
