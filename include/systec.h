@@ -111,8 +111,8 @@ typedef struct systec_plan_s *systec_plan;
 typedef struct systec_plan_opts {
     int32_t band_shift;          /* stream order: 0 = auto, -1 = lexicographic, s > 0 = group  */
                                  /* entries by band c_{n-1} >> s (band-major, lexicographic    */
-                                 /* within a band) when the band number fits the 64-bit sort   */
-                                 /* key beside the indices, else lexicographic.  Auto bands    */
+                                 /* within a band; at most 2^16 bands, else lexicographic)     */
+                                 /* by one stable radix pass over the band numbers.  Auto bands */
                                  /* order-3 plans with dim >= 2^19 into up to 16 bands (no     */
                                  /* fewer than 2^16 rows each; fewer bands when leading runs   */
                                  /* are short): the rows that positions >= 1 gather and update */
@@ -129,6 +129,8 @@ typedef struct systec_plan_opts {
  * plan_create + plan_execute + plan_destroy.  idx/vals/B/C are DEVICE
  * pointers; C [dim][R] is OVERWRITTEN.  Synchronises `stream` inside plan
  * creation (validation verdict and statistics); the execute part is async.
+ * The plan is used once, so it keeps the lexicographic stream order (no band
+ * re-sort, systec_plan_opts).
  */
 SYSTEC_API int systec_mttkrp(int order, int64_t dim, int64_t nnz, const int32_t *idx, const float *vals,
                   const float *B, int R, float *C, systec_stream_t stream);

@@ -86,6 +86,8 @@ void fill_stats(Plan *p, const DevStats &hst) {
 // (its only reuse is the leading run, which bands cut) and is never banded
 // automatically.  Bands: the largest power of two <= mean leading run / 5,
 // at most 16 and at least 2^16 rows each (profiles/r01_band_sweep*.jsonl).
+// One-shot calls (systec_mttkrp, systec_mttkrp_host) stay lexicographic: the
+// re-sort is paid once per plan and pays back only over repeated executes.
 int choose_band_shift(int request, int order, int64_t dim, int bits, int64_t nnz, int64_t lead_runs, bool general) {
     if (request < 0 || nnz < 2 || (general && request == 0)) return -1;
     int shift;
@@ -101,12 +103,13 @@ int choose_band_shift(int request, int order, int64_t dim, int bits, int64_t nnz
     if (shift >= 31) return -1;
     const int64_t bands = ((dim - 1) >> shift) + 1;
     if (bands < 2) return -1;
-    const int band_bits = ceil_log2(bands);
-    return bits * order + band_bits <= 64 ? shift : -1;
+    return ceil_log2(bands) <= 16 ? shift : -1;  // band numbers are sorted as 16-bit keys
 }
 
-// Re-sorts a plan's prepared stream band-major (key: band of c_{n-1}, then the
-// lexicographic fields) into new storage and refreshes its run statistics.
+// Re-sorts a plan's prepared stream band-major: a stable radix sort of the
+// entries' band numbers alone (the stream is already lexicographic, so one
+// digit pass keeps that order within each band), then a permuting copy into
+// new storage; refreshes the run statistics.
 int apply_bands(Plan *p, int shift, bool pooled, cudaStream_t s) {
     const int64_t nnz = p->nnz;
     const size_t nk = static_cast<size_t>(nnz);
@@ -114,12 +117,12 @@ int apply_bands(Plan *p, int shift, bool pooled, cudaStream_t s) {
     const size_t bytes = static_cast<size_t>(p->order + 1) * p->ld * 4;
     void *storage = nullptr;
     DevStats *dst = nullptr;
-    unsigned long long *keys = nullptr, *keys2 = nullptr;
+    uint16_t *bk = nullptr, *bk2 = nullptr;
     uint32_t *perm = nullptr, *perm2 = nullptr;
     auto cleanup = [&]() {
         if (dst) cudaFreeAsync(dst, s);
-        if (keys) cudaFreeAsync(keys, s);
-        if (keys2) cudaFreeAsync(keys2, s);
+        if (bk) cudaFreeAsync(bk, s);
+        if (bk2) cudaFreeAsync(bk2, s);
         if (perm) cudaFreeAsync(perm, s);
         if (perm2) cudaFreeAsync(perm2, s);
     };
@@ -128,27 +131,26 @@ int apply_bands(Plan *p, int shift, bool pooled, cudaStream_t s) {
         if (storage) { if (pooled) cudaFreeAsync(storage, s); else cudaFree(storage); }
         return cuda_fail(err);
     };
+    if (band_bits > 16) return SYSTEC_ERR_UNSUPPORTED;
     cudaError_t e = pooled ? cudaMallocAsync(&storage, bytes, s) : cudaMalloc(&storage, bytes);
     if (e != cudaSuccess) { storage = nullptr; return fail(e); }
     int32_t *coords = static_cast<int32_t *>(storage);
     float *vals = reinterpret_cast<float *>(coords + static_cast<size_t>(p->order) * p->ld);
     if ((e = cudaMallocAsync(&dst, sizeof(DevStats), s)) != cudaSuccess) return fail(e);
-    if ((e = cudaMallocAsync(&keys, nk * 8, s)) != cudaSuccess) return fail(e);
-    if ((e = cudaMallocAsync(&keys2, nk * 8, s)) != cudaSuccess) return fail(e);
+    if ((e = cudaMallocAsync(&bk, nk * 2, s)) != cudaSuccess) return fail(e);
+    if ((e = cudaMallocAsync(&bk2, nk * 2, s)) != cudaSuccess) return fail(e);
     if ((e = cudaMallocAsync(&perm, nk * 4, s)) != cudaSuccess) return fail(e);
     if ((e = cudaMallocAsync(&perm2, nk * 4, s)) != cudaSuccess) return fail(e);
     if ((e = cudaMemsetAsync(dst, 0, sizeof(DevStats), s)) != cudaSuccess) return fail(e);
-    if ((e = launch_band_keys(p->order, nnz, p->ld, p->coords, p->key_bits, shift, keys, perm, s)) != cudaSuccess)
-        return fail(e);
-    if ((e = sort_keys(nnz, p->key_bits * p->order + band_bits, keys, keys2, perm, perm2, s)) != cudaSuccess)
-        return fail(e);
-    if ((e = launch_gather(p->order, nnz, p->ld, p->key_bits, keys2, perm2, p->vals, coords, vals, s)) != cudaSuccess)
+    if ((e = launch_band_keys(p->order, nnz, p->ld, p->coords, shift, bk, perm, s)) != cudaSuccess) return fail(e);
+    if ((e = sort_band_keys(nnz, band_bits, bk, bk2, perm, perm2, s)) != cudaSuccess) return fail(e);
+    if ((e = launch_permute(p->order, nnz, p->ld, perm2, p->coords, p->vals, coords, vals, s)) != cudaSuccess)
         return fail(e);
     if ((e = launch_stats(p->order, nnz, p->ld, coords, shift, dst, s)) != cudaSuccess) return fail(e);
     DevStats hst;
     if ((e = cudaMemcpyAsync(&hst, dst, sizeof(hst), cudaMemcpyDeviceToHost, s)) != cudaSuccess) return fail(e);
     cleanup();
-    dst = nullptr; keys = nullptr; keys2 = nullptr; perm = nullptr; perm2 = nullptr;
+    dst = nullptr; bk = nullptr; bk2 = nullptr; perm = nullptr; perm2 = nullptr;
     if (p->pooled) cudaFreeAsync(p->storage, s); else cudaFree(p->storage);
     p->storage = storage;
     p->coords = coords;
@@ -215,7 +217,7 @@ int plan_create_impl(Plan **out, int order, int64_t dim, int64_t nnz, const int3
     if ((e = cudaMemcpyAsync(dst, &hst, sizeof(hst), cudaMemcpyHostToDevice, s)) != cudaSuccess) return fail(e);
 
     // a1: validate + canonicalise + pack keys
-    if ((e = launch_canonicalize(order, dim, nnz, bits, -1, idx, keys, perm, dst, s, !general)) != cudaSuccess)
+    if ((e = launch_canonicalize(order, dim, nnz, bits, idx, keys, perm, dst, s, !general)) != cudaSuccess)
         return fail(e);
     if ((e = cudaMemcpyAsync(&hst, dst, sizeof(hst), cudaMemcpyDeviceToHost, s)) != cudaSuccess) return fail(e);
     if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return fail(e);  // sync 1: validation verdict
@@ -759,7 +761,7 @@ int systec_mttkrp(int order, int64_t dim, int64_t nnz, const int32_t *idx, const
         systec::overlap(C, cb, vals, static_cast<size_t>(nnz) * 4))
         return SYSTEC_ERR_ALIAS;
     Plan *p = nullptr;
-    rc = systec::plan_create_impl(&p, order, dim, nnz, idx, vals, s, true);
+    rc = systec::plan_create_impl(&p, order, dim, nnz, idx, vals, s, true, false, -1);  // used once: no band re-sort
     if (rc) return rc;
     rc = systec::execute_impl(p, B, R, C, nullptr, s);
     systec::destroy_impl(p);
@@ -849,7 +851,7 @@ int mttkrp_host_pipelined(int order, int64_t dim, int64_t nnz, int bits, const i
         for (int k = 0; k < nch; ++k) {
             const int64_t lo = k * per, n = std::min(per, nnz - lo);
             if ((e = cudaStreamWaitEvent(s, ev[k], 0)) != cudaSuccess) break;
-            if ((e = launch_canonicalize(order, dim, n, bits, -1, d_idx + lo * order, keys, perm, dst, s, true, lo)) != cudaSuccess)
+            if ((e = launch_canonicalize(order, dim, n, bits, d_idx + lo * order, keys, perm, dst, s, true, lo)) != cudaSuccess)
                 break;
             if ((e = launch_gather_range(order, n, ld, bits, keys, d_vals + lo, coords + lo, svals + lo, s)) != cudaSuccess) break;
             if (k == 0) {  // chunk-0 statistics decide position-1 accumulation (one sync)
@@ -921,7 +923,7 @@ int systec_mttkrp_host(int order, int64_t dim, int64_t nnz, const int32_t *idx_h
         if (ib && (e = cudaMemcpyAsync(d_idx, idx_host, ib, cudaMemcpyHostToDevice, s)) != cudaSuccess) break;
         if (vb && (e = cudaMemcpyAsync(d_vals, vals_host, vb, cudaMemcpyHostToDevice, s)) != cudaSuccess) break;
         if ((e = cudaMemcpyAsync(d_B, B_host, bb, cudaMemcpyHostToDevice, s)) != cudaSuccess) break;
-        rc = systec::plan_create_impl(&p, order, dim, nnz, d_idx, d_vals, s, true);
+        rc = systec::plan_create_impl(&p, order, dim, nnz, d_idx, d_vals, s, true, false, -1);
         if (rc) break;
         rc = systec::execute_impl(p, d_B, R, d_C, nullptr, s);
         if (rc) break;

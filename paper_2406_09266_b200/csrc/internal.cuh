@@ -41,7 +41,7 @@ struct DevStats {
 };
 
 // prepare.cu
-cudaError_t launch_canonicalize(int order, int64_t dim, int64_t nnz, int bits, int band_shift, const int32_t *idx,
+cudaError_t launch_canonicalize(int order, int64_t dim, int64_t nnz, int bits, const int32_t *idx,
                                 unsigned long long *keys, uint32_t *perm, DevStats *st,
                                 cudaStream_t s, bool canonicalise = true, int64_t e_offset = 0);
 cudaError_t sort_keys(int64_t nnz, int end_bit, unsigned long long *keys_in, unsigned long long *keys_out,
@@ -51,8 +51,12 @@ cudaError_t launch_gather(int order, int64_t nnz, int64_t ld, int bits, const un
                           int32_t *coords, float *vals_out, cudaStream_t s);
 cudaError_t launch_stats(int order, int64_t nnz, int64_t ld, const int32_t *coords, int band_shift, DevStats *st,
                          cudaStream_t s);
-cudaError_t launch_band_keys(int order, int64_t nnz, int64_t ld, const int32_t *coords, int bits, int band_shift,
-                             unsigned long long *keys, uint32_t *perm, cudaStream_t s);
+cudaError_t launch_band_keys(int order, int64_t nnz, int64_t ld, const int32_t *coords, int band_shift,
+                             uint16_t *band, uint32_t *perm, cudaStream_t s);
+cudaError_t sort_band_keys(int64_t nnz, int band_bits, uint16_t *keys_in, uint16_t *keys_out, uint32_t *perm_in,
+                           uint32_t *perm_out, cudaStream_t s);
+cudaError_t launch_permute(int order, int64_t nnz, int64_t ld, const uint32_t *perm, const int32_t *cin,
+                           const float *vin, int32_t *cout, float *vout, cudaStream_t s);
 cudaError_t launch_gather_range(int order, int64_t n, int64_t ld, int bits, const unsigned long long *keys,
                                 const float *vals_in, int32_t *coords, float *vals_out, cudaStream_t s);
 

@@ -30,14 +30,11 @@ __device__ __forceinline__ void sort_net(int32_t (&c)[N]) {
     }
 }
 
-// key = [band of c_{N-1}] [c_0] ... [c_{N-1}], `bits` per index; band = c_{N-1} >> band_shift
-// (band_shift < 0: no band field, plain lexicographic order)
 template <int N>
-__device__ __forceinline__ unsigned long long pack_key(const int32_t (&c)[N], int bits, int band_shift) {
+__device__ __forceinline__ unsigned long long pack_key(const int32_t (&c)[N], int bits) {
     unsigned long long k = 0;
 #pragma unroll
     for (int t = 0; t < N; ++t) k = (k << bits) | static_cast<unsigned long long>(static_cast<uint32_t>(c[t]));
-    if (band_shift >= 0) k |= static_cast<unsigned long long>(static_cast<uint32_t>(c[N - 1]) >> band_shift) << (bits * N);
     return k;
 }
 
@@ -55,8 +52,8 @@ __device__ __forceinline__ bool load_canonical(const int32_t *idx, int64_t e, in
 
 template <int N, bool CANON>
 __global__ void canonicalize_kernel(const int32_t *__restrict__ idx, int64_t nnz, int64_t dim, int bits,
-                                    int band_shift, unsigned long long *__restrict__ keys,
-                                    uint32_t *__restrict__ perm, DevStats *st, int64_t e_offset) {
+                                    unsigned long long *__restrict__ keys, uint32_t *__restrict__ perm,
+                                    DevStats *st, int64_t e_offset) {
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz;
          e += (int64_t)gridDim.x * blockDim.x) {
         int32_t c[N];
@@ -68,12 +65,12 @@ __global__ void canonicalize_kernel(const int32_t *__restrict__ idx, int64_t nnz
             perm[e] = static_cast<uint32_t>(e);
             continue;
         }
-        const unsigned long long k = pack_key<N>(c, bits, band_shift);
+        const unsigned long long k = pack_key<N>(c, bits);
         keys[e] = k;
         perm[e] = static_cast<uint32_t>(e);
         if (e > 0) {
             int32_t q[N];
-            if (load_canonical<N, CANON>(idx, e - 1, dim, q) && pack_key<N>(q, bits, band_shift) > k) st->unsorted = 1ull;
+            if (load_canonical<N, CANON>(idx, e - 1, dim, q) && pack_key<N>(q, bits) > k) st->unsorted = 1ull;
         }
     }
 }
@@ -118,18 +115,36 @@ __global__ void gather_range_kernel(int64_t n, int64_t ld, int bits, const unsig
     }
 }
 
-// banded stream order (systec_plan_opts.band_shift): keys of the prepared SoA
-// stream with the band of c_{N-1} above the lexicographic fields
+// banded stream order (systec_plan_opts.band_shift): the band number of each
+// prepared entry, c_{N-1} >> band_shift, with its position
 template <int N>
-__global__ void band_keys_kernel(int64_t nnz, int64_t ld, const int32_t *__restrict__ coords, int bits,
-                                 int band_shift, unsigned long long *__restrict__ keys, uint32_t *__restrict__ perm) {
+__global__ void band_keys_kernel(int64_t nnz, int64_t ld, const int32_t *__restrict__ coords, int band_shift,
+                                 uint16_t *__restrict__ band, uint32_t *__restrict__ perm) {
+    const int32_t *cl = coords + static_cast<int64_t>(N - 1) * ld;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz;
          e += (int64_t)gridDim.x * blockDim.x) {
-        int32_t c[N];
-#pragma unroll
-        for (int t = 0; t < N; ++t) c[t] = coords[t * ld + e];
-        keys[e] = pack_key<N>(c, bits, band_shift);
+        band[e] = static_cast<uint16_t>(static_cast<uint32_t>(cl[e]) >> band_shift);
         perm[e] = static_cast<uint32_t>(e);
+    }
+}
+
+// out[t][e] = in[t][perm[e]], vals likewise; the padding tail is zeroed
+template <int N>
+__global__ void permute_kernel(int64_t nnz, int64_t ld, const uint32_t *__restrict__ perm,
+                               const int32_t *__restrict__ cin, const float *__restrict__ vin,
+                               int32_t *__restrict__ cout, float *__restrict__ vout) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < ld;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        if (e < nnz) {
+            const int64_t src = perm[e];
+#pragma unroll
+            for (int t = 0; t < N; ++t) cout[t * ld + e] = cin[t * ld + src];
+            vout[e] = vin[src];
+        } else {
+#pragma unroll
+            for (int t = 0; t < N; ++t) cout[t * ld + e] = 0;
+            vout[e] = 0.0f;
+        }
     }
 }
 
@@ -241,15 +256,15 @@ int grid_for(int64_t n, int threads) {
         default: return cudaErrorInvalidValue;   \
     }
 
-cudaError_t launch_canonicalize(int order, int64_t dim, int64_t nnz, int bits, int band_shift, const int32_t *idx,
+cudaError_t launch_canonicalize(int order, int64_t dim, int64_t nnz, int bits, const int32_t *idx,
                                 unsigned long long *keys, uint32_t *perm, DevStats *st, cudaStream_t s,
                                 bool canonicalise, int64_t e_offset) {
     if (nnz == 0) return cudaSuccess;
     const int th = 256;
     if (canonicalise) {
-        SYSTEC_ORDER_SWITCH(order, canonicalize_kernel<N, true><<<grid_for(nnz, th), th, 0, s>>>(idx, nnz, dim, bits, band_shift, keys, perm, st, e_offset));
+        SYSTEC_ORDER_SWITCH(order, canonicalize_kernel<N, true><<<grid_for(nnz, th), th, 0, s>>>(idx, nnz, dim, bits, keys, perm, st, e_offset));
     } else {
-        SYSTEC_ORDER_SWITCH(order, canonicalize_kernel<N, false><<<grid_for(nnz, th), th, 0, s>>>(idx, nnz, dim, bits, band_shift, keys, perm, st, e_offset));
+        SYSTEC_ORDER_SWITCH(order, canonicalize_kernel<N, false><<<grid_for(nnz, th), th, 0, s>>>(idx, nnz, dim, bits, keys, perm, st, e_offset));
     }
     return cudaGetLastError();
 }
@@ -278,11 +293,35 @@ cudaError_t launch_gather(int order, int64_t nnz, int64_t ld, int bits, const un
     return cudaGetLastError();
 }
 
-cudaError_t launch_band_keys(int order, int64_t nnz, int64_t ld, const int32_t *coords, int bits, int band_shift,
-                             unsigned long long *keys, uint32_t *perm, cudaStream_t s) {
+cudaError_t launch_band_keys(int order, int64_t nnz, int64_t ld, const int32_t *coords, int band_shift,
+                             uint16_t *band, uint32_t *perm, cudaStream_t s) {
     if (nnz == 0) return cudaSuccess;
     const int th = 256;
-    SYSTEC_ORDER_SWITCH(order, band_keys_kernel<N><<<grid_for(nnz, th), th, 0, s>>>(nnz, ld, coords, bits, band_shift, keys, perm));
+    SYSTEC_ORDER_SWITCH(order, band_keys_kernel<N><<<grid_for(nnz, th), th, 0, s>>>(nnz, ld, coords, band_shift, band, perm));
+    return cudaGetLastError();
+}
+
+// stable (LSD radix) sort of (band, position) pairs on the band's bits only
+cudaError_t sort_band_keys(int64_t nnz, int band_bits, uint16_t *keys_in, uint16_t *keys_out, uint32_t *perm_in,
+                           uint32_t *perm_out, cudaStream_t s) {
+    size_t temp = 0;
+    cudaError_t e = cub::DeviceRadixSort::SortPairs(nullptr, temp, keys_in, keys_out, perm_in, perm_out,
+                                                    static_cast<int>(nnz), 0, band_bits, s);
+    if (e != cudaSuccess) return e;
+    void *tmp = nullptr;
+    e = cudaMallocAsync(&tmp, temp ? temp : 16, s);
+    if (e != cudaSuccess) return e;
+    e = cub::DeviceRadixSort::SortPairs(tmp, temp, keys_in, keys_out, perm_in, perm_out, static_cast<int>(nnz), 0,
+                                        band_bits, s);
+    cudaError_t f = cudaFreeAsync(tmp, s);
+    return e != cudaSuccess ? e : f;
+}
+
+cudaError_t launch_permute(int order, int64_t nnz, int64_t ld, const uint32_t *perm, const int32_t *cin,
+                           const float *vin, int32_t *cout, float *vout, cudaStream_t s) {
+    if (ld == 0) return cudaSuccess;
+    const int th = 256;
+    SYSTEC_ORDER_SWITCH(order, permute_kernel<N><<<grid_for(ld, th), th, 0, s>>>(nnz, ld, perm, cin, vin, cout, vout));
     return cudaGetLastError();
 }
 
