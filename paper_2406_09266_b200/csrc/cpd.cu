@@ -69,11 +69,28 @@ __device__ __forceinline__ void stage_rows(float *__restrict__ dst, const float 
     }
 }
 
+// Asynchronous form for contiguous rows (R % 4 == 0): 16-byte cp.async.cg
+// copies (L2 -> smem, no registers held), one commit group per call; the
+// caller double-buffers tiles so the next tile's copies overlap this tile's
+// arithmetic.
+__device__ __forceinline__ void stage_rows_async(float *__restrict__ dst, const float *__restrict__ X, int64_t r0,
+                                                 int nr, int R) {
+    const int n4 = nr * R / 4;
+    const float4 *s4 = reinterpret_cast<const float4 *>(X + r0 * R);
+    const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
+    for (int q = threadIdx.x; q < n4; q += blockDim.x)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d + 16u * q), "l"(s4 + q) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_prev() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
 __global__ void __launch_bounds__(256) gram_dots_partial_kernel(const float *__restrict__ B, const float *__restrict__ M,
                                                                 int64_t dim, int R, double *__restrict__ part) {
     extern __shared__ __align__(16) unsigned char cpd_smem[];
-    float *tb = reinterpret_cast<float *>(cpd_smem);  // [kTileRows][Rp] of B
-    float *tm = tb + kTileRows * kRp;                 // [kTileRows][Rp] of M
+    // two tile buffers, each [kTileRows][Rp] of B then of M (double-buffered)
+    float *tbuf = reinterpret_cast<float *>(cpd_smem);
+    constexpr int kTile = kTileRows * kRp;
     double *red = reinterpret_cast<double *>(cpd_smem);  // reused after the row loop
     const int Rp = (R + 3) & ~3;
     const int T4 = Rp / 4;           // 4-wide column blocks
@@ -90,11 +107,28 @@ __global__ void __launch_bounds__(256) gram_dots_partial_kernel(const float *__r
     for (int k = 0; k < 16; ++k) acc[k] = 0.0;
     double dacc = 0.0;  // column dot: thread (column tid % R, row lane tid / R)
     const int dl = tid / R, dn = blockDim.x / R;
-    for (int64_t r0 = lo; r0 < hi; r0 += kTileRows) {
+    const bool async_rows = Rp == R;  // contiguous rows: cp.async double buffering
+    auto issue = [&](int64_t q0, int buf) {
+        const int n = static_cast<int>(min(static_cast<int64_t>(kTileRows), hi - q0));
+        stage_rows_async(tbuf + buf * 2 * kTile, B, q0, n, R);
+        stage_rows_async(tbuf + buf * 2 * kTile + kTile, M, q0, n, R);
+    };
+    if (async_rows && lo < hi) issue(lo, 0);
+    cp_async_commit();
+    int k = 0;
+    for (int64_t r0 = lo; r0 < hi; r0 += kTileRows, ++k) {
         const int nr = static_cast<int>(min(static_cast<int64_t>(kTileRows), hi - r0));
-        __syncthreads();
-        stage_rows(tb, B, r0, nr, R, Rp);
-        stage_rows(tm, M, r0, nr, R, Rp);
+        const int buf = async_rows ? (k & 1) : 0;
+        float *tb = tbuf + buf * 2 * kTile;
+        float *tm = tb + kTile;
+        if (async_rows) {
+            if (r0 + kTileRows < hi) issue(r0 + kTileRows, buf ^ 1);  // the other buffer: freed by the barrier below
+            cp_async_commit();
+            cp_async_wait_prev();                                    // this thread's copies of tile k landed
+        } else {
+            stage_rows(tb, B, r0, nr, R, Rp);
+            stage_rows(tm, M, r0, nr, R, Rp);
+        }
         __syncthreads();
         if (active) {
             float f[16];
@@ -119,7 +153,9 @@ __global__ void __launch_bounds__(256) gram_dots_partial_kernel(const float *__r
             for (int i = dl; i < nr; i += dn) d = fmaf(tm[i * Rp + c], tb[i * Rp + c], d);
             dacc += d;
         }
+        __syncthreads();  // tile k consumed: its buffer may be refilled
     }
+    cp_async_wait_all();
     __syncthreads();  // tiles no longer needed: sum the row groups in shared memory
     double *dred = red + kRp / 4 * (kRp / 4) * 16;  // [256] after the pair sums
     dred[tid] = dl < dn ? dacc : 0.0;
@@ -361,7 +397,8 @@ __global__ void __launch_bounds__(256) apply_inverse_kernel(const float *__restr
                                                             int64_t dim, int R, float *__restrict__ Bout,
                                                             double *__restrict__ part, const int *skip) {
     if (skip && *skip) return;  // device-side loop: last iteration evaluates the fit only
-    __shared__ __align__(16) float Ms[kTileRows * RT];
+    constexpr int kAR = RT > 32 ? 64 : kTileRows;  // rows per tile (two buffers within 48 KB)
+    __shared__ __align__(16) float Msb[2][kAR * RT];  // double-buffered M tiles
     __shared__ double sq[256];
     const int tid = threadIdx.x;
     const int b = tid % RT, rg = tid / RT;
@@ -373,10 +410,23 @@ __global__ void __launch_bounds__(256) apply_inverse_kernel(const float *__restr
     const int64_t rows = (dim + gridDim.x - 1) / gridDim.x;
     const int64_t lo = blockIdx.x * rows, hi = min(dim, lo + rows);
     double acc = 0.0;
-    for (int64_t r0 = lo; r0 < hi; r0 += kTileRows) {
-        const int nr = static_cast<int>(min(static_cast<int64_t>(kTileRows), hi - r0));
-        __syncthreads();
-        stage_rows(Ms, M, r0, nr, R, RT);
+    const bool async_rows = R == RT;  // contiguous rows: cp.async double buffering
+    if (async_rows && lo < hi) stage_rows_async(Msb[0], M, lo, static_cast<int>(min(static_cast<int64_t>(kAR), hi - lo)), R);
+    cp_async_commit();
+    int k = 0;
+    for (int64_t r0 = lo; r0 < hi; r0 += kAR, ++k) {
+        const int nr = static_cast<int>(min(static_cast<int64_t>(kAR), hi - r0));
+        const int buf = async_rows ? (k & 1) : 0;
+        float *Ms = Msb[buf];
+        if (async_rows) {
+            if (r0 + kAR < hi)
+                stage_rows_async(Msb[buf ^ 1], M, r0 + kAR,
+                                 static_cast<int>(min(static_cast<int64_t>(kAR), hi - r0 - kAR)), R);
+            cp_async_commit();
+            cp_async_wait_prev();
+        } else {
+            stage_rows(Ms, M, r0, nr, R, RT);
+        }
         __syncthreads();
         if (active) {
             float t = 0.f;
@@ -396,7 +446,9 @@ __global__ void __launch_bounds__(256) apply_inverse_kernel(const float *__restr
             }
             acc += t;
         }
+        __syncthreads();  // tile k consumed: its buffer may be refilled
     }
+    cp_async_wait_all();
     sq[tid] = active ? acc : 0.0;
     __syncthreads();
     if (tid < R) {
@@ -496,9 +548,9 @@ cudaError_t cpd_tensor_norm2(const Plan &p, double *out, cudaStream_t s) {
 int cpd_partial_blocks() { return sm_count() * 2; }
 
 size_t gram_smem_bytes() {
-    const size_t tiles = 2ull * kTileRows * kRp * sizeof(float);
+    const size_t tiles = 4ull * kTileRows * kRp * sizeof(float);  // two buffers of B and M tiles
     const size_t redb = (static_cast<size_t>(kRp / 4) * (kRp / 4) * 16 + 256) * sizeof(double);  // row-group sums
-    return std::max(tiles, redb);  // 48 KB: within the default dynamic shared-memory limit
+    return std::max(tiles, redb);  // 96 KB (R <= 48): needs the opt-in dynamic shared-memory limit
 }
 
 // scratch (doubles): G[R*R], dots[R] (contiguous: one reduction), norms[R],
@@ -518,7 +570,12 @@ cudaError_t cpd_fit_pieces(const Plan &p, const float *M, const float *B, const 
     // registers leave one block per SM)
     if (R <= 8) gram_dots_warp_kernel<8><<<PB, 256, 0, s>>>(B, M, p.dim, R, part);
     else if (R <= 16) gram_dots_warp_kernel<16><<<PB, 256, 0, s>>>(B, M, p.dim, R, part);
-    else gram_dots_partial_kernel<<<PB, 256, gram_smem_bytes(), s>>>(B, M, p.dim, R, part);
+    else {
+        static const cudaError_t attr = cudaFuncSetAttribute(
+            gram_dots_partial_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(gram_smem_bytes()));
+        if (attr != cudaSuccess) return attr;
+        gram_dots_partial_kernel<<<PB, 256, gram_smem_bytes(), s>>>(B, M, p.dim, R, part);
+    }
     reduce_partials_kernel<<<(W + 7) / 8, 256, 0, s>>>(part, PB, W, G, nullptr);  // G and dots (contiguous)
     if (R <= 16) small_solve_kernel<1><<<1, 1024, 0, s>>>(G, R, p.order, Hinv, lam, dots, xhat2);
     else if (R <= 32) small_solve_kernel<2><<<1, 1024, 0, s>>>(G, R, p.order, Hinv, lam, dots, xhat2);
