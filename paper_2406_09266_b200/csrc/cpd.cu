@@ -23,6 +23,7 @@
 #include <cmath>
 
 #include "internal.cuh"
+#include "ptx.cuh"
 
 namespace systec {
 
@@ -69,26 +70,47 @@ __device__ __forceinline__ void stage_rows(float *__restrict__ dst, const float 
     }
 }
 
-// Asynchronous form for contiguous rows (R % 4 == 0): 16-byte cp.async.cg
-// copies (L2 -> smem, no registers held), one commit group per call; the
-// caller double-buffers tiles so the next tile's copies overlap this tile's
-// arithmetic.
-__device__ __forceinline__ void stage_rows_async(float *__restrict__ dst, const float *__restrict__ X, int64_t r0,
-                                                 int nr, int R) {
-    const int n4 = nr * R / 4;
-    const float4 *s4 = reinterpret_cast<const float4 *>(X + r0 * R);
-    const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
-    for (int q = threadIdx.x; q < n4; q += blockDim.x)
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d + 16u * q), "l"(s4 + q) : "memory");
+// S-stage ring of row tiles [kTileRows][R] of one or two matrices, filled by
+// 1-D bulk copies (TMA engine, one per matrix and tile, completing on the
+// stage's mbarrier) that thread 0 issues S-1 tiles ahead of the block's
+// arithmetic — contiguous rows only (R % 4 == 0, 16-byte aligned bases).
+// (Double-buffered per-thread cp.async copies measured Gram 115 us on c3, the
+// bulk ring below is what runs now.)
+constexpr int kRingS = 3;
+struct TileRing {
+    float *buf;       // [kRingS][NM][kTileRows * R]
+    uint64_t *bars;   // [kRingS]
+    const float *X0, *X1;
+    int NM, R;
+    int64_t lo, hi;
+    __device__ int64_t ntiles() const { return (hi - lo + kTileRows - 1) / kTileRows; }
+    __device__ float *tile(int64_t k, int m) const {
+        return buf + (static_cast<size_t>(k % kRingS) * NM + m) * kTileRows * R;
+    }
+    __device__ void init() const {  // thread 0, then a block barrier
+        for (int st = 0; st < kRingS; ++st) mbar_init(&bars[st], 1);
+        fence_mbar_init();
+    }
+    __device__ void issue(int64_t k) const {  // thread 0
+        const int64_t r0 = lo + k * kTileRows;
+        const uint32_t bytes = static_cast<uint32_t>(min(static_cast<int64_t>(kTileRows), hi - r0) * R * 4);
+        uint64_t *bar = &bars[k % kRingS];
+        const uint64_t pol = policy_evict_first();
+        mbar_arrive_expect_tx(bar, bytes * NM);
+        bulk_g2s(tile(k, 0), X0 + r0 * R, bytes, bar, pol);
+        if (NM > 1) bulk_g2s(tile(k, 1), X1 + r0 * R, bytes, bar, pol);
+    }
+    __device__ void wait(int64_t k) const { mbar_wait(&bars[k % kRingS], static_cast<uint32_t>((k / kRingS) & 1)); }
+};
+__host__ __device__ constexpr size_t ring_bytes(int NM, int R) {
+    return static_cast<size_t>(kRingS) * NM * kTileRows * R * 4 + kRingS * 8;
 }
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_prev() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
 __global__ void __launch_bounds__(256) gram_dots_partial_kernel(const float *__restrict__ B, const float *__restrict__ M,
-                                                                int64_t dim, int R, double *__restrict__ part) {
+                                                                int64_t dim, int R, double *__restrict__ part, bool ring) {
     extern __shared__ __align__(16) unsigned char cpd_smem[];
-    // two tile buffers, each [kTileRows][Rp] of B then of M (double-buffered)
+    // ring: kRingS stages of [kTileRows][R] tiles of B and M (bulk copies); else
+    // one synchronously staged [kTileRows][Rp] tile of each
     float *tbuf = reinterpret_cast<float *>(cpd_smem);
     constexpr int kTile = kTileRows * kRp;
     double *red = reinterpret_cast<double *>(cpd_smem);  // reused after the row loop
@@ -107,29 +129,35 @@ __global__ void __launch_bounds__(256) gram_dots_partial_kernel(const float *__r
     for (int k = 0; k < 16; ++k) acc[k] = 0.0;
     double dacc = 0.0;  // column dot: thread (column tid % R, row lane tid / R)
     const int dl = tid / R, dn = blockDim.x / R;
-    const bool async_rows = Rp == R;  // contiguous rows: cp.async double buffering
-    auto issue = [&](int64_t q0, int buf) {
-        const int n = static_cast<int>(min(static_cast<int64_t>(kTileRows), hi - q0));
-        stage_rows_async(tbuf + buf * 2 * kTile, B, q0, n, R);
-        stage_rows_async(tbuf + buf * 2 * kTile + kTile, M, q0, n, R);
-    };
-    if (async_rows && lo < hi) issue(lo, 0);
-    cp_async_commit();
-    int k = 0;
-    for (int64_t r0 = lo; r0 < hi; r0 += kTileRows, ++k) {
-        const int nr = static_cast<int>(min(static_cast<int64_t>(kTileRows), hi - r0));
-        const int buf = async_rows ? (k & 1) : 0;
-        float *tb = tbuf + buf * 2 * kTile;
-        float *tm = tb + kTile;
-        if (async_rows) {
-            if (r0 + kTileRows < hi) issue(r0 + kTileRows, buf ^ 1);  // the other buffer: freed by the barrier below
-            cp_async_commit();
-            cp_async_wait_prev();                                    // this thread's copies of tile k landed
-        } else {
-            stage_rows(tb, B, r0, nr, R, Rp);
-            stage_rows(tm, M, r0, nr, R, Rp);
+    const bool async_rows = ring;  // contiguous, aligned rows: the bulk-copy ring
+    TileRing tr{tbuf, reinterpret_cast<uint64_t *>(cpd_smem + ring_bytes(2, R) - kRingS * 8), B, M, 2, R, lo, hi};
+    const int64_t nt = async_rows && lo < hi ? tr.ntiles() : 0;
+    if (async_rows) {
+        if (tid == 0) {
+            tr.init();
+            for (int64_t q = 0; q < min(static_cast<int64_t>(kRingS - 1), nt); ++q) tr.issue(q);
         }
         __syncthreads();
+    }
+    int64_t k = 0;
+    for (int64_t r0 = lo; r0 < hi; r0 += kTileRows, ++k) {
+        const int nr = static_cast<int>(min(static_cast<int64_t>(kTileRows), hi - r0));
+        float *tb, *tm;
+        if (async_rows) {
+            if (tid == 0 && k + kRingS - 1 < nt) {
+                fence_proxy_async_smem();  // the slot's last generic reads (tile k-1) precede the copy
+                tr.issue(k + kRingS - 1);
+            }
+            tb = tr.tile(k, 0);
+            tm = tr.tile(k, 1);
+            tr.wait(k);
+        } else {
+            tb = tbuf;
+            tm = tbuf + kTile;
+            stage_rows(tb, B, r0, nr, R, Rp);
+            stage_rows(tm, M, r0, nr, R, Rp);
+            __syncthreads();
+        }
         if (active) {
             float f[16];
 #pragma unroll
@@ -153,9 +181,8 @@ __global__ void __launch_bounds__(256) gram_dots_partial_kernel(const float *__r
             for (int i = dl; i < nr; i += dn) d = fmaf(tm[i * Rp + c], tb[i * Rp + c], d);
             dacc += d;
         }
-        __syncthreads();  // tile k consumed: its buffer may be refilled
+        __syncthreads();  // tile k consumed: its slot may be refilled
     }
-    cp_async_wait_all();
     __syncthreads();  // tiles no longer needed: sum the row groups in shared memory
     double *dred = red + kRp / 4 * (kRp / 4) * 16;  // [256] after the pair sums
     dred[tid] = dl < dn ? dacc : 0.0;
@@ -176,6 +203,122 @@ __global__ void __launch_bounds__(256) gram_dots_partial_kernel(const float *__r
     if (tid < R) {
         double d = 0.0;
         for (int l = 0; l < dn; ++l) d += dred[l * R + tid];
+        out[R * R + tid] = d;
+    }
+}
+
+// The same partial sums for R % 4 == 0, R <= 32 (aligned rows): tiles arrive
+// through the bulk-copy ring, and only the upper triangle of 4x4 micro-tiles
+// (a-block <= b-block: 36 of 64 at R = 32) is accumulated and mirrored at the
+// end — the Gram matrix is symmetric.  Row pointers advance by increments (no
+// per-row index arithmetic); the column dots use float4 lanes.  Per row at
+// R = 32: 36 threads x (2 LDS.128 + 16 FFMA) instead of 64.
+__global__ void __launch_bounds__(256) gram_dots_sym_kernel(const float *__restrict__ B, const float *__restrict__ M,
+                                                            int64_t dim, int R, double *__restrict__ part) {
+    extern __shared__ __align__(16) unsigned char cpd_smem[];
+    const int T4 = R / 4;
+    const int NT = T4 * (T4 + 1) / 2;  // upper-triangle micro-tiles
+    const int RG = blockDim.x / NT;    // row groups
+    const int tid = threadIdx.x;
+    const int mt = tid % NT, g = tid / NT;
+    const bool active = g < RG;
+    int a4 = 0, rem = mt;  // mt -> (a4, b4), a4 <= b4, row-major over the upper triangle
+    while (rem >= T4 - a4) {
+        rem -= T4 - a4;
+        ++a4;
+    }
+    const int b4 = a4 + rem;
+    const int cq = tid % T4, rl = tid / T4, nrl = blockDim.x / T4;  // column dots: (row lane, float4 column)
+    const int64_t rows = (dim + gridDim.x - 1) / gridDim.x;
+    const int64_t lo = blockIdx.x * rows, hi = min(dim, lo + rows);
+    TileRing tr{reinterpret_cast<float *>(cpd_smem), reinterpret_cast<uint64_t *>(cpd_smem + ring_bytes(2, R) - kRingS * 8),
+                B, M, 2, R, lo, hi};
+    const int64_t nt = lo < hi ? tr.ntiles() : 0;
+    if (tid == 0) {
+        tr.init();
+        for (int64_t q = 0; q < min(static_cast<int64_t>(kRingS - 1), nt); ++q) tr.issue(q);
+    }
+    __syncthreads();
+    double acc[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) acc[k] = 0.0;
+    double dacc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int64_t k = 0; k < nt; ++k) {
+        const int nr = static_cast<int>(min(static_cast<int64_t>(kTileRows), hi - lo - k * kTileRows));
+        if (tid == 0 && k + kRingS - 1 < nt) {
+            fence_proxy_async_smem();
+            tr.issue(k + kRingS - 1);
+        }
+        const float *tb = tr.tile(k, 0), *tm = tr.tile(k, 1);
+        tr.wait(k);
+        if (active && g < nr) {
+            float f[16];
+#pragma unroll
+            for (int q = 0; q < 16; ++q) f[q] = 0.f;
+            const float *px = tb + g * R + 4 * a4, *py = tb + g * R + 4 * b4;
+            const float *pend = tb + nr * R;
+            const int step = RG * R;
+#pragma unroll 2
+            for (; px < pend; px += step, py += step) {
+                const float4 x = *reinterpret_cast<const float4 *>(px);
+                const float4 y = *reinterpret_cast<const float4 *>(py);
+                const float xa[4] = {x.x, x.y, x.z, x.w}, yb[4] = {y.x, y.y, y.z, y.w};
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+#pragma unroll
+                    for (int v = 0; v < 4; ++v) f[u * 4 + v] = fmaf(xa[u], yb[v], f[u * 4 + v]);
+            }
+#pragma unroll
+            for (int q = 0; q < 16; ++q) acc[q] += f[q];
+        }
+        if (rl < nrl) {
+            float4 d = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int i = rl; i < nr; i += nrl) {
+                const float4 m4 = *reinterpret_cast<const float4 *>(tm + i * R + 4 * cq);
+                const float4 b4v = *reinterpret_cast<const float4 *>(tb + i * R + 4 * cq);
+                d.x = fmaf(m4.x, b4v.x, d.x);
+                d.y = fmaf(m4.y, b4v.y, d.y);
+                d.z = fmaf(m4.z, b4v.z, d.z);
+                d.w = fmaf(m4.w, b4v.w, d.w);
+            }
+            dacc[0] += d.x;
+            dacc[1] += d.y;
+            dacc[2] += d.z;
+            dacc[3] += d.w;
+        }
+        __syncthreads();  // tile k consumed: its slot may be refilled
+    }
+    // sum the row groups (and the dot lanes) in shared memory; the ring is idle
+    double *red = reinterpret_cast<double *>(cpd_smem);  // [NT][16]
+    double *dred = red + 36 * 16;                          // [nrl][R]
+    for (int grp = 0; grp < RG; ++grp) {
+        if (active && g == grp) {
+#pragma unroll
+            for (int q = 0; q < 16; ++q) red[mt * 16 + q] = (grp == 0 ? 0.0 : red[mt * 16 + q]) + acc[q];
+        }
+        __syncthreads();
+    }
+    if (rl < nrl) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) dred[rl * R + 4 * cq + c] = dacc[c];
+    }
+    __syncthreads();
+    const int W = R * R + R;
+    double *out = part + static_cast<int64_t>(blockIdx.x) * W;
+    for (int q = tid; q < NT * 16; q += blockDim.x) {
+        const int m = q / 16, e = q % 16;
+        int ta = 0, rr = m;
+        while (rr >= T4 - ta) {
+            rr -= T4 - ta;
+            ++ta;
+        }
+        const int a = ta * 4 + e / 4, b = (ta + rr) * 4 + e % 4;
+        out[a * R + b] = red[q];
+        out[b * R + a] = red[q];  // mirror (the diagonal tiles write their own mirror image)
+    }
+    if (tid < R) {
+        double d = 0.0;
+        for (int l = 0; l < nrl; ++l) d += dred[l * R + tid];
         out[R * R + tid] = d;
     }
 }
@@ -395,10 +538,10 @@ __global__ void __launch_bounds__(1024) small_solve_kernel(const double *__restr
 template <int RT>
 __global__ void __launch_bounds__(256) apply_inverse_kernel(const float *__restrict__ M, const float *__restrict__ Hinv,
                                                             int64_t dim, int R, float *__restrict__ Bout,
-                                                            double *__restrict__ part, const int *skip) {
+                                                            double *__restrict__ part, const int *skip, bool ring) {
     if (skip && *skip) return;  // device-side loop: last iteration evaluates the fit only
-    constexpr int kAR = RT > 32 ? 64 : kTileRows;  // rows per tile (two buffers within 48 KB)
-    __shared__ __align__(16) float Msb[2][kAR * RT];  // double-buffered M tiles
+    extern __shared__ __align__(16) unsigned char cpd_smem[];  // ring: kRingS tiles of M (bulk copies)
+    __shared__ __align__(16) float Msync[kTileRows * RT];      // else one synchronously staged tile
     __shared__ double sq[256];
     const int tid = threadIdx.x;
     const int b = tid % RT, rg = tid / RT;
@@ -410,24 +553,32 @@ __global__ void __launch_bounds__(256) apply_inverse_kernel(const float *__restr
     const int64_t rows = (dim + gridDim.x - 1) / gridDim.x;
     const int64_t lo = blockIdx.x * rows, hi = min(dim, lo + rows);
     double acc = 0.0;
-    const bool async_rows = R == RT;  // contiguous rows: cp.async double buffering
-    if (async_rows && lo < hi) stage_rows_async(Msb[0], M, lo, static_cast<int>(min(static_cast<int64_t>(kAR), hi - lo)), R);
-    cp_async_commit();
-    int k = 0;
-    for (int64_t r0 = lo; r0 < hi; r0 += kAR, ++k) {
-        const int nr = static_cast<int>(min(static_cast<int64_t>(kAR), hi - r0));
-        const int buf = async_rows ? (k & 1) : 0;
-        float *Ms = Msb[buf];
-        if (async_rows) {
-            if (r0 + kAR < hi)
-                stage_rows_async(Msb[buf ^ 1], M, r0 + kAR,
-                                 static_cast<int>(min(static_cast<int64_t>(kAR), hi - r0 - kAR)), R);
-            cp_async_commit();
-            cp_async_wait_prev();
-        } else {
-            stage_rows(Ms, M, r0, nr, R, RT);
+    TileRing tr{reinterpret_cast<float *>(cpd_smem), reinterpret_cast<uint64_t *>(cpd_smem + ring_bytes(1, R) - kRingS * 8),
+                M, nullptr, 1, R, lo, hi};
+    const int64_t nt = ring && lo < hi ? tr.ntiles() : 0;
+    if (ring) {
+        if (tid == 0) {
+            tr.init();
+            for (int64_t q = 0; q < min(static_cast<int64_t>(kRingS - 1), nt); ++q) tr.issue(q);
         }
         __syncthreads();
+    }
+    int64_t k = 0;
+    for (int64_t r0 = lo; r0 < hi; r0 += kTileRows, ++k) {
+        const int nr = static_cast<int>(min(static_cast<int64_t>(kTileRows), hi - r0));
+        const float *Ms;
+        if (ring) {  // rows of R == RT floats
+            if (tid == 0 && k + kRingS - 1 < nt) {
+                fence_proxy_async_smem();
+                tr.issue(k + kRingS - 1);
+            }
+            Ms = tr.tile(k, 0);
+            tr.wait(k);
+        } else {
+            stage_rows(Msync, M, r0, nr, R, RT);
+            Ms = Msync;
+            __syncthreads();
+        }
         if (active) {
             float t = 0.f;
             for (int i = rg; i < nr; i += RGN) {
@@ -446,9 +597,8 @@ __global__ void __launch_bounds__(256) apply_inverse_kernel(const float *__restr
             }
             acc += t;
         }
-        __syncthreads();  // tile k consumed: its buffer may be refilled
+        __syncthreads();  // tile k consumed: its slot may be refilled
     }
-    cp_async_wait_all();
     sq[tid] = active ? acc : 0.0;
     __syncthreads();
     if (tid < R) {
@@ -547,10 +697,27 @@ cudaError_t cpd_tensor_norm2(const Plan &p, double *out, cudaStream_t s) {
 // partial blocks: >= 256 rows each, at most 2 per SM
 int cpd_partial_blocks() { return sm_count() * 2; }
 
-size_t gram_smem_bytes() {
-    const size_t tiles = 4ull * kTileRows * kRp * sizeof(float);  // two buffers of B and M tiles
+// one opt-in of the ring's dynamic shared memory per instantiation
+template <int RT>
+cudaError_t launch_apply_inverse(int PB, size_t rb, cudaStream_t s, const float *M, const float *Hinv, int64_t dim,
+                                 int R, float *B, double *part, const int *skip, bool ring) {
+    static const cudaError_t attr = cudaFuncSetAttribute(apply_inverse_kernel<RT>,
+                                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                         static_cast<int>(ring_bytes(1, 32)));
+    if (attr != cudaSuccess) return attr;
+    apply_inverse_kernel<RT><<<PB, 256, rb, s>>>(M, Hinv, dim, R, B, part, skip, ring);
+    return cudaSuccess;
+}
+
+bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// ring form: R % 4 == 0 (contiguous 16-byte rows), R <= 32, 16-byte aligned bases
+bool gram_ring(int R, const float *B, const float *M) { return R % 4 == 0 && R <= 32 && aligned16(B) && aligned16(M); }
+
+size_t gram_smem_bytes(int R, bool ring) {
+    const size_t tiles = ring ? ring_bytes(2, R) : 2ull * kTileRows * kRp * sizeof(float);
     const size_t redb = (static_cast<size_t>(kRp / 4) * (kRp / 4) * 16 + 256) * sizeof(double);  // row-group sums
-    return std::max(tiles, redb);  // 96 KB (R <= 48): needs the opt-in dynamic shared-memory limit
+    return std::max(tiles, redb);  // ring at R = 32: 96 KB (opt-in dynamic shared-memory limit)
 }
 
 // scratch (doubles): G[R*R], dots[R] (contiguous: one reduction), norms[R],
@@ -572,9 +739,17 @@ cudaError_t cpd_fit_pieces(const Plan &p, const float *M, const float *B, const 
     else if (R <= 16) gram_dots_warp_kernel<16><<<PB, 256, 0, s>>>(B, M, p.dim, R, part);
     else {
         static const cudaError_t attr = cudaFuncSetAttribute(
-            gram_dots_partial_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(gram_smem_bytes()));
+            gram_dots_partial_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            static_cast<int>(std::max(gram_smem_bytes(32, true), gram_smem_bytes(kMaxCpR, false))));
         if (attr != cudaSuccess) return attr;
-        gram_dots_partial_kernel<<<PB, 256, gram_smem_bytes(), s>>>(B, M, p.dim, R, part);
+        if (gram_ring(R, B, M)) {
+            static const cudaError_t attr2 = cudaFuncSetAttribute(
+                gram_dots_sym_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(gram_smem_bytes(32, true)));
+            if (attr2 != cudaSuccess) return attr2;
+            gram_dots_sym_kernel<<<PB, 256, gram_smem_bytes(R, true), s>>>(B, M, p.dim, R, part);
+        } else {
+            gram_dots_partial_kernel<<<PB, 256, gram_smem_bytes(R, false), s>>>(B, M, p.dim, R, part, false);
+        }
     }
     reduce_partials_kernel<<<(W + 7) / 8, 256, 0, s>>>(part, PB, W, G, nullptr);  // G and dots (contiguous)
     if (R <= 16) small_solve_kernel<1><<<1, 1024, 0, s>>>(G, R, p.order, Hinv, lam, dots, xhat2);
@@ -588,14 +763,19 @@ cudaError_t cpd_update(const Plan &p, const float *M, float *B, float *lam, int 
     double *G = dscratch, *dots = G + R * R, *norms = dots + R, *xhat2 = norms + R, *part = xhat2 + 2;
     float *Hinv = fscratch;
     const int PB = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(cpd_partial_blocks(), (p.dim + 31) / 32)));
+    // ring form for R in {8, 16, 24, 32} (rows of exactly RT floats), aligned M
+    const bool ring = R % 8 == 0 && R <= 32 && aligned16(M);
+    const size_t rb = ring ? ring_bytes(1, R) : 0;
+    cudaError_t e;
     switch ((R + 7) / 8) {
-        case 1: apply_inverse_kernel<8><<<PB, 256, 0, s>>>(M, Hinv, p.dim, R, B, part, skip); break;
-        case 2: apply_inverse_kernel<16><<<PB, 256, 0, s>>>(M, Hinv, p.dim, R, B, part, skip); break;
-        case 3: apply_inverse_kernel<24><<<PB, 256, 0, s>>>(M, Hinv, p.dim, R, B, part, skip); break;
-        case 4: apply_inverse_kernel<32><<<PB, 256, 0, s>>>(M, Hinv, p.dim, R, B, part, skip); break;
-        case 5: apply_inverse_kernel<40><<<PB, 256, 0, s>>>(M, Hinv, p.dim, R, B, part, skip); break;
-        default: apply_inverse_kernel<48><<<PB, 256, 0, s>>>(M, Hinv, p.dim, R, B, part, skip); break;
+        case 1: e = launch_apply_inverse<8>(PB, rb, s, M, Hinv, p.dim, R, B, part, skip, ring); break;
+        case 2: e = launch_apply_inverse<16>(PB, rb, s, M, Hinv, p.dim, R, B, part, skip, ring); break;
+        case 3: e = launch_apply_inverse<24>(PB, rb, s, M, Hinv, p.dim, R, B, part, skip, ring); break;
+        case 4: e = launch_apply_inverse<32>(PB, rb, s, M, Hinv, p.dim, R, B, part, skip, ring); break;
+        case 5: e = launch_apply_inverse<40>(PB, rb, s, M, Hinv, p.dim, R, B, part, skip, ring); break;
+        default: e = launch_apply_inverse<48>(PB, rb, s, M, Hinv, p.dim, R, B, part, skip, ring); break;
     }
+    if (e != cudaSuccess) return e;
     reduce_partials_kernel<<<(R + 7) / 8, 256, 0, s>>>(part, PB, R, norms, skip);
     const int64_t total = p.dim * R;
     const int ab = static_cast<int>(std::min<int64_t>((total / 4 + 255) / 256 + 1, static_cast<int64_t>(sm_count()) * 8));
