@@ -128,17 +128,27 @@ def bytes_eff(order, nnz, G, R, dim):
 
 def l2_model(w, st, nnz_local, kern_ms, launch):
     """Lower bound from the measured L2 rates (profiles/r01_microbench.json):
-    t >= max(stream / HBM read, gathers / L2 gather rate, reds / L2 red rate)."""
+    t >= max(stream / HBM read, gathers / L2 gather rate, reds / L2 red rate),
+    with the rates of the row size (64-B rows for R = 16, 128-B rows
+    otherwise) and of the measured table size nearest the footprint (B for
+    the gathers; C and its replicas for the reductions)."""
+    import math
     try:
         with open(os.path.join(ROOT, "profiles", "r01_microbench.json")) as f:
             mb = json.load(f)
-        hbm = mb["hbm_read_gbs"] * 1e9
-        gat = mb["gather_128B_rows_gbs"]["12.800MB"] * 1e9
-        red = mb["red_v4_128B_rows_gbs"]["12.800MB"] * 1e9
     except Exception:
         return None
     n, R = w.order, w.R
     row = R * 4
+    kind = "64B" if row == 64 and "gather_64B_rows_gbs" in mb else "128B"
+
+    def nearest(table, mbytes):
+        key = min(table, key=lambda k: abs(math.log(float(k[:-2])) - math.log(max(mbytes, 1e-3))))
+        return table[key] * 1e9, key
+
+    hbm = mb["hbm_read_gbs"] * 1e9
+    gat, gkey = nearest(mb[f"gather_{kind}_rows_gbs"], w.dim * row / 1e6)
+    red, rkey = nearest(mb[f"red_v4_{kind}_rows_gbs"], max(1, launch.get("copies", 1)) * w.dim * row / 1e6)
     stream = nnz_local * (4 * n + 4)
     gathers = st["G"] * row
     n1 = sum(h for code, h in enumerate(st["pattern_hist"]) if not code & 1)   # entries with c1 != c0
@@ -149,7 +159,8 @@ def l2_model(w, st, nnz_local, kern_ms, launch):
     return {"stream_bytes": stream, "gather_bytes": gathers, "red_payload_bytes": reds,
             "hbm_read_gbs": hbm / 1e9, "l2_gather_gbs": gat / 1e9, "l2_red_gbs": red / 1e9,
             "t_lower_ms": t * 1e3, "frac_of_l2_bound": t * 1e3 / kern_ms,
-            "source": "profiles/r01_microbench.json (tools/microbench.cu, 128-B rows, 12.8 MB tables)"}
+            "source": f"profiles/r01_microbench.json (tools/microbench.cu): {kind} rows, gathers from a "
+                      f"{gkey} table, red.v4 into a {rkey} table"}
 
 
 def cpu_baseline(w, target_wall=4.0, max_entries=None, threads=0):

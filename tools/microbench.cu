@@ -61,6 +61,31 @@ __global__ void red_rows_scalar(float *C, uint32_t rows, int iters) {
     }
 }
 
+// 64-byte rows (R = 16 floats): groups of 4 lanes, 8 rows per warp instruction
+__global__ void gather_rows64(const float *__restrict__ B, uint32_t rows, int iters, float *sink) {
+    const int lane = threadIdx.x & 31, g = lane >> 2, j = lane & 3;
+    const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    float4 acc = make_float4(0, 0, 0, 0);
+#pragma unroll 4
+    for (int it = 0; it < iters; ++it) {
+        const uint32_t r = hash32(gw * 131071u + it * 8u + g) % rows;
+        float4 v = __ldg(reinterpret_cast<const float4 *>(B + (size_t)r * 16) + j);
+        acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+    }
+    if (acc.x + acc.y + acc.z + acc.w == 12345.f) *sink = acc.x;
+}
+
+__global__ void red_rows64(float *C, uint32_t rows, int iters) {
+    const int lane = threadIdx.x & 31, g = lane >> 2, j = lane & 3;
+    const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const float4 v = make_float4(1.f, 1.f, 1.f, 1.f);
+    for (int it = 0; it < iters; ++it) {
+        const uint32_t r = hash32(gw * 131071u + it * 8u + g) % rows;
+        float *p = C + (size_t)r * 16 + j * 4;
+        asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
+    }
+}
+
 // gather 3 rows + red 2 rows per "entry": the c2 inner loop without index streaming
 __global__ void mttkrp_like(const float *__restrict__ B, float *C, uint32_t rows, int iters) {
     const int lane = threadIdx.x & 31, g = lane >> 3, j = lane & 7;
@@ -230,6 +255,33 @@ int main() {
         CK(cudaFree(C));
     }
     printf("}");
+    // 3a) the same for 64-byte rows (R = 16: c4, c5), gathers and red.v4
+    const double t64_mb[] = {0.064, 0.64, 2.048, 12.8, 20.48};
+    for (int kind = 0; kind < 2; ++kind) {
+        printf(kind == 0 ? ", \"gather_64B_rows_gbs\": {" : ", \"red_v4_64B_rows_gbs\": {");
+        for (int t = 0; t < 5; ++t) {
+            uint32_t rows = (uint32_t)(t64_mb[t] * 1e6 / 64);
+            float *X;
+            CK(cudaMalloc(&X, (size_t)rows * 64));
+            CK(cudaMemset(X, 0, (size_t)rows * 64));
+            const int iters = kind == 0 ? 256 : 128, blocks = sms * 8, threads = 256;
+            float best = 1e30f;
+            for (int r = 0; r < 4; ++r) {
+                CK(cudaEventRecord(e0));
+                if (kind == 0) gather_rows64<<<blocks, threads>>>(X, rows, iters, sink);
+                else red_rows64<<<blocks, threads>>>(X, rows, iters);
+                CK(cudaEventRecord(e1));
+                CK(cudaEventSynchronize(e1));
+                float ms;
+                CK(cudaEventElapsedTime(&ms, e0, e1));
+                best = ms < best ? ms : best;
+            }
+            double bytes = (double)blocks * threads / 4 * iters * 64;
+            printf("%s\"%.3fMB\": %.1f", t ? ", " : "", t64_mb[t], bytes / (best * 1e-3) / 1e9);
+            CK(cudaFree(X));
+        }
+        printf("}");
+    }
     // 3b) scalar atomicAdd, 12.8 MB
     {
         uint32_t rows = 100000;
