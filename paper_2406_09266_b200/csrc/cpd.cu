@@ -623,15 +623,25 @@ __global__ void normalize_kernel(float *__restrict__ B, int64_t dim, int R, cons
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
     if ((R & 3) == 0) {
         float4 *B4 = reinterpret_cast<float4 *>(B);
-        for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total / 4; q += stride) {
+        const int64_t n4 = total / 4;
+        auto scale = [&](float4 v, int64_t q) {
             const int b = static_cast<int>((q * 4) % R);
-            float4 v = B4[q];
             if (nb[b + 0] > 0.f) v.x /= nb[b + 0];
             if (nb[b + 1] > 0.f) v.y /= nb[b + 1];
             if (nb[b + 2] > 0.f) v.z /= nb[b + 2];
             if (nb[b + 3] > 0.f) v.w /= nb[b + 3];
-            B4[q] = v;
+            return v;
+        };
+        // four independent float4 loads in flight per thread
+        int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+        for (; q + 3 * stride < n4; q += 4 * stride) {
+            float4 v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) v[u] = B4[q + u * stride];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) B4[q + u * stride] = scale(v[u], q + u * stride);
         }
+        for (; q < n4; q += stride) B4[q] = scale(B4[q], q);
     } else {
         for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total; q += stride) {
             const int b = static_cast<int>(q % R);
