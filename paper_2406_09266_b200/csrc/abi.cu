@@ -771,17 +771,24 @@ int systec_mttkrp(int order, int64_t dim, int64_t nnz, const int32_t *idx, const
 namespace systec {
 namespace {
 
-// One non-blocking stream per device for the pipeline's host->device copies
-// (created on first use, thread-safe, kept for the process lifetime).
-cudaStream_t copy_stream() {
+// Non-blocking streams per device for the pipeline's copies: which = 0 for
+// host->device, 1 for device->host (created on first use, thread-safe, kept
+// for the process lifetime).
+cudaStream_t copy_stream(int which = 0) {
     static std::mutex mu;
-    static cudaStream_t streams[64] = {};
+    static cudaStream_t streams[2][64] = {};
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
     std::lock_guard<std::mutex> lock(mu);
-    if (!streams[dev] && cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking) != cudaSuccess)
-        streams[dev] = nullptr;
-    return streams[dev];
+    cudaStream_t &st = streams[which & 1][dev];
+    if (!st && cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) st = nullptr;
+    return st;
+}
+
+// canonical (ascending) copy of one host tuple
+void canon_tuple(const int32_t *t, int order, int32_t *out) {
+    for (int i = 0; i < order; ++i) out[i] = t[i];
+    std::sort(out, out + order);
 }
 
 // Pipelined end-to-end call: chunk k's host->device copy (copy stream) overlaps
@@ -790,6 +797,13 @@ cudaStream_t copy_stream() {
 // executed into C as it lands; the sort is skipped (lexicographic input stays
 // sorted per chunk; any other order is still correct, only with shorter runs).
 // Position-1 accumulation is decided from chunk 0's statistics (one sync).
+// Lexicographically sorted canonical input (the storage format) gives every
+// later entry indices >= the next chunk's leading index c0, so once chunk k
+// is executed the C rows below chunk k+1's first c0 are final: they are
+// copied back on a device->host stream while later chunks still transfer and
+// run (PCIe is full duplex).  Sortedness is confirmed afterwards — chunk
+// boundaries on the host, inside chunks by the canonicalisation kernel's
+// flag — and an unsorted input gets one more full copy of C at the end.
 int mttkrp_host_pipelined(int order, int64_t dim, int64_t nnz, int bits, const int32_t *idx_host,
                           const float *vals_host, const float *B_host, int R, float *C_host, cudaStream_t s) {
     static const int kChunks = [] {  // SYSTEC_HOST_CHUNKS: tuning knob for the pipeline depth (default 16)
@@ -825,6 +839,7 @@ int mttkrp_host_pipelined(int order, int64_t dim, int64_t nnz, int bits, const i
     hst.bad_entry = ULLONG_MAX;
     cudaStream_t cs = copy_stream();
     if (!cs) cs = s;  // no copy stream: copies on the caller's stream (no overlap, same result)
+    cudaStream_t ds = s;  // device->host stream of the early C copies (set below)
     std::vector<cudaEvent_t> ev(nch + 2, nullptr);
     int rc = SYSTEC_OK;
     do {
@@ -848,6 +863,16 @@ int mttkrp_host_pipelined(int order, int64_t dim, int64_t nnz, int bits, const i
         systec_exec_opts o;
         std::memset(&o, 0, sizeof(o));
         o.no_zero = 1;
+        // early copies only into page-locked C (a pageable destination would
+        // make each copy block the host thread that is feeding the pipeline)
+        cudaPointerAttributes pa;
+        const bool c_pinned = cudaPointerGetAttributes(&pa, C_host) == cudaSuccess && pa.type == cudaMemoryTypeHost;
+        cudaGetLastError();  // clear a possible error from the query
+        ds = c_pinned ? copy_stream(1) : nullptr;
+        if (!ds) ds = s;
+        bool bounds_sorted = true;  // chunk boundaries in canonical lexicographic order (host check)
+        int64_t done_rows = 0;      // C rows [0, done_rows) already copied back
+        const size_t row_bytes = static_cast<size_t>(R) * 4;
         for (int k = 0; k < nch; ++k) {
             const int64_t lo = k * per, n = std::min(per, nnz - lo);
             if ((e = cudaStreamWaitEvent(s, ev[k], 0)) != cudaSuccess) break;
@@ -871,6 +896,22 @@ int mttkrp_host_pipelined(int order, int64_t dim, int64_t nnz, int bits, const i
             pk.vals = svals + lo;
             pk.stream = s;
             if ((e = launch_mttkrp(pk, d_B, R, d_C, o, s)) != cudaSuccess) break;
+            if (k + 1 < nch && bounds_sorted) {  // early copy of the rows no later chunk can touch
+                int32_t a[8], b[8];
+                canon_tuple(idx_host + (lo + n - 1) * order, order, a);
+                canon_tuple(idx_host + (lo + n) * order, order, b);
+                bounds_sorted = !std::lexicographical_compare(b, b + order, a, a + order);
+                const int64_t bound = std::min<int64_t>(std::max<int64_t>(b[0], 0), dim);
+                if (bounds_sorted && bound > done_rows && ds != s) {
+                    if ((e = cudaEventRecord(ev[k], s)) != cudaSuccess) break;  // chunk k executed
+                    if ((e = cudaStreamWaitEvent(ds, ev[k], 0)) != cudaSuccess) break;
+                    if ((e = cudaMemcpyAsync(reinterpret_cast<char *>(C_host) + done_rows * row_bytes,
+                                             reinterpret_cast<const char *>(d_C) + done_rows * row_bytes,
+                                             (bound - done_rows) * row_bytes, cudaMemcpyDeviceToHost, ds)) != cudaSuccess)
+                        break;
+                    done_rows = bound;
+                }
+            }
         }
         if (e != cudaSuccess) break;
         if (hst.err) {
@@ -879,14 +920,23 @@ int mttkrp_host_pipelined(int order, int64_t dim, int64_t nnz, int bits, const i
             break;
         }
         if ((e = cudaMemcpyAsync(&hst, dst, sizeof(hst), cudaMemcpyDeviceToHost, s)) != cudaSuccess) break;
-        if ((e = cudaMemcpyAsync(C_host, d_C, bb, cudaMemcpyDeviceToHost, s)) != cudaSuccess) break;
+        if ((e = cudaMemcpyAsync(reinterpret_cast<char *>(C_host) + done_rows * row_bytes,
+                                 reinterpret_cast<const char *>(d_C) + done_rows * row_bytes,
+                                 bb - done_rows * row_bytes, cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+            break;
         if ((e = cudaStreamSynchronize(s)) != cudaSuccess) break;
+        if ((e = cudaStreamSynchronize(ds)) != cudaSuccess) break;
         if (hst.err) {  // a later chunk held a bad index: C is not valid
             g_last_bad_entry = static_cast<int64_t>(hst.bad_entry);
             rc = SYSTEC_ERR_INDEX;
+        } else if (done_rows > 0 && (hst.unsorted || !bounds_sorted)) {
+            // not sorted after all: rows copied early may have changed since
+            if ((e = cudaMemcpyAsync(C_host, d_C, done_rows * row_bytes, cudaMemcpyDeviceToHost, s)) != cudaSuccess) break;
+            if ((e = cudaStreamSynchronize(s)) != cudaSuccess) break;
         }
     } while (false);
     cudaStreamSynchronize(cs);
+    cudaStreamSynchronize(ds);  // no copy into C_host outlives the call
     cudaFreeAsync(buf, s);
     for (auto &x : ev)
         if (x) cudaEventDestroy(x);

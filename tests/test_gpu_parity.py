@@ -717,6 +717,30 @@ def test_host_call_pipelined(systec, n, dim, nnz, R, shuffle):
         systec.mttkrp_host(n, dim, bad, vals, w.B)
 
 
+def test_host_call_early_c_copy_falls_back_on_interior_disorder(systec):
+    """The pipelined host call copies C rows back early when the input is
+    lexicographically sorted.  An entry with a small leading index moved into
+    a later chunk's interior (chunk boundaries still sorted) must be caught by
+    the device-side order flag and C copied again: every row matches."""
+    import torch
+    n, dim, nnz, R = 3, 5000, 1_200_000, 16
+    w = make("pipe_disorder", n, dim, nnz, R, seed=11, mode="uniform")
+    idx, vals = w.idx.copy(), w.vals.copy()
+    per = ((nnz + 15) // 16 + 3) & ~3          # the library's chunk size (16 chunks)
+    a, b = 1000, 9 * per + 1234                  # chunk 0 interior <-> chunk 9 interior
+    idx[[a, b]] = idx[[b, a]]
+    vals[[a, b]] = vals[[b, a]]
+    rows = np.unique(np.concatenate([idx[a], idx[b], w.idx[:200, 0], np.arange(0, dim, 97)]))
+    Cref, S = oracle.mttkrp_rows(n, dim, w.idx, w.vals, w.B, rows)
+    pin = [torch.from_numpy(np.ascontiguousarray(x)).pin_memory() for x in (idx, vals, w.B)]
+    Cp = torch.empty((dim, R), dtype=torch.float32).pin_memory()
+    systec.mttkrp_host(n, dim, *pin, C=Cp)
+    parity(Cp.numpy()[rows], Cref, S)
+    # pageable destination: no early copies, same result
+    Cq = systec.mttkrp_host(n, dim, idx, vals, w.B)
+    parity(np.asarray(Cq)[rows], Cref, S)
+
+
 def test_fault_injection_is_detected_and_located(systec):
     """A single corrupted stored value must fail the parity check, and exactly
     the output rows its (distinct) indices name must be the ones that differ."""
