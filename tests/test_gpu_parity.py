@@ -593,7 +593,8 @@ def test_cp_als_iterates_match_oracle(systec, order, dim, R):
 
 
 @pytest.mark.parametrize("order,dim,nnz,R", [(3, 600, 20000, 8), (3, 700, 30000, 13), (4, 300, 20000, 32),
-                                             (3, 1000, 40000, 37), (5, 60, 20000, 48), (3, 40000, 100000, 16)])
+                                             (3, 1000, 40000, 37), (5, 60, 20000, 48), (3, 40000, 100000, 16),
+                                             (3, 5000, 60000, 24), (4, 200, 20000, 20), (3, 3000, 50000, 28)])
 def test_cp_als_ranks_and_tiles(systec, order, dim, nnz, R):
     """CP-ALS kernels at every rank template (R padded to 8..48, R % 4 != 0
     staging, register-tableau widths 1/2/6) and row ranges spanning several
