@@ -107,10 +107,10 @@ __host__ __device__ constexpr size_t ring_bytes(int NM, int R) {
 }
 
 __global__ void __launch_bounds__(256) gram_dots_partial_kernel(const float *__restrict__ B, const float *__restrict__ M,
-                                                                int64_t dim, int R, double *__restrict__ part, bool ring) {
+                                                                int64_t dim, int R, double *__restrict__ part) {
     extern __shared__ __align__(16) unsigned char cpd_smem[];
-    // ring: kRingS stages of [kTileRows][R] tiles of B and M (bulk copies); else
-    // one synchronously staged [kTileRows][Rp] tile of each
+    // one synchronously staged [kTileRows][Rp] tile of B and of M (general R;
+    // R % 4 == 0, R <= 32 runs gram_dots_sym_kernel on the bulk-copy ring)
     float *tbuf = reinterpret_cast<float *>(cpd_smem);
     constexpr int kTile = kTileRows * kRp;
     double *red = reinterpret_cast<double *>(cpd_smem);  // reused after the row loop
@@ -129,35 +129,12 @@ __global__ void __launch_bounds__(256) gram_dots_partial_kernel(const float *__r
     for (int k = 0; k < 16; ++k) acc[k] = 0.0;
     double dacc = 0.0;  // column dot: thread (column tid % R, row lane tid / R)
     const int dl = tid / R, dn = blockDim.x / R;
-    const bool async_rows = ring;  // contiguous, aligned rows: the bulk-copy ring
-    TileRing tr{tbuf, reinterpret_cast<uint64_t *>(cpd_smem + ring_bytes(2, R) - kRingS * 8), B, M, 2, R, lo, hi};
-    const int64_t nt = async_rows && lo < hi ? tr.ntiles() : 0;
-    if (async_rows) {
-        if (tid == 0) {
-            tr.init();
-            for (int64_t q = 0; q < min(static_cast<int64_t>(kRingS - 1), nt); ++q) tr.issue(q);
-        }
-        __syncthreads();
-    }
-    int64_t k = 0;
-    for (int64_t r0 = lo; r0 < hi; r0 += kTileRows, ++k) {
+    for (int64_t r0 = lo; r0 < hi; r0 += kTileRows) {
         const int nr = static_cast<int>(min(static_cast<int64_t>(kTileRows), hi - r0));
-        float *tb, *tm;
-        if (async_rows) {
-            if (tid == 0 && k + kRingS - 1 < nt) {
-                fence_proxy_async_smem();  // the slot's last generic reads (tile k-1) precede the copy
-                tr.issue(k + kRingS - 1);
-            }
-            tb = tr.tile(k, 0);
-            tm = tr.tile(k, 1);
-            tr.wait(k);
-        } else {
-            tb = tbuf;
-            tm = tbuf + kTile;
-            stage_rows(tb, B, r0, nr, R, Rp);
-            stage_rows(tm, M, r0, nr, R, Rp);
-            __syncthreads();
-        }
+        float *tb = tbuf, *tm = tbuf + kTile;
+        stage_rows(tb, B, r0, nr, R, Rp);
+        stage_rows(tm, M, r0, nr, R, Rp);
+        __syncthreads();
         if (active) {
             float f[16];
 #pragma unroll
@@ -758,7 +735,7 @@ cudaError_t cpd_fit_pieces(const Plan &p, const float *M, const float *B, const 
             if (attr2 != cudaSuccess) return attr2;
             gram_dots_sym_kernel<<<PB, 256, gram_smem_bytes(R, true), s>>>(B, M, p.dim, R, part);
         } else {
-            gram_dots_partial_kernel<<<PB, 256, gram_smem_bytes(R, false), s>>>(B, M, p.dim, R, part, false);
+            gram_dots_partial_kernel<<<PB, 256, gram_smem_bytes(R, false), s>>>(B, M, p.dim, R, part);
         }
     }
     reduce_partials_kernel<<<(W + 7) / 8, 256, 0, s>>>(part, PB, W, G, nullptr);  // G and dots (contiguous)
