@@ -558,8 +558,34 @@ __global__ void __launch_bounds__(256) apply_inverse_kernel(const float *__restr
         }
         if (active) {
             float t = 0.f;
-            for (int i = rg; i < nr; i += RGN) {
-                const float4 *m4 = reinterpret_cast<const float4 *>(Ms + i * RT);
+            // pointer increments (no per-row 64-bit index arithmetic)
+            float *o = Bout + (r0 + rg) * R + b;
+            const float *mrow = Ms + rg * RT;
+            const float *mend = Ms + nr * RT;
+            // two rows per step: two independent FMA chains per thread
+            for (; mrow + RGN * RT < mend; mrow += 2 * RGN * RT, o += 2 * RGN * R) {
+                const float4 *m4 = reinterpret_cast<const float4 *>(mrow);
+                const float4 *n4 = reinterpret_cast<const float4 *>(mrow + RGN * RT);
+                float s = 0.f, u = 0.f;
+#pragma unroll
+                for (int a4 = 0; a4 < RT / 4; ++a4) {
+                    const float4 x = m4[a4], y = n4[a4];
+                    s = fmaf(x.x, h[4 * a4 + 0], s);
+                    u = fmaf(y.x, h[4 * a4 + 0], u);
+                    s = fmaf(x.y, h[4 * a4 + 1], s);
+                    u = fmaf(y.y, h[4 * a4 + 1], u);
+                    s = fmaf(x.z, h[4 * a4 + 2], s);
+                    u = fmaf(y.z, h[4 * a4 + 2], u);
+                    s = fmaf(x.w, h[4 * a4 + 3], s);
+                    u = fmaf(y.w, h[4 * a4 + 3], u);
+                }
+                o[0] = s;
+                o[RGN * R] = u;
+                t = fmaf(s, s, t);
+                t = fmaf(u, u, t);
+            }
+            for (; mrow < mend; mrow += RGN * RT, o += RGN * R) {
+                const float4 *m4 = reinterpret_cast<const float4 *>(mrow);
                 float s = 0.f;
 #pragma unroll
                 for (int a4 = 0; a4 < RT / 4; ++a4) {
@@ -569,7 +595,7 @@ __global__ void __launch_bounds__(256) apply_inverse_kernel(const float *__restr
                     s = fmaf(x.z, h[4 * a4 + 2], s);
                     s = fmaf(x.w, h[4 * a4 + 3], s);
                 }
-                Bout[(r0 + i) * R + b] = s;
+                *o = s;
                 t = fmaf(s, s, t);
             }
             acc += t;
