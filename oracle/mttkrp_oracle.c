@@ -47,9 +47,6 @@
 #include <string.h>
 
 #define ORACLE_MAX_ORDER 8
-#ifndef ORACLE_MUTATION
-#define ORACLE_MUTATION 0   /* 0 = the oracle; 1..7 = deliberate bugs for the mutation tests */
-#endif
 
 /* Step 3: rearrange p[0..n) into the next lexicographically greater
  * permutation of its multiset; returns 0 when p was the last one. */
@@ -89,9 +86,7 @@ static void *run_job(void *arg) {
     int32_t p[ORACLE_MAX_ORDER];
     for (int64_t e = J->e_begin; e < J->e_end; e++) {
         for (int t = 0; t < n; t++) p[t] = J->idx[e * n + t];
-#if ORACLE_MUTATION != 1            /* mutation tests (tests/test_oracle_mutations.py) only */
         sort_small(p, n);                                   /* step 2 */
-#endif
         const double v = (double)J->vals[e];                /* step 1 */
         do {                                                /* step 3 */
             int64_t row = p[0];
@@ -104,34 +99,13 @@ static void *run_job(void *arg) {
                 out = row - J->row_lo;
             }
             for (int r = 0; r < R; r++) J->term[r] = v;     /* step 4 */
-#if ORACLE_MUTATION == 2
-            for (int t = 1; t < n - 1; t++) {
-#else
             for (int t = 1; t < n; t++) {
-#endif
-#if ORACLE_MUTATION == 3
-                const float *b = J->B + (int64_t)p[t - 1] * R;
-#else
                 const float *b = J->B + (int64_t)p[t] * R;
-#endif
                 for (int r = 0; r < R; r++) J->term[r] *= (double)b[r];
             }
-#if ORACLE_MUTATION == 4
-            out = J->rowslot ? out : p[n - 1] - J->row_lo;
-#endif
             double *c = J->C + out * R, *s = J->S + out * R;
-#if ORACLE_MUTATION == 5
-            for (int r = 0; r < R; r++) { c[r] -= J->term[r]; s[r] += fabs(J->term[r]); }
-#elif ORACLE_MUTATION == 7
-            for (int r = 0; r < R; r++) { c[r] += (p[0] == p[n - 1] ? 1.0 : 2.0) * J->term[r]; s[r] += fabs(J->term[r]); }
-#else
             for (int r = 0; r < R; r++) { c[r] += J->term[r]; s[r] += fabs(J->term[r]); }
-#endif
-#if ORACLE_MUTATION == 6
-        } while (0);                    /* only the first permutation */
-#else
         } while (next_perm(p, n));
-#endif
     }
     return NULL;
 }

@@ -736,11 +736,12 @@ int systec_plan_last_launch(systec_plan plan, int32_t *grid_x, int32_t *grid_y, 
                             int32_t *kernel_id) {
     if (!plan) return SYSTEC_ERR_ARG;
     Plan *p = reinterpret_cast<Plan *>(plan);
-    if (grid_x) *grid_x = p->last_grid_x;
-    if (grid_y) *grid_y = p->last_grid_y;
-    if (block) *block = p->last_block;
-    if (smem) *smem = p->last_smem;
-    if (kernel_id) *kernel_id = p->last_kernel;
+    const Plan::LaunchInfo l = p->last_launch();
+    if (grid_x) *grid_x = l.grid_x;
+    if (grid_y) *grid_y = l.grid_y;
+    if (block) *block = l.block;
+    if (smem) *smem = l.smem;
+    if (kernel_id) *kernel_id = l.kernel;
     return SYSTEC_OK;
 }
 

@@ -710,13 +710,13 @@ cudaError_t cpd_tensor_norm2(const Plan &p, double *out, cudaStream_t s) {
 // partial blocks: >= 256 rows each, at most 2 per SM
 int cpd_partial_blocks() { return sm_count() * 2; }
 
-// one opt-in of the ring's dynamic shared memory per instantiation
+// the ring's dynamic shared-memory opt-in is per device: set before every
+// launch (a host-side attribute write), so a plan on any device gets it
 template <int RT>
 cudaError_t launch_apply_inverse(int PB, size_t rb, cudaStream_t s, const float *M, const float *Hinv, int64_t dim,
                                  int R, float *B, double *part, const int *skip, bool ring) {
-    static const cudaError_t attr = cudaFuncSetAttribute(apply_inverse_kernel<RT>,
-                                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                         static_cast<int>(ring_bytes(1, 32)));
+    const cudaError_t attr = cudaFuncSetAttribute(apply_inverse_kernel<RT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                  static_cast<int>(ring_bytes(1, 32)));
     if (attr != cudaSuccess) return attr;
     apply_inverse_kernel<RT><<<PB, 256, rb, s>>>(M, Hinv, dim, R, B, part, skip, ring);
     return cudaSuccess;
@@ -751,12 +751,12 @@ cudaError_t cpd_fit_pieces(const Plan &p, const float *M, const float *B, const 
     if (R <= 8) gram_dots_warp_kernel<8><<<PB, 256, 0, s>>>(B, M, p.dim, R, part);
     else if (R <= 16) gram_dots_warp_kernel<16><<<PB, 256, 0, s>>>(B, M, p.dim, R, part);
     else {
-        static const cudaError_t attr = cudaFuncSetAttribute(
+        const cudaError_t attr = cudaFuncSetAttribute(  // per device: set at every launch
             gram_dots_partial_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
             static_cast<int>(std::max(gram_smem_bytes(32, true), gram_smem_bytes(kMaxCpR, false))));
         if (attr != cudaSuccess) return attr;
         if (gram_ring(R, B, M)) {
-            static const cudaError_t attr2 = cudaFuncSetAttribute(
+            const cudaError_t attr2 = cudaFuncSetAttribute(
                 gram_dots_sym_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(gram_smem_bytes(32, true)));
             if (attr2 != cudaSuccess) return attr2;
             gram_dots_sym_kernel<<<PB, 256, gram_smem_bytes(R, true), s>>>(B, M, p.dim, R, part);

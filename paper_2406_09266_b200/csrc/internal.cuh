@@ -2,6 +2,7 @@
 // of libsystec (not part of the public ABI; see include/systec.h).
 #pragma once
 #include <cstdint>
+#include <mutex>
 #include <cuda_runtime.h>
 
 #include "../../include/systec.h"
@@ -23,8 +24,22 @@ struct Plan {
     bool general = false;      // non-symmetric tensor: tuples kept as given, naive kernel
     cudaStream_t stream = nullptr;
     systec_stats stats{};
-    // last launch (for reporting)
-    int last_grid_x = 0, last_grid_y = 0, last_block = 0, last_smem = 0, last_kernel = -1;
+    // last launch (for reporting).  Concurrent executes of one plan may run
+    // on several host threads: the record is written and read under a mutex,
+    // so a reader sees one whole launch (the most recent to finish recording).
+    struct LaunchInfo {
+        int grid_x = 0, grid_y = 0, block = 0, smem = 0, kernel = -1;
+    };
+    mutable std::mutex last_mu;
+    mutable LaunchInfo last;
+    void record_launch(const LaunchInfo &l) const {
+        std::lock_guard<std::mutex> g(last_mu);
+        last = l;
+    }
+    LaunchInfo last_launch() const {
+        std::lock_guard<std::mutex> g(last_mu);
+        return last;
+    }
 };
 
 // Device-side counters filled by the prepare kernels (all unsigned 64-bit).
@@ -103,7 +118,7 @@ cudaError_t launch_ttm(const Plan &p, const float *B, int R, float *Cp, cudaStre
 cudaError_t launch_ttm_unpack(int64_t dim, int R, const float *Cp, float *C, cudaStream_t s);
 
 // mttkrp.cu
-cudaError_t launch_mttkrp(Plan &p, const float *B, int R, float *C, const systec_exec_opts &o,
+cudaError_t launch_mttkrp(const Plan &p, const float *B, int R, float *C, const systec_exec_opts &o,
                           cudaStream_t s, float *scratch = nullptr);
 // floats of replica scratch launch_mttkrp needs for (plan, R, opts); 0 = none.
 // Passing that much as `scratch` makes the launch allocation-free (graph bodies).

@@ -150,7 +150,7 @@ __global__ void zero_output_kernel(float *__restrict__ C, int64_t plane, int vec
         C[i] = 0.f;
 }
 
-cudaError_t launch_mttkrp(Plan &p, const float *B, int R, float *C, const systec_exec_opts &o, cudaStream_t s,
+cudaError_t launch_mttkrp(const Plan &p, const float *B, int R, float *C, const systec_exec_opts &o, cudaStream_t s,
                           float *scratch_in) {
     cudaError_t e;
     const int64_t plane = p.dim * static_cast<int64_t>(R);
@@ -340,13 +340,15 @@ cudaError_t launch_mttkrp(Plan &p, const float *B, int R, float *C, const systec
         reduce_copies_kernel<8><<<rb, 256, 0, s>>>(scratch, C, plane, copies, vec, o.no_zero ? 1 : 0);
     }
     if (scratch && own_scratch) cudaFreeAsync(scratch, s);
-    p.last_grid_x = static_cast<int>(blocks);
-    p.last_grid_y = tiles;
-    p.last_block = threads;
-    p.last_smem = static_cast<int>(smem);
+    Plan::LaunchInfo li;
+    li.grid_x = static_cast<int>(blocks);
+    li.grid_y = tiles;
+    li.block = threads;
+    li.smem = static_cast<int>(smem);
     // kernel id, decimal fields: general | copies (2 digits) | pf + 2*dynamic | order | vw | lpe (2 digits) | vpl | pos1;
     // the occupancy variant sets vpl's digit to 5 (vpl itself is 1 there)
-    p.last_kernel = (p.general ? 1000000000 : 0) + copies * 10000000 + ((pf ? 1 : 0) + (kp.ctr ? 2 : 0) + (full ? 4 : 0)) * 1000000 + p.order * 100000 + vw * 10000 + lpe * 100 + (occ5 ? 5 : vpl) * 10 + (pos1 ? 1 : 0);
+    li.kernel = (p.general ? 1000000000 : 0) + copies * 10000000 + ((pf ? 1 : 0) + (kp.ctr ? 2 : 0) + (full ? 4 : 0)) * 1000000 + p.order * 100000 + vw * 10000 + lpe * 100 + (occ5 ? 5 : vpl) * 10 + (pos1 ? 1 : 0);
+    p.record_launch(li);
     return cudaGetLastError();
 }
 

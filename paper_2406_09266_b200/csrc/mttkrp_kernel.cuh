@@ -209,7 +209,6 @@ __device__ __forceinline__ void mttkrp_sym_body(const KParams &p) {
     // dynamic distribution: lane 0 walks units taken from the counter; a
     // stage whose descriptor base is -1 ends the warp's stream
     // (entry positions fit in int32: nnz < 2^31, include/systec.h)
-    const int nnz32 = static_cast<int>(p.nnz);
     const unsigned units = dyn ? static_cast<unsigned>((p.nnz + p.unit - 1) / p.unit) : 0u;
     unsigned du = 0;
     int dnext = 0, dend = 0;  // lane 0: current unit, next chunk base, unit end
@@ -218,7 +217,7 @@ __device__ __forceinline__ void mttkrp_sym_body(const KParams &p) {
     auto take_unit = [&]() {
         du = atomicAdd(p.ctr + (kFull ? 0 : blockIdx.y), 1u);  // one counter per rank tile
         dnext = static_cast<int>(min(static_cast<int64_t>(du) * p.unit, p.nnz));
-        dend = min(nnz32, dnext + p.unit);
+        dend = static_cast<int>(min(p.nnz, static_cast<int64_t>(dnext) + p.unit));  // int64: no overflow near 2^31
     };
     auto issue_dyn = [&](int64_t k) {
         const int s = static_cast<int>(k % S);

@@ -334,22 +334,31 @@ def mttkrp_host(order: int, dim: int, idx, vals, B, C=None, stream=None):
     """``systec_mttkrp_host`` on host arrays (numpy or pinned CPU tensors); returns C."""
     lib = load()
 
-    def host_ptr(a, dtype, name):
-        if hasattr(a, "data_ptr"):          # torch CPU tensor (possibly pinned)
+    import torch
+
+    def host_ptr(a, dtype, name, shape):
+        if hasattr(a, "data_ptr"):          # torch CPU tensor (possibly pinned): used in place, so it must
+            tdt = torch.int32 if dtype == np.int32 else torch.float32    # already be what the ABI reads
             if a.is_cuda or not a.is_contiguous():
                 raise TypeError(f"{name} must be a contiguous host tensor")
+            if a.dtype != tdt:
+                raise TypeError(f"{name} must be {tdt}, got {a.dtype}")
+            if tuple(a.shape) != shape:
+                raise TypeError(f"{name} must have shape {shape}, got {tuple(a.shape)}")
             return ctypes.c_void_p(a.data_ptr() if a.numel() else 0), a
         arr = np.ascontiguousarray(a, dtype=dtype)
+        if arr.size != int(np.prod(shape)):
+            raise ValueError(f"{name} must have shape {shape}, got {arr.shape}")
         return ctypes.c_void_p(arr.ctypes.data if arr.size else 0), arr
 
     nnz = int(vals.shape[0])
     R = int(B.shape[1])
     if C is None:
         C = np.empty((dim, R), np.float32)
-    ip, _i = host_ptr(idx, np.int32, "idx")
-    vp_, _v = host_ptr(vals, np.float32, "vals")
-    bp, _b = host_ptr(B, np.float32, "B")
-    cp, _c = host_ptr(C, np.float32, "C")
+    ip, _i = host_ptr(idx, np.int32, "idx", (nnz, order))
+    vp_, _v = host_ptr(vals, np.float32, "vals", (nnz,))
+    bp, _b = host_ptr(B, np.float32, "B", (dim, R))
+    cp, _c = host_ptr(C, np.float32, "C", (dim, R))
     if not hasattr(C, "data_ptr") and _c is not C:
         raise ValueError("C must be a contiguous float32 array")
     _check(lib.systec_mttkrp_host(order, dim, nnz, ip, vp_, bp, R, cp, _stream_handle(stream)),

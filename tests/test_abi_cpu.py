@@ -149,3 +149,24 @@ def test_ctypes_structs_match_the_c_header(tmp_path):
                    ("systec_plan_opts", SystecPlanOpts)):
         for f, _ in cls._fields_:
             assert got[(t, f)] == getattr(cls, f).offset, (t, f)
+
+
+def test_host_call_rejects_wrong_torch_dtypes_and_shapes(lib):
+    """Torch host tensors are passed to systec_mttkrp_host in place, so a
+    wrong dtype or shape must raise before the call."""
+    import torch
+
+    import paper_2406_09266_b200 as systec
+    idx = torch.zeros((5, 3), dtype=torch.int32)
+    vals = torch.zeros(5, dtype=torch.float32)
+    B = torch.zeros((10, 4), dtype=torch.float32)
+    with pytest.raises(TypeError):
+        systec.mttkrp_host(3, 10, idx.long(), vals, B)
+    with pytest.raises(TypeError):
+        systec.mttkrp_host(3, 10, idx, vals.double(), B)
+    with pytest.raises(TypeError):
+        systec.mttkrp_host(3, 10, idx, vals, B.double())
+    with pytest.raises(TypeError):
+        systec.mttkrp_host(3, 10, idx[:, :2].contiguous(), vals, B)
+    with pytest.raises(TypeError):
+        systec.mttkrp_host(3, 10, idx, vals, B, C=torch.zeros((10, 5)))

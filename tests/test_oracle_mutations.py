@@ -1,6 +1,7 @@
 """The pins catch plausible oracle mistakes: each deliberately broken variant
-of mttkrp_oracle.c (-DORACLE_MUTATION=k) must fail at least one pin that the
-real oracle passes.  CPU only."""
+of mttkrp_oracle.c must fail at least one pin that the real oracle passes.
+The variants are made here, by a textual patch of a temporary copy of the
+oracle source (the oracle itself carries no mutation hooks).  CPU only."""
 import itertools
 import os
 import subprocess
@@ -12,14 +13,24 @@ import oracle
 from synth import scramble, small_random
 from test_oracle_pins import dense_from_entries, dense_mttkrp, load_worked, rel_err
 
+# k: (what the bug is, the exact source text it replaces, its replacement)
 MUTATIONS = {
-    1: "tuple not sorted before the permutation walk",
-    2: "last factor of the product dropped",
-    3: "product indexes p[t-1] instead of p[t]",
-    4: "update lands on the last index instead of the first",
-    5: "sign flipped on the update",
-    6: "only the first permutation of each entry",
-    7: "off-diagonal permutations counted twice (a wrong multiplicity)",
+    1: ("tuple not sorted before the permutation walk",
+        "sort_small(p, n);                                   /* step 2 */", ""),
+    2: ("last factor of the product dropped",
+        "for (int t = 1; t < n; t++) {", "for (int t = 1; t < n - 1; t++) {"),
+    3: ("product indexes p[t-1] instead of p[t]",
+        "J->B + (int64_t)p[t] * R;", "J->B + (int64_t)p[t - 1] * R;"),
+    4: ("update lands on the last index instead of the first",
+        "double *c = J->C + out * R, *s = J->S + out * R;",
+        "out = J->rowslot ? out : p[n - 1] - J->row_lo;\n            double *c = J->C + out * R, *s = J->S + out * R;"),
+    5: ("sign flipped on the update",
+        "c[r] += J->term[r]; s[r] += fabs(J->term[r]);", "c[r] -= J->term[r]; s[r] += fabs(J->term[r]);"),
+    6: ("only the first permutation of each entry",
+        "} while (next_perm(p, n));\n    }\n    return NULL;", "} while (0);\n    }\n    return NULL;"),
+    7: ("off-diagonal permutations counted twice (a wrong multiplicity)",
+        "c[r] += J->term[r]; s[r] += fabs(J->term[r]);",
+        "c[r] += (p[0] == p[n - 1] ? 1.0 : 2.0) * J->term[r]; s[r] += fabs(J->term[r]);"),
 }
 
 
@@ -52,10 +63,18 @@ def pins_fail(lib, golden_dir):
 
 
 def build_variant(k, tmp):
-    src = os.path.join(os.path.dirname(oracle.__file__), "mttkrp_oracle.c")
+    """k = 0: the oracle source as committed; k >= 1: a patched copy."""
+    with open(os.path.join(os.path.dirname(oracle.__file__), "mttkrp_oracle.c")) as f:
+        text = f.read()
+    if k:
+        _, old, new = MUTATIONS[k]
+        assert text.count(old) == 1, f"mutation {k}: the patched text must occur exactly once"
+        text = text.replace(old, new)
+    src = os.path.join(tmp, f"oracle_m{k}.c")
+    with open(src, "w") as f:
+        f.write(text)
     out = os.path.join(tmp, f"liboracle_m{k}.so")
-    subprocess.check_call(["gcc", "-O2", "-std=c11", "-fPIC", "-shared", "-pthread", f"-DORACLE_MUTATION={k}",
-                           "-o", out, src, "-lm"])
+    subprocess.check_call(["gcc", "-O2", "-std=c11", "-fPIC", "-shared", "-pthread", "-o", out, src, "-lm"])
     return oracle.load_variant(out)
 
 
@@ -67,4 +86,4 @@ def test_real_oracle_passes_the_pin_subset(golden_dir, tmp_path):
 @pytest.mark.parametrize("k", sorted(MUTATIONS))
 def test_each_mutation_is_caught(k, golden_dir, tmp_path):
     failed = pins_fail(build_variant(k, str(tmp_path)), golden_dir)
-    assert failed, f"mutation {k} ({MUTATIONS[k]}) passed every pin"
+    assert failed, f"mutation {k} ({MUTATIONS[k][0]}) passed every pin"
