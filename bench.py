@@ -8,8 +8,9 @@ kernel over every stored non-zero of the config (inputs resident in HBM, the
 plan — canonicalised sorted stream — built once before timing, as the paper
 excludes rearrangement).  With N > 1 (torchrun) the sorted
 stream is split into N contiguous nnz-balanced slices, each rank computes a
-partial C, and C is summed with one NCCL all-reduce per step:
-strong scaling of one problem.
+partial C, and C is summed with one NCCL all-reduce per step — or, with
+``--collective reduce_scatter``, reduce-scattered into row blocks
+(SURVEY.md §8(e)): strong scaling of one problem.
 
 Prints ONE JSON line on rank 0.  See DESIGN.md §Measurement for every field.
 """
@@ -49,6 +50,14 @@ def parse():
     ap.add_argument("--dist-backend", default="nccl", help="collective backend for N>1 (gloo: code-path tests)")
     ap.add_argument("--same-device", action="store_true",
                     help="test mode: every rank on cuda:0 (with --dist-backend gloo; no kernel waits on another)")
+    ap.add_argument("--collective", default="all_reduce", choices=["all_reduce", "reduce_scatter"],
+                    help="N>1 exchange: whole C on every rank, or a row block of C per rank")
+    ap.add_argument("--no-bounds", action="store_true", help="skip the in-run L2/HBM bound measurement")
+    ap.add_argument("--no-ncu", action="store_true", help="skip the in-run ncu DRAM-traffic capture")
+    ap.add_argument("--paper-rule-s", type=float, default=3.0,
+                    help="the paper's timing rule (min over up to 10,000 runs or this many seconds, PAPER.md:740)")
+    ap.add_argument("--dump-c", default="",
+                    help="test mode: after timing, write the final C (rank 0; row blocks gathered) to this .npy")
     return ap.parse_args()
 
 
@@ -61,15 +70,75 @@ def load_peaks():
         return 6650.0, "fallback"
 
 
-def load_traffic(config):
-    """DRAM bytes per launch of the kernel from the committed ncu summary."""
-    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+def ncu_traffic(config, opts_str, timeout=240):
+    """DRAM traffic of one launch of the MTTKRP kernel, measured by ncu in a
+    child process of THIS bench run (same box, same build, same plan): the
+    physical HBM bytes behind the roofline.  Returns a dict, or the reason it
+    is unavailable."""
+    import shutil
+    import subprocess
+    ncu = shutil.which("ncu") or "/usr/local/cuda/bin/ncu"
+    if not os.path.exists(ncu):
+        return {"unavailable": "ncu not found"}
+    metrics = ["dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__time_duration.sum",
+               "l1tex__m_l1tex2xbar_req_cycles_active.avg.pct_of_peak_sustained_elapsed",
+               "lts__t_requests_srcunit_tex_op_red.sum", "lts__t_sector_hit_rate.pct"]
+    cmd = [ncu, "--metrics", ",".join(metrics), "--clock-control", "none", "--print-units", "base", "--csv",
+           "-k", "regex:mttkrp_sym", "-s", "2", "-c", "1",
+           sys.executable, os.path.join(ROOT, "tools", "profile_one.py"), "--config", config, "--iters", "3"]
+    if opts_str:
+        cmd += ["--opts", opts_str]
     try:
-        with open(path) as f:
-            d = json.load(f)
-        return d.get(config, {}).get("dram_bytes_per_launch")
-    except Exception:
-        return None
+        out = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout, cwd=ROOT)
+    except Exception as e:  # noqa: BLE001
+        return {"unavailable": f"ncu failed: {e!r}"[:200]}
+    import csv
+    import io
+    vals = {}
+    for row in csv.reader(io.StringIO("\n".join(l for l in out.stdout.splitlines() if l.startswith('"')))):
+        if len(row) > 3 and row[-3] in metrics:
+            try:
+                vals[row[-3]] = float(row[-1].replace(",", ""))
+            except ValueError:
+                pass
+    if "dram__bytes_read.sum" not in vals:
+        return {"unavailable": f"ncu rc={out.returncode}: " + (out.stderr or out.stdout)[-200:]}
+    return {"dram_bytes_per_launch": vals["dram__bytes_read.sum"] + vals.get("dram__bytes_write.sum", 0.0),
+            "dram_read_bytes": vals["dram__bytes_read.sum"], "dram_write_bytes": vals.get("dram__bytes_write.sum"),
+            "ncu_kernel_ms": vals.get("gpu__time_duration.sum", 0.0) / 1e6,
+            "sm_l2_port_pct": vals.get("l1tex__m_l1tex2xbar_req_cycles_active.avg.pct_of_peak_sustained_elapsed"),
+            "l2_red_requests": vals.get("lts__t_requests_srcunit_tex_op_red.sum"),
+            "l2_hit_rate_pct": vals.get("lts__t_sector_hit_rate.pct"),
+            "how": "ncu --metrics dram__bytes_{read,write}.sum --clock-control none -k regex:mttkrp_sym -s 2 -c 1 "
+                   "python tools/profile_one.py (cold L2: ncu flushes caches per replay), in this bench run"}
+
+
+def in_run_bounds(w, launch, dev_index=0):
+    """The three memory-system rates of this workload, measured on this GPU
+    right now (tools/bounds.cu): HBM stream read, random row gathers from a
+    table of B's footprint, red.global.add.v4.f32 of rows into a table of C's
+    footprint (x the replicas the launch used), rows of R*4 bytes."""
+    import ctypes
+    import __graft_entry__
+    lib = ctypes.CDLL(__graft_entry__.build_bounds())
+    for f in (lib.bounds_gather, lib.bounds_red):
+        f.argtypes = [ctypes.c_int, ctypes.c_int64, ctypes.c_int, ctypes.POINTER(ctypes.c_double)]
+    lib.bounds_hbm_read.argtypes = [ctypes.c_int64, ctypes.c_int, ctypes.POINTER(ctypes.c_double)]
+    row = w.R * 4
+    rb = min(512, 1 << max(4, (row - 1).bit_length()))   # the kernel's float4 row tile
+    hbm, gat, red = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
+    copies = max(1, launch.get("copies", 1))
+    with ClockSampler(dev_index, period=0.01) as clk:
+        rc = [lib.bounds_hbm_read(2 << 30, 5, ctypes.byref(hbm)),
+              lib.bounds_gather(rb, w.dim * rb, 5, ctypes.byref(gat)),
+              lib.bounds_red(rb, copies * w.dim * rb, 5, ctypes.byref(red))]
+    if any(rc):
+        return {"unavailable": f"bounds library returned {rc}"}
+    return {"hbm_read_gbs": hbm.value, "l2_gather_gbs": gat.value, "l2_red_gbs": red.value, "row_bytes": rb,
+            "gather_table_bytes": w.dim * rb, "red_table_bytes": copies * w.dim * rb,
+            "clocks": clk.report(),
+            "how": "tools/bounds.cu in this run: best of 5 launches each (148x8 blocks of 256 threads), "
+                   "2 GiB stream read; random whole-row float4 gathers / red.global.add.v4.f32"}
 
 
 class ClockSampler:
@@ -126,41 +195,54 @@ def bytes_eff(order, nnz, G, R, dim):
     return nnz * (4 * order + 4) + G * R * 4 + dim * R * 4
 
 
-def l2_model(w, st, nnz_local, kern_ms, launch):
-    """Lower bound from the measured L2 rates (profiles/r01_microbench.json):
-    t >= max(stream / HBM read, gathers / L2 gather rate, reds / L2 red rate),
-    with the rates of the row size (64-B rows for R = 16, 128-B rows
-    otherwise) and of the measured table size nearest the footprint (B for
-    the gathers; C and its replicas for the reductions)."""
-    import math
-    try:
-        with open(os.path.join(ROOT, "profiles", "r01_microbench.json")) as f:
-            mb = json.load(f)
-    except Exception:
-        return None
+def memory_terms(w, st, nnz_local, launch):
+    """Algorithmic bytes of each memory operation class of one launch
+    (SURVEY.md §8(d) per-entry figures x the entries of the launch):
+    the stream (indices + value, read once), the B-row gathers (one row per
+    distinct index of each entry, G rows) and the C-row reductions (one row
+    per run-first position >= 1 of each entry, G - nnz, less the position-1
+    runs accumulated in registers when the launch did that, plus one row per
+    leading-run fragment)."""
     n, R = w.order, w.R
     row = R * 4
-    kind = "64B" if row == 64 and "gather_64B_rows_gbs" in mb else "128B"
-
-    def nearest(table, mbytes):
-        key = min(table, key=lambda k: abs(math.log(float(k[:-2])) - math.log(max(mbytes, 1e-3))))
-        return table[key] * 1e9, key
-
-    hbm = mb["hbm_read_gbs"] * 1e9
-    gat, gkey = nearest(mb[f"gather_{kind}_rows_gbs"], w.dim * row / 1e6)
-    red, rkey = nearest(mb[f"red_v4_{kind}_rows_gbs"], max(1, launch.get("copies", 1)) * w.dim * row / 1e6)
-    stream = nnz_local * (4 * n + 4)
-    gathers = st["G"] * row
     n1 = sum(h for code, h in enumerate(st["pattern_hist"]) if not code & 1)   # entries with c1 != c0
     pos1 = launch.get("pos1", 0) == 1
     red_rows = st["lead_runs"] + (st["G"] - nnz_local) - ((n1 - min(n1, st["pos1_runs"])) if pos1 else 0)
-    reds = red_rows * row
-    t = max(stream / hbm, gathers / gat, reds / red)
-    return {"stream_bytes": stream, "gather_bytes": gathers, "red_payload_bytes": reds,
-            "hbm_read_gbs": hbm / 1e9, "l2_gather_gbs": gat / 1e9, "l2_red_gbs": red / 1e9,
-            "t_lower_ms": t * 1e3, "frac_of_l2_bound": t * 1e3 / kern_ms,
-            "source": f"profiles/r01_microbench.json (tools/microbench.cu): {kind} rows, gathers from a "
-                      f"{gkey} table, red.v4 into a {rkey} table"}
+    return {"stream": nnz_local * (4 * n + 4), "gather": st["G"] * row, "red": red_rows * row,
+            "red_rows": red_rows}
+
+
+def roofline(terms, bounds, kern_ms, local_bytes_eff, peak_hbm, traffic):
+    """The kernel against the bound of the unit that binds it.  Each memory
+    class alone at its measured rate gives a time; the largest is the bound.
+    achieved = that class's algorithmic bytes / kernel time, peak = its
+    measured rate, frac = achieved / peak (= t_bound / t_kernel)."""
+    t = kern_ms * 1e-3
+    eff = {"effective_gbs": local_bytes_eff / t / 1e9, "frac_of_measured_copy_peak": local_bytes_eff / t / 1e9 / peak_hbm,
+           "frac_of_8tbs": local_bytes_eff / t / 8e12, "algorithmic_bytes_per_launch": local_bytes_eff}
+    phys = None
+    if traffic and "dram_bytes_per_launch" in traffic:
+        phys = traffic["dram_bytes_per_launch"] / t / 1e9
+    if not bounds or "unavailable" in bounds:
+        return {"bound": "hbm", "achieved": eff["effective_gbs"], "peak": peak_hbm, "unit": "GB/s",
+                "frac": eff["effective_gbs"] / peak_hbm, "traffic": traffic.get("dram_bytes_per_launch") if traffic else None,
+                "note": "in-run bounds unavailable: effective bytes against the HBM copy peak", "hbm": eff}
+    rates = {"stream": bounds["hbm_read_gbs"], "gather": bounds["l2_gather_gbs"], "red": bounds["l2_red_gbs"]}
+    times = {k: terms[k] / (rates[k] * 1e9) for k in rates}
+    bind = max(times, key=times.get)
+    achieved = terms[bind] / t / 1e9
+    out = {"bound": "hbm" if bind == "stream" else "l2",
+           "binding_op": {"stream": "index/value stream read (HBM)",
+                          "gather": "random B-row gathers (L2)",
+                          "red": "red.global.add.v4.f32 of C rows (SM->L2 request/write port, L2 atomic units)"}[bind],
+           "achieved": achieved, "peak": rates[bind], "unit": "GB/s", "frac": achieved / rates[bind],
+           "traffic": traffic.get("dram_bytes_per_launch") if traffic else None,
+           "algorithmic_bytes_per_launch": terms[bind], "kernel_ms": kern_ms, "t_bound_ms": times[bind] * 1e3,
+           "terms_ms": {k: v * 1e3 for k, v in times.items()}, "terms_bytes": {k: terms[k] for k in rates},
+           "rates_gbs": rates, "peak_kind": "measured in this run on this GPU (tools/bounds.cu), clocks in bounds",
+           "bounds": bounds,
+           "hbm": dict(eff, physical_gbs=phys, physical_frac_of_copy_peak=(phys / peak_hbm) if phys else None)}
+    return out
 
 
 def cpu_baseline(w, target_wall=4.0, max_entries=None, threads=0):
@@ -244,7 +326,7 @@ def config_dict(w, args):
     return {"workload": f"{w.name}: {CONFIGS[w.name].describe}" if w.name in CONFIGS else w.name,
             "order": w.order, "dim": w.dim, "nnz": w.nnz, "R": w.R,
             "l2": "flushed between timed steps (256 MiB write outside the events)",
-            "parallelism": f"nnz-slices x{args.gpus} + all-reduce(C)" if args.gpus > 1 else "1 GPU"}
+            "parallelism": f"nnz-slices x{args.gpus} + {args.collective}(C)" if args.gpus > 1 else "1 GPU"}
 
 
 def parse_opts(s):
@@ -269,7 +351,7 @@ def main():
 
     import torch
     import paper_2406_09266_b200 as systec
-    from paper_2406_09266_b200.shard import reduce_partials, shard_range
+    from paper_2406_09266_b200.shard import ShardedMTTKRP, shard_range
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -292,22 +374,23 @@ def main():
     idx_d = torch.from_numpy(w.idx[lo:hi]).to(dev)
     vals_d = torch.from_numpy(w.vals[lo:hi]).to(dev)
     B_d = torch.from_numpy(w.B).to(dev)
-    C_d = torch.empty((w.dim, w.R), dtype=torch.float32, device=dev)
-    plan = systec.Plan(w.order, w.dim, idx_d, vals_d)
+    sh = ShardedMTTKRP(w.order, w.dim, idx_d, vals_d, w.R, collective=args.collective)
+    plan = sh.plan
     del idx_d, vals_d
     st = plan.stats()
     opts = parse_opts(args.opts)
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
 
     def step(ev=None):
-        # one pass of the hot path: zero C (+ replicas) + MTTKRP kernel (+ replica sum)
+        # one pass of the hot path: zero C (+ replicas) + MTTKRP kernel (+ replica sum),
+        # then (N > 1) the exchange of the partial C's
         if ev:
             ev[0].record(stream)
-        plan.execute(B_d, C_d, **opts)
+        sh.compute(B_d, **opts)
         if ev:
             ev[1].record(stream)
         if dist is not None:
-            reduce_partials(C_d)
+            sh.exchange()
         if ev:
             ev[2].record(stream)
 
@@ -315,6 +398,9 @@ def main():
         flush.fill_(1.0)
         step()
     torch.cuda.synchronize()
+    launch = plan.last_launch()
+    # the memory-system bounds of this workload, measured on this GPU before the timed region
+    bounds = None if args.no_bounds else in_run_bounds(w, launch, local)
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
     if dist is not None:
         dist.barrier()
@@ -343,44 +429,79 @@ def main():
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(20):
-        plan.execute(B_d, C_d, **opts)
+        sh.compute(B_d, **opts)
     e1.record(stream)
     torch.cuda.synchronize()
     warm_ms = e0.elapsed_time(e1) / 20
 
+    # the paper's timing rule: minimum over up to 10,000 runs or
+    # a time budget, each run L2-flushed and timed alone (kernel only, rank 0)
+    paper_rule = None
+    if rank == 0 and args.paper_rule_s > 0:
+        runs, best, t_start = 0, float("inf"), time.perf_counter()
+        while runs < 10_000 and time.perf_counter() - t_start < args.paper_rule_s:
+            batch = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(100)]
+            for a_, b_ in batch:
+                flush.fill_(0.5)
+                a_.record(stream)
+                sh.compute(B_d, **opts)
+                b_.record(stream)
+            torch.cuda.synchronize()
+            best = min(best, min(a_.elapsed_time(b_) for a_, b_ in batch))
+            runs += len(batch)
+        paper_rule = {"ms_min": best, "runs": runs, "rule": "min over up to 10,000 runs or the time budget "
+                      f"({args.paper_rule_s} s), L2 flushed before each run (PAPER.md:740)",
+                      "value_at_min": (hi - lo) / (best * 1e-3)}
+
+    # the final C of the step (test mode): rank 0 writes it to disk
+    if args.dump_c:
+        out = sh.execute(B_d, **opts)
+        if sh.collective == "reduce_scatter" and dist is not None:
+            per = sh.C_rows.shape[0]
+            full = torch.empty((per * world, w.R), dtype=torch.float32, device=dev)
+            if args.dist_backend == "gloo":
+                f_cpu = full.cpu()
+                dist.all_gather_into_tensor(f_cpu, sh.C_rows.cpu())
+                full.copy_(f_cpu)
+            else:
+                dist.all_gather_into_tensor(full, sh.C_rows)
+            out = full[: w.dim]
+        torch.cuda.synchronize()
+        if rank == 0:
+            np.save(args.dump_c, out.cpu().numpy())
+
     value = w.nnz / (ms_per_step * 1e-3)          # all ranks together process the whole tensor
-    # roofline of the dominant kernel (mttkrp_sym_kernel) on this rank's slice
     G_all = st["G"]
     if dist is not None:
         t = torch.tensor([G_all], device=dev, dtype=torch.float64)
         dist.all_reduce(t)
         G_all = int(t.item())
+    # roofline of the dominant kernel (mttkrp_sym_kernel) on this rank's slice
     local_bytes = bytes_eff(w.order, hi - lo, st["G"], w.R, w.dim)
-    achieved = local_bytes / (kern_avg_ms * 1e-3) / 1e9
     peak, peak_kind = load_peaks()
-    traffic = load_traffic(w.name) if world == 1 else None
+    traffic = ncu_traffic(w.name, args.opts) if (rank == 0 and world == 1 and not args.no_ncu) else None
 
     line = None
     if rank == 0:
-        launch = plan.last_launch()
+        terms = memory_terms(w, st, hi - lo, launch)
+        rl = roofline(terms, bounds, kern_avg_ms, local_bytes, peak, traffic)
+        rl.update(kernel="mttkrp_sym_kernel", kernel_ms=kern_avg_ms,
+                  kernel_ms_includes="C zeroing + kernel (+ replica sum when C < 4 MB), CUDA events on the launch stream",
+                  hbm_peak_kind=f"{peak_kind} copy bandwidth (MEASURED_PEAKS.json hbm_gbs = {peak})")
+        if traffic is not None:
+            rl["ncu"] = traffic
+        be = bytes_eff(w.order, w.nnz, G_all, w.R, w.dim)
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": config_dict(w, args),
-            "eff_gbs": bytes_eff(w.order, w.nnz, G_all, w.R, w.dim) / (ms_per_step * 1e-3) / 1e9,
-            "bytes_eff_per_step": bytes_eff(w.order, w.nnz, G_all, w.R, w.dim),
-            "frac_of_8tbs": bytes_eff(w.order, w.nnz, G_all, w.R, w.dim) / (ms_per_step * 1e-3) / 8e12,
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "mttkrp_sym_kernel", "kernel_ms": kern_avg_ms,
-                         "kernel_ms_includes": "C zeroing (memset) + kernel (+ replica sum when C < 4 MB)",
-                         "peak_kind": f"{peak_kind} copy bandwidth (MEASURED_PEAKS.json hbm_gbs)",
-                         "algorithmic_bytes_per_launch": local_bytes,
-                         "note": "B gathers and C reductions are served by L2 (B, C L2-resident): "
-                                 "bytes_eff/t can exceed the HBM copy peak; l2_model gives the "
-                                 "binding L2 bound"},
-            "l2_model": l2_model(w, st, hi - lo, kern_avg_ms, launch),
+            "eff_gbs": be / (ms_per_step * 1e-3) / 1e9, "bytes_eff_per_step": be,
+            "frac_of_8tbs": be / (ms_per_step * 1e-3) / 8e12,
+            "roofline": rl,
+            "timing": {"value": "whole-job nnz / mean step time over the K timed steps (driver contract)",
+                       "step_ms_min": float(np.min(step_ms)), "step_ms_median": float(np.median(step_ms)),
+                       "paper_rule": paper_rule},
             "warm_ms_per_step": warm_ms,
             "step_ms_min": float(np.min(step_ms)), "step_ms_median": float(np.median(step_ms)),
             # our kernels per execute: the MTTKRP kernel, + the replica sum (copies > 1; the
@@ -422,41 +543,44 @@ def main():
         pin_idx = torch.from_numpy(np.ascontiguousarray(w.idx[lo:hi])).pin_memory()
         pin_vals = torch.from_numpy(np.ascontiguousarray(w.vals[lo:hi])).pin_memory()
         pin_B = torch.from_numpy(w.B).pin_memory()
-        pin_C = torch.empty((w.dim, w.R), dtype=torch.float32).pin_memory()
+        rows = sh.C_rows.shape[0] if sh.collective == "reduce_scatter" else w.dim
+        pin_C = torch.empty((rows, w.R), dtype=torch.float32).pin_memory()
 
         def e2e_step():
             di = pin_idx.to(dev, non_blocking=True)
             dv = pin_vals.to(dev, non_blocking=True)
             dB = pin_B.to(dev, non_blocking=True)
-            pl = systec.Plan(w.order, w.dim, di, dv)
-            Cd = pl.execute(dB)
-            reduce_partials(Cd)
-            pin_C.copy_(Cd, non_blocking=True)
+            s2 = ShardedMTTKRP(w.order, w.dim, di, dv, w.R, collective=args.collective)
+            out = s2.execute(dB)
+            pin_C[: out.shape[0]].copy_(out, non_blocking=True)
             torch.cuda.synchronize()
-            pl.destroy()
+            s2.destroy()
 
         e2e_step()
         ts = []
         for _ in range(args.e2e_steps):
             dist.barrier()
             torch.cuda.synchronize()
-            t0 = time.perf_counter()
+            a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a_.record(stream)
             e2e_step()
-            ts.append(time.perf_counter() - t0)
+            b_.record(stream)
+            b_.synchronize()
+            ts.append(a_.elapsed_time(b_))
         t = torch.tensor([float(np.mean(ts))], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         if rank == 0:
-            e2e_ms = t.item() * 1e3
+            e2e_ms = t.item()
             line["e2e"] = {"value": w.nnz / (e2e_ms * 1e-3), "unit": UNIT,
                            "h2d_bytes_per_step": (w.idx.nbytes + w.vals.nbytes) + world * w.B.nbytes,
                            "d2h_bytes_per_step": world * pin_C.numel() * 4, "ms_per_step": e2e_ms,
-                           "includes": "per rank: H2D slice + plan creation + execute + all-reduce(C) + D2H; "
-                                       "max over ranks (host clock around synchronised steps)"}
+                           "includes": f"per rank: H2D slice + B, plan creation + execute + {args.collective}(C) "
+                                       "+ D2H of the rank's result; CUDA events, max over ranks"}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(w, threads=args.oracle_threads)
     if rank == 0:
         print(json.dumps(line), flush=True)
-    plan.destroy()
+    sh.destroy()
     if dist is not None:
         dist.destroy_process_group()
 

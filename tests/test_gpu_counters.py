@@ -1,0 +1,90 @@
+"""Counter tests (SPEC.md:587-588 analogue): ncu counts
+what the symmetric kernel does against the plan statistics and against the
+naive kernel over the expanded tensor (reads of A x 1/n!,
+computations x 1/(n-1)!).
+
+* reads of A: the stream's TMA bytes = nnz * (4n + 4) (one read per STORED
+  entry; 16-byte rounding of chunk tails aside); the naive kernel reads every
+  expanded entry, so on strict inputs the ratio is exactly 1/n!;
+* reductions: L2 red requests = one per reduced C row = the plan's
+  run-first positions >= 1 (G - nnz), less the position-1 runs accumulated in
+  registers, plus one per leading-run fragment (unit/chunk boundaries add a
+  few more);
+* floating-point work: the naive kernel executes at least (n-1)! times the
+  symmetric kernel's FP instructions.
+"""
+import csv
+import io
+import json
+import math
+import os
+import shutil
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+pytestmark = pytest.mark.gpu
+
+METRICS = ["l1tex__m_xbar2l1tex_read_bytes_mem_global_op_tma_ld.sum", "lts__t_requests_srcunit_tex_op_red.sum",
+           "sm__sass_thread_inst_executed_op_fmul_pred_on.sum", "sm__sass_thread_inst_executed_op_fadd_pred_on.sum",
+           "sm__sass_thread_inst_executed_op_ffma_pred_on.sum"]
+
+
+def ncu_counts(tool_args):
+    ncu = shutil.which("ncu") or "/usr/local/cuda/bin/ncu"
+    if not os.path.exists(ncu):
+        pytest.skip("ncu not available")
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    cmd = [ncu, "--metrics", ",".join(METRICS), "--clock-control", "none", "--print-units", "base", "--csv",
+           "-k", "regex:mttkrp_sym", sys.executable, os.path.join(ROOT, "tools", "counters_sym_vs_naive.py"),
+           *tool_args]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert out.returncode == 0, (out.stderr or out.stdout)[-2000:]
+    stats = json.loads([l for l in out.stdout.splitlines() if l.startswith("STATS ")][0][6:])
+    rows = list(csv.reader(io.StringIO("\n".join(l for l in out.stdout.splitlines() if l.startswith('"')))))
+    hdr = rows[0]
+    iid, iname, ival = hdr.index("ID"), hdr.index("Metric Name"), hdr.index("Metric Value")
+    per = {}
+    for r in rows[1:]:
+        if len(r) == len(hdr) and r[iname] in METRICS:
+            per.setdefault(int(r[iid]), {})[r[iname]] = float(r[ival].replace(",", ""))
+    launches = [per[k] for k in sorted(per)]
+    assert len(launches) == 2, f"expected the symmetric and the naive launch, got {len(launches)}"
+    return stats, launches[0], launches[1]
+
+
+def fp_ops(c):
+    return sum(c[m] for m in METRICS[2:])
+
+
+@pytest.mark.parametrize("case", ["c2", "4:60:300000:16", "5:40:300000:16"])
+def test_counters_match_plan_stats_and_paper_ratios(case):
+    args = ["--config", case] if case.startswith("c") else ["--make", case]
+    st, sym, naive = ncu_counts(args)
+    n, nnz, G = st["order"], st["nnz"], st["G"]
+    stride = 4 * n + 4
+    # reads of A: the stream once (chunk tails round up to 16 bytes: < 1 %)
+    reads = sym[METRICS[0]]
+    assert nnz * stride <= reads <= nnz * stride * 1.01, (reads, nnz * stride)
+    naive_reads = naive[METRICS[0]]
+    assert st["expanded"] * stride <= naive_reads <= st["expanded"] * stride * 1.01
+    if not case.startswith("c"):        # strict inputs: every orbit has n! members
+        assert st["expanded"] == nnz * math.factorial(n)
+        assert abs(naive_reads / reads - math.factorial(n)) / math.factorial(n) < 0.01
+    # reductions: the plan's reduced rows (one L2 red request per row)
+    hist = st["pattern_hist"]
+    n1 = sum(h for code, h in enumerate(hist) if not code & 1)
+    pos1 = st["launch"].get("pos1", 0) == 1
+    model = st["lead_runs"] + (G - nnz) - ((n1 - min(n1, st["pos1_runs"])) if pos1 else 0)
+    red = sym[METRICS[1]]
+    assert model <= red <= model + 2 * nnz / 128 + 1, (red, model)
+    # computations: the naive kernel's FP work is at least (n-1)! x the symmetric kernel's
+    ratio = fp_ops(naive) / fp_ops(sym)
+    assert ratio >= 0.9 * math.factorial(n - 1), ratio
+    print(f"{case}: reads {reads:.4g} B (= nnz*{stride}), naive/sym reads {naive_reads / reads:.2f} "
+          f"(n! = {math.factorial(n)}), red requests {red:.0f} vs model {model}, FP naive/sym {ratio:.2f} "
+          f"((n-1)! = {math.factorial(n - 1)})")
