@@ -67,14 +67,16 @@ def test_counters_match_plan_stats_and_paper_ratios(case):
     st, sym, naive = ncu_counts(args)
     n, nnz, G = st["order"], st["nnz"], st["G"]
     stride = 4 * n + 4
-    # reads of A: the stream once (chunk tails round up to 16 bytes: < 1 %)
+    # reads of A: the stream once.  The counter is in 32-byte sectors: a
+    # chunk's bulk copy (16-byte aligned, ~0.5 KB per array) touches one
+    # partial sector more on average (c2: 544 / 528 B = +3 %)
     reads = sym[METRICS[0]]
-    assert nnz * stride <= reads <= nnz * stride * 1.01, (reads, nnz * stride)
+    assert nnz * stride <= reads <= nnz * stride * 1.05, (reads, nnz * stride)
     naive_reads = naive[METRICS[0]]
-    assert st["expanded"] * stride <= naive_reads <= st["expanded"] * stride * 1.01
+    assert st["expanded"] * stride <= naive_reads <= st["expanded"] * stride * 1.05
     if not case.startswith("c"):        # strict inputs: every orbit has n! members
         assert st["expanded"] == nnz * math.factorial(n)
-        assert abs(naive_reads / reads - math.factorial(n)) / math.factorial(n) < 0.01
+        assert abs(naive_reads / reads - math.factorial(n)) / math.factorial(n) < 0.02
     # reductions: the plan's reduced rows (one L2 red request per row)
     hist = st["pattern_hist"]
     n1 = sum(h for code, h in enumerate(hist) if not code & 1)
