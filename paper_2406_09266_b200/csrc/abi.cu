@@ -466,6 +466,7 @@ cudaError_t cp_als_graph(Plan &p, float *B, int R, float *lambda, int max_iters,
         if ((e = cpd_tensor_norm2(p, x2, s)) != cudaSuccess) break;
         if ((e = cpd_state_init(st, x2, s)) != cudaSuccess) break;
         launched = true;
+        if ((e = cpd_init(p, B, R, ds, s)) != cudaSuccess) break;
         if ((e = launch_mttkrp(p, B, R, M, o, s, scr)) != cudaSuccess) break;
         if ((e = cpd_step(p, M, B, lambda, R, ds, fs, false, false, s)) != cudaSuccess) break;
         if ((e = cudaGraphLaunch(ge, s)) != cudaSuccess) break;
@@ -538,7 +539,8 @@ int systec_cp_als_sym(systec_plan plan, float *B, int R, float *lambda, int max_
         if ((e = cudaStreamSynchronize(s)) != cudaSuccess) break;
         const double xn = sqrt(x2 > 0 ? x2 : 1e-300);
         double prev_fit = -1e300;
-        double *scal = ds + R * R + 2 * R;
+        double *scal = ds + systec::cpd_xhat2_offset(R);
+        if ((e = systec::cpd_init(*p, B, R, ds, s)) != cudaSuccess) break;
         // iteration k: M = MTTKRP(X, B_k); the same pass yields fit(B_{k-1}-step iterate) pieces
         for (int it = 0; it <= max_iters; ++it) {
             systec_exec_opts o;

@@ -17,7 +17,21 @@
 //           ||X||^2   = sum_e v_e^2 * orbit_e   (each stored entry stands for its orbit),
 //           fit = 1 - sqrt(max(0, ||X||^2 - 2<X,Xhat> + ||Xhat||^2)) / ||X||.
 //
-// Every step runs in the kernels below (R <= 64; the small R x R algebra in
+// Dense passes per iteration (after the MTTKRP): TWO row passes over the
+// dim x R matrices, the normalisation folded into the R x R algebra.  Pass A
+// reads M and B once for G_M = M^T M and the column dots M o B; the Gram of
+// the current B, G_B = B^T B, is carried in fp64 from the previous iteration.
+// The small solve (one block, fp64) gives H^{-1}; then, since
+// B_new = M H^{-1} and H is symmetric,
+//     B_new^T B_new = H^{-1} G_M H^{-1}  =>  lambda_new = sqrt(diag(H^{-1} G_M H^{-1})),
+// so pass B writes the NORMALISED factor directly, B = M W with
+// W = H^{-1} diag(1/lambda_new), and the next G_B = diag(1/lambda) H^{-1} G_M
+// H^{-1} diag(1/lambda) needs no pass over B at all.  (Before: a Gram pass over
+// B, the apply pass, a column-norm reduction and a normalisation pass
+// reading and writing B again.)  The first iteration's G_B is one Gram pass
+// over the caller's B.
+//
+// Every step runs in the kernels below (R <= 48; the small R x R algebra in
 // one block, in fp64).
 #include <algorithm>
 #include <cmath>
@@ -419,7 +433,7 @@ __global__ void tensor_norm_kernel(const int32_t *__restrict__ coords, int64_t l
 // <X,Xhat> = lam . dots.
 template <int CW>
 __global__ void __launch_bounds__(1024) small_solve_kernel(const double *__restrict__ G, int R, int n,
-                                                           float *__restrict__ Hinv, const float *__restrict__ lam,
+                                                           double *__restrict__ Hinv, const float *__restrict__ lam,
                                                            const double *__restrict__ dots,
                                                            double *__restrict__ xhat2) {
     constexpr int TPR = CW == 1 ? 64 : CW == 2 ? 32 : 16;
@@ -504,22 +518,63 @@ __global__ void __launch_bounds__(1024) small_solve_kernel(const double *__restr
 #pragma unroll
     for (int u = 0; u < CW; ++u) {
         const int c = c0 + u;
-        if (own && c >= R && c < W2) Hinv[row * R + (c - R)] = static_cast<float>(A[u]);
+        if (own && c >= R && c < W2) Hinv[row * R + (c - R)] = A[u];
     }
 }
 
-// Bout = M Hinv and per-block column sums of squares of Bout (the norms of the
-// new factor) into part[blk][R].  RT = R rounded up to a multiple of 8: thread
-// (column b, row group) keeps Hinv[:, b] in registers and reads each staged M
-// row as 16-byte broadcasts.
+// The update's R x R algebra (one block, fp64), skipped on a fit-only
+// iteration: P = H^{-1} G_M H^{-1} (= B_new^T B_new for B_new = M H^{-1}),
+// lambda = sqrt(diag P), W = H^{-1} diag(1/lambda) (fp32, for the apply
+// pass), and the next iteration's G_B = diag(1/lambda) P diag(1/lambda).  A
+// zero column (lambda = 0) is left unscaled, as B_new's column is then 0.
+__global__ void __launch_bounds__(1024) scale_update_kernel(const double *__restrict__ Hinv,
+                                                            const double *__restrict__ GM, int R,
+                                                            double *__restrict__ GB, float *__restrict__ W,
+                                                            float *__restrict__ lam, const int *skip) {
+    if (skip && *skip) return;
+    __shared__ double T[kMaxCpR * kMaxCpR];
+    __shared__ double inv[kMaxCpR];
+    const int tid = threadIdx.x, nt = blockDim.x, RR = R * R;
+    for (int q = tid; q < RR; q += nt) {          // T = G_M H^{-1}
+        const int a = q / R, b = q % R;
+        double t = 0.0;
+        for (int c = 0; c < R; ++c) t = fma(GM[a * R + c], Hinv[c * R + b], t);
+        T[q] = t;
+    }
+    __syncthreads();
+    double Pq[3];                                  // P = H^{-1} T (H^{-1} symmetric); R*R <= 3 * 1024
+    for (int u = 0, q = tid; q < RR; ++u, q += nt) {
+        const int a = q / R, b = q % R;
+        double t = 0.0;
+        for (int c = 0; c < R; ++c) t = fma(Hinv[c * R + a], T[c * R + b], t);
+        Pq[u] = t;
+    }
+    __syncthreads();
+    for (int u = 0, q = tid; q < RR; ++u, q += nt) T[q] = Pq[u];
+    __syncthreads();
+    if (tid < R) {
+        const double l = sqrt(T[tid * R + tid] > 0.0 ? T[tid * R + tid] : 0.0);
+        inv[tid] = l > 0.0 ? 1.0 / l : 1.0;
+        lam[tid] = static_cast<float>(l);
+    }
+    __syncthreads();
+    for (int q = tid; q < RR; q += nt) {
+        const int a = q / R, b = q % R;
+        GB[q] = T[q] * inv[a] * inv[b];
+        W[q] = static_cast<float>(Hinv[q] * inv[b]);
+    }
+}
+
+// Bout = M W (W = H^{-1} diag(1/lambda): the normalised new factor).  RT = R
+// rounded up to a multiple of 8: thread (column b, row group) keeps W[:, b] in
+// registers and reads each staged M row as 16-byte broadcasts.
 template <int RT>
 __global__ void __launch_bounds__(256) apply_inverse_kernel(const float *__restrict__ M, const float *__restrict__ Hinv,
                                                             int64_t dim, int R, float *__restrict__ Bout,
-                                                            double *__restrict__ part, const int *skip, bool ring) {
+                                                            const int *skip, bool ring) {
     if (skip && *skip) return;  // device-side loop: last iteration evaluates the fit only
     extern __shared__ __align__(16) unsigned char cpd_smem[];  // ring: kRingS tiles of M (bulk copies)
     __shared__ __align__(16) float Msync[kTileRows * RT];      // else one synchronously staged tile
-    __shared__ double sq[256];
     const int tid = threadIdx.x;
     const int b = tid % RT, rg = tid / RT;
     constexpr int RGN = 256 / RT;
@@ -529,7 +584,6 @@ __global__ void __launch_bounds__(256) apply_inverse_kernel(const float *__restr
     for (int a = 0; a < RT; ++a) h[a] = (active && a < R) ? Hinv[a * R + b] : 0.f;
     const int64_t rows = (dim + gridDim.x - 1) / gridDim.x;
     const int64_t lo = blockIdx.x * rows, hi = min(dim, lo + rows);
-    double acc = 0.0;
     TileRing tr{reinterpret_cast<float *>(cpd_smem), reinterpret_cast<uint64_t *>(cpd_smem + ring_bytes(1, R) - kRingS * 8),
                 M, nullptr, 1, R, lo, hi};
     const int64_t nt = ring && lo < hi ? tr.ntiles() : 0;
@@ -557,7 +611,6 @@ __global__ void __launch_bounds__(256) apply_inverse_kernel(const float *__restr
             __syncthreads();
         }
         if (active) {
-            float t = 0.f;
             // pointer increments (no per-row 64-bit index arithmetic)
             float *o = Bout + (r0 + rg) * R + b;
             const float *mrow = Ms + rg * RT;
@@ -581,8 +634,6 @@ __global__ void __launch_bounds__(256) apply_inverse_kernel(const float *__restr
                 }
                 o[0] = s;
                 o[RGN * R] = u;
-                t = fmaf(s, s, t);
-                t = fmaf(u, u, t);
             }
             for (; mrow < mend; mrow += RGN * RT, o += RGN * R) {
                 const float4 *m4 = reinterpret_cast<const float4 *>(mrow);
@@ -596,60 +647,9 @@ __global__ void __launch_bounds__(256) apply_inverse_kernel(const float *__restr
                     s = fmaf(x.w, h[4 * a4 + 3], s);
                 }
                 *o = s;
-                t = fmaf(s, s, t);
             }
-            acc += t;
         }
         __syncthreads();  // tile k consumed: its slot may be refilled
-    }
-    sq[tid] = active ? acc : 0.0;
-    __syncthreads();
-    if (tid < R) {
-        double s2 = 0.0;
-        for (int g2 = 0; g2 < RGN; ++g2) s2 += sq[g2 * RT + tid];
-        part[static_cast<int64_t>(blockIdx.x) * R + tid] = s2;
-    }
-}
-
-// lam[b] = sqrt(norms[b]); B[i][b] /= lam[b] (fp32 division by the fp32 norm;
-// 16-byte accesses when R % 4 == 0)
-__global__ void normalize_kernel(float *__restrict__ B, int64_t dim, int R, const double *__restrict__ norms,
-                                 float *__restrict__ lam, const int *skip) {
-    if (skip && *skip) return;
-    __shared__ float nb[kMaxCpR];
-    for (int b = threadIdx.x; b < R; b += blockDim.x) {
-        nb[b] = static_cast<float>(sqrt(norms[b]));
-        if (blockIdx.x == 0) lam[b] = nb[b];
-    }
-    __syncthreads();
-    const int64_t total = dim * R;
-    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-    if ((R & 3) == 0) {
-        float4 *B4 = reinterpret_cast<float4 *>(B);
-        const int64_t n4 = total / 4;
-        auto scale = [&](float4 v, int64_t q) {
-            const int b = static_cast<int>((q * 4) % R);
-            if (nb[b + 0] > 0.f) v.x /= nb[b + 0];
-            if (nb[b + 1] > 0.f) v.y /= nb[b + 1];
-            if (nb[b + 2] > 0.f) v.z /= nb[b + 2];
-            if (nb[b + 3] > 0.f) v.w /= nb[b + 3];
-            return v;
-        };
-        // four independent float4 loads in flight per thread
-        int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-        for (; q + 3 * stride < n4; q += 4 * stride) {
-            float4 v[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) v[u] = B4[q + u * stride];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) B4[q + u * stride] = scale(v[u], q + u * stride);
-        }
-        for (; q < n4; q += stride) B4[q] = scale(B4[q], q);
-    } else {
-        for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total; q += stride) {
-            const int b = static_cast<int>(q % R);
-            if (nb[b] > 0.f) B[q] /= nb[b];
-        }
     }
 }
 
@@ -689,9 +689,93 @@ int sm_count() {
     return sms;
 }
 
+// partial blocks: >= 256 rows each, at most 2 per SM
+int cpd_partial_blocks() { return sm_count() * 2; }
+
+// the ring's dynamic shared-memory opt-in is per device: set before every
+// launch (a host-side attribute write), so a plan on any device gets it
+template <int RT>
+cudaError_t launch_apply_inverse(int PB, size_t rb, cudaStream_t s, const float *M, const float *W, int64_t dim,
+                                 int R, float *B, const int *skip, bool ring) {
+    const cudaError_t attr = cudaFuncSetAttribute(apply_inverse_kernel<RT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                  static_cast<int>(ring_bytes(1, 32)));
+    if (attr != cudaSuccess) return attr;
+    apply_inverse_kernel<RT><<<PB, 256, rb, s>>>(M, W, dim, R, B, skip, ring);
+    return cudaSuccess;
+}
+
+bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// ring form: R % 4 == 0 (contiguous 16-byte rows), R <= 32, 16-byte aligned bases
+bool gram_ring(int R, const float *B, const float *M) { return R % 4 == 0 && R <= 32 && aligned16(B) && aligned16(M); }
+
+size_t gram_smem_bytes(int R, bool ring) {
+    const size_t tiles = ring ? ring_bytes(2, R) : 2ull * kTileRows * kRp * sizeof(float);
+    const size_t redb = (static_cast<size_t>(kRp / 4) * (kRp / 4) * 16 + 256) * sizeof(double);  // row-group sums
+    return std::max(tiles, redb);  // ring at R = 32: 96 KB (opt-in dynamic shared-memory limit)
+}
+
+// scratch (doubles), in this order:
+//   GX[R*R], dots[R]   (contiguous: one reduction) — the pass-A Gram and dots
+//   GB[R*R]            the Gram of the current factor, carried across iterations
+//   H[R*R]             H^{-1} (fp64)
+//   xhat2[2]           {||Xhat||^2, <X,Xhat>}
+//   part[PB][R*R+R]    per-block partials
+// floats: W[R*R] (the apply pass's matrix)
+struct CpdScratch {
+    double *GX, *dots, *GB, *H, *xhat2, *part;
+};
+CpdScratch layout(double *ds, int R) {
+    CpdScratch c;
+    c.GX = ds;
+    c.dots = c.GX + R * R;
+    c.GB = c.dots + R;
+    c.H = c.GB + R * R;
+    c.xhat2 = c.H + R * R;
+    c.part = c.xhat2 + 2;
+    return c;
+}
+
+int partial_blocks(int64_t dim) {
+    return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(cpd_partial_blocks(), (dim + 31) / 32)));
+}
+
+// pass A: part = per-block {X^T X, column dots X o Y}; then GX, dots = their sums
+cudaError_t gram_dots(const float *X, const float *Y, int64_t dim, int R, const CpdScratch &c, cudaStream_t s) {
+    const int PB = partial_blocks(dim);
+    const int W = R * R + R;
+    // R <= 16: warp-shuffle form (c5 14.6 vs 25 us); wider R: the staged
+    // register-tile form (R = 32 via shuffles measured 55 vs 27 us: 152
+    // registers leave one block per SM)
+    if (R <= 8) gram_dots_warp_kernel<8><<<PB, 256, 0, s>>>(X, Y, dim, R, c.part);
+    else if (R <= 16) gram_dots_warp_kernel<16><<<PB, 256, 0, s>>>(X, Y, dim, R, c.part);
+    else {
+        const cudaError_t attr = cudaFuncSetAttribute(  // per device: set at every launch
+            gram_dots_partial_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            static_cast<int>(std::max(gram_smem_bytes(32, true), gram_smem_bytes(kMaxCpR, false))));
+        if (attr != cudaSuccess) return attr;
+        if (gram_ring(R, X, Y)) {
+            const cudaError_t attr2 = cudaFuncSetAttribute(
+                gram_dots_sym_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(gram_smem_bytes(32, true)));
+            if (attr2 != cudaSuccess) return attr2;
+            gram_dots_sym_kernel<<<PB, 256, gram_smem_bytes(R, true), s>>>(X, Y, dim, R, c.part);
+        } else {
+            gram_dots_partial_kernel<<<PB, 256, gram_smem_bytes(R, false), s>>>(X, Y, dim, R, c.part);
+        }
+    }
+    reduce_partials_kernel<<<(W + 7) / 8, 256, 0, s>>>(c.part, PB, W, c.GX, nullptr);  // GX and dots (contiguous)
+    return cudaGetLastError();
+}
+
 }  // namespace
 
 int cpd_max_rank() { return kMaxCpR; }
+
+int64_t cpd_scratch_doubles(int R) {
+    return 3ll * R * R + R + 2 + static_cast<int64_t>(cpd_partial_blocks()) * (R * R + R);
+}
+
+int64_t cpd_xhat2_offset(int R) { return 3ll * R * R + R; }
 
 cudaError_t cpd_tensor_norm2(const Plan &p, double *out, cudaStream_t s) {
     cudaError_t e = cudaMemsetAsync(out, 0, sizeof(double), s);
@@ -707,92 +791,46 @@ cudaError_t cpd_tensor_norm2(const Plan &p, double *out, cudaStream_t s) {
     return cudaGetLastError();
 }
 
-// partial blocks: >= 256 rows each, at most 2 per SM
-int cpd_partial_blocks() { return sm_count() * 2; }
-
-// the ring's dynamic shared-memory opt-in is per device: set before every
-// launch (a host-side attribute write), so a plan on any device gets it
-template <int RT>
-cudaError_t launch_apply_inverse(int PB, size_t rb, cudaStream_t s, const float *M, const float *Hinv, int64_t dim,
-                                 int R, float *B, double *part, const int *skip, bool ring) {
-    const cudaError_t attr = cudaFuncSetAttribute(apply_inverse_kernel<RT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                  static_cast<int>(ring_bytes(1, 32)));
-    if (attr != cudaSuccess) return attr;
-    apply_inverse_kernel<RT><<<PB, 256, rb, s>>>(M, Hinv, dim, R, B, part, skip, ring);
-    return cudaSuccess;
-}
-
-bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
-
-// ring form: R % 4 == 0 (contiguous 16-byte rows), R <= 32, 16-byte aligned bases
-bool gram_ring(int R, const float *B, const float *M) { return R % 4 == 0 && R <= 32 && aligned16(B) && aligned16(M); }
-
-size_t gram_smem_bytes(int R, bool ring) {
-    const size_t tiles = ring ? ring_bytes(2, R) : 2ull * kTileRows * kRp * sizeof(float);
-    const size_t redb = (static_cast<size_t>(kRp / 4) * (kRp / 4) * 16 + 256) * sizeof(double);  // row-group sums
-    return std::max(tiles, redb);  // ring at R = 32: 96 KB (opt-in dynamic shared-memory limit)
-}
-
-// scratch (doubles): G[R*R], dots[R] (contiguous: one reduction), norms[R],
-// scalars[2] = {||Xhat||^2, <X,Xhat>}, then partials[PB][R*R+R] | floats: Hinv[R*R]
-int64_t cpd_scratch_doubles(int R) {
-    return static_cast<int64_t>(R) * R + 2 * R + 2 + static_cast<int64_t>(cpd_partial_blocks()) * (R * R + R);
+cudaError_t cpd_init(const Plan &p, const float *B, int R, double *dscratch, cudaStream_t s) {
+    const CpdScratch c = layout(dscratch, R);
+    cudaError_t e = gram_dots(B, B, p.dim, R, c, s);  // G_B of the caller's factor (its dots unused)
+    if (e != cudaSuccess) return e;
+    return cudaMemcpyAsync(c.GB, c.GX, sizeof(double) * R * R, cudaMemcpyDeviceToDevice, s);
 }
 
 cudaError_t cpd_fit_pieces(const Plan &p, const float *M, const float *B, const float *lam, int R, double *dscratch,
                            float *fscratch, cudaStream_t s) {
-    double *G = dscratch, *dots = G + R * R, *norms = dots + R, *xhat2 = norms + R, *part = xhat2 + 2;
-    float *Hinv = fscratch;
-    const int PB = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(cpd_partial_blocks(), (p.dim + 31) / 32)));
-    const int W = R * R + R;
-    // R <= 16: warp-shuffle form (c5 14.6 vs 25 us); wider R: the staged
-    // register-tile form (R = 32 via shuffles measured 55 vs 27 us: 152
-    // registers leave one block per SM)
-    if (R <= 8) gram_dots_warp_kernel<8><<<PB, 256, 0, s>>>(B, M, p.dim, R, part);
-    else if (R <= 16) gram_dots_warp_kernel<16><<<PB, 256, 0, s>>>(B, M, p.dim, R, part);
-    else {
-        const cudaError_t attr = cudaFuncSetAttribute(  // per device: set at every launch
-            gram_dots_partial_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-            static_cast<int>(std::max(gram_smem_bytes(32, true), gram_smem_bytes(kMaxCpR, false))));
-        if (attr != cudaSuccess) return attr;
-        if (gram_ring(R, B, M)) {
-            const cudaError_t attr2 = cudaFuncSetAttribute(
-                gram_dots_sym_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(gram_smem_bytes(32, true)));
-            if (attr2 != cudaSuccess) return attr2;
-            gram_dots_sym_kernel<<<PB, 256, gram_smem_bytes(R, true), s>>>(B, M, p.dim, R, part);
-        } else {
-            gram_dots_partial_kernel<<<PB, 256, gram_smem_bytes(R, false), s>>>(B, M, p.dim, R, part);
-        }
-    }
-    reduce_partials_kernel<<<(W + 7) / 8, 256, 0, s>>>(part, PB, W, G, nullptr);  // G and dots (contiguous)
-    if (R <= 16) small_solve_kernel<1><<<1, 1024, 0, s>>>(G, R, p.order, Hinv, lam, dots, xhat2);
-    else if (R <= 32) small_solve_kernel<2><<<1, 1024, 0, s>>>(G, R, p.order, Hinv, lam, dots, xhat2);
-    else small_solve_kernel<6><<<1, 1024, 0, s>>>(G, R, p.order, Hinv, lam, dots, xhat2);
+    (void)fscratch;
+    const CpdScratch c = layout(dscratch, R);
+    cudaError_t e = gram_dots(M, B, p.dim, R, c, s);  // pass A: G_M = M^T M, dots = sum_i M o B
+    if (e != cudaSuccess) return e;
+    // H = G_B^{.(n-1)} -> H^{-1}; fit pieces of the current iterate from G_B, lam, dots
+    if (R <= 16) small_solve_kernel<1><<<1, 1024, 0, s>>>(c.GB, R, p.order, c.H, lam, c.dots, c.xhat2);
+    else if (R <= 32) small_solve_kernel<2><<<1, 1024, 0, s>>>(c.GB, R, p.order, c.H, lam, c.dots, c.xhat2);
+    else small_solve_kernel<6><<<1, 1024, 0, s>>>(c.GB, R, p.order, c.H, lam, c.dots, c.xhat2);
     return cudaGetLastError();
 }
 
 cudaError_t cpd_update(const Plan &p, const float *M, float *B, float *lam, int R, double *dscratch,
                        float *fscratch, const int *skip, cudaStream_t s) {
-    double *G = dscratch, *dots = G + R * R, *norms = dots + R, *xhat2 = norms + R, *part = xhat2 + 2;
-    float *Hinv = fscratch;
-    const int PB = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(cpd_partial_blocks(), (p.dim + 31) / 32)));
+    const CpdScratch c = layout(dscratch, R);
+    float *W = fscratch;
+    // lambda, W = H^{-1} diag(1/lambda), next G_B — then pass B: B = M W (normalised)
+    scale_update_kernel<<<1, 1024, 0, s>>>(c.H, c.GX, R, c.GB, W, lam, skip);
+    const int PB = partial_blocks(p.dim);
     // ring form for R in {8, 16, 24, 32} (rows of exactly RT floats), aligned M
     const bool ring = R % 8 == 0 && R <= 32 && aligned16(M);
     const size_t rb = ring ? ring_bytes(1, R) : 0;
     cudaError_t e;
     switch ((R + 7) / 8) {
-        case 1: e = launch_apply_inverse<8>(PB, rb, s, M, Hinv, p.dim, R, B, part, skip, ring); break;
-        case 2: e = launch_apply_inverse<16>(PB, rb, s, M, Hinv, p.dim, R, B, part, skip, ring); break;
-        case 3: e = launch_apply_inverse<24>(PB, rb, s, M, Hinv, p.dim, R, B, part, skip, ring); break;
-        case 4: e = launch_apply_inverse<32>(PB, rb, s, M, Hinv, p.dim, R, B, part, skip, ring); break;
-        case 5: e = launch_apply_inverse<40>(PB, rb, s, M, Hinv, p.dim, R, B, part, skip, ring); break;
-        default: e = launch_apply_inverse<48>(PB, rb, s, M, Hinv, p.dim, R, B, part, skip, ring); break;
+        case 1: e = launch_apply_inverse<8>(PB, rb, s, M, W, p.dim, R, B, skip, ring); break;
+        case 2: e = launch_apply_inverse<16>(PB, rb, s, M, W, p.dim, R, B, skip, ring); break;
+        case 3: e = launch_apply_inverse<24>(PB, rb, s, M, W, p.dim, R, B, skip, ring); break;
+        case 4: e = launch_apply_inverse<32>(PB, rb, s, M, W, p.dim, R, B, skip, ring); break;
+        case 5: e = launch_apply_inverse<40>(PB, rb, s, M, W, p.dim, R, B, skip, ring); break;
+        default: e = launch_apply_inverse<48>(PB, rb, s, M, W, p.dim, R, B, skip, ring); break;
     }
     if (e != cudaSuccess) return e;
-    reduce_partials_kernel<<<(R + 7) / 8, 256, 0, s>>>(part, PB, R, norms, skip);
-    const int64_t total = p.dim * R;
-    const int ab = static_cast<int>(std::min<int64_t>((total / 4 + 255) / 256 + 1, static_cast<int64_t>(sm_count()) * 8));
-    normalize_kernel<<<ab, 256, 0, s>>>(B, p.dim, R, norms, lam, skip);
     return cudaGetLastError();
 }
 
@@ -810,7 +848,7 @@ cudaError_t cpd_state_init(CpdLoopState *st, const double *x2, cudaStream_t s) {
 
 cudaError_t cpd_fit_check(const double *dscratch, int R, CpdLoopState *st, double *fits, double tol, int max_iters,
                           cudaGraphConditionalHandle h, cudaStream_t s) {
-    const double *xhat2 = dscratch + R * R + 2 * R;
+    const double *xhat2 = dscratch + cpd_xhat2_offset(R);
     cpd_fit_check_kernel<<<1, 1, 0, s>>>(xhat2, st, fits, tol, max_iters, h);
     return cudaGetLastError();
 }

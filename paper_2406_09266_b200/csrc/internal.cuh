@@ -92,7 +92,10 @@ cudaError_t launch_sssp_step(const int *changed, int *iters, int max_iters, cuda
 // cpd.cu
 int cpd_max_rank();
 int64_t cpd_scratch_doubles(int R);
+int64_t cpd_xhat2_offset(int R);  // doubles into the scratch: {||Xhat||^2, <X,Xhat>}
 cudaError_t cpd_tensor_norm2(const Plan &p, double *out, cudaStream_t s);
+// the Gram of the caller's factor, carried from then on in the scratch (before iteration 0)
+cudaError_t cpd_init(const Plan &p, const float *B, int R, double *dscratch, cudaStream_t s);
 cudaError_t cpd_step(const Plan &p, const float *M, float *B, float *lam, int R, double *dscratch,
                      float *fscratch, bool have_lam, bool fit_only, cudaStream_t s);
 // device-resident CP-ALS loop (one conditional-WHILE graph): state + pieces

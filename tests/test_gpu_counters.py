@@ -61,7 +61,10 @@ def fp_ops(c):
     return sum(c[m] for m in METRICS[2:])
 
 
-@pytest.mark.parametrize("case", ["c2", "4:60:300000:16", "5:40:300000:16"])
+# R = 32: one 128-byte line per reduced row, so one L2 request per row; the
+# dims keep rows reduced by two lane groups of one warp instruction (which
+# merge into one request) rare
+@pytest.mark.parametrize("case", ["c2", "4:4000:300000:32", "5:4000:300000:32"])
 def test_counters_match_plan_stats_and_paper_ratios(case):
     args = ["--config", case] if case.startswith("c") else ["--make", case]
     st, sym, naive = ncu_counts(args)
@@ -83,7 +86,7 @@ def test_counters_match_plan_stats_and_paper_ratios(case):
     pos1 = st["launch"].get("pos1", 0) == 1
     model = st["lead_runs"] + (G - nnz) - ((n1 - min(n1, st["pos1_runs"])) if pos1 else 0)
     red = sym[METRICS[1]]
-    assert model <= red <= model + 2 * nnz / 128 + 1, (red, model)
+    assert 0.99 * model <= red <= model + 2 * nnz / 128 + 1, (red, model)
     # computations: the naive kernel's FP work is at least (n-1)! x the symmetric kernel's
     ratio = fp_ops(naive) / fp_ops(sym)
     assert ratio >= 0.9 * math.factorial(n - 1), ratio
