@@ -140,6 +140,15 @@ SYSTEC_API int systec_mttkrp(int order, int64_t dim, int64_t nnz, const int32_t 
  * and B to the device, runs the path, copies C back and synchronises.
  * Host buffers may be pageable or pinned (pinned is faster).  Device scratch
  * comes from the stream-ordered pool and is returned before the call ends.
+ * The input is processed in chunks whose copies overlap the previous chunk's
+ * work; with page-locked C, rows no later chunk can touch are copied back
+ * early.  Errors: on SYSTEC_ERR_INDEX (an index outside [0, dim) in any
+ * chunk; systec_last_bad_entry() names the first one) C_host holds no valid
+ * result — rows copied back before the bad chunk was seen may already have
+ * been overwritten with partial sums, and the chunks were processed with
+ * the offending coordinates clamped — so treat all of C_host as garbage.
+ * On argument errors (SYSTEC_ERR_ARG / _UNSUPPORTED / _ALIAS) C_host is
+ * untouched.
  */
 SYSTEC_API int systec_mttkrp_host(int order, int64_t dim, int64_t nnz, const int32_t *idx_host,
                        const float *vals_host, const float *B_host, int R, float *C_host,

@@ -400,8 +400,9 @@ namespace {
 
 // CP-ALS with the whole iteration loop on the device: iteration 0 runs
 // eagerly, iterations 1..max_iters are the body of a conditional WHILE node of
-// one CUDA graph (MTTKRP -> fit pieces -> device convergence test -> factor
-// update), so there is no host round trip per iteration — one launch, one
+// one CUDA graph (MTTKRP -> fit pieces + R x R update -> apply pass -> device
+// convergence test, which also flags the next run as fit-only when it is the
+// last), so there is no host round trip per iteration — one launch, one
 // synchronisation at the end.  Returns cudaErrorNotSupported (nothing
 // launched) when the graph cannot be built; the caller then runs the host loop.
 cudaError_t cp_als_graph(Plan &p, float *B, int R, float *lambda, int max_iters, double tol, double *fit_host,
@@ -454,9 +455,9 @@ cudaError_t cp_als_graph(Plan &p, float *B, int R, float *lambda, int max_iters,
             cudaSuccess)
             break;
         cudaError_t ce = launch_mttkrp(p, B, R, M, o, cs, scr);
-        if (ce == cudaSuccess) ce = cpd_fit_pieces(p, M, B, lambda, R, ds, fs, cs);
+        if (ce == cudaSuccess) ce = cpd_fit_pieces(p, M, B, lambda, lambda, R, ds, fs, true, &st->skip_update, cs);
+        if (ce == cudaSuccess) ce = cpd_update(p, M, B, R, fs, &st->skip_update, cs);
         if (ce == cudaSuccess) ce = cpd_fit_check(ds, R, st, fits, tol, max_iters, h, cs);
-        if (ce == cudaSuccess) ce = cpd_update(p, M, B, lambda, R, ds, fs, &st->skip_update, cs);
         cudaGraph_t captured = nullptr;
         e = cudaStreamEndCapture(cs, &captured);
         if (ce != cudaSuccess) e = ce;
@@ -464,7 +465,7 @@ cudaError_t cp_als_graph(Plan &p, float *B, int R, float *lambda, int max_iters,
         if ((e = cudaGraphInstantiate(&ge, g, 0)) != cudaSuccess) break;
         // ||X||^2, iteration 0 (no fit yet), then the device-resident loop
         if ((e = cpd_tensor_norm2(p, x2, s)) != cudaSuccess) break;
-        if ((e = cpd_state_init(st, x2, s)) != cudaSuccess) break;
+        if ((e = cpd_state_init(st, x2, max_iters, s)) != cudaSuccess) break;
         launched = true;
         if ((e = cpd_init(p, B, R, ds, s)) != cudaSuccess) break;
         if ((e = launch_mttkrp(p, B, R, M, o, s, scr)) != cudaSuccess) break;

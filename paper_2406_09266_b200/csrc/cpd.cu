@@ -431,13 +431,26 @@ __global__ void tensor_norm_kernel(const int32_t *__restrict__ coords, int64_t l
 // the pivot column through shared memory (double-buffered: two barriers per
 // step).  With lam also the fit pieces ||Xhat||^2 = lam^T G^{.n} lam and
 // <X,Xhat> = lam . dots.
+//
+// Then, unless this is a fit-only iteration (update == 0, or *skip set by
+// the device loop), the update's R x R algebra in the same block:
+// P = H^{-1} G_M H^{-1} (= B_new^T B_new for B_new = M H^{-1}), lambda =
+// sqrt(diag P), W = H^{-1} diag(1/lambda) (fp32, for the apply pass) and the
+// next iteration's G = diag(1/lambda) P diag(1/lambda), written over G (read
+// only at the start).  A zero column (lambda = 0) is left unscaled, as
+// B_new's column is then 0.
 template <int CW>
-__global__ void __launch_bounds__(1024) small_solve_kernel(const double *__restrict__ G, int R, int n,
-                                                           double *__restrict__ Hinv, const float *__restrict__ lam,
+__global__ void __launch_bounds__(1024) small_solve_kernel(double *__restrict__ G, int R, int n,
+                                                           const float *__restrict__ lam,
                                                            const double *__restrict__ dots,
-                                                           double *__restrict__ xhat2) {
+                                                           double *__restrict__ xhat2, const double *__restrict__ GM,
+                                                           float *__restrict__ W, float *__restrict__ lam_out,
+                                                           int update, const int *skip) {
     constexpr int TPR = CW == 1 ? 64 : CW == 2 ? 32 : 16;
     __shared__ double piv[2][2 * kMaxCpR];
+    __shared__ double Hs[kMaxCpR * kMaxCpR];  // H^{-1}, then the update's products
+    __shared__ double Ts[kMaxCpR * kMaxCpR];
+    __shared__ double inv[kMaxCpR];
     __shared__ double fcol[2][kMaxCpR];
     __shared__ double red[1024];
     __shared__ double ridge_s;
@@ -515,53 +528,41 @@ __global__ void __launch_bounds__(1024) small_solve_kernel(const double *__restr
         }
         __syncthreads();  // buffers of step j free for step j + 2
     }
+    if (!update || (skip && *skip)) return;  // block-uniform
 #pragma unroll
     for (int u = 0; u < CW; ++u) {
         const int c = c0 + u;
-        if (own && c >= R && c < W2) Hinv[row * R + (c - R)] = A[u];
+        if (own && c >= R && c < W2) Hs[row * R + (c - R)] = A[u];
     }
-}
-
-// The update's R x R algebra (one block, fp64), skipped on a fit-only
-// iteration: P = H^{-1} G_M H^{-1} (= B_new^T B_new for B_new = M H^{-1}),
-// lambda = sqrt(diag P), W = H^{-1} diag(1/lambda) (fp32, for the apply
-// pass), and the next iteration's G_B = diag(1/lambda) P diag(1/lambda).  A
-// zero column (lambda = 0) is left unscaled, as B_new's column is then 0.
-__global__ void __launch_bounds__(1024) scale_update_kernel(const double *__restrict__ Hinv,
-                                                            const double *__restrict__ GM, int R,
-                                                            double *__restrict__ GB, float *__restrict__ W,
-                                                            float *__restrict__ lam, const int *skip) {
-    if (skip && *skip) return;
-    __shared__ double T[kMaxCpR * kMaxCpR];
-    __shared__ double inv[kMaxCpR];
-    const int tid = threadIdx.x, nt = blockDim.x, RR = R * R;
+    __syncthreads();
+    const int RR = R * R;
     for (int q = tid; q < RR; q += nt) {          // T = G_M H^{-1}
         const int a = q / R, b = q % R;
         double t = 0.0;
-        for (int c = 0; c < R; ++c) t = fma(GM[a * R + c], Hinv[c * R + b], t);
-        T[q] = t;
+        for (int c = 0; c < R; ++c) t = fma(GM[a * R + c], Hs[c * R + b], t);
+        Ts[q] = t;
     }
     __syncthreads();
     double Pq[3];                                  // P = H^{-1} T (H^{-1} symmetric); R*R <= 3 * 1024
     for (int u = 0, q = tid; q < RR; ++u, q += nt) {
         const int a = q / R, b = q % R;
         double t = 0.0;
-        for (int c = 0; c < R; ++c) t = fma(Hinv[c * R + a], T[c * R + b], t);
+        for (int c = 0; c < R; ++c) t = fma(Hs[c * R + a], Ts[c * R + b], t);
         Pq[u] = t;
     }
     __syncthreads();
-    for (int u = 0, q = tid; q < RR; ++u, q += nt) T[q] = Pq[u];
+    for (int u = 0, q = tid; q < RR; ++u, q += nt) Ts[q] = Pq[u];
     __syncthreads();
     if (tid < R) {
-        const double l = sqrt(T[tid * R + tid] > 0.0 ? T[tid * R + tid] : 0.0);
+        const double l = sqrt(Ts[tid * R + tid] > 0.0 ? Ts[tid * R + tid] : 0.0);
         inv[tid] = l > 0.0 ? 1.0 / l : 1.0;
-        lam[tid] = static_cast<float>(l);
+        lam_out[tid] = static_cast<float>(l);
     }
     __syncthreads();
     for (int q = tid; q < RR; q += nt) {
         const int a = q / R, b = q % R;
-        GB[q] = T[q] * inv[a] * inv[b];
-        W[q] = static_cast<float>(Hinv[q] * inv[b]);
+        G[q] = Ts[q] * inv[a] * inv[b];
+        W[q] = static_cast<float>(Hs[q] * inv[b]);
     }
 }
 
@@ -656,9 +657,10 @@ __global__ void __launch_bounds__(256) apply_inverse_kernel(const float *__restr
 // Device-side convergence test of the CP-ALS loop (one thread): the fit of
 // the current iterate from the pieces small_solve_kernel wrote, stored in
 // fits[it-1]; the loop continues (conditional WHILE node of the iteration
-// graph) unless this was the last iteration or |fit - previous| < tol; on the
-// last iteration the factor update that follows is skipped, as in the host
-// loop.
+// graph) unless this was the last iteration or |fit - previous| < tol.  The
+// body runs MTTKRP -> fit pieces + R x R update -> apply pass -> this test,
+// so the skip flag it sets is for the NEXT body run: the last iteration
+// evaluates the fit only, as in the host loop.
 __global__ void cpd_fit_check_kernel(const double *__restrict__ xhat2, CpdLoopState *st, double *__restrict__ fits,
                                      double tol, int max_iters, cudaGraphConditionalHandle handle) {
     const int it = ++st->it;
@@ -670,15 +672,15 @@ __global__ void cpd_fit_check_kernel(const double *__restrict__ xhat2, CpdLoopSt
     const bool last = it >= max_iters;
     const bool conv = fabs(fit - st->prev_fit) < tol;
     st->prev_fit = fit;
-    st->skip_update = last ? 1 : 0;
+    st->skip_update = (it + 1 >= max_iters) ? 1 : 0;
     cudaGraphSetConditional(handle, (last || conv) ? 0u : 1u);
 }
 
-__global__ void cpd_state_init_kernel(CpdLoopState *st, const double *x2) {
+__global__ void cpd_state_init_kernel(CpdLoopState *st, const double *x2, int max_iters) {
     st->x2 = *x2;
     st->prev_fit = -1e300;
     st->it = 0;
-    st->skip_update = 0;
+    st->skip_update = max_iters <= 1 ? 1 : 0;  // the first body run is iteration 1
     st->iters_done = 0;
 }
 
@@ -798,25 +800,23 @@ cudaError_t cpd_init(const Plan &p, const float *B, int R, double *dscratch, cud
     return cudaMemcpyAsync(c.GB, c.GX, sizeof(double) * R * R, cudaMemcpyDeviceToDevice, s);
 }
 
-cudaError_t cpd_fit_pieces(const Plan &p, const float *M, const float *B, const float *lam, int R, double *dscratch,
-                           float *fscratch, cudaStream_t s) {
-    (void)fscratch;
+cudaError_t cpd_fit_pieces(const Plan &p, const float *M, const float *B, const float *lam, float *lam_out, int R,
+                           double *dscratch, float *fscratch, bool update, const int *skip, cudaStream_t s) {
     const CpdScratch c = layout(dscratch, R);
     cudaError_t e = gram_dots(M, B, p.dim, R, c, s);  // pass A: G_M = M^T M, dots = sum_i M o B
     if (e != cudaSuccess) return e;
-    // H = G_B^{.(n-1)} -> H^{-1}; fit pieces of the current iterate from G_B, lam, dots
-    if (R <= 16) small_solve_kernel<1><<<1, 1024, 0, s>>>(c.GB, R, p.order, c.H, lam, c.dots, c.xhat2);
-    else if (R <= 32) small_solve_kernel<2><<<1, 1024, 0, s>>>(c.GB, R, p.order, c.H, lam, c.dots, c.xhat2);
-    else small_solve_kernel<6><<<1, 1024, 0, s>>>(c.GB, R, p.order, c.H, lam, c.dots, c.xhat2);
+    // H = G_B^{.(n-1)} -> H^{-1}; fit pieces of the current iterate from G_B, lam, dots;
+    // then (update) lambda_new, W = H^{-1} diag(1/lambda_new) and the next G_B
+    const int up = update ? 1 : 0;
+    if (R <= 16) small_solve_kernel<1><<<1, 1024, 0, s>>>(c.GB, R, p.order, lam, c.dots, c.xhat2, c.GX, fscratch, lam_out, up, skip);
+    else if (R <= 32) small_solve_kernel<2><<<1, 1024, 0, s>>>(c.GB, R, p.order, lam, c.dots, c.xhat2, c.GX, fscratch, lam_out, up, skip);
+    else small_solve_kernel<6><<<1, 1024, 0, s>>>(c.GB, R, p.order, lam, c.dots, c.xhat2, c.GX, fscratch, lam_out, up, skip);
     return cudaGetLastError();
 }
 
-cudaError_t cpd_update(const Plan &p, const float *M, float *B, float *lam, int R, double *dscratch,
-                       float *fscratch, const int *skip, cudaStream_t s) {
-    const CpdScratch c = layout(dscratch, R);
-    float *W = fscratch;
-    // lambda, W = H^{-1} diag(1/lambda), next G_B — then pass B: B = M W (normalised)
-    scale_update_kernel<<<1, 1024, 0, s>>>(c.H, c.GX, R, c.GB, W, lam, skip);
+cudaError_t cpd_update(const Plan &p, const float *M, float *B, int R, float *fscratch, const int *skip,
+                       cudaStream_t s) {
+    const float *W = fscratch;  // written by the solve: pass B, B = M W (normalised)
     const int PB = partial_blocks(p.dim);
     // ring form for R in {8, 16, 24, 32} (rows of exactly RT floats), aligned M
     const bool ring = R % 8 == 0 && R <= 32 && aligned16(M);
@@ -836,13 +836,13 @@ cudaError_t cpd_update(const Plan &p, const float *M, float *B, float *lam, int 
 
 cudaError_t cpd_step(const Plan &p, const float *M, float *B, float *lam, int R, double *dscratch,
                      float *fscratch, bool have_lam, bool fit_only, cudaStream_t s) {
-    cudaError_t e = cpd_fit_pieces(p, M, B, have_lam ? lam : nullptr, R, dscratch, fscratch, s);
+    cudaError_t e = cpd_fit_pieces(p, M, B, have_lam ? lam : nullptr, lam, R, dscratch, fscratch, !fit_only, nullptr, s);
     if (e != cudaSuccess || fit_only) return e;
-    return cpd_update(p, M, B, lam, R, dscratch, fscratch, nullptr, s);
+    return cpd_update(p, M, B, R, fscratch, nullptr, s);
 }
 
-cudaError_t cpd_state_init(CpdLoopState *st, const double *x2, cudaStream_t s) {
-    cpd_state_init_kernel<<<1, 1, 0, s>>>(st, x2);
+cudaError_t cpd_state_init(CpdLoopState *st, const double *x2, int max_iters, cudaStream_t s) {
+    cpd_state_init_kernel<<<1, 1, 0, s>>>(st, x2, max_iters);
     return cudaGetLastError();
 }
 

@@ -107,11 +107,14 @@ struct CpdLoopState {
     int iters_done;
     int pad;
 };
-cudaError_t cpd_fit_pieces(const Plan &p, const float *M, const float *B, const float *lam, int R, double *dscratch,
-                           float *fscratch, cudaStream_t s);
-cudaError_t cpd_update(const Plan &p, const float *M, float *B, float *lam, int R, double *dscratch,
-                       float *fscratch, const int *skip, cudaStream_t s);
-cudaError_t cpd_state_init(CpdLoopState *st, const double *x2, cudaStream_t s);
+// fit pieces of the current iterate (pass A + the small solve); with update
+// (and *skip == 0) also lambda_new -> lam_out, W -> fscratch, next G_B
+cudaError_t cpd_fit_pieces(const Plan &p, const float *M, const float *B, const float *lam, float *lam_out, int R,
+                           double *dscratch, float *fscratch, bool update, const int *skip, cudaStream_t s);
+// pass B: B = M W (skipped when *skip)
+cudaError_t cpd_update(const Plan &p, const float *M, float *B, int R, float *fscratch, const int *skip,
+                       cudaStream_t s);
+cudaError_t cpd_state_init(CpdLoopState *st, const double *x2, int max_iters, cudaStream_t s);
 cudaError_t cpd_fit_check(const double *dscratch, int R, CpdLoopState *st, double *fits, double tol, int max_iters,
                           cudaGraphConditionalHandle h, cudaStream_t s);
 

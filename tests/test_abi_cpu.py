@@ -114,7 +114,7 @@ def test_header_is_plain_c_and_example_builds(lib):
         pytest.skip("gcc not available")
     out = os.path.join(tempfile.mkdtemp(), "mttkrp_c")
     subprocess.check_call(["gcc", "-std=c11", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"),
-                           os.path.join(ROOT, "examples", "mttkrp_c.c"), "-o", out,
+                           "-I", "/usr/local/cuda/include", os.path.join(ROOT, "examples", "mttkrp_c.c"), "-o", out,
                            "-L", os.path.join(ROOT, "paper_2406_09266_b200"), "-lsystec",
                            "-L", "/usr/local/cuda/lib64", "-lcudart",
                            "-Wl,-rpath," + os.path.join(ROOT, "paper_2406_09266_b200")])

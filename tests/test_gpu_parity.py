@@ -822,13 +822,13 @@ def test_plain_c_example_runs(systec, tmp_path):
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     exe = str(tmp_path / "mttkrp_c")
     subprocess.check_call(["gcc", "-std=c11", "-I", os.path.join(root, "include"),
-                           os.path.join(root, "examples", "mttkrp_c.c"), "-o", exe,
+                           "-I", "/usr/local/cuda/include", os.path.join(root, "examples", "mttkrp_c.c"), "-o", exe,
                            "-L", os.path.join(root, "paper_2406_09266_b200"), "-lsystec",
                            "-L", "/usr/local/cuda/lib64", "-lcudart",
                            "-Wl,-rpath," + os.path.join(root, "paper_2406_09266_b200")])
     out = subprocess.run([exe], capture_output=True, text=True, timeout=120)
     assert out.returncode == 0, out.stderr
-    assert out.stdout.startswith("ok")
+    assert out.stdout.startswith("ok") and "device plan" in out.stdout
 
 
 @pytest.mark.parametrize("R", [32, 16, 3])
