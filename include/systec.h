@@ -99,7 +99,7 @@ typedef struct systec_exec_opts {
     int32_t static_ranges;       /* 1 = one static nnz-balanced range per warp; 0 = dynamic units */
                                  /* of ~4 chunks taken from a per-launch counter (default)       */
     int32_t occupancy;           /* order-3 R=32 kernel built for 5 blocks/SM: 1 on, -1 off,    */
-                                 /* 0 auto (on when B > 64 MB)                                  */
+                                 /* 0 auto (on when B > 64 MB and the plan is lexicographic)   */
     int32_t fixed_rank;          /* kernels built for R = 16 / 32 exactly (one float4 tile):    */
                                  /* 0 auto (on when R matches), -1 off                          */
     int32_t reserved[1];

@@ -242,12 +242,17 @@ cudaError_t launch_mttkrp(const Plan &p, const float *B, int R, float *C, const 
     const bool pf = o.prefetch > 0;
     KernelFn fn = p.general ? pick_naive(p.order, vw, lpe, pf) : pick(p.order, vw, lpe, vpl, pos1, pf);
     // occupancy variant: 5 resident blocks (48 registers) for the order-3 R=32
-    // kernel when B is too large to stay L2-resident, so gathers wait on DRAM
-    // and more warps in flight pay (c3: 2.65 -> 2.40 ms; c2 with its 12.8 MB
-    // B is L2-resident and loses 2 %).  opts.occupancy: 1 on, -1 off, 0 auto.
+    // kernel when B is too large to stay L2-resident and the stream is
+    // lexicographic, so gathers wait on DRAM and more warps in flight pay
+    // (c3 lexicographic: 2.65 -> 2.40 ms; c2 with its 12.8 MB B is
+    // L2-resident and loses 2 %).  A banded plan (c3's default) keeps its
+    // gathers in an L2 window and the 64-register fixed-rank kernel is faster
+    // there (c3: 1.67-1.72 vs 1.73-1.76 ms, profiles/r02_c3_occupancy.jsonl).
+    // opts.occupancy: 1 on, -1 off, 0 auto.
     const bool occ_shape = vw == 4 && vpl == 1 && !pf && !p.general &&
                            ((p.order == 3 && lpe == 8) || (p.order >= 4 && lpe == 4));
-    const bool occ5 = occ_shape && (o.occupancy > 0 || (o.occupancy == 0 && p.order == 3 && plane * 4 > (64ll << 20)));
+    const bool occ5 = occ_shape && (o.occupancy > 0 || (o.occupancy == 0 && p.order == 3 && p.band_shift < 0 &&
+                                                         plane * 4 > (64ll << 20)));
     if (occ5) fn = p.order == 3 ? occupancy3(pos1) : p.order == 4 ? occupancy4(pos1) : occupancy5(pos1);
     // fixed-rank build when R is exactly one float4 tile of 16 or 32 columns
     // (opts.fixed_rank: 0 auto = on, -1 off)
