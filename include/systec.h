@@ -78,6 +78,9 @@ typedef struct systec_stats {
     int32_t band_shift;          /* -1: stream in lexicographic order; s >= 0: grouped by band */
                                  /* c_{n-1} >> s, lexicographic within a band (plan options)   */
     int64_t bad_entry;           /* first entry with an index outside [0,dim), else -1         */
+    int64_t bandwidth;           /* order 2: max (c_1 - c_0) over entries; else 0              */
+    int64_t window_blocks;       /* order 2: row blocks of the atomic-free windowed kernel     */
+                                 /* (0 = the plan runs the general kernel; see execute opts)   */
 } systec_stats;
 
 /* Kernel tuning options for systec_plan_execute_ex; zero fields = defaults. */
@@ -102,7 +105,10 @@ typedef struct systec_exec_opts {
                                  /* 0 auto (on when B > 64 MB and the plan is lexicographic)   */
     int32_t fixed_rank;          /* kernels built for R = 16 / 32 exactly (one float4 tile):    */
                                  /* 0 auto (on when R matches), -1 off                          */
-    int32_t reserved[1];
+    int32_t window;              /* order-2 plans: the atomic-free windowed kernel (each row    */
+                                 /* block builds its rows' transposed entries in shared memory */
+                                 /* and writes every output row once): 0 auto (on when the     */
+                                 /* plan has row blocks, stats.window_blocks > 0), -1 off      */
 } systec_exec_opts;
 
 typedef struct systec_plan_s *systec_plan;

@@ -15,7 +15,7 @@
 #include "internal.cuh"
 
 static_assert(sizeof(systec_exec_opts) == 64, "systec_exec_opts layout is part of the ABI");
-static_assert(sizeof(systec_stats) == 208, "systec_stats layout is part of the ABI");
+static_assert(sizeof(systec_stats) == 224, "systec_stats layout is part of the ABI");
 static_assert(sizeof(systec_plan_opts) == 32, "systec_plan_opts layout is part of the ABI");
 
 namespace systec {
@@ -162,6 +162,13 @@ int apply_bands(Plan *p, int shift, bool pooled, cudaStream_t s) {
     return SYSTEC_OK;
 }
 
+void free_window(Plan *p, bool pooled, cudaStream_t s) {
+    if (!p->win_rowptr) return;
+    if (pooled) cudaFreeAsync(p->win_rowptr, s); else cudaFree(p->win_rowptr);
+    p->win_rowptr = p->win_colptr = nullptr;
+    p->win_capp = 0;
+}
+
 // Builds the plan.  `pooled` plans keep their storage in the stream-ordered pool.
 int plan_create_impl(Plan **out, int order, int64_t dim, int64_t nnz, const int32_t *idx, const float *vals,
                      cudaStream_t s, bool pooled, bool general = false, int band_request = 0) {
@@ -204,6 +211,7 @@ int plan_create_impl(Plan **out, int order, int64_t dim, int64_t nnz, const int3
     };
     auto fail = [&](cudaError_t err) {
         cleanup();
+        free_window(p, pooled, s);
         if (pooled) cudaFreeAsync(p->storage, s); else cudaFree(p->storage);
         delete p;
         return cuda_fail(err);
@@ -243,12 +251,33 @@ int plan_create_impl(Plan **out, int order, int64_t dim, int64_t nnz, const int3
         return fail(e);
     if ((e = launch_stats(order, nnz, p->ld, p->coords, -1, dst, s)) != cudaSuccess) return fail(e);
     if ((e = cudaMemcpyAsync(&hst, dst, sizeof(hst), cudaMemcpyDeviceToHost, s)) != cudaSuccess) return fail(e);
+    // order-2 symmetric plans: the windowed kernel's row / column pointers and
+    // bandwidth, read back with the statistics (sym2_window.cu)
+    unsigned long long win_host[2] = {0, 0};  // {bandwidth, largest column count}
+    int32_t win_items = 0;
+    if (order == 2 && !general) {
+        const size_t wb = static_cast<size_t>(dim + 1) * 8 + 16;
+        void *w = nullptr;
+        if ((e = pooled ? cudaMallocAsync(&w, wb, s) : cudaMalloc(&w, wb)) != cudaSuccess) return fail(e);
+        p->win_rowptr = static_cast<int32_t *>(w);
+        p->win_colptr = p->win_rowptr + (dim + 1);
+        auto *wv = reinterpret_cast<unsigned long long *>(p->win_colptr + (dim + 1));
+        if ((e = win_build(*p, p->win_rowptr, p->win_colptr, wv, wv + 1, s)) != cudaSuccess) return fail(e);
+        if ((e = cudaMemcpyAsync(win_host, wv, 16, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return fail(e);
+        if ((e = cudaMemcpyAsync(&win_items, p->win_colptr + dim, 4, cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+            return fail(e);
+    }
     cleanup();
     dst = nullptr; keys = nullptr; keys2 = nullptr; perm = nullptr; perm2 = nullptr;
     if ((e = cudaStreamSynchronize(s)) != cudaSuccess) {  // sync 2: statistics
+        free_window(p, pooled, s);
         if (pooled) cudaFreeAsync(p->storage, s); else cudaFree(p->storage);
         delete p;
         return cuda_fail(e);
+    }
+    if (p->win_rowptr) {
+        p->win_bw = static_cast<int64_t>(win_host[0]);
+        p->win_capp = win_partition(dim, win_items, p->win_bw, static_cast<int64_t>(win_host[1]), &p->win_nblk);
     }
     systec_stats &st = p->stats;
     st.nnz = nnz;
@@ -262,10 +291,14 @@ int plan_create_impl(Plan **out, int order, int64_t dim, int64_t nnz, const int3
     // banded stream order (a second device sort of the prepared stream)
     const int shift = choose_band_shift(band_request, order, dim, bits, nnz, st.lead_runs, general);
     if (shift >= 0 && (rc = apply_bands(p, shift, pooled, s)) != SYSTEC_OK) {
+        free_window(p, pooled, s);
         if (pooled) cudaFreeAsync(p->storage, s); else cudaFree(p->storage);
         delete p;
         return rc;
     }
+    if (shift >= 0) p->win_capp = 0;  // the windowed kernel needs the row-sorted stream
+    st.bandwidth = p->win_rowptr ? p->win_bw : 0;
+    st.window_blocks = p->win_capp > 0 ? p->win_nblk : 0;
     *out = p;
     return SYSTEC_OK;
 }
@@ -287,6 +320,7 @@ int execute_impl(Plan *p, const float *B, int R, float *C, const systec_exec_opt
 
 void destroy_impl(Plan *p) {
     if (!p) return;
+    free_window(p, p->pooled, p->stream);
     if (p->pooled) cudaFreeAsync(p->storage, p->stream);
     else cudaFree(p->storage);
     delete p;

@@ -24,6 +24,12 @@ struct Plan {
     bool general = false;      // non-symmetric tensor: tuples kept as given, naive kernel
     cudaStream_t stream = nullptr;
     systec_stats stats{};
+    // order-2 windowed kernel (sym2_window.cu): row pointer and the upper
+    // triangle's column pointer, [dim + 1] each, in one allocation
+    int32_t *win_rowptr = nullptr, *win_colptr = nullptr;
+    int64_t win_bw = 0;
+    int win_capp = 0;          // partition step; 0 = no windowed path
+    int win_nblk = 0;
     // last launch (for reporting).  Concurrent executes of one plan may run
     // on several host threads: the record is written and read under a mutex,
     // so a reader sees one whole launch (the most recent to finish recording).
@@ -122,6 +128,13 @@ cudaError_t cpd_fit_check(const double *dscratch, int R, CpdLoopState *st, doubl
 int64_t ttm_packed_rows(int64_t dim);
 cudaError_t launch_ttm(const Plan &p, const float *B, int R, float *Cp, cudaStream_t s);
 cudaError_t launch_ttm_unpack(int64_t dim, int R, const float *Cp, float *C, cudaStream_t s);
+
+// sym2_window.cu
+cudaError_t win_build(const Plan &p, int32_t *rowptr, int32_t *colptr, unsigned long long *bw_dev,
+                      unsigned long long *maxcol_dev, cudaStream_t s);
+int win_partition(int64_t dim, int64_t items, int64_t bw, int64_t maxcol, int *nblk);
+// cudaErrorNotSupported: the plan has no windowed path for this R / layout (nothing launched)
+cudaError_t launch_sym2_window(const Plan &p, const float *B, int R, float *C, bool accumulate, cudaStream_t s);
 
 // mttkrp.cu
 cudaError_t launch_mttkrp(const Plan &p, const float *B, int R, float *C, const systec_exec_opts &o,

@@ -153,6 +153,12 @@ __global__ void zero_output_kernel(float *__restrict__ C, int64_t plane, int vec
 cudaError_t launch_mttkrp(const Plan &p, const float *B, int R, float *C, const systec_exec_opts &o, cudaStream_t s,
                           float *scratch_in) {
     cudaError_t e;
+    // order 2: the atomic-free windowed kernel writes every row of C once (no zeroing pass)
+    if (p.order == 2 && !p.general && o.window >= 0 && p.win_capp > 0 && o.ablation <= 0 && !o.force_scalar) {
+        e = launch_sym2_window(p, B, R, C, o.no_zero != 0, s);
+        if (e != cudaErrorNotSupported) return e;
+        cudaGetLastError();
+    }
     const int64_t plane = p.dim * static_cast<int64_t>(R);
     const int copies = replica_count(p, R, o);
     if (copies > 64) return cudaErrorInvalidValue;

@@ -24,7 +24,7 @@ class SystecStats(ctypes.Structure):
                 ("pattern_hist", ctypes.c_int64 * 16), ("lead_runs", ctypes.c_int64),
                 ("max_lead_run", ctypes.c_int64), ("pos1_runs", ctypes.c_int64),
                 ("input_was_sorted", ctypes.c_int32), ("band_shift", ctypes.c_int32),
-                ("bad_entry", ctypes.c_int64)]
+                ("bad_entry", ctypes.c_int64), ("bandwidth", ctypes.c_int64), ("window_blocks", ctypes.c_int64)]
 
 
 class SystecExecOpts(ctypes.Structure):
@@ -34,7 +34,7 @@ class SystecExecOpts(ctypes.Structure):
                 ("chunk_k", ctypes.c_int32), ("stages", ctypes.c_int32), ("vpl", ctypes.c_int32),
                 ("prefetch", ctypes.c_int32), ("copies", ctypes.c_int32), ("ablation", ctypes.c_int32),
                 ("static_ranges", ctypes.c_int32), ("occupancy", ctypes.c_int32), ("fixed_rank", ctypes.c_int32),
-                ("reserved", ctypes.c_int32 * 1)]
+                ("window", ctypes.c_int32)]
 
 
 class SystecPlanOpts(ctypes.Structure):

@@ -199,9 +199,21 @@ def _forced(rng, order, dim, total, bits):
     return np.concatenate(out, axis=0) if out else np.zeros((0, order), np.int64)
 
 
+def _banded_draw(rng, dim, band):
+    """Order 2: pairs (i, i + d), i uniform, d uniform in [0, band] (rows near
+    the diagonal only, the profile of FEM / structural matrices)."""
+    def draw(m):
+        i = rng.integers(0, dim, size=m, dtype=np.int64)
+        j = i + rng.integers(0, band + 1, size=m, dtype=np.int64)
+        ok = j < dim
+        return np.stack([i[ok], j[ok]], axis=1)
+    return draw
+
+
 def make(name: str, order: int, dim: int, nnz: int, R: int, seed: int,
-         mode: str = "strict", n_forced: int = 0, zipf_s: float = 1.1) -> Workload:
-    """Draw one workload (see module docstring)."""
+         mode: str = "strict", n_forced: int = 0, zipf_s: float = 1.1, band: int = 0) -> Workload:
+    """Draw one workload (see module docstring).  mode "banded" (order 2 only):
+    entries (i, j) with 0 <= j - i <= band."""
     if order < 1 or dim < 1 or nnz < 0 or R < 1:
         raise ValueError("bad workload shape")
     if nnz > math.comb(dim + order - 1, order):
@@ -214,6 +226,10 @@ def make(name: str, order: int, dim: int, nnz: int, R: int, seed: int,
         c = _distinct_first(_uniform_draw(rng, order, dim), nnz, bits, batch=int(nnz * 1.05) + 64)
     elif mode == "zipf":
         c = _distinct_first(_zipf_draw(rng, order, dim, zipf_s), nnz, bits, batch=int(nnz * 1.6) + 64)
+    elif mode == "banded":
+        if order != 2 or band < 0 or nnz > dim * (band + 1):
+            raise ValueError("banded: order 2 and nnz <= dim * (band + 1)")
+        c = _distinct_first(_banded_draw(rng, dim, band), nnz, bits, batch=int(nnz * 1.3) + 64)
     elif mode == "strict":
         n_strict = nnz - n_forced
         parts = []
@@ -232,7 +248,7 @@ def make(name: str, order: int, dim: int, nnz: int, R: int, seed: int,
     vals = rng.uniform(-1.0, 1.0, nnz).astype(np.float32)
     B = rng.uniform(-1.0, 1.0, (dim, R)).astype(np.float32)
     return Workload(name, order, dim, R, c, vals, B,
-                    meta={"seed": seed, "mode": mode, "n_forced": n_forced, "gen": GEN_VERSION})
+                    meta={"seed": seed, "mode": mode, "n_forced": n_forced, "band": band, "gen": GEN_VERSION})
 
 
 def _cache_dir() -> str:

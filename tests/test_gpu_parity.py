@@ -898,3 +898,76 @@ def test_execute_argument_errors(systec):
     torch.cuda.synchronize()
     Cref, S = oracle.mttkrp(3, 50, w.idx, w.vals, w.B)
     parity(C.cpu().numpy(), Cref, S)
+
+
+# ---------------------------------------------------------------- NEXT-3: order-2 windowed (atomic-free) kernel
+@pytest.mark.parametrize("R", [1, 3, 4, 8, 16, 32, 64, 128])
+def test_order2_window_kernel_parity(systec, R):
+    """Banded symmetric matrices take the windowed order-2 kernel (column
+    lists in shared memory, one plain store per row): parity with the oracle
+    at every lane geometry, equal (up to rounding) to the general kernel,
+    accumulate mode, and the integer-valued case bit-exact."""
+    import torch
+    w = make(f"b{R}", 2, 20000, 300000, R, seed=R, mode="banded", band=60)
+    Cref, S = oracle.mttkrp(2, w.dim, w.idx, w.vals, w.B)
+    di, dv, dB = to_dev(w.idx, w.vals, w.B)
+    plan = systec.Plan(2, w.dim, di, dv)
+    st = plan.stats()
+    assert st["bandwidth"] == int((w.idx[:, 1] - w.idx[:, 0]).max()) and st["window_blocks"] > 0
+    C = plan.execute(dB)
+    assert plan.last_launch()["kernel_id"] >= 2_000_000_000      # the windowed kernel ran
+    parity(C.cpu().numpy(), Cref, S)
+    parity(plan.execute(dB, window=-1).cpu().numpy(), Cref, S)     # the general kernel
+    assert plan.last_launch()["kernel_id"] < 2_000_000_000
+    C2 = torch.ones_like(C)                                         # no_zero: C += result
+    plan.execute(dB, C2, no_zero=1)
+    parity(C2.cpu().numpy() - 1.0, Cref, S, tol=1e-4 + 1e-6)
+    wi = integer_workload(w, seed=R)
+    Ci, _ = oracle.mttkrp(2, w.dim, wi.idx, wi.vals, wi.B)
+    pi = systec.Plan(2, w.dim, *to_dev(wi.idx, wi.vals))
+    assert np.array_equal(pi.execute(to_dev(wi.B)[0]).cpu().numpy().astype(np.float64), Ci)
+    plan.destroy()
+    pi.destroy()
+
+
+def test_order2_window_edges(systec):
+    """Empty rows between blocks, nnz = 0 (every row written 0 without a
+    zeroing pass), a hub column (lists too long: general kernel), a wide
+    band (halo too large: general kernel), and a banded plan order."""
+    import torch
+    dim = 3000
+    # rows 1000..1999 empty, diagonal-only rows elsewhere plus a narrow band
+    w = make("edge", 2, dim, 8000, 8, seed=9, mode="banded", band=5)
+    keep = (w.idx[:, 0] < 1000) | (w.idx[:, 0] >= 2000)
+    idx, vals = w.idx[keep], w.vals[keep]
+    Cref, S = oracle.mttkrp(2, dim, idx, vals, w.B)
+    plan = systec.Plan(2, dim, *to_dev(idx, vals))
+    assert plan.stats()["window_blocks"] > 0
+    dB = to_dev(w.B)[0]
+    C = torch.full((dim, 8), 7.0, device="cuda")
+    plan.execute(dB, C)
+    assert plan.last_launch()["kernel_id"] >= 2_000_000_000
+    parity(C.cpu().numpy(), Cref, S)
+    plan.destroy()
+    empty = systec.Plan(2, dim, *to_dev(np.zeros((0, 2), np.int32), np.zeros(0, np.float32)))
+    C = torch.full((dim, 8), 7.0, device="cuda")
+    empty.execute(dB, C)
+    assert float(C.abs().max()) == 0.0
+    empty.destroy()
+    # a hub column: column 2999 holds an entry from every row
+    hub = np.stack([np.arange(dim), np.full(dim, dim - 1)], axis=1).astype(np.int32)
+    hv = np.random.default_rng(1).uniform(-1, 1, dim).astype(np.float32)
+    hp = systec.Plan(2, dim, *to_dev(hub, hv))
+    assert hp.stats()["window_blocks"] == 0
+    Cref, S = oracle.mttkrp(2, dim, hub, hv, w.B)
+    parity(hp.execute(dB).cpu().numpy(), Cref, S)
+    hp.destroy()
+    u = make("wide", 2, 100000, 200000, 8, seed=2, mode="uniform")
+    up = systec.Plan(2, u.dim, *to_dev(u.idx, u.vals))
+    assert up.stats()["window_blocks"] == 0
+    up.destroy()
+    bp = systec.Plan(2, w.dim, *to_dev(w.idx, w.vals), band_shift=4)
+    assert bp.stats()["window_blocks"] == 0
+    Cref, S = oracle.mttkrp(2, dim, w.idx, w.vals, w.B)
+    parity(bp.execute(dB).cpu().numpy(), Cref, S)
+    bp.destroy()

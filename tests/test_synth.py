@@ -79,3 +79,18 @@ def test_config_table_matches_baseline():
     assert [CONFIGS[k].nnz for k in ("c1", "c2", "c3", "c4", "c5")] == [2000, 10**7, 5 * 10**7, 2 * 10**7, 10**7]
     assert [CONFIGS[k].R for k in ("c1", "c2", "c3", "c4", "c5")] == [8, 32, 32, 16, 16]
     assert run_lengths(5, 0b1010) == [1, 2, 2]
+
+
+def test_banded_order2_generator():
+    """mode "banded" (order-2 stand-in for the paper's FEM-like SSYMV matrices):
+    canonical, sorted, distinct, within the band, deterministic."""
+    import numpy as np
+
+    from synth.workloads import make
+    w = make("b", 2, 5000, 60000, 4, seed=3, mode="banded", band=40)
+    w2 = make("b", 2, 5000, 60000, 4, seed=3, mode="banded", band=40)
+    assert np.array_equal(w.idx, w2.idx) and np.array_equal(w.vals, w2.vals)
+    d = w.idx[:, 1] - w.idx[:, 0]
+    assert d.min() >= 0 and d.max() <= 40
+    keys = w.idx[:, 0].astype(np.int64) * 5000 + w.idx[:, 1]
+    assert np.all(np.diff(keys) > 0)          # sorted and distinct

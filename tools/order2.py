@@ -37,13 +37,17 @@ def main():
     ap.add_argument("--nnz", type=int, default=10_000_000)
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--variants", default="", help="';'-separated option sets to also time for R=1")
+    ap.add_argument("--mode", default="uniform", help="uniform | banded (FEM-like profile, --band)")
+    ap.add_argument("--band", type=int, default=64)
+    ap.add_argument("--ranks", default="1,32")
+    ap.add_argument("--no-sssp", action="store_true")
     a = ap.parse_args()
     import numpy as np
     import torch
 
     import paper_2406_09266_b200 as systec
     from synth.workloads import make
-    w = make("sym2", 2, a.dim, a.nnz, 1, seed=11, mode="uniform")
+    w = make("sym2", 2, a.dim, a.nnz, 1, seed=11, mode=a.mode, band=a.band)
     rng = np.random.default_rng(12)
     flush = torch.empty(64 << 20, device="cuda")
     di, dv = torch.from_numpy(w.idx).cuda(), torch.from_numpy(w.vals).cuda()
@@ -51,16 +55,21 @@ def main():
     ei, ev = systec.expand_symmetric(2, a.dim, di, dv)
     gen = systec.plan_create_general(2, a.dim, ei, ev)
     m = int(ev.shape[0])
-    for R in (1, 32):
+    for R in (int(r) for r in a.ranks.split(",")):
         B = torch.from_numpy(rng.uniform(-1, 1, (a.dim, R)).astype(np.float32)).cuda()
         C1 = torch.empty((a.dim, R), device="cuda")
         C2 = torch.empty((a.dim, R), device="cuda")
-        t_sym = timed(lambda: sym.execute(B, C1), a.reps, flush)
+        t_atomic = timed(lambda: sym.execute(B, C1, window=-1), a.reps, flush)   # general kernel: one red per entry
+        t_sym = timed(lambda: sym.execute(B, C1), a.reps, flush)                  # auto: windowed when available
+        launch = sym.last_launch()
         t_gen = timed(lambda: gen.execute(B, C2), a.reps, flush)
         rel = float(((C1 - C2).abs().max() / C1.abs().max()).item())
         st = sym.stats()
         eff = (a.nnz * 12 + st["G"] * R * 4 + a.dim * R * 4) / (t_sym * 1e-3) / 1e9
-        print(json.dumps({"kernel": "SSYMV" if R == 1 else f"SSYMM R={R}", "dim": a.dim, "stored_nnz": a.nnz,
+        print(json.dumps({"kernel": "SSYMV" if R == 1 else f"SSYMM R={R}", "matrix": a.mode,
+                          "band": a.band if a.mode == "banded" else None, "dim": a.dim, "stored_nnz": a.nnz,
+                          "bandwidth": st["bandwidth"], "window_blocks": st["window_blocks"],
+                          "windowed": launch["kernel_id"] >= 2_000_000_000, "t_sym_atomic_ms": t_atomic,
                           "expanded_nnz": m, "t_sym_ms": t_sym, "t_naive_ms": t_gen, "speedup": t_gen / t_sym,
                           "gnnz_s": a.nnz / t_sym / 1e6, "eff_gbs": eff, "paper_ssymv_speedup_vs_naive_finch": 1.45,
                           "max_rel_diff": rel}), flush=True)
@@ -73,6 +82,8 @@ def main():
             t2 = timed(lambda: gen.execute(B, C1, **o), a.reps, flush)
             print(json.dumps({"kernel": "SSYMV", "opts": o, "t_sym_ms": t1, "t_naive_ms": t2,
                               "launch": sym.last_launch()}), flush=True)
+    if a.no_sssp:
+        return
     # Bellman-Ford to convergence (device-graph loop vs host loop); positive
     # weights (the uniform(-1, 1) values above would hold negative cycles)
     sp = systec.Plan(2, a.dim, di, (dv.abs() + 0.1).contiguous())
