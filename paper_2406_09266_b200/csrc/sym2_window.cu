@@ -144,13 +144,24 @@ __global__ void __launch_bounds__(256) sym2_window_kernel(const WinParams p) {
     __syncthreads();
     // 1. column lists of the block's rows from the stream segment of rows [r0 - bw, r1)
     const int h0 = p.rowptr[max(0, r0 - p.bw)], h1 = p.rowptr[r1];
-    for (int e = h0 + tid; e < h1; e += nt) {
-        const int j = p.c1[e];
-        if (j >= r0 && j < r1) {
-            const int i = p.c0[e];
-            if (i != j) {
+    // (four entries per thread per step: their loads are independent)
+    for (int e0 = h0 + tid; e0 < h1; e0 += 4 * nt) {
+        int jj[4], ii[4];
+        float vv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int e = e0 + u * nt;
+            const bool in = e < h1;
+            jj[u] = in ? __ldg(p.c1 + e) : -1;
+            ii[u] = in ? __ldg(p.c0 + e) : -1;
+            vv[u] = in ? __ldg(p.vals + e) : 0.f;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int j = jj[u];
+            if (j >= r0 && j < r1 && ii[u] != j) {
                 const int slot = cp[j - r0] + atomicAdd(&cur[j - r0], 1);
-                items[slot] = make_int2(i, __float_as_int(p.vals[e]));
+                items[slot] = make_int2(ii[u], __float_as_int(vv[u]));
             }
         }
     }
@@ -163,17 +174,40 @@ __global__ void __launch_bounds__(256) sym2_window_kernel(const WinParams p) {
     const int R = p.R;
     for (int qq = (tid >> 5) * E + g; qq < n; qq += (nt >> 5) * E) {
         const int q = r0 + qq;
-        T acc = V::zero();
+        // four independent accumulators, four entries' loads in flight (a row
+        // is a short dependent chain of index load -> row gather otherwise)
+        T a0 = V::zero(), a1 = V::zero(), a2 = V::zero(), a3 = V::zero();
+        const float *Bc = p.B + colo;
+        int e = p.rowptr[q];
         const int e1 = p.rowptr[q + 1];
-        for (int e = p.rowptr[q]; e < e1; ++e) {        // the row part: the stored entries of row q
-            const int j = __ldg(p.c1 + e);
-            const float v = __ldg(p.vals + e);
-            acc = V::fma(v, V::load(p.B + static_cast<int64_t>(j) * R + colo), acc);
+        for (; e + 4 <= e1; e += 4) {                    // the row part: the stored entries of row q
+            const int j0 = __ldg(p.c1 + e), j1 = __ldg(p.c1 + e + 1), j2 = __ldg(p.c1 + e + 2), j3 = __ldg(p.c1 + e + 3);
+            const float v0 = __ldg(p.vals + e), v1 = __ldg(p.vals + e + 1), v2 = __ldg(p.vals + e + 2),
+                        v3 = __ldg(p.vals + e + 3);
+            const T b0 = V::load(Bc + static_cast<int64_t>(j0) * R), b1 = V::load(Bc + static_cast<int64_t>(j1) * R);
+            const T b2 = V::load(Bc + static_cast<int64_t>(j2) * R), b3 = V::load(Bc + static_cast<int64_t>(j3) * R);
+            a0 = V::fma(v0, b0, a0);
+            a1 = V::fma(v1, b1, a1);
+            a2 = V::fma(v2, b2, a2);
+            a3 = V::fma(v3, b3, a3);
         }
-        for (int t = cp[qq], t1 = cp[qq + 1]; t < t1; ++t) {  // the transposed part: entries (i, q), i < q
+        for (; e < e1; ++e) a0 = V::fma(__ldg(p.vals + e), V::load(Bc + static_cast<int64_t>(__ldg(p.c1 + e)) * R), a0);
+        int t = cp[qq];
+        const int t1 = cp[qq + 1];
+        for (; t + 4 <= t1; t += 4) {                    // the transposed part: entries (i, q), i < q
+            const int2 i0 = items[t], i1 = items[t + 1], i2 = items[t + 2], i3 = items[t + 3];
+            const T b0 = V::load(Bc + static_cast<int64_t>(i0.x) * R), b1 = V::load(Bc + static_cast<int64_t>(i1.x) * R);
+            const T b2 = V::load(Bc + static_cast<int64_t>(i2.x) * R), b3 = V::load(Bc + static_cast<int64_t>(i3.x) * R);
+            a0 = V::fma(__int_as_float(i0.y), b0, a0);
+            a1 = V::fma(__int_as_float(i1.y), b1, a1);
+            a2 = V::fma(__int_as_float(i2.y), b2, a2);
+            a3 = V::fma(__int_as_float(i3.y), b3, a3);
+        }
+        for (; t < t1; ++t) {
             const int2 it = items[t];
-            acc = V::fma(__int_as_float(it.y), V::load(p.B + static_cast<int64_t>(it.x) * R + colo), acc);
+            a0 = V::fma(__int_as_float(it.y), V::load(Bc + static_cast<int64_t>(it.x) * R), a0);
         }
+        T acc = V::add(V::add(a0, a1), V::add(a2, a3));
         float *out = p.C + static_cast<int64_t>(q) * R + colo;
         if (act) {
             if (ACC) acc = V::add(acc, V::load(out));
