@@ -109,6 +109,9 @@ typedef struct systec_exec_opts {
                                  /* block builds its rows' transposed entries in shared memory */
                                  /* and writes every output row once): 0 auto (on when the     */
                                  /* plan has row blocks, stats.window_blocks > 0), -1 off      */
+    int32_t lane_bytes;          /* columns per lane of the fixed-rank builds: 16 (4 floats,   */
+                                 /* 128-bit gathers) or 32 (8 floats, 256-bit gathers, R = 16 */
+                                 /* / 32 with 32-byte aligned B and C); 0 = auto              */
 } systec_exec_opts;
 
 typedef struct systec_plan_s *systec_plan;

@@ -14,7 +14,7 @@
 
 #include "internal.cuh"
 
-static_assert(sizeof(systec_exec_opts) == 64, "systec_exec_opts layout is part of the ABI");
+static_assert(sizeof(systec_exec_opts) == 68, "systec_exec_opts layout is part of the ABI");
 static_assert(sizeof(systec_stats) == 224, "systec_stats layout is part of the ABI");
 static_assert(sizeof(systec_plan_opts) == 32, "systec_plan_opts layout is part of the ABI");
 

@@ -228,7 +228,14 @@ cudaError_t launch_mttkrp(const Plan &p, const float *B, int R, float *C, const 
         vpl = std::min(want, tile_vecs);
         if (vpl != 1 && vpl != 2 && vpl != 4) return cudaErrorInvalidValue;
     }
-    const int lpe = tile_vecs / vpl;
+    // 32-byte lanes (opts.lane_bytes = 32): the fixed-rank shapes with 8
+    // columns per lane and one 256-bit gather per row — half the lanes per
+    // entry, twice the entries per warp instruction
+    const bool al32 = (reinterpret_cast<uintptr_t>(B) % 32 == 0) && (reinterpret_cast<uintptr_t>(C) % 32 == 0);
+    const bool v8 = o.lane_bytes == 32 && al32 && vw == 4 && !p.general && o.fixed_rank >= 0 && o.vpl <= 1 &&
+                    o.prefetch <= 0 && o.ablation <= 0 && o.occupancy <= 0 && o.chunk_k <= 0 &&
+                    ((p.order == 3 && R == 32) || (p.order >= 4 && p.order <= 5 && R == 16));
+    const int lpe = v8 ? R / 8 : tile_vecs / vpl;
     const int E = 32 / lpe;
     const int tiles = (R + tile_vecs * vw - 1) / (tile_vecs * vw);
     int K = o.chunk_k > 0 ? o.chunk_k : default_K(E);
@@ -263,12 +270,17 @@ cudaError_t launch_mttkrp(const Plan &p, const float *B, int R, float *C, const 
     // fixed-rank build when R is exactly one float4 tile of 16 or 32 columns
     // (opts.fixed_rank: 0 auto = on, -1 off)
     bool full = false;
-    if (o.fixed_rank >= 0 && vw == 4 && vpl == 1 && !pf && !p.general && tiles == 1 && R == lpe * 4 &&
+    if (!v8 && o.fixed_rank >= 0 && vw == 4 && vpl == 1 && !pf && !p.general && tiles == 1 && R == lpe * 4 &&
         o.ablation <= 0 && K == default_K(E)) {
         if (KernelFn ff = pick_full(p.order, lpe, pos1, occ5)) {
             fn = ff;
             full = true;
         }
+    }
+    if (v8) {
+        fn = p.order == 3 ? pick_full_v8_kernel<3>(pos1) : p.order == 4 ? pick_full_v8_kernel<4>(pos1)
+                                                                         : pick_full_v8_kernel<5>(pos1);
+        full = true;
     }
     const int abl = o.ablation;
     if (abl > 0) {  // ablation study: only the c2 / c5 kernel shapes exist
@@ -358,7 +370,7 @@ cudaError_t launch_mttkrp(const Plan &p, const float *B, int R, float *C, const 
     li.smem = static_cast<int>(smem);
     // kernel id, decimal fields: general | copies (2 digits) | pf + 2*dynamic | order | vw | lpe (2 digits) | vpl | pos1;
     // the occupancy variant sets vpl's digit to 5 (vpl itself is 1 there)
-    li.kernel = (p.general ? 1000000000 : 0) + copies * 10000000 + ((pf ? 1 : 0) + (kp.ctr ? 2 : 0) + (full ? 4 : 0)) * 1000000 + p.order * 100000 + vw * 10000 + lpe * 100 + (occ5 ? 5 : vpl) * 10 + (pos1 ? 1 : 0);
+    li.kernel = (p.general ? 1000000000 : 0) + copies * 10000000 + ((pf ? 1 : 0) + (kp.ctr ? 2 : 0) + (full ? 4 : 0)) * 1000000 + p.order * 100000 + (v8 ? 8 : vw) * 10000 + lpe * 100 + (occ5 ? 5 : vpl) * 10 + (pos1 ? 1 : 0);
     p.record_launch(li);
     return cudaGetLastError();
 }

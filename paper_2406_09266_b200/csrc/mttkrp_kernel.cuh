@@ -89,6 +89,31 @@ template <> struct VecT<4> {
                            __shfl_sync(0xffffffffu, v.z, src), __shfl_sync(0xffffffffu, v.w, src));
     }
 };
+// 32-byte lanes: 8 consecutive columns per lane, one 256-bit gather; the
+// reduction is two red.v4 (the widest f32 vector red)
+template <> struct VecT<8> {
+    using T = float8;
+    static __device__ __forceinline__ float4 m4(float4 a, float4 b) { return make_float4(a.x * b.x, a.y * b.y, a.z * b.z, a.w * b.w); }
+    static __device__ __forceinline__ float4 s4(float s, float4 a) { return make_float4(s * a.x, s * a.y, s * a.z, s * a.w); }
+    static __device__ __forceinline__ float4 a4(float4 a, float4 b) { return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w); }
+    static __device__ __forceinline__ T zero() { return T{make_float4(0.f, 0.f, 0.f, 0.f), make_float4(0.f, 0.f, 0.f, 0.f)}; }
+    static __device__ __forceinline__ T mul(T a, T b) { return T{m4(a.lo, b.lo), m4(a.hi, b.hi)}; }
+    static __device__ __forceinline__ T scale(float s, T a) { return T{s4(s, a.lo), s4(s, a.hi)}; }
+    static __device__ __forceinline__ T add(T a, T b) { return T{a4(a.lo, b.lo), a4(a.hi, b.hi)}; }
+    static __device__ __forceinline__ T load(const float *p, uint64_t pol) { return ldg8_hint(p, pol); }
+    static __device__ __forceinline__ void red(float *p, T v) {
+        red_add4(p, v.lo);
+        red_add4(p + 4, v.hi);
+    }
+    static __device__ __forceinline__ void red_if(float *p, T v, bool pred) {
+        red_add4_if(p, v.lo, pred);
+        red_add4_if(p + 4, v.hi, pred);
+    }
+    static __device__ __forceinline__ T shfl_down(T v, int d) {
+        return T{VecT<4>::shfl_down(v.lo, d), VecT<4>::shfl_down(v.hi, d)};
+    }
+    static __device__ __forceinline__ T shfl(T v, int src) { return T{VecT<4>::shfl(v.lo, src), VecT<4>::shfl(v.hi, src)}; }
+};
 template <> struct VecT<1> {
     using T = float;
     static __device__ __forceinline__ T zero() { return 0.f; }
@@ -517,6 +542,12 @@ template <int N> KernelFn pick_full_kernel(int lpe, bool pos1, bool occ);
 template <> KernelFn pick_full_kernel<3>(int lpe, bool pos1, bool occ);
 template <> KernelFn pick_full_kernel<4>(int lpe, bool pos1, bool occ);
 template <> KernelFn pick_full_kernel<5>(int lpe, bool pos1, bool occ);
+// fixed-rank builds with 32-byte lanes (8 columns per lane, 256-bit gathers):
+// order 3 at R = 32 (4 lanes per entry), orders 4/5 at R = 16 (2 lanes)
+template <int N> KernelFn pick_full_v8_kernel(bool pos1);
+template <> KernelFn pick_full_v8_kernel<3>(bool pos1);
+template <> KernelFn pick_full_v8_kernel<4>(bool pos1);
+template <> KernelFn pick_full_v8_kernel<5>(bool pos1);
 // the non-symmetric (expanded-tensor) baseline: position 0 only, one float4/float per lane
 template <int N> KernelFn pick_naive_kernel(int vw, int lpe, bool pf);
 template <> KernelFn pick_naive_kernel<2>(int vw, int lpe, bool pf);

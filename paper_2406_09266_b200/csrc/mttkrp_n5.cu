@@ -99,4 +99,10 @@ KernelFn pick_full_kernel<5>(int lpe, bool pos1, bool occ) {
     }
 }
 
+template <>
+KernelFn pick_full_v8_kernel<5>(bool pos1) {
+    return pos1 ? mttkrp_sym_kernel<5, 2, 1, 8, true, false, false, 0, 16>
+                : mttkrp_sym_kernel<5, 2, 1, 8, false, false, false, 0, 16>;
+}
+
 }  // namespace systec

@@ -77,6 +77,18 @@ __device__ __forceinline__ float4 ldg4_hint(const float *p, uint64_t policy) {
                  : "l"(p), "l"(policy));
     return v;
 }
+// 8 floats, one 32-byte load (sm_100a LDG.E.ENL2.256); p 32-byte aligned
+struct float8 {
+    float4 lo, hi;
+};
+__device__ __forceinline__ float8 ldg8_hint(const float *p, uint64_t policy) {
+    float8 v;
+    asm volatile("ld.global.nc" SYSTEC_LD_L1 ".L2::cache_hint.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %9;"
+                 : "=f"(v.lo.x), "=f"(v.lo.y), "=f"(v.lo.z), "=f"(v.lo.w), "=f"(v.hi.x), "=f"(v.hi.y),
+                   "=f"(v.hi.z), "=f"(v.hi.w)
+                 : "l"(p), "l"(policy));
+    return v;
+}
 __device__ __forceinline__ float ldg1_hint(const float *p, uint64_t policy) {
     float v;
     asm volatile("ld.global.nc" SYSTEC_LD_L1 ".L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(policy));

@@ -34,7 +34,7 @@ class SystecExecOpts(ctypes.Structure):
                 ("chunk_k", ctypes.c_int32), ("stages", ctypes.c_int32), ("vpl", ctypes.c_int32),
                 ("prefetch", ctypes.c_int32), ("copies", ctypes.c_int32), ("ablation", ctypes.c_int32),
                 ("static_ranges", ctypes.c_int32), ("occupancy", ctypes.c_int32), ("fixed_rank", ctypes.c_int32),
-                ("window", ctypes.c_int32)]
+                ("window", ctypes.c_int32), ("lane_bytes", ctypes.c_int32)]
 
 
 class SystecPlanOpts(ctypes.Structure):

@@ -971,3 +971,38 @@ def test_order2_window_edges(systec):
     Cref, S = oracle.mttkrp(2, dim, w.idx, w.vals, w.B)
     parity(bp.execute(dB).cpu().numpy(), Cref, S)
     bp.destroy()
+
+
+# ---------------------------------------------------------------- 32-byte lanes (256-bit gathers)
+@pytest.mark.parametrize("n,dim,nnz,R", [(3, 400, 60001, 32), (4, 60, 50003, 16), (5, 30, 40009, 16),
+                                          (3, 300, 5000, 32), (4, 40, 3001, 16)])
+def test_lane_bytes_32_parity(systec, n, dim, nnz, R):
+    """The fixed-rank builds with 8 columns per lane (one LDG.256 per row,
+    two red.v4): parity with the oracle, both work distributions, position-1
+    accumulation on and off, C replicas, and bit-exact integer data."""
+    w = small_random(n, dim, nnz, R, seed=nnz, diag_frac=0.15)
+    Cref, S = oracle.mttkrp(n, dim, w.idx, w.vals, w.B)
+    for opts in ({}, {"static_ranges": 1}, {"pos1_accumulate": 1}, {"pos1_accumulate": -1}, {"copies": 4}):
+        parity(run(systec, w, lane_bytes=32, **opts), Cref, S)
+    wi = integer_workload(w, seed=3)
+    Ci, _ = oracle.mttkrp(n, dim, wi.idx, wi.vals, wi.B)
+    assert np.array_equal(run(systec, wi, lane_bytes=32).astype(np.float64), Ci)
+
+
+def test_lane_bytes_32_launch_and_fallback(systec):
+    """lane_bytes = 32 takes the 8-column build (vw digit 8 in the kernel id)
+    where it exists and falls back to 16-byte lanes elsewhere (R = 8, or B
+    not 32-byte aligned)."""
+    import torch
+    w = small_random(3, 200, 20000, 32, seed=4, diag_frac=0.1)
+    Cref, S = oracle.mttkrp(3, 200, w.idx, w.vals, w.B)
+    di, dv, dB = to_dev(w.idx, w.vals, w.B)
+    plan = systec.Plan(3, 200, di, dv)
+    parity(plan.execute(dB, lane_bytes=32).cpu().numpy(), Cref, S)
+    assert plan.last_launch()["vw"] == 8 and plan.last_launch()["lpe"] == 4
+    Bbig = torch.zeros(200 * 32 + 4, device="cuda")
+    Bv = Bbig[4:].view(200, 32)                     # 16-byte, not 32-byte, aligned
+    Bv.copy_(dB)
+    parity(plan.execute(Bv, lane_bytes=32).cpu().numpy(), Cref, S)
+    assert plan.last_launch()["vw"] == 4
+    plan.destroy()

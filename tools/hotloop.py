@@ -30,7 +30,7 @@ def functions(lib):
 
 
 def hot_loop(body):
-    """Smallest backward-branch loop that contains a 128-bit global gather."""
+    """Smallest backward-branch loop that contains a 128- or 256-bit global gather."""
     best = None
     for addr, ins in body:
         m = re.search(r"BRA (?:`\()?\.?L?_?x?_?(0x[0-9a-f]+|\d+)", ins)
@@ -43,7 +43,7 @@ def hot_loop(body):
         if tgt >= addr:
             continue
         loop = [(a, i) for a, i in body if tgt <= a <= addr]
-        if any("LDG.E.128" in i for _, i in loop) and (best is None or len(loop) < len(best)):
+        if any(("LDG.E.128" in i or ".256" in i and "LDG" in i) for _, i in loop) and (best is None or len(loop) < len(best)):
             best = loop
     return best or []
 
