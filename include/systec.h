@@ -105,10 +105,11 @@ typedef struct systec_exec_opts {
                                  /* 0 auto (on when B > 64 MB and the plan is lexicographic)   */
     int32_t fixed_rank;          /* kernels built for R = 16 / 32 exactly (one float4 tile):    */
                                  /* 0 auto (on when R matches), -1 off                          */
-    int32_t window;              /* order-2 plans: the atomic-free windowed kernel (each row    */
-                                 /* block builds its rows' transposed entries in shared memory */
-                                 /* and writes every output row once): 0 auto (on when the     */
-                                 /* plan has row blocks, stats.window_blocks > 0), -1 off      */
+    int32_t window;              /* order-2 plans created with systec_plan_opts.window = 1: the */
+                                 /* atomic-free windowed kernel (each row block builds its     */
+                                 /* rows' transposed entries in shared memory and writes every */
+                                 /* output row once): 0 auto (on when stats.window_blocks > 0), */
+                                 /* -1 off                                                      */
     int32_t lane_bytes;          /* columns per lane of the fixed-rank builds: 16 (4 floats,   */
                                  /* 128-bit gathers) or 32 (8 floats, 256-bit gathers, R = 16 */
                                  /* / 32 with 32-byte aligned B and C); 0 = auto              */
@@ -130,7 +131,11 @@ typedef struct systec_plan_opts {
                                  /* General plans are banded only on request (explicit s).     */
     int32_t general;             /* 1 = a general (non-symmetric) tensor, as                   */
                                  /* systec_plan_create_general; 0 = symmetric                  */
-    int32_t reserved[6];
+    int32_t window;              /* order-2 symmetric plans: 1 = also build the row / column   */
+                                 /* pointers of the atomic-free windowed kernel (used when the */
+                                 /* bandwidth is small; measured slower than the default       */
+                                 /* kernel on the banded stand-in); 0 = no      */
+    int32_t reserved[5];
 } systec_plan_opts;
 
 /*

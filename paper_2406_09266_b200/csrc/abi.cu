@@ -171,7 +171,8 @@ void free_window(Plan *p, bool pooled, cudaStream_t s) {
 
 // Builds the plan.  `pooled` plans keep their storage in the stream-ordered pool.
 int plan_create_impl(Plan **out, int order, int64_t dim, int64_t nnz, const int32_t *idx, const float *vals,
-                     cudaStream_t s, bool pooled, bool general = false, int band_request = 0) {
+                     cudaStream_t s, bool pooled, bool general = false, int band_request = 0,
+                     bool window = false) {
     *out = nullptr;
     int bits = 0;
     int rc = check_shape(order, dim, nnz, &bits);
@@ -255,7 +256,7 @@ int plan_create_impl(Plan **out, int order, int64_t dim, int64_t nnz, const int3
     // bandwidth, read back with the statistics (sym2_window.cu)
     unsigned long long win_host[2] = {0, 0};  // {bandwidth, largest column count}
     int32_t win_items = 0;
-    if (order == 2 && !general) {
+    if (order == 2 && !general && window) {
         const size_t wb = static_cast<size_t>(dim + 1) * 8 + 16;
         void *w = nullptr;
         if ((e = pooled ? cudaMallocAsync(&w, wb, s) : cudaMalloc(&w, wb)) != cudaSuccess) return fail(e);
@@ -347,17 +348,19 @@ int systec_plan_create_ex(systec_plan *out, int order, int64_t dim, int64_t nnz,
     if (!out) return SYSTEC_ERR_ARG;
     *out = nullptr;
     int band = 0;
-    bool general = false;
+    bool general = false, window = false;
     if (opts) {
-        if (opts->band_shift < -1 || opts->general < 0 || opts->general > 1) return SYSTEC_ERR_ARG;
+        if (opts->band_shift < -1 || opts->general < 0 || opts->general > 1 || opts->window < 0 || opts->window > 1)
+            return SYSTEC_ERR_ARG;
         for (int r : opts->reserved)
             if (r) return SYSTEC_ERR_ARG;
         band = opts->band_shift;
         general = opts->general == 1;
+        window = opts->window == 1;
     }
     Plan *p = nullptr;
     int rc = systec::plan_create_impl(&p, order, dim, nnz, idx, vals, reinterpret_cast<cudaStream_t>(stream), false,
-                                      general, band);
+                                      general, band, window);
     *out = reinterpret_cast<systec_plan>(p);
     return rc;
 }

@@ -38,7 +38,8 @@ class SystecExecOpts(ctypes.Structure):
 
 
 class SystecPlanOpts(ctypes.Structure):
-    _fields_ = [("band_shift", ctypes.c_int32), ("general", ctypes.c_int32), ("reserved", ctypes.c_int32 * 6)]
+    _fields_ = [("band_shift", ctypes.c_int32), ("general", ctypes.c_int32), ("window", ctypes.c_int32),
+                ("reserved", ctypes.c_int32 * 5)]
 
 
 EXPORTS = ["systec_mttkrp", "systec_mttkrp_host", "systec_plan_create", "systec_plan_execute",
@@ -143,12 +144,13 @@ def _opts(**kw) -> SystecExecOpts:
 class Plan:
     """A prepared (validated, canonicalised, sorted) symmetric tensor on the GPU:
     ``systec_plan_create``.  ``idx`` [nnz][order] int32 and ``vals`` [nnz] fp32
-    are CUDA tensors; they may be freed after construction.  ``band_shift``
+    are CUDA tensors; they may be freed after construction.  ``window``
+    (order 2): also build the atomic-free windowed kernel's pointers.  ``band_shift``
     (``systec_plan_create_ex``): None/0 = auto, -1 = lexicographic stream,
     s > 0 = band-major by c_{n-1} >> s."""
 
     def __init__(self, order: int, dim: int, idx, vals, stream=None, general: bool = False,
-                 band_shift: int | None = None):
+                 band_shift: int | None = None, window: bool = False):
         import torch
         lib = load()
         nnz = int(vals.shape[0])
@@ -156,8 +158,8 @@ class Plan:
             raise ValueError("idx must be [nnz][order]")
         h = ctypes.c_void_p()
         ip, vp_ = _dev(idx, torch.int32, "idx"), _dev(vals, torch.float32, "vals")
-        if band_shift is not None:
-            po = SystecPlanOpts(band_shift=band_shift, general=int(general))
+        if band_shift is not None or window:
+            po = SystecPlanOpts(band_shift=band_shift or 0, general=int(general), window=int(window))
             _check(lib.systec_plan_create_ex(ctypes.byref(h), order, dim, nnz, ip, vp_, ctypes.byref(po),
                                              _stream_handle(stream)), "systec_plan_create_ex")
         else:

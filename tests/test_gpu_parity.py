@@ -911,7 +911,8 @@ def test_order2_window_kernel_parity(systec, R):
     w = make(f"b{R}", 2, 20000, 300000, R, seed=R, mode="banded", band=60)
     Cref, S = oracle.mttkrp(2, w.dim, w.idx, w.vals, w.B)
     di, dv, dB = to_dev(w.idx, w.vals, w.B)
-    plan = systec.Plan(2, w.dim, di, dv)
+    assert systec.Plan(2, w.dim, di, dv).stats()["window_blocks"] == 0     # built only on request
+    plan = systec.Plan(2, w.dim, di, dv, window=True)
     st = plan.stats()
     assert st["bandwidth"] == int((w.idx[:, 1] - w.idx[:, 0]).max()) and st["window_blocks"] > 0
     C = plan.execute(dB)
@@ -924,7 +925,7 @@ def test_order2_window_kernel_parity(systec, R):
     parity(C2.cpu().numpy() - 1.0, Cref, S, tol=1e-4 + 1e-6)
     wi = integer_workload(w, seed=R)
     Ci, _ = oracle.mttkrp(2, w.dim, wi.idx, wi.vals, wi.B)
-    pi = systec.Plan(2, w.dim, *to_dev(wi.idx, wi.vals))
+    pi = systec.Plan(2, w.dim, *to_dev(wi.idx, wi.vals), window=True)
     assert np.array_equal(pi.execute(to_dev(wi.B)[0]).cpu().numpy().astype(np.float64), Ci)
     plan.destroy()
     pi.destroy()
@@ -941,7 +942,7 @@ def test_order2_window_edges(systec):
     keep = (w.idx[:, 0] < 1000) | (w.idx[:, 0] >= 2000)
     idx, vals = w.idx[keep], w.vals[keep]
     Cref, S = oracle.mttkrp(2, dim, idx, vals, w.B)
-    plan = systec.Plan(2, dim, *to_dev(idx, vals))
+    plan = systec.Plan(2, dim, *to_dev(idx, vals), window=True)
     assert plan.stats()["window_blocks"] > 0
     dB = to_dev(w.B)[0]
     C = torch.full((dim, 8), 7.0, device="cuda")
@@ -949,7 +950,7 @@ def test_order2_window_edges(systec):
     assert plan.last_launch()["kernel_id"] >= 2_000_000_000
     parity(C.cpu().numpy(), Cref, S)
     plan.destroy()
-    empty = systec.Plan(2, dim, *to_dev(np.zeros((0, 2), np.int32), np.zeros(0, np.float32)))
+    empty = systec.Plan(2, dim, *to_dev(np.zeros((0, 2), np.int32), np.zeros(0, np.float32)), window=True)
     C = torch.full((dim, 8), 7.0, device="cuda")
     empty.execute(dB, C)
     assert float(C.abs().max()) == 0.0
@@ -957,16 +958,16 @@ def test_order2_window_edges(systec):
     # a hub column: column 2999 holds an entry from every row
     hub = np.stack([np.arange(dim), np.full(dim, dim - 1)], axis=1).astype(np.int32)
     hv = np.random.default_rng(1).uniform(-1, 1, dim).astype(np.float32)
-    hp = systec.Plan(2, dim, *to_dev(hub, hv))
+    hp = systec.Plan(2, dim, *to_dev(hub, hv), window=True)
     assert hp.stats()["window_blocks"] == 0
     Cref, S = oracle.mttkrp(2, dim, hub, hv, w.B)
     parity(hp.execute(dB).cpu().numpy(), Cref, S)
     hp.destroy()
     u = make("wide", 2, 100000, 200000, 8, seed=2, mode="uniform")
-    up = systec.Plan(2, u.dim, *to_dev(u.idx, u.vals))
+    up = systec.Plan(2, u.dim, *to_dev(u.idx, u.vals), window=True)
     assert up.stats()["window_blocks"] == 0
     up.destroy()
-    bp = systec.Plan(2, w.dim, *to_dev(w.idx, w.vals), band_shift=4)
+    bp = systec.Plan(2, w.dim, *to_dev(w.idx, w.vals), band_shift=4, window=True)
     assert bp.stats()["window_blocks"] == 0
     Cref, S = oracle.mttkrp(2, dim, w.idx, w.vals, w.B)
     parity(bp.execute(dB).cpu().numpy(), Cref, S)
