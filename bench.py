@@ -113,80 +113,52 @@ def ncu_traffic(config, opts_str, timeout=240):
                    "python tools/profile_one.py (cold L2: ncu flushes caches per replay), in this bench run"}
 
 
-def in_run_bounds(w, launch, dev_index=0):
-    """The three memory-system rates of this workload, measured on this GPU
-    right now (tools/bounds.cu): HBM stream read, random row gathers from a
-    table of B's footprint, red.global.add.v4.f32 of rows into a table of C's
-    footprint (x the replicas the launch used), rows of R*4 bytes."""
+def mix_ratio(gathers, reds):
+    """Small integers (ng, nr) <= 8 with ng / nr closest to gathers / reds."""
+    if reds <= 0:
+        return 1, 0
+    if gathers <= 0:
+        return 0, 1
+    best = min(((g, r) for g in range(1, 9) for r in range(1, 9)),
+               key=lambda gr: (abs(gr[0] / gr[1] - gathers / reds), gr[0] + gr[1]))
+    return best
+
+
+def in_run_bounds(w, launch, st, nnz_local, dev_index=0):
+    """The memory-system rates of this workload, measured on this GPU right
+    now (tools/bounds.cu): HBM stream read, random row gathers from a table of
+    B's footprint, red.global.add.v4.f32 of rows into a table of C's footprint
+    (x the replicas the launch used), and the kernel's MIX of the two (the
+    plan's ratio of gathered to reduced rows, reduced values depending on
+    gathered ones), rows of R*4 bytes."""
     import ctypes
     import __graft_entry__
     lib = ctypes.CDLL(__graft_entry__.build_bounds())
     for f in (lib.bounds_gather, lib.bounds_red):
         f.argtypes = [ctypes.c_int, ctypes.c_int64, ctypes.c_int, ctypes.POINTER(ctypes.c_double)]
     lib.bounds_hbm_read.argtypes = [ctypes.c_int64, ctypes.c_int, ctypes.POINTER(ctypes.c_double)]
+    lib.bounds_mix.argtypes = [ctypes.c_int, ctypes.c_int64, ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                               ctypes.POINTER(ctypes.c_double)]
     row = w.R * 4
     rb = min(512, 1 << max(4, (row - 1).bit_length()))   # the kernel's float4 row tile
-    hbm, gat, red = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
+    hbm, gat, red, mix = ctypes.c_double(), ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
     copies = max(1, launch.get("copies", 1))
+    terms = memory_terms(w, st, nnz_local, launch)
+    ng, nr = mix_ratio(st["G"], terms["red_rows"])
     with ClockSampler(dev_index, period=0.01) as clk:
         rc = [lib.bounds_hbm_read(2 << 30, 5, ctypes.byref(hbm)),
               lib.bounds_gather(rb, w.dim * rb, 5, ctypes.byref(gat)),
-              lib.bounds_red(rb, copies * w.dim * rb, 5, ctypes.byref(red))]
+              lib.bounds_red(rb, copies * w.dim * rb, 5, ctypes.byref(red)),
+              lib.bounds_mix(rb, w.dim * rb, copies * w.dim * rb, ng, nr, 5, ctypes.byref(mix))]
     if any(rc):
         return {"unavailable": f"bounds library returned {rc}"}
-    return {"hbm_read_gbs": hbm.value, "l2_gather_gbs": gat.value, "l2_red_gbs": red.value, "row_bytes": rb,
+    return {"hbm_read_gbs": hbm.value, "l2_gather_gbs": gat.value, "l2_red_gbs": red.value,
+            "l2_mix_gbs": mix.value * (ng + nr) * rb / 1e9, "mix_ratio": [ng, nr], "row_bytes": rb,
             "gather_table_bytes": w.dim * rb, "red_table_bytes": copies * w.dim * rb,
             "clocks": clk.report(),
             "how": "tools/bounds.cu in this run: best of 5 launches each (148x8 blocks of 256 threads), "
-                   "2 GiB stream read; random whole-row float4 gathers / red.global.add.v4.f32"}
-
-
-class ClockSampler:
-    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
-               0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
-               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
-
-    def __init__(self, index=0, period=0.02):
-        self.samples, self.reasons, self.max_mhz = [], 0, None
-        self.period, self.index = period, index
-        self._stop = threading.Event()
-        self.ok = False
-        try:
-            import pynvml
-            pynvml.nvmlInit()
-            self.nv = pynvml
-            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
-            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
-            self.ok = True
-        except Exception:
-            pass
-
-    def _run(self):
-        while not self._stop.is_set():
-            try:
-                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
-                self.reasons |= int(self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h))
-            except Exception:
-                pass
-            time.sleep(self.period)
-
-    def __enter__(self):
-        if self.ok:
-            self.t = threading.Thread(target=self._run, daemon=True)
-            self.t.start()
-        return self
-
-    def __exit__(self, *a):
-        if self.ok:
-            self._stop.set()
-            self.t.join()
-
-    def report(self):
-        if not self.ok or not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml unavailable"], "samples": 0}
-        names = [n for b, n in self.REASONS.items() if self.reasons & b and n != "gpu_idle"]
-        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz,
-                "reasons": names, "samples": len(self.samples)}
+                   "2 GiB stream read; random whole-row float4 gathers / red.global.add.v4.f32; the mix "
+                   f"= {ng} gathers + {nr} reductions per unit, reduced values from the gathered rows"}
 
 
 def bytes_eff(order, nnz, G, R, dim):
@@ -214,9 +186,11 @@ def memory_terms(w, st, nnz_local, launch):
 
 def roofline(terms, bounds, kern_ms, local_bytes_eff, peak_hbm, traffic):
     """The kernel against the bound of the unit that binds it.  Each memory
-    class alone at its measured rate gives a time; the largest is the bound.
-    achieved = that class's algorithmic bytes / kernel time, peak = its
-    measured rate, frac = achieved / peak (= t_bound / t_kernel)."""
+    class at its measured rate gives a time — the stream alone, the gathers
+    alone, the reductions alone, and the gathers and reductions together in
+    the kernel's mix (they share the SM->L2 port and the L2); the largest is
+    the bound.  achieved = that class's algorithmic bytes / kernel time,
+    peak = its measured rate, frac = achieved / peak (= t_bound / t_kernel)."""
     t = kern_ms * 1e-3
     eff = {"effective_gbs": local_bytes_eff / t / 1e9, "frac_of_measured_copy_peak": local_bytes_eff / t / 1e9 / peak_hbm,
            "frac_of_8tbs": local_bytes_eff / t / 8e12, "algorithmic_bytes_per_launch": local_bytes_eff}
@@ -227,14 +201,18 @@ def roofline(terms, bounds, kern_ms, local_bytes_eff, peak_hbm, traffic):
         return {"bound": "hbm", "achieved": eff["effective_gbs"], "peak": peak_hbm, "unit": "GB/s",
                 "frac": eff["effective_gbs"] / peak_hbm, "traffic": traffic.get("dram_bytes_per_launch") if traffic else None,
                 "note": "in-run bounds unavailable: effective bytes against the HBM copy peak", "hbm": eff}
-    rates = {"stream": bounds["hbm_read_gbs"], "gather": bounds["l2_gather_gbs"], "red": bounds["l2_red_gbs"]}
+    rates = {"stream": bounds["hbm_read_gbs"], "gather": bounds["l2_gather_gbs"], "red": bounds["l2_red_gbs"],
+             "mix": bounds["l2_mix_gbs"]}
+    terms = dict(terms, mix=terms["gather"] + terms["red"])
     times = {k: terms[k] / (rates[k] * 1e9) for k in rates}
     bind = max(times, key=times.get)
     achieved = terms[bind] / t / 1e9
     out = {"bound": "hbm" if bind == "stream" else "l2",
            "binding_op": {"stream": "index/value stream read (HBM)",
                           "gather": "random B-row gathers (L2)",
-                          "red": "red.global.add.v4.f32 of C rows (SM->L2 request/write port, L2 atomic units)"}[bind],
+                          "red": "red.global.add.v4.f32 of C rows (SM->L2 request/write port, L2 atomic units)",
+                          "mix": "the kernel's mix of random B-row gathers and red.v4 C-row reductions (SM->L2 "
+                                 "request port / L2)"}[bind],
            "achieved": achieved, "peak": rates[bind], "unit": "GB/s", "frac": achieved / rates[bind],
            "traffic": traffic.get("dram_bytes_per_launch") if traffic else None,
            "algorithmic_bytes_per_launch": terms[bind], "kernel_ms": kern_ms, "t_bound_ms": times[bind] * 1e3,
@@ -400,7 +378,7 @@ def main():
     torch.cuda.synchronize()
     launch = plan.last_launch()
     # the memory-system bounds of this workload, measured on this GPU before the timed region
-    bounds = None if args.no_bounds else in_run_bounds(w, launch, local)
+    bounds = None if args.no_bounds else in_run_bounds(w, launch, st, hi - lo, local)
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
     if dist is not None:
         dist.barrier()

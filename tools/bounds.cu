@@ -12,8 +12,11 @@
 //                        per row) from a table of `table_bytes` (B's footprint);
 //   bounds_red        — random whole-row `red.global.add.v4.f32` into a table
 //                        of `table_bytes` (C's footprint, times the replicas).
-// Each returns the best of `reps` timed launches in GB/s (CUDA events on the
-// default stream; one warm-up launch first).  Returns 0 on success, else the
+//   bounds_mix        — the kernel's mix of the two: per unit NG gathers and
+//                        NR reductions (the ratio of the plan's G to its
+//                        reduced rows), in units per second.
+// Each returns the best of `reps` timed launches (CUDA events on the default
+// stream; one warm-up launch first).  Returns 0 on success, else the
 // cudaError_t.
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -63,6 +66,34 @@ __global__ void red_rows(float *T, uint32_t rows, int iters) {
         float *p = T + (size_t)r * (4 * LPE) + j * 4;
         asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
                      : "memory");
+    }
+}
+
+// the kernel's memory-operation MIX without its stream or arithmetic: per
+// unit, NG random whole-row gathers from T (B's footprint) and NR random
+// whole-row red.global.add.v4.f32 into U (C's footprint), the reduced values
+// depending on the gathered ones (as in the MTTKRP: products of gathered rows)
+template <int LPE>
+__global__ void mix_rows(const float *__restrict__ T, uint32_t rows_t, float *U, uint32_t rows_u, int ng, int nr,
+                         int iters) {
+    constexpr int E = 32 / LPE;
+    const int lane = threadIdx.x & 31, g = lane / LPE, j = lane % LPE;
+    const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    for (int it = 0; it < iters; ++it) {
+        const uint32_t h = (gw * 131071u + it) * E + g;
+        float4 acc = make_float4(1.f, 1.f, 1.f, 1.f);
+        for (int q = 0; q < ng; ++q) {
+            const uint32_t r = hash32(h * 8u + q) % rows_t;
+            const float4 v = __ldg(reinterpret_cast<const float4 *>(T + (size_t)r * (4 * LPE)) + j);
+            acc.x *= v.x; acc.y *= v.y; acc.z *= v.z; acc.w *= v.w;
+        }
+        for (int q = 0; q < nr; ++q) {
+            const uint32_t r = hash32((h * 8u + q) ^ 0x9e3779b9u) % rows_u;
+            float *p = U + (size_t)r * (4 * LPE) + j * 4;
+            asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(acc.x), "f"(acc.y), "f"(acc.z),
+                         "f"(acc.w)
+                         : "memory");
+        }
     }
 }
 
@@ -164,4 +195,40 @@ BOUNDS_API int bounds_gather(int row_bytes, int64_t table_bytes, int reps, doubl
 
 BOUNDS_API int bounds_red(int row_bytes, int64_t table_bytes, int reps, double *gbs) {
     return rows_bound(1, row_bytes, table_bytes, reps, gbs);
+}
+
+// units of (ng gathers + nr reductions) per second, rows of row_bytes, tables
+// of table_b / table_c bytes; ng, nr in [0, 8]
+BOUNDS_API int bounds_mix(int row_bytes, int64_t table_b, int64_t table_c, int ng, int nr, int reps,
+                          double *units_per_s) {
+    const int lpe = row_bytes / 16;
+    if (!units_per_s || ng < 0 || nr < 0 || ng > 8 || nr > 8 || ng + nr == 0 || table_b < row_bytes ||
+        table_c < row_bytes || (lpe != 1 && lpe != 2 && lpe != 4 && lpe != 8 && lpe != 16 && lpe != 32))
+        return static_cast<int>(cudaErrorInvalidValue);
+    const uint32_t rb = static_cast<uint32_t>(table_b / row_bytes), rc = static_cast<uint32_t>(table_c / row_bytes);
+    float *T = nullptr, *U = nullptr;
+    cudaError_t e = cudaMalloc(&T, static_cast<size_t>(rb) * row_bytes);
+    if (e != cudaSuccess) return static_cast<int>(e);
+    if ((e = cudaMalloc(&U, static_cast<size_t>(rc) * row_bytes)) == cudaSuccess &&
+        (e = cudaMemset(T, 0, static_cast<size_t>(rb) * row_bytes)) == cudaSuccess &&
+        (e = cudaMemset(U, 0, static_cast<size_t>(rc) * row_bytes)) == cudaSuccess) {
+        const int blocks = sm_count() * 8, threads = 256, iters = 64;
+        auto launch = [&] {
+            switch (lpe) {
+                case 1: mix_rows<1><<<blocks, threads>>>(T, rb, U, rc, ng, nr, iters); break;
+                case 2: mix_rows<2><<<blocks, threads>>>(T, rb, U, rc, ng, nr, iters); break;
+                case 4: mix_rows<4><<<blocks, threads>>>(T, rb, U, rc, ng, nr, iters); break;
+                case 8: mix_rows<8><<<blocks, threads>>>(T, rb, U, rc, ng, nr, iters); break;
+                case 16: mix_rows<16><<<blocks, threads>>>(T, rb, U, rc, ng, nr, iters); break;
+                default: mix_rows<32><<<blocks, threads>>>(T, rb, U, rc, ng, nr, iters); break;
+            }
+        };
+        float ms = 0.f;
+        e = best_ms(reps, launch, &ms);
+        const double units = static_cast<double>(blocks) * threads / lpe * iters;
+        *units_per_s = units / (ms * 1e-3);
+    }
+    cudaFree(T);
+    cudaFree(U);
+    return static_cast<int>(e);
 }
