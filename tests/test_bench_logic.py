@@ -1,0 +1,54 @@
+"""bench.py's host logic on CPU: the roofline arithmetic (the bound of the
+binding memory class, achieved / peak), the gather:reduction mix ratio, the
+reduced-row count from plan statistics, and the clock sampler's report
+without NVML samples."""
+import math
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import bench  # noqa: E402
+
+
+class W:
+    order, dim, R = 3, 100, 32
+
+
+def test_mix_ratio():
+    assert bench.mix_ratio(30, 20) == (3, 2)
+    assert bench.mix_ratio(149.3, 58.6) in ((5, 2), (8, 3))
+    assert bench.mix_ratio(10, 0) == (1, 0)
+    g, r = bench.mix_ratio(78.5, 52.0)
+    assert abs(g / r - 78.5 / 52.0) < 0.05
+
+
+def test_memory_terms_counts_reduced_rows():
+    # 10 entries, all strict (code 0: c1 != c0), G = 30; 4 leading runs; 6 position-1 runs
+    st = {"G": 30, "lead_runs": 4, "pos1_runs": 6, "pattern_hist": [10, 0, 0, 0] + [0] * 12}
+    t = bench.memory_terms(W, st, 10, {"pos1": 0})
+    assert t["red_rows"] == 4 + 20 and t["stream"] == 10 * 16 and t["gather"] == 30 * 128
+    t1 = bench.memory_terms(W, st, 10, {"pos1": 1})
+    assert t1["red_rows"] == 4 + 20 - (10 - 6)
+
+
+def test_roofline_picks_the_binding_class():
+    terms = {"stream": 160e6, "gather": 3.84e9, "red": 2.56e9}
+    bounds = {"hbm_read_gbs": 6700.0, "l2_gather_gbs": 15000.0, "l2_red_gbs": 6000.0, "l2_mix_gbs": 13000.0,
+              "clocks": {}}
+    r = bench.roofline(dict(terms), bounds, 0.48, 4.0e9, 6553.0, {"dram_bytes_per_launch": 192e6})
+    times = {"stream": 160e6 / 6700e9, "gather": 3.84e9 / 15000e9, "red": 2.56e9 / 6000e9,
+             "mix": 6.4e9 / 13000e9}
+    bind = max(times, key=times.get)
+    assert r["bound"] == "l2" and r["terms_ms"].keys() == times.keys()
+    assert math.isclose(r["frac"], r["achieved"] / r["peak"]) and math.isclose(r["frac"], times[bind] / 0.48e-3)
+    assert math.isclose(r["hbm"]["physical_gbs"], 192e6 / 0.48e-3 / 1e9)
+    r2 = bench.roofline(dict(terms), {"unavailable": "x"}, 0.48, 4.0e9, 6553.0, None)
+    assert r2["bound"] == "hbm" and math.isclose(r2["frac"], 4.0e9 / 0.48e-3 / 1e9 / 6553.0)
+
+
+def test_clock_sampler_reports_without_samples():
+    rep = bench.ClockSampler.__new__(bench.ClockSampler)
+    rep.ok, rep.samples, rep.max_mhz, rep.reasons = False, [], None, 0
+    assert rep.report()["samples"] == 0
