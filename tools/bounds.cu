@@ -29,6 +29,10 @@ __device__ __forceinline__ uint32_t hash32(uint32_t x) {
     x ^= x >> 16; x *= 0x7feb352dU; x ^= x >> 15; x *= 0x846ca68bU; x ^= x >> 16;
     return x;
 }
+// a uniform row in [0, rows): multiply-shift range reduction (one IMAD.HI, not a division)
+__device__ __forceinline__ uint32_t pick(uint32_t h, uint32_t rows) {
+    return static_cast<uint32_t>((static_cast<uint64_t>(h) * rows) >> 32);
+}
 
 __global__ void stream_read(const float4 *__restrict__ a, size_t n4, float *sink) {
     float4 acc = make_float4(0, 0, 0, 0);
@@ -48,7 +52,7 @@ __global__ void gather_rows(const float *__restrict__ T, uint32_t rows, int iter
     float4 acc = make_float4(0, 0, 0, 0);
 #pragma unroll 4
     for (int it = 0; it < iters; ++it) {
-        const uint32_t r = hash32(gw * 131071u + it * E + g) % rows;
+        const uint32_t r = pick(hash32(gw * 131071u + it * E + g), rows);
         const float4 v = __ldg(reinterpret_cast<const float4 *>(T + (size_t)r * (4 * LPE)) + j);
         acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
     }
@@ -62,7 +66,7 @@ __global__ void red_rows(float *T, uint32_t rows, int iters) {
     const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const float4 v = make_float4(1.f, 1.f, 1.f, 1.f);
     for (int it = 0; it < iters; ++it) {
-        const uint32_t r = hash32(gw * 131071u + it * E + g) % rows;
+        const uint32_t r = pick(hash32(gw * 131071u + it * E + g), rows);
         float *p = T + (size_t)r * (4 * LPE) + j * 4;
         asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
                      : "memory");
@@ -81,18 +85,31 @@ __global__ void mix_rows(const float *__restrict__ T, uint32_t rows_t, float *U,
     const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     for (int it = 0; it < iters; ++it) {
         const uint32_t h = (gw * 131071u + it) * E + g;
-        float4 acc = make_float4(1.f, 1.f, 1.f, 1.f);
-        for (int q = 0; q < ng; ++q) {
-            const uint32_t r = hash32(h * 8u + q) % rows_t;
-            const float4 v = __ldg(reinterpret_cast<const float4 *>(T + (size_t)r * (4 * LPE)) + j);
-            acc.x *= v.x; acc.y *= v.y; acc.z *= v.z; acc.w *= v.w;
+        // unrolled to the maximum with predicates: every gather of the unit in
+        // flight before the products (a runtime-length loop serialises them)
+        float4 v[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            v[q] = make_float4(1.f, 1.f, 1.f, 1.f);
+            if (q < ng) {
+                const uint32_t r = pick(hash32(h * 8u + q), rows_t);
+                v[q] = __ldg(reinterpret_cast<const float4 *>(T + (size_t)r * (4 * LPE)) + j);
+            }
         }
-        for (int q = 0; q < nr; ++q) {
-            const uint32_t r = hash32((h * 8u + q) ^ 0x9e3779b9u) % rows_u;
-            float *p = U + (size_t)r * (4 * LPE) + j * 4;
-            asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(acc.x), "f"(acc.y), "f"(acc.z),
-                         "f"(acc.w)
-                         : "memory");
+        float4 acc = v[0];
+#pragma unroll
+        for (int q = 1; q < 8; ++q) {
+            acc.x *= v[q].x; acc.y *= v[q].y; acc.z *= v[q].z; acc.w *= v[q].w;
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            if (q < nr) {
+                const uint32_t r = pick(hash32((h * 8u + q) ^ 0x9e3779b9u), rows_u);
+                float *p = U + (size_t)r * (4 * LPE) + j * 4;
+                asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(acc.x), "f"(acc.y), "f"(acc.z),
+                             "f"(acc.w)
+                             : "memory");
+            }
         }
     }
 }
