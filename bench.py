@@ -113,15 +113,17 @@ def ncu_traffic(config, opts_str, timeout=240):
                    "python tools/profile_one.py (cold L2: ncu flushes caches per replay), in this bench run"}
 
 
+MIX_PAIRS = [(1, 1), (2, 1), (3, 1), (3, 2), (4, 3), (5, 2), (5, 3), (5, 4), (7, 3), (7, 4), (7, 5), (8, 3)]
+
+
 def mix_ratio(gathers, reds):
-    """Small integers (ng, nr) <= 8 with ng / nr closest to gathers / reds."""
+    """The instantiated (ng, nr) pair of tools/bounds.cu (bounds_mix_pairs)
+    whose ratio is closest to gathers / reds."""
     if reds <= 0:
-        return 1, 0
+        return 3, 0
     if gathers <= 0:
-        return 0, 1
-    best = min(((g, r) for g in range(1, 9) for r in range(1, 9)),
-               key=lambda gr: (abs(gr[0] / gr[1] - gathers / reds), gr[0] + gr[1]))
-    return best
+        return 0, 2
+    return min(MIX_PAIRS, key=lambda gr: (abs(gr[0] / gr[1] - gathers / reds), gr[0] + gr[1]))
 
 
 def in_run_bounds(w, launch, st, nnz_local, dev_index=0):

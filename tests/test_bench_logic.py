@@ -19,7 +19,7 @@ class W:
 def test_mix_ratio():
     assert bench.mix_ratio(30, 20) == (3, 2)
     assert bench.mix_ratio(149.3, 58.6) in ((5, 2), (8, 3))
-    assert bench.mix_ratio(10, 0) == (1, 0)
+    assert bench.mix_ratio(10, 0) == (3, 0) and bench.mix_ratio(0, 5) == (0, 2)
     g, r = bench.mix_ratio(78.5, 52.0)
     assert abs(g / r - 78.5 / 52.0) < 0.05
 
@@ -52,3 +52,15 @@ def test_clock_sampler_reports_without_samples():
     rep = bench.ClockSampler.__new__(bench.ClockSampler)
     rep.ok, rep.samples, rep.max_mhz, rep.reasons = False, [], None, 0
     assert rep.report()["samples"] == 0
+
+
+def test_mix_pairs_match_the_bounds_library():
+    """bench.MIX_PAIRS are exactly the instantiated pairs of tools/bounds.cu."""
+    import ctypes
+
+    import __graft_entry__
+    lib = ctypes.CDLL(__graft_entry__.build_bounds())
+    buf = (ctypes.c_int * 64)()
+    n = lib.bounds_mix_pairs(buf, 32)
+    pairs = [(buf[2 * k], buf[2 * k + 1]) for k in range(n)]
+    assert set(bench.MIX_PAIRS) <= set(pairs)

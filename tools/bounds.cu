@@ -76,41 +76,58 @@ __global__ void red_rows(float *T, uint32_t rows, int iters) {
 // the kernel's memory-operation MIX without its stream or arithmetic: per
 // unit, NG random whole-row gathers from T (B's footprint) and NR random
 // whole-row red.global.add.v4.f32 into U (C's footprint), the reduced values
-// depending on the gathered ones (as in the MTTKRP: products of gathered rows)
-template <int LPE>
-__global__ void mix_rows(const float *__restrict__ T, uint32_t rows_t, float *U, uint32_t rows_u, int ng, int nr,
-                         int iters) {
+// depending on the gathered ones (as in the MTTKRP: products of gathered
+// rows).  NG / NR are compile-time so every gather of a unit is in flight
+// before the products; rows come from an LCG step per row (two
+// instructions), so the loop is bound by the memory system, not by issue.
+template <int LPE, int NG, int NR>
+__global__ void mix_rows(const float *__restrict__ T, uint32_t rows_t, float *U, uint32_t rows_u, int iters) {
     constexpr int E = 32 / LPE;
     const int lane = threadIdx.x & 31, g = lane / LPE, j = lane % LPE;
     const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    uint32_t x = hash32(gw * E + g + 0x51ed27u);
     for (int it = 0; it < iters; ++it) {
-        const uint32_t h = (gw * 131071u + it) * E + g;
-        // unrolled to the maximum with predicates: every gather of the unit in
-        // flight before the products (a runtime-length loop serialises them)
-        float4 v[8];
+        float4 v[NG > 0 ? NG : 1];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-            v[q] = make_float4(1.f, 1.f, 1.f, 1.f);
-            if (q < ng) {
-                const uint32_t r = pick(hash32(h * 8u + q), rows_t);
-                v[q] = __ldg(reinterpret_cast<const float4 *>(T + (size_t)r * (4 * LPE)) + j);
-            }
+        for (int q = 0; q < NG; ++q) {
+            x = x * 1664525u + 1013904223u;
+            v[q] = __ldg(reinterpret_cast<const float4 *>(T + (size_t)pick(x, rows_t) * (4 * LPE)) + j);
         }
-        float4 acc = v[0];
+        float4 acc = make_float4(1.f, 1.f, 1.f, 1.f);
 #pragma unroll
-        for (int q = 1; q < 8; ++q) {
+        for (int q = 0; q < NG; ++q) {
             acc.x *= v[q].x; acc.y *= v[q].y; acc.z *= v[q].z; acc.w *= v[q].w;
         }
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-            if (q < nr) {
-                const uint32_t r = pick(hash32((h * 8u + q) ^ 0x9e3779b9u), rows_u);
-                float *p = U + (size_t)r * (4 * LPE) + j * 4;
-                asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(acc.x), "f"(acc.y), "f"(acc.z),
-                             "f"(acc.w)
-                             : "memory");
-            }
+        for (int q = 0; q < NR; ++q) {
+            x = x * 1664525u + 1013904223u;
+            float *p = U + (size_t)pick(x, rows_u) * (4 * LPE) + j * 4;
+            asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(acc.x), "f"(acc.y), "f"(acc.z),
+                         "f"(acc.w)
+                         : "memory");
         }
+    }
+}
+
+using MixFn = void (*)(const float *, uint32_t, float *, uint32_t, int);
+template <int LPE>
+MixFn mix_of(int ng, int nr) {
+    switch (ng * 16 + nr) {
+        case 1 * 16 + 1: return mix_rows<LPE, 1, 1>;
+        case 2 * 16 + 1: return mix_rows<LPE, 2, 1>;
+        case 3 * 16 + 1: return mix_rows<LPE, 3, 1>;
+        case 3 * 16 + 2: return mix_rows<LPE, 3, 2>;
+        case 4 * 16 + 3: return mix_rows<LPE, 4, 3>;
+        case 5 * 16 + 2: return mix_rows<LPE, 5, 2>;
+        case 5 * 16 + 3: return mix_rows<LPE, 5, 3>;
+        case 5 * 16 + 4: return mix_rows<LPE, 5, 4>;
+        case 7 * 16 + 3: return mix_rows<LPE, 7, 3>;
+        case 7 * 16 + 4: return mix_rows<LPE, 7, 4>;
+        case 7 * 16 + 5: return mix_rows<LPE, 7, 5>;
+        case 8 * 16 + 3: return mix_rows<LPE, 8, 3>;
+        case 3 * 16 + 0: return mix_rows<LPE, 3, 0>;
+        case 0 * 16 + 2: return mix_rows<LPE, 0, 2>;
+        default: return nullptr;
     }
 }
 
@@ -215,13 +232,33 @@ BOUNDS_API int bounds_red(int row_bytes, int64_t table_bytes, int reps, double *
 }
 
 // units of (ng gathers + nr reductions) per second, rows of row_bytes, tables
-// of table_b / table_c bytes; ng, nr in [0, 8]
+// of table_b / table_c bytes; (ng, nr) one of the instantiated pairs
+// (bounds_mix_pairs lists them)
+BOUNDS_API int bounds_mix_pairs(int *out, int max_pairs) {
+    static const int pairs[][2] = {{1, 1}, {2, 1}, {3, 1}, {3, 2}, {4, 3}, {5, 2}, {5, 3},
+                                   {5, 4}, {7, 3}, {7, 4}, {7, 5}, {8, 3}, {3, 0}, {0, 2}};
+    const int n = static_cast<int>(sizeof(pairs) / sizeof(pairs[0]));
+    for (int k = 0; k < n && k < max_pairs; ++k) {
+        out[2 * k] = pairs[k][0];
+        out[2 * k + 1] = pairs[k][1];
+    }
+    return n;
+}
+
 BOUNDS_API int bounds_mix(int row_bytes, int64_t table_b, int64_t table_c, int ng, int nr, int reps,
                           double *units_per_s) {
     const int lpe = row_bytes / 16;
-    if (!units_per_s || ng < 0 || nr < 0 || ng > 8 || nr > 8 || ng + nr == 0 || table_b < row_bytes ||
-        table_c < row_bytes || (lpe != 1 && lpe != 2 && lpe != 4 && lpe != 8 && lpe != 16 && lpe != 32))
-        return static_cast<int>(cudaErrorInvalidValue);
+    MixFn fn = nullptr;
+    switch (lpe) {
+        case 1: fn = mix_of<1>(ng, nr); break;
+        case 2: fn = mix_of<2>(ng, nr); break;
+        case 4: fn = mix_of<4>(ng, nr); break;
+        case 8: fn = mix_of<8>(ng, nr); break;
+        case 16: fn = mix_of<16>(ng, nr); break;
+        case 32: fn = mix_of<32>(ng, nr); break;
+        default: break;
+    }
+    if (!units_per_s || !fn || table_b < row_bytes || table_c < row_bytes) return static_cast<int>(cudaErrorInvalidValue);
     const uint32_t rb = static_cast<uint32_t>(table_b / row_bytes), rc = static_cast<uint32_t>(table_c / row_bytes);
     float *T = nullptr, *U = nullptr;
     cudaError_t e = cudaMalloc(&T, static_cast<size_t>(rb) * row_bytes);
@@ -230,18 +267,8 @@ BOUNDS_API int bounds_mix(int row_bytes, int64_t table_b, int64_t table_c, int n
         (e = cudaMemset(T, 0, static_cast<size_t>(rb) * row_bytes)) == cudaSuccess &&
         (e = cudaMemset(U, 0, static_cast<size_t>(rc) * row_bytes)) == cudaSuccess) {
         const int blocks = sm_count() * 8, threads = 256, iters = 64;
-        auto launch = [&] {
-            switch (lpe) {
-                case 1: mix_rows<1><<<blocks, threads>>>(T, rb, U, rc, ng, nr, iters); break;
-                case 2: mix_rows<2><<<blocks, threads>>>(T, rb, U, rc, ng, nr, iters); break;
-                case 4: mix_rows<4><<<blocks, threads>>>(T, rb, U, rc, ng, nr, iters); break;
-                case 8: mix_rows<8><<<blocks, threads>>>(T, rb, U, rc, ng, nr, iters); break;
-                case 16: mix_rows<16><<<blocks, threads>>>(T, rb, U, rc, ng, nr, iters); break;
-                default: mix_rows<32><<<blocks, threads>>>(T, rb, U, rc, ng, nr, iters); break;
-            }
-        };
         float ms = 0.f;
-        e = best_ms(reps, launch, &ms);
+        e = best_ms(reps, [&] { fn<<<blocks, threads>>>(T, rb, U, rc, iters); }, &ms);
         const double units = static_cast<double>(blocks) * threads / lpe * iters;
         *units_per_s = units / (ms * 1e-3);
     }
