@@ -126,13 +126,19 @@ def mix_ratio(gathers, reds):
     return min(MIX_PAIRS, key=lambda gr: (abs(gr[0] / gr[1] - gathers / reds), gr[0] + gr[1]))
 
 
+L2_TABLE_CAP = 48 << 20     # the L2 roofline: tables of at most 48 MB stay L2-resident (L2 126 MB)
+
+
 def in_run_bounds(w, launch, st, nnz_local, dev_index=0):
     """The memory-system rates of this workload, measured on this GPU right
-    now (tools/bounds.cu): HBM stream read, random row gathers from a table of
-    B's footprint, red.global.add.v4.f32 of rows into a table of C's footprint
-    (x the replicas the launch used), and the kernel's MIX of the two (the
-    plan's ratio of gathered to reduced rows, reduced values depending on
-    gathered ones), rows of R*4 bytes."""
+    now (tools/bounds.cu), for the L2 roofline: HBM stream read; random
+    whole-row gathers from a table of B's footprint; red.global.add.v4.f32 of
+    rows into a table of C's footprint (x the replicas the launch used); and
+    the kernel's MIX of the two (its ratio of L2 gathers to reduced rows,
+    reduced values depending on gathered ones).  Rows of R*4 bytes; tables
+    capped at L2_TABLE_CAP (L2-resident) — where a footprint exceeds L2
+    (c3), DRAM misses are the kernel's distance to this bound and the
+    physical DRAM traffic is reported beside it."""
     import ctypes
     import __graft_entry__
     lib = ctypes.CDLL(__graft_entry__.build_bounds())
@@ -146,21 +152,24 @@ def in_run_bounds(w, launch, st, nnz_local, dev_index=0):
     hbm, gat, red, mix = ctypes.c_double(), ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
     copies = max(1, launch.get("copies", 1))
     terms = memory_terms(w, st, nnz_local, launch)
-    ng, nr = mix_ratio(st["G"], terms["red_rows"])
+    ng, nr = mix_ratio(terms["gather_rows"], terms["red_rows"])
+    tb = min(w.dim * rb, L2_TABLE_CAP)
+    tc = min(copies * w.dim * rb, L2_TABLE_CAP)
     with ClockSampler(dev_index, period=0.01) as clk:
         rc = [lib.bounds_hbm_read(2 << 30, 5, ctypes.byref(hbm)),
-              lib.bounds_gather(rb, w.dim * rb, 5, ctypes.byref(gat)),
-              lib.bounds_red(rb, copies * w.dim * rb, 5, ctypes.byref(red)),
-              lib.bounds_mix(rb, w.dim * rb, copies * w.dim * rb, ng, nr, 5, ctypes.byref(mix))]
+              lib.bounds_gather(rb, tb, 5, ctypes.byref(gat)),
+              lib.bounds_red(rb, tc, 5, ctypes.byref(red)),
+              lib.bounds_mix(rb, tb, tc, ng, nr, 5, ctypes.byref(mix))]
     if any(rc):
         return {"unavailable": f"bounds library returned {rc}"}
     return {"hbm_read_gbs": hbm.value, "l2_gather_gbs": gat.value, "l2_red_gbs": red.value,
             "l2_mix_gbs": mix.value * (ng + nr) * rb / 1e9, "mix_ratio": [ng, nr], "row_bytes": rb,
-            "gather_table_bytes": w.dim * rb, "red_table_bytes": copies * w.dim * rb,
+            "gather_table_bytes": tb, "red_table_bytes": tc,
             "clocks": clk.report(),
             "how": "tools/bounds.cu in this run: best of 5 launches each (148x8 blocks of 256 threads), "
-                   "2 GiB stream read; random whole-row float4 gathers / red.global.add.v4.f32; the mix "
-                   f"= {ng} gathers + {nr} reductions per unit, reduced values from the gathered rows"}
+                   "2 GiB stream read; random whole-row float4 gathers / red.global.add.v4.f32 over tables of "
+                   "the footprints (capped at 48 MB: L2-resident); the mix = "
+                   f"{ng} gathers + {nr} reductions per unit, reduced values from the gathered rows"}
 
 
 class ClockSampler:
@@ -218,20 +227,28 @@ def bytes_eff(order, nnz, G, R, dim):
 
 
 def memory_terms(w, st, nnz_local, launch):
-    """Algorithmic bytes of each memory operation class of one launch
-    (SURVEY.md §8(d) per-entry figures x the entries of the launch):
-    the stream (indices + value, read once), the B-row gathers (one row per
-    distinct index of each entry, G rows) and the C-row reductions (one row
-    per run-first position >= 1 of each entry, G - nnz, less the position-1
-    runs accumulated in registers when the launch did that, plus one row per
-    leading-run fragment)."""
+    """Bytes of each memory operation class of one launch, from the plan
+    statistics (SURVEY.md §8(d) per-entry figures x the entries of the
+    launch):
+      stream   indices + value of every stored entry, read once;
+      gather   the B rows the kernel must fetch past L1: one per distinct
+               index of each entry (G), less the leading-index rows equal to
+               the previous entry's (a leading run gathers its row once) and
+               the position-1 rows equal to the previous entry's (c_1 runs);
+               `gather_alg` is the north_star's algorithmic G rows;
+      red      the C rows reduced: one per run-first position >= 1 of each
+               entry (G - nnz), less the position-1 runs accumulated in
+               registers when the launch did that, plus one row per
+               leading-run fragment."""
     n, R = w.order, w.R
     row = R * 4
     n1 = sum(h for code, h in enumerate(st["pattern_hist"]) if not code & 1)   # entries with c1 != c0
     pos1 = launch.get("pos1", 0) == 1
-    red_rows = st["lead_runs"] + (st["G"] - nnz_local) - ((n1 - min(n1, st["pos1_runs"])) if pos1 else 0)
-    return {"stream": nnz_local * (4 * n + 4), "gather": st["G"] * row, "red": red_rows * row,
-            "red_rows": red_rows}
+    rep1 = n1 - min(n1, st["pos1_runs"])                                        # c1 equal to the previous entry's
+    red_rows = st["lead_runs"] + (st["G"] - nnz_local) - (rep1 if pos1 else 0)
+    gather_rows = st["G"] - (nnz_local - st["lead_runs"]) - rep1
+    return {"stream": nnz_local * (4 * n + 4), "gather": gather_rows * row, "red": red_rows * row,
+            "gather_alg": st["G"] * row, "gather_rows": gather_rows, "red_rows": red_rows}
 
 
 def roofline(terms, bounds, kern_ms, local_bytes_eff, peak_hbm, traffic):
@@ -254,6 +271,7 @@ def roofline(terms, bounds, kern_ms, local_bytes_eff, peak_hbm, traffic):
     rates = {"stream": bounds["hbm_read_gbs"], "gather": bounds["l2_gather_gbs"], "red": bounds["l2_red_gbs"],
              "mix": bounds["l2_mix_gbs"]}
     terms = dict(terms, mix=terms["gather"] + terms["red"])
+    extra = {k: terms[k] for k in ("gather_alg", "gather_rows", "red_rows") if k in terms}
     times = {k: terms[k] / (rates[k] * 1e9) for k in rates}
     bind = max(times, key=times.get)
     achieved = terms[bind] / t / 1e9
@@ -267,6 +285,7 @@ def roofline(terms, bounds, kern_ms, local_bytes_eff, peak_hbm, traffic):
            "traffic": traffic.get("dram_bytes_per_launch") if traffic else None,
            "algorithmic_bytes_per_launch": terms[bind], "kernel_ms": kern_ms, "t_bound_ms": times[bind] * 1e3,
            "terms_ms": {k: v * 1e3 for k, v in times.items()}, "terms_bytes": {k: terms[k] for k in rates},
+           "counts": extra,
            "rates_gbs": rates, "peak_kind": "measured in this run on this GPU (tools/bounds.cu), clocks in bounds",
            "bounds": bounds,
            "hbm": dict(eff, physical_gbs=phys, physical_frac_of_copy_peak=(phys / peak_hbm) if phys else None)}

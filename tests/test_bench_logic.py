@@ -28,7 +28,9 @@ def test_memory_terms_counts_reduced_rows():
     # 10 entries, all strict (code 0: c1 != c0), G = 30; 4 leading runs; 6 position-1 runs
     st = {"G": 30, "lead_runs": 4, "pos1_runs": 6, "pattern_hist": [10, 0, 0, 0] + [0] * 12}
     t = bench.memory_terms(W, st, 10, {"pos1": 0})
-    assert t["red_rows"] == 4 + 20 and t["stream"] == 10 * 16 and t["gather"] == 30 * 128
+    assert t["red_rows"] == 4 + 20 and t["stream"] == 10 * 16 and t["gather_alg"] == 30 * 128
+    # L2 gathers: G less the 6 repeated leading rows and the 4 repeated position-1 rows
+    assert t["gather_rows"] == 30 - (10 - 4) - (10 - 6) and t["gather"] == t["gather_rows"] * 128
     t1 = bench.memory_terms(W, st, 10, {"pos1": 1})
     assert t1["red_rows"] == 4 + 20 - (10 - 6)
 
