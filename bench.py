@@ -54,8 +54,11 @@ def parse():
                     help="N>1 exchange: whole C on every rank, or a row block of C per rank")
     ap.add_argument("--no-bounds", action="store_true", help="skip the in-run L2/HBM bound measurement")
     ap.add_argument("--no-ncu", action="store_true", help="skip the in-run ncu DRAM-traffic capture")
-    ap.add_argument("--paper-rule-s", type=float, default=3.0,
+    ap.add_argument("--paper-rule-s", "--budget-s", type=float, default=3.0,
                     help="the paper's timing rule (min over up to 10,000 runs or this many seconds, PAPER.md:740)")
+    ap.add_argument("--seed", type=int, default=None, help="another draw of the config's shape (default: its seed)")
+    ap.add_argument("--warm", action="store_true",
+                    help="no L2 flush between timed steps (B warm in L2); default: flushed (cold)")
     ap.add_argument("--dump-c", default="",
                     help="test mode: after timing, write the final C (rank 0; row blocks gathered) to this .npy")
     return ap.parse_args()
@@ -372,7 +375,9 @@ def config_dict(w, args):
     from synth import CONFIGS
     return {"workload": f"{w.name}: {CONFIGS[w.name].describe}" if w.name in CONFIGS else w.name,
             "order": w.order, "dim": w.dim, "nnz": w.nnz, "R": w.R,
-            "l2": "flushed between timed steps (256 MiB write outside the events)",
+            "l2": ("not flushed (--warm)" if args.warm else
+                   "flushed between timed steps (256 MiB write outside the events)"),
+            "seed": w.meta.get("seed"),
             "parallelism": f"nnz-slices x{args.gpus} + {args.collective}(C)" if args.gpus > 1 else "1 GPU"}
 
 
@@ -387,7 +392,7 @@ def parse_opts(s):
 def main():
     args = parse()
     from synth import generate
-    w = generate(args.config)
+    w = generate(args.config, seed=args.seed)
     if args.impl == "reference":
         run_reference(args, w)
         return
@@ -454,7 +459,8 @@ def main():
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
         for k in range(args.steps):
-            flush.fill_(float(k))              # L2 flush between timed steps, outside the events
+            if not args.warm:
+                flush.fill_(float(k))          # L2 flush between timed steps, outside the events
             step(ev[k])
         torch.cuda.synchronize()
     if dist is not None:

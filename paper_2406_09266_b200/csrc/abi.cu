@@ -173,6 +173,7 @@ void free_window(Plan *p, bool pooled, cudaStream_t s) {
 int plan_create_impl(Plan **out, int order, int64_t dim, int64_t nnz, const int32_t *idx, const float *vals,
                      cudaStream_t s, bool pooled, bool general = false, int band_request = 0,
                      bool window = false) {
+    NvtxRange nvtx_range_("systec_plan_create");
     *out = nullptr;
     int bits = 0;
     int rc = check_shape(order, dim, nnz, &bits);
@@ -305,6 +306,7 @@ int plan_create_impl(Plan **out, int order, int64_t dim, int64_t nnz, const int3
 }
 
 int execute_impl(Plan *p, const float *B, int R, float *C, const systec_exec_opts *opts, cudaStream_t s) {
+    NvtxRange nvtx_range_("systec_plan_execute");
     if (!p || !B || !C || R < 1) return SYSTEC_ERR_ARG;
     const size_t bytes = static_cast<size_t>(p->dim) * R * sizeof(float);
     if (overlap(B, bytes, C, bytes)) return SYSTEC_ERR_ALIAS;
@@ -537,6 +539,7 @@ cudaError_t cp_als_graph(Plan &p, float *B, int R, float *lambda, int max_iters,
 
 int systec_cp_als_sym(systec_plan plan, float *B, int R, float *lambda, int max_iters, double tol,
                       double *fit_host, int *iters_done, systec_stream_t stream) {
+    systec::NvtxRange nvtx_range_("systec_cp_als_sym");
     Plan *p = reinterpret_cast<Plan *>(plan);
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     if (!p || !B || !lambda || R < 1 || max_iters < 0) return SYSTEC_ERR_ARG;
@@ -792,6 +795,7 @@ int systec_plan_destroy(systec_plan plan) {
 
 int systec_mttkrp(int order, int64_t dim, int64_t nnz, const int32_t *idx, const float *vals, const float *B,
                   int R, float *C, systec_stream_t stream) {
+    systec::NvtxRange nvtx_range_("systec_mttkrp");
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     int bits = 0;
     int rc = systec::check_shape(order, dim, nnz, &bits);
@@ -991,6 +995,7 @@ int mttkrp_host_pipelined(int order, int64_t dim, int64_t nnz, int bits, const i
 
 int systec_mttkrp_host(int order, int64_t dim, int64_t nnz, const int32_t *idx_host, const float *vals_host,
                        const float *B_host, int R, float *C_host, systec_stream_t stream) {
+    systec::NvtxRange nvtx_range_("systec_mttkrp_host");
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     int bits = 0;
     int rc = systec::check_shape(order, dim, nnz, &bits);

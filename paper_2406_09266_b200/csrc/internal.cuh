@@ -4,10 +4,20 @@
 #include <cstdint>
 #include <mutex>
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include "../../include/systec.h"
 
 namespace systec {
+
+// NVTX range around an ABI call (prepare / execute / host call / CP-ALS):
+// visible in Nsight timelines, a no-op without an attached tool
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange &) = delete;
+    NvtxRange &operator=(const NvtxRange &) = delete;
+};
 
 // Prepared, canonicalised, lexicographically sorted structure-of-arrays stream.
 struct Plan {

@@ -255,29 +255,48 @@ def _cache_dir() -> str:
     return os.environ.get("SYSTEC_CACHE", "/tmp/systec_workloads")
 
 
-def generate(name: str, cache: bool = True) -> Workload:
+def _digest(w_idx, w_vals, w_B) -> dict:
+    import hashlib
+    return {k: hashlib.sha256(np.ascontiguousarray(a).view(np.uint8)).hexdigest()
+            for k, a in (("idx", w_idx), ("vals", w_vals), ("B", w_B))}
+
+
+def generate(name: str, cache: bool = True, seed: int | None = None) -> Workload:
     """The BASELINE.json config ``name`` (c1..c5), optionally cached on disk
-    (the cache only saves time; it is regenerated when absent)."""
+    (the cache only saves time; it is regenerated when absent or when its
+    SHA-256 manifest does not match the arrays).  ``seed`` overrides the
+    config's seed (a different draw of the same shape)."""
     s = CONFIGS[name]
-    path = os.path.join(_cache_dir(), f"{name}_{GEN_VERSION}.npz")
-    if cache and os.path.exists(path):
+    sd = s.seed if seed is None else int(seed)
+    tag = f"{name}_{GEN_VERSION}" + ("" if seed is None else f"_s{sd}")
+    path = os.path.join(_cache_dir(), f"{tag}.npz")
+    manifest = path[:-4] + ".sha256.json"
+    if cache and os.path.exists(path) and os.path.exists(manifest):
         try:
+            import json
             z = np.load(path)
-            return Workload(name, s.order, s.dim, s.R, z["idx"], z["vals"], z["B"],
-                            meta={"seed": s.seed, "mode": s.mode, "gen": GEN_VERSION, "cached": True})
+            idx, vals, B = z["idx"], z["vals"], z["B"]
+            with open(manifest) as f:
+                want = json.load(f)
+            if _digest(idx, vals, B) == want:
+                return Workload(name, s.order, s.dim, s.R, idx, vals, B,
+                                meta={"seed": sd, "mode": s.mode, "gen": GEN_VERSION, "cached": True})
         except Exception:
             pass
-    w = make(name, s.order, s.dim, s.nnz, s.R, s.seed, s.mode, s.n_forced, s.zipf_s)
+    w = make(name, s.order, s.dim, s.nnz, s.R, sd, s.mode, s.n_forced, s.zipf_s)
     if cache:
         try:
+            import json
             os.makedirs(_cache_dir(), exist_ok=True)
             tmp = path + f".{os.getpid()}.tmp.npz"
             np.savez(tmp, idx=w.idx, vals=w.vals, B=w.B)
+            with open(manifest + f".{os.getpid()}.tmp", "w") as f:
+                json.dump(_digest(w.idx, w.vals, w.B), f)
             os.replace(tmp, path)
+            os.replace(manifest + f".{os.getpid()}.tmp", manifest)
         except OSError:
             pass
     return w
-
 
 def small_random(order: int, dim: int, nnz: int, R: int, seed: int,
                  diag_frac: float = 0.2, mode: str = "strict") -> Workload:

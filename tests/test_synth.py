@@ -94,3 +94,24 @@ def test_banded_order2_generator():
     assert d.min() >= 0 and d.max() <= 40
     keys = w.idx[:, 0].astype(np.int64) * 5000 + w.idx[:, 1]
     assert np.all(np.diff(keys) > 0)          # sorted and distinct
+
+
+def test_cache_manifest_detects_corruption(tmp_path, monkeypatch):
+    """The on-disk workload cache carries a SHA-256 manifest: a corrupted
+    cache file is detected and the workload regenerated."""
+    import glob
+
+    import numpy as np
+
+    from synth import generate
+    monkeypatch.setenv("SYSTEC_CACHE", str(tmp_path))
+    w = generate("c1")
+    assert generate("c1").meta.get("cached")
+    f = glob.glob(str(tmp_path / "c1_*.npz"))[0]
+    z = dict(np.load(f))
+    z["vals"] = z["vals"] + 1
+    np.savez(f, **z)
+    w2 = generate("c1")
+    assert not w2.meta.get("cached") and np.array_equal(w2.vals, w.vals)
+    w3 = generate("c1", seed=9)
+    assert w3.meta["seed"] == 9 and not np.array_equal(w3.idx, w.idx)
