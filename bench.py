@@ -116,20 +116,25 @@ def ncu_traffic(config, opts_str, timeout=240):
                    "python tools/profile_one.py (cold L2: ncu flushes caches per replay), in this bench run"}
 
 
-MIX_PAIRS = [(1, 1), (2, 1), (3, 1), (3, 2), (4, 3), (5, 2), (5, 3), (5, 4), (7, 3), (7, 4), (7, 5), (8, 3)]
+MIX_PAIRS = [(1, 1), (2, 2), (3, 3), (4, 4), (2, 1), (3, 1), (3, 2), (4, 3), (5, 2), (5, 3), (5, 4), (7, 3), (7, 4),
+             (7, 5), (8, 3)]
 
 
-def mix_ratio(gathers, reds):
+def mix_ratio(gathers, reds, entries=0):
     """The instantiated (ng, nr) pair of tools/bounds.cu (bounds_mix_pairs)
-    whose ratio is closest to gathers / reds."""
+    whose ratio is closest to gathers / reds; among pairs within 5 % of it,
+    the one whose ng is closest to the gathers per stored entry (a unit then
+    has an entry's gathers in flight before its reductions, as the kernel)."""
     if reds <= 0:
         return 3, 0
     if gathers <= 0:
         return 0, 2
-    return min(MIX_PAIRS, key=lambda gr: (abs(gr[0] / gr[1] - gathers / reds), gr[0] + gr[1]))
-
-
-L2_TABLE_CAP = 48 << 20     # the L2 roofline: tables of at most 48 MB stay L2-resident (L2 126 MB)
+    target = gathers / reds
+    err = {p: abs(p[0] / p[1] - target) / target for p in MIX_PAIRS}
+    best = min(err.values())
+    close = [p for p in MIX_PAIRS if err[p] <= max(0.05, best + 1e-12)]
+    per_entry = gathers / entries if entries > 0 else 1.0
+    return min(close, key=lambda p: (abs(p[0] - per_entry), err[p]))
 
 
 def in_run_bounds(w, launch, st, nnz_local, dev_index=0):
@@ -155,7 +160,7 @@ def in_run_bounds(w, launch, st, nnz_local, dev_index=0):
     hbm, gat, red, mix = ctypes.c_double(), ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
     copies = max(1, launch.get("copies", 1))
     terms = memory_terms(w, st, nnz_local, launch)
-    ng, nr = mix_ratio(terms["gather_rows"], terms["red_rows"])
+    ng, nr = mix_ratio(terms["gather_rows"], terms["red_rows"], nnz_local)
     tb = min(w.dim * rb, L2_TABLE_CAP)
     tc = min(copies * w.dim * rb, L2_TABLE_CAP)
     with ClockSampler(dev_index, period=0.01) as clk:

@@ -114,6 +114,9 @@ template <int LPE>
 MixFn mix_of(int ng, int nr) {
     switch (ng * 16 + nr) {
         case 1 * 16 + 1: return mix_rows<LPE, 1, 1>;
+        case 2 * 16 + 2: return mix_rows<LPE, 2, 2>;
+        case 3 * 16 + 3: return mix_rows<LPE, 3, 3>;
+        case 4 * 16 + 4: return mix_rows<LPE, 4, 4>;
         case 2 * 16 + 1: return mix_rows<LPE, 2, 1>;
         case 3 * 16 + 1: return mix_rows<LPE, 3, 1>;
         case 3 * 16 + 2: return mix_rows<LPE, 3, 2>;
@@ -235,7 +238,7 @@ BOUNDS_API int bounds_red(int row_bytes, int64_t table_bytes, int reps, double *
 // of table_b / table_c bytes; (ng, nr) one of the instantiated pairs
 // (bounds_mix_pairs lists them)
 BOUNDS_API int bounds_mix_pairs(int *out, int max_pairs) {
-    static const int pairs[][2] = {{1, 1}, {2, 1}, {3, 1}, {3, 2}, {4, 3}, {5, 2}, {5, 3},
+    static const int pairs[][2] = {{1, 1}, {2, 2}, {3, 3}, {4, 4}, {2, 1}, {3, 1}, {3, 2}, {4, 3}, {5, 2}, {5, 3},
                                    {5, 4}, {7, 3}, {7, 4}, {7, 5}, {8, 3}, {3, 0}, {0, 2}};
     const int n = static_cast<int>(sizeof(pairs) / sizeof(pairs[0]));
     for (int k = 0; k < n && k < max_pairs; ++k) {
