@@ -137,6 +137,9 @@ def mix_ratio(gathers, reds, entries=0):
     return min(close, key=lambda p: (abs(p[0] - per_entry), err[p]))
 
 
+L2_TABLE_CAP = 48 << 20     # the L2 roofline: tables of at most 48 MB stay L2-resident (L2 126 MB)
+
+
 def in_run_bounds(w, launch, st, nnz_local, dev_index=0):
     """The memory-system rates of this workload, measured on this GPU right
     now (tools/bounds.cu), for the L2 roofline: HBM stream read; random

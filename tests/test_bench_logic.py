@@ -68,3 +68,32 @@ def test_mix_pairs_match_the_bounds_library():
     n = lib.bounds_mix_pairs(buf, 32)
     pairs = [(buf[2 * k], buf[2 * k + 1]) for k in range(n)]
     assert set(bench.MIX_PAIRS) <= set(pairs)
+
+
+def test_bench_functions_reference_defined_globals():
+    """Every global name a bench.py function loads (LOAD_GLOBAL, nested code
+    included) is defined in the module or a builtin — a NameError there would
+    only show on the GPU box."""
+    import builtins
+    import dis
+    import types
+
+    def globals_of(code):
+        for ins in dis.get_instructions(code):
+            if ins.opname == "LOAD_GLOBAL":
+                yield ins.argval
+        for c in code.co_consts:
+            if isinstance(c, types.CodeType):
+                yield from globals_of(c)
+
+    checked = 0
+    for name, obj in list(vars(bench).items()):
+        fns = [obj] if isinstance(obj, types.FunctionType) else \
+            [f for f in vars(obj).values() if isinstance(f, types.FunctionType)] if isinstance(obj, type) else []
+        for fn in fns:
+            if fn.__module__ != "bench":
+                continue
+            for ref in globals_of(fn.__code__):
+                assert ref in vars(bench) or hasattr(builtins, ref), f"{name} loads undefined global {ref}"
+                checked += 1
+    assert checked > 50
