@@ -1007,3 +1007,41 @@ def test_lane_bytes_32_launch_and_fallback(systec):
     parity(plan.execute(Bv, lane_bytes=32).cpu().numpy(), Cref, S)
     assert plan.last_launch()["vw"] == 4
     plan.destroy()
+
+
+@pytest.mark.slow
+def test_large_nnz_closed_form(systec):
+    """Half a billion stored entries (2^29 + 777, ragged): the prepared stream
+    spans 8.6 GB, so every 64-bit address path (bulk copies, gathers, unit
+    counters, 64-bit SoA offsets) runs past 2^32 bytes.  Integer closed form:
+    values and B = 1, entries (i, i+1, i+2) (strict: coefficient 2 at each
+    position) and (i, i, i) (coefficient 1 at position 0), so
+    C[q, r] = 2 * #strict entries naming q + #diagonal entries at q, exact in
+    fp32 (every row stays < 2^24); the expected counts come from np.bincount."""
+    import torch
+    dim = 1 << 16
+    nnz = (1 << 29) + 777
+    e = np.arange(nnz, dtype=np.int64)
+    i = (e * 40503) % (dim - 2)
+    diag = (e % 7) == 0
+    idx = np.empty((nnz, 3), np.int32)
+    idx[:, 0] = i
+    idx[:, 1] = np.where(diag, i, i + 1)
+    idx[:, 2] = np.where(diag, i, i + 2)
+    want = 2.0 * (np.bincount(idx[~diag].ravel(), minlength=dim)) + np.bincount(idx[diag, 0], minlength=dim)
+    assert want.max() < 2 ** 24
+    di = torch.from_numpy(idx).cuda()
+    del idx, e, i, diag
+    dv = torch.ones(nnz, dtype=torch.float32, device="cuda")
+    plan = systec.Plan(3, dim, di, dv)
+    del di, dv
+    st = plan.stats()
+    assert st["nnz"] == nnz and st["input_was_sorted"] == 0
+    B = torch.ones((dim, 8), dtype=torch.float32, device="cuda")
+    C = plan.execute(B).cpu().numpy()
+    launch = plan.last_launch()
+    plan.destroy()
+    for r in range(8):
+        assert np.array_equal(C[:, r].astype(np.float64), want), r
+    assert launch["dynamic"] == 1
+    print(f"nnz={nnz}: all {C.size} elements exact")
