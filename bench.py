@@ -120,21 +120,20 @@ MIX_PAIRS = [(1, 1), (2, 2), (3, 3), (4, 4), (2, 1), (3, 1), (3, 2), (4, 3), (5,
              (7, 5), (8, 3)]
 
 
-def mix_ratio(gathers, reds, entries=0):
-    """The instantiated (ng, nr) pair of tools/bounds.cu (bounds_mix_pairs)
-    whose ratio is closest to gathers / reds; among pairs within 5 % of it,
-    the one whose ng is closest to the gathers per stored entry (a unit then
-    has an entry's gathers in flight before its reductions, as the kernel)."""
+def mix_shapes(gathers, reds):
+    """The instantiated (ng, nr) pairs of tools/bounds.cu (bounds_mix_pairs)
+    within 5 % of the ratio gathers / reds (at least the closest one): the
+    mix is measured with each and its fastest rate is the bound — the rate
+    the memory system reaches for this mix given enough operations in
+    flight per unit."""
     if reds <= 0:
-        return 3, 0
+        return [(3, 0)]
     if gathers <= 0:
-        return 0, 2
+        return [(0, 2)]
     target = gathers / reds
     err = {p: abs(p[0] / p[1] - target) / target for p in MIX_PAIRS}
     best = min(err.values())
-    close = [p for p in MIX_PAIRS if err[p] <= max(0.05, best + 1e-12)]
-    per_entry = gathers / entries if entries > 0 else 1.0
-    return min(close, key=lambda p: (abs(p[0] - per_entry), err[p]))
+    return sorted((p for p in MIX_PAIRS if err[p] <= max(0.05, best + 1e-12)), key=lambda p: (err[p], p))
 
 
 L2_TABLE_CAP = 48 << 20     # the L2 roofline: tables of at most 48 MB stay L2-resident (L2 126 MB)
@@ -163,24 +162,28 @@ def in_run_bounds(w, launch, st, nnz_local, dev_index=0):
     hbm, gat, red, mix = ctypes.c_double(), ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
     copies = max(1, launch.get("copies", 1))
     terms = memory_terms(w, st, nnz_local, launch)
-    ng, nr = mix_ratio(terms["gather_rows"], terms["red_rows"], nnz_local)
+    shapes = mix_shapes(terms["gather_rows"], terms["red_rows"])
     tb = min(w.dim * rb, L2_TABLE_CAP)
     tc = min(copies * w.dim * rb, L2_TABLE_CAP)
+    mix_gbs = {}
     with ClockSampler(dev_index, period=0.01) as clk:
         rc = [lib.bounds_hbm_read(2 << 30, 5, ctypes.byref(hbm)),
               lib.bounds_gather(rb, tb, 5, ctypes.byref(gat)),
-              lib.bounds_red(rb, tc, 5, ctypes.byref(red)),
-              lib.bounds_mix(rb, tb, tc, ng, nr, 5, ctypes.byref(mix))]
+              lib.bounds_red(rb, tc, 5, ctypes.byref(red))]
+        for ng, nr in shapes:
+            rc.append(lib.bounds_mix(rb, tb, tc, ng, nr, 5, ctypes.byref(mix)))
+            mix_gbs[f"{ng}g{nr}r"] = mix.value * (ng + nr) * rb / 1e9
     if any(rc):
         return {"unavailable": f"bounds library returned {rc}"}
+    best = max(mix_gbs, key=mix_gbs.get)
     return {"hbm_read_gbs": hbm.value, "l2_gather_gbs": gat.value, "l2_red_gbs": red.value,
-            "l2_mix_gbs": mix.value * (ng + nr) * rb / 1e9, "mix_ratio": [ng, nr], "row_bytes": rb,
+            "l2_mix_gbs": mix_gbs[best], "mix_shape": best, "mix_shapes_gbs": mix_gbs, "row_bytes": rb,
             "gather_table_bytes": tb, "red_table_bytes": tc,
             "clocks": clk.report(),
             "how": "tools/bounds.cu in this run: best of 5 launches each (148x8 blocks of 256 threads), "
                    "2 GiB stream read; random whole-row float4 gathers / red.global.add.v4.f32 over tables of "
-                   "the footprints (capped at 48 MB: L2-resident); the mix = "
-                   f"{ng} gathers + {nr} reductions per unit, reduced values from the gathered rows"}
+                   "the footprints (capped at 48 MB: L2-resident); the mix = ng gathers + nr reductions per "
+                   "unit in the plan's ratio, reduced values from the gathered rows, fastest unit shape"}
 
 
 class ClockSampler:
