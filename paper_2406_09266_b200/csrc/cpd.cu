@@ -55,7 +55,16 @@ constexpr int kMaxCpR = 48;  // [R][2R] fp64 Gauss-Jordan tableau (36 KB) in sta
 // accumulates a tile in fp32 before adding it to fp64; the row groups are
 // summed in shared memory.  (Reading the rows straight from L1 instead, no
 // staging, measured 3x slower.)
-constexpr int kTileRows = 128;
+#ifndef SYSTEC_CPD_TILE_ROWS
+#define SYSTEC_CPD_TILE_ROWS 128
+#endif
+#ifndef SYSTEC_CPD_RING
+#define SYSTEC_CPD_RING 3
+#endif
+#ifndef SYSTEC_CPD_BPS
+#define SYSTEC_CPD_BPS 2
+#endif
+constexpr int kTileRows = SYSTEC_CPD_TILE_ROWS;
 constexpr int kRp = (kMaxCpR + 3) / 4 * 4;  // padded column count (multiple of 4)
 
 // rows [r0, r0+nr) of X[.][R] -> dst[nr][Rp] (zero-padded columns; 16-byte
@@ -90,7 +99,7 @@ __device__ __forceinline__ void stage_rows(float *__restrict__ dst, const float 
 // arithmetic — contiguous rows only (R % 4 == 0, 16-byte aligned bases).
 // (Double-buffered per-thread cp.async copies measured Gram 115 us on c3, the
 // bulk ring below is what runs now.)
-constexpr int kRingS = 3;
+constexpr int kRingS = SYSTEC_CPD_RING;
 struct TileRing {
     float *buf;       // [kRingS][NM][kTileRows * R]
     uint64_t *bars;   // [kRingS]
@@ -574,8 +583,10 @@ __global__ void __launch_bounds__(256) apply_inverse_kernel(const float *__restr
                                                             int64_t dim, int R, float *__restrict__ Bout,
                                                             const int *skip, bool ring) {
     if (skip && *skip) return;  // device-side loop: last iteration evaluates the fit only
-    extern __shared__ __align__(16) unsigned char cpd_smem[];  // ring: kRingS tiles of M (bulk copies)
-    __shared__ __align__(16) float Msync[kTileRows * RT];      // else one synchronously staged tile
+    // dynamic shared memory: the ring of kRingS tiles of M (bulk copies), or
+    // one synchronously staged tile [kTileRows][RT] when the ring cannot run
+    extern __shared__ __align__(16) unsigned char cpd_smem[];
+    float *Msync = reinterpret_cast<float *>(cpd_smem);
     const int tid = threadIdx.x;
     const int b = tid % RT, rg = tid / RT;
     constexpr int RGN = 256 / RT;
@@ -692,17 +703,19 @@ int sm_count() {
 }
 
 // partial blocks: >= 256 rows each, at most 2 per SM
-int cpd_partial_blocks() { return sm_count() * 2; }
+int cpd_partial_blocks() { return sm_count() * SYSTEC_CPD_BPS; }
 
 // the ring's dynamic shared-memory opt-in is per device: set before every
 // launch (a host-side attribute write), so a plan on any device gets it
 template <int RT>
 cudaError_t launch_apply_inverse(int PB, size_t rb, cudaStream_t s, const float *M, const float *W, int64_t dim,
                                  int R, float *B, const int *skip, bool ring) {
+    // the ring (RT == R) or one synchronously staged tile [kTileRows][RT]
+    const size_t smem = ring ? rb : static_cast<size_t>(kTileRows) * RT * 4;
     const cudaError_t attr = cudaFuncSetAttribute(apply_inverse_kernel<RT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                  static_cast<int>(ring_bytes(1, 32)));
+                                                  static_cast<int>(smem));
     if (attr != cudaSuccess) return attr;
-    apply_inverse_kernel<RT><<<PB, 256, rb, s>>>(M, W, dim, R, B, skip, ring);
+    apply_inverse_kernel<RT><<<PB, 256, smem, s>>>(M, W, dim, R, B, skip, ring);
     return cudaSuccess;
 }
 
