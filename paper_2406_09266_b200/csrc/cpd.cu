@@ -35,6 +35,7 @@
 // one block, in fp64).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "internal.cuh"
 #include "ptx.cuh"
@@ -204,6 +205,255 @@ __global__ void __launch_bounds__(256) gram_dots_partial_kernel(const float *__r
         double d = 0.0;
         for (int l = 0; l < dn; ++l) d += dred[l * R + tid];
         out[R * R + tid] = d;
+    }
+}
+
+// ---- tensor-core forms (R = 32): 3xTF32 mma.sync ----------------------------
+// Both dense passes are contractions over a dim x 32 matrix: pass A's Gram
+// M^T M (K = the rows) and pass B's M W (K = 32).  On FFMAs they are bound by
+// issue (c3: 41M / 52M warp instructions, 55-62 % issue-active, ncu
+// profiles/r02/cpd_c3_ncu_raw.csv); as m16n8k8 TF32 tensor-core MMAs they need a
+// tenth of the instructions.  fp32 accuracy is kept by the 3xTF32 split: x =
+// x_hi + x_lo with x_hi = tf32(x), x_lo = tf32(x - x_hi), and
+// a b ~ a_hi b_hi + a_hi b_lo + a_lo b_hi (relative error ~2^-21 per
+// product, fp32 accumulation inside the MMA, fp64 across tiles).
+__device__ __forceinline__ uint32_t tf32_of(float x) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ void split_tf32(float x, uint32_t &hi, uint32_t &lo) {
+    hi = tf32_of(x);
+    lo = tf32_of(x - __uint_as_float(hi));
+}
+// D (16x8, fp32) += A (16x8, tf32, row) * B (8x8, tf32, col)
+__device__ __forceinline__ void mma_tf32(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+    asm volatile("mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+                 "{%0,%1,%2,%3};"
+                 : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+                 : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ void mma3(float (&d)[4], const uint32_t (&ah)[4], const uint32_t (&al)[4], uint32_t bh0,
+                                     uint32_t bh1, uint32_t bl0, uint32_t bl1) {
+    mma_tf32(d, al, bh0, bh1);  // small terms first
+    mma_tf32(d, ah, bl0, bl1);
+    mma_tf32(d, ah, bh0, bh1);
+}
+
+// Pass A at R = 32 on tensor cores: part[blk] = {M^T M (32 x 32), dots M o B}.
+// Warp w takes rows [16w, 16w+16) of each 128-row tile (two K steps of 8
+// rows).  The output columns are permuted so that one LDS.128 gives a thread
+// all its fragments: logical column n = 8 nt + g lives at physical column
+// 4 g + nt, so thread (g = lane/4, t = lane%4) reads physical columns 4g..4g+3
+// of rows t and t+4 — the B fragments of the four n-tiles — and, the Gram
+// being M^T M, the A fragments of m-tile mb are the B fragments of n-tiles
+// 2mb and 2mb+1.  Only the upper block triangle is computed (6 of 8 16x8
+// tiles) and mirrored.  The column dots use float4 lanes as the FFMA form.
+__global__ void __launch_bounds__(256) gram_tc32_kernel(const float *__restrict__ X, const float *__restrict__ Y,
+                                                        int64_t dim, double *__restrict__ part) {
+    constexpr int R = 32;
+    extern __shared__ __align__(16) unsigned char cpd_smem[];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+    const int cq = tid % 8, rl = tid / 8, nrl = blockDim.x / 8;  // column dots: (row lane, float4 column)
+    const int64_t rows = (dim + gridDim.x - 1) / gridDim.x;
+    const int64_t lo = blockIdx.x * rows, hi = min(dim, lo + rows);
+    TileRing tr{reinterpret_cast<float *>(cpd_smem), reinterpret_cast<uint64_t *>(cpd_smem + ring_bytes(2, R) - kRingS * 8),
+                X, Y, 2, R, lo, hi};
+    const int64_t nt = lo < hi ? tr.ntiles() : 0;
+    if (tid == 0) {
+        tr.init();
+        for (int64_t q = 0; q < min(static_cast<int64_t>(kRingS - 1), nt); ++q) tr.issue(q);
+    }
+    __syncthreads();
+    // output tiles: (mb, nb) = (0,0) (0,1) (0,2) (0,3) (1,2) (1,3)
+    constexpr int kTiles = 6;
+    double acc[kTiles][4];
+#pragma unroll
+    for (int q = 0; q < kTiles; ++q)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc[q][e] = 0.0;
+    double dacc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int64_t k = 0; k < nt; ++k) {
+        const int nr = static_cast<int>(min(static_cast<int64_t>(kTileRows), hi - lo - k * kTileRows));
+        if (tid == 0 && k + kRingS - 1 < nt) {
+            fence_proxy_async_smem();
+            tr.issue(k + kRingS - 1);
+        }
+        const float *tx = tr.tile(k, 0), *ty = tr.tile(k, 1);
+        tr.wait(k);
+        for (int w0 = warp * 16; w0 < nr; w0 += 8 * 16) {  // (kTileRows 128: one slab per warp)
+            float f[kTiles][4];
+#pragma unroll
+            for (int q = 0; q < kTiles; ++q)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) f[q][e] = 0.f;
+#pragma unroll
+            for (int ks = 0; ks < 2; ++ks) {
+                const int r0 = w0 + ks * 8 + t, r1 = r0 + 4;  // rows past nr are zero-weighted below
+                const float4 v0 = r0 < nr ? *reinterpret_cast<const float4 *>(tx + r0 * R + 4 * g) : make_float4(0.f, 0.f, 0.f, 0.f);
+                const float4 v1 = r1 < nr ? *reinterpret_cast<const float4 *>(tx + r1 * R + 4 * g) : make_float4(0.f, 0.f, 0.f, 0.f);
+                uint32_t bh[4][2], bl[4][2];  // [n-tile][b0 / b1]
+                split_tf32(v0.x, bh[0][0], bl[0][0]); split_tf32(v1.x, bh[0][1], bl[0][1]);
+                split_tf32(v0.y, bh[1][0], bl[1][0]); split_tf32(v1.y, bh[1][1], bl[1][1]);
+                split_tf32(v0.z, bh[2][0], bl[2][0]); split_tf32(v1.z, bh[2][1], bl[2][1]);
+                split_tf32(v0.w, bh[3][0], bl[3][0]); split_tf32(v1.w, bh[3][1], bl[3][1]);
+#pragma unroll
+                for (int mb = 0; mb < 2; ++mb) {
+                    const uint32_t ah[4] = {bh[2 * mb][0], bh[2 * mb + 1][0], bh[2 * mb][1], bh[2 * mb + 1][1]};
+                    const uint32_t al[4] = {bl[2 * mb][0], bl[2 * mb + 1][0], bl[2 * mb][1], bl[2 * mb + 1][1]};
+#pragma unroll
+                    for (int nb = 2 * mb; nb < 4; ++nb) {
+                        const int q = mb == 0 ? nb : 2 + nb;  // (1,2) -> 4, (1,3) -> 5
+                        mma3(f[q], ah, al, bh[nb][0], bh[nb][1], bl[nb][0], bl[nb][1]);
+                    }
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < kTiles; ++q)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) acc[q][e] += f[q][e];
+        }
+        if (rl < nrl) {
+            float4 d = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int i = rl; i < nr; i += nrl) {
+                const float4 x4 = *reinterpret_cast<const float4 *>(tx + i * R + 4 * cq);
+                const float4 y4 = *reinterpret_cast<const float4 *>(ty + i * R + 4 * cq);
+                d.x = fmaf(x4.x, y4.x, d.x);
+                d.y = fmaf(x4.y, y4.y, d.y);
+                d.z = fmaf(x4.z, y4.z, d.z);
+                d.w = fmaf(x4.w, y4.w, d.w);
+            }
+            dacc[0] += d.x;
+            dacc[1] += d.y;
+            dacc[2] += d.z;
+            dacc[3] += d.w;
+        }
+        __syncthreads();  // tile k consumed: its slot may be refilled
+    }
+    // the 8 warps' tile sums in shared memory (fixed order), then the
+    // un-permuted, mirrored Gram and the dots into this block's partial
+    double *red = reinterpret_cast<double *>(cpd_smem);  // [R][R]
+    double *dred = red + R * R;                           // [nrl][R]
+    for (int w = 0; w < 8; ++w) {
+        if (warp == w) {
+#pragma unroll
+            for (int q = 0; q < kTiles; ++q) {
+                const int mb = q < 4 ? 0 : 1, nb = q < 4 ? q : q - 2;
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const int m = mb * 16 + g + ((e & 2) ? 8 : 0);  // logical row
+                    const int n = nb * 8 + 2 * t + (e & 1);           // logical column
+                    const int pm = (m % 8) * 4 + m / 8, pn = (n % 8) * 4 + n / 8;  // physical columns
+                    double &slot = red[pm * R + pn];
+                    slot = (w == 0 ? 0.0 : slot) + acc[q][e];
+                }
+            }
+        }
+        __syncthreads();
+    }
+    if (rl < nrl) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) dred[rl * R + 4 * cq + c] = dacc[c];
+    }
+    __syncthreads();
+    constexpr int W = R * R + R;
+    double *out = part + static_cast<int64_t>(blockIdx.x) * W;
+    for (int q = tid; q < R * R; q += blockDim.x) {
+        const int a = q / R, b = q % R;
+        // the computed block triangle: logical (m, n) with m/16 <= n/16, i.e. computed iff
+        // (logical index of a) block <= (logical index of b) block; take that entry or its mirror
+        const int la = (a % 4) * 8 + a / 4, lb = (b % 4) * 8 + b / 4;  // physical -> logical
+        out[q] = (la / 16 <= lb / 16) ? red[q] : red[b * R + a];
+    }
+    if (tid < R) {
+        double d = 0.0;
+        for (int l = 0; l < nrl; ++l) d += dred[l * R + tid];
+        out[R * R + tid] = d;
+    }
+}
+
+// Pass B at R = 32 on tensor cores: Bout = M W.  Warp w computes rows
+// [16w, 16w+16) of each 128-row tile, all 32 columns (four n-tiles, four K
+// steps).  K is permuted so that thread (g, t) reads physical columns
+// 8t..8t+7 of its two rows (two LDS.128 each): logical k = 8 ks + kk maps to
+// physical column 8 (kk % 4) + 2 ks + kk / 4, and W's fragments (loaded once,
+// split hi/lo, in registers) use the same map.  The result is written over
+// the warp's own rows of the staged tile and stored with coalesced float4
+// stores.
+__global__ void __launch_bounds__(256) apply_tc32_kernel(const float *__restrict__ M, const float *__restrict__ W,
+                                                         int64_t dim, float *__restrict__ Bout, const int *skip) {
+    if (skip && *skip) return;
+    constexpr int R = 32;
+    extern __shared__ __align__(16) unsigned char cpd_smem[];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+    uint32_t wh[4][4][2], wl[4][4][2];  // [k-step][n-tile][b0 / b1]
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks)
+#pragma unroll
+        for (int nb = 0; nb < 4; ++nb) {
+            const int k0 = 8 * t + 2 * ks, k1 = k0 + 1;  // physical rows of W for logical kk = t, t + 4
+            split_tf32(W[k0 * R + nb * 8 + g], wh[ks][nb][0], wl[ks][nb][0]);
+            split_tf32(W[k1 * R + nb * 8 + g], wh[ks][nb][1], wl[ks][nb][1]);
+        }
+    const int64_t rows = (dim + gridDim.x - 1) / gridDim.x;
+    const int64_t lo = blockIdx.x * rows, hi = min(dim, lo + rows);
+    TileRing tr{reinterpret_cast<float *>(cpd_smem), reinterpret_cast<uint64_t *>(cpd_smem + ring_bytes(1, R) - kRingS * 8),
+                M, nullptr, 1, R, lo, hi};
+    const int64_t nt = lo < hi ? tr.ntiles() : 0;
+    if (tid == 0) {
+        tr.init();
+        for (int64_t q = 0; q < min(static_cast<int64_t>(kRingS - 1), nt); ++q) tr.issue(q);
+    }
+    __syncthreads();
+    for (int64_t k = 0; k < nt; ++k) {
+        const int64_t r0g = lo + k * kTileRows;
+        const int nr = static_cast<int>(min(static_cast<int64_t>(kTileRows), hi - r0g));
+        if (tid == 0 && k + kRingS - 1 < nt) {
+            fence_proxy_async_smem();
+            tr.issue(k + kRingS - 1);
+        }
+        float *tm = tr.tile(k, 0);
+        tr.wait(k);
+        for (int w0 = warp * 16; w0 < nr; w0 += 8 * 16) {
+            const int ra = w0 + g, rb = ra + 8;  // rows past nr: garbage in, never stored
+            float acc[4][4];
+#pragma unroll
+            for (int nb = 0; nb < 4; ++nb)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) acc[nb][e] = 0.f;
+            const float4 a0 = *reinterpret_cast<const float4 *>(tm + ra * R + 8 * t);
+            const float4 a1 = *reinterpret_cast<const float4 *>(tm + ra * R + 8 * t + 4);
+            const float4 b0 = *reinterpret_cast<const float4 *>(tm + rb * R + 8 * t);
+            const float4 b1 = *reinterpret_cast<const float4 *>(tm + rb * R + 8 * t + 4);
+            const float ra8[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+            const float rb8[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+            for (int ks = 0; ks < 4; ++ks) {
+                // A fragment: (row g, kk = t) -> ra8[2 ks], (row g + 8, t) -> rb8[2 ks],
+                //             (row g, t + 4) -> ra8[2 ks + 1], (row g + 8, t + 4) -> rb8[2 ks + 1]
+                uint32_t ah[4], al[4];
+                split_tf32(ra8[2 * ks], ah[0], al[0]);
+                split_tf32(rb8[2 * ks], ah[1], al[1]);
+                split_tf32(ra8[2 * ks + 1], ah[2], al[2]);
+                split_tf32(rb8[2 * ks + 1], ah[3], al[3]);
+#pragma unroll
+                for (int nb = 0; nb < 4; ++nb)
+                    mma3(acc[nb], ah, al, wh[ks][nb][0], wh[ks][nb][1], wl[ks][nb][0], wl[ks][nb][1]);
+            }
+            __syncwarp();  // every lane has read the warp's rows
+#pragma unroll
+            for (int nb = 0; nb < 4; ++nb) {
+                *reinterpret_cast<float2 *>(tm + ra * R + nb * 8 + 2 * t) = make_float2(acc[nb][0], acc[nb][1]);
+                *reinterpret_cast<float2 *>(tm + rb * R + nb * 8 + 2 * t) = make_float2(acc[nb][2], acc[nb][3]);
+            }
+            __syncwarp();
+            const int nrow = min(16, nr - w0);
+            float4 *o4 = reinterpret_cast<float4 *>(Bout + (r0g + w0) * R);
+            const float4 *s4 = reinterpret_cast<const float4 *>(tm + w0 * R);
+            for (int q = lane; q < nrow * (R / 4); q += 32) o4[q] = s4[q];
+        }
+        fence_proxy_async_smem();  // this thread's writes to the slot precede the TMA refill
+        __syncthreads();           // tile k consumed: its slot may be refilled
     }
 }
 
@@ -721,6 +971,13 @@ cudaError_t launch_apply_inverse(int PB, size_t rb, cudaStream_t s, const float 
 
 bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
+// the tensor-core (3xTF32) forms of the R = 32 dense passes; SYSTEC_CPD_TC=0
+// selects the FFMA forms (measurements, A/B)
+bool use_tensor_cores() {
+    const char *v = std::getenv("SYSTEC_CPD_TC");  // read per call: the tests switch it
+    return !(v && v[0] == '0');
+}
+
 // ring form: R % 4 == 0 (contiguous 16-byte rows), R <= 32, 16-byte aligned bases
 bool gram_ring(int R, const float *B, const float *M) { return R % 4 == 0 && R <= 32 && aligned16(B) && aligned16(M); }
 
@@ -769,7 +1026,12 @@ cudaError_t gram_dots(const float *X, const float *Y, int64_t dim, int R, const 
             gram_dots_partial_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
             static_cast<int>(std::max(gram_smem_bytes(32, true), gram_smem_bytes(kMaxCpR, false))));
         if (attr != cudaSuccess) return attr;
-        if (gram_ring(R, X, Y)) {
+        if (R == 32 && gram_ring(R, X, Y) && use_tensor_cores()) {
+            const cudaError_t attr2 = cudaFuncSetAttribute(
+                gram_tc32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(gram_smem_bytes(32, true)));
+            if (attr2 != cudaSuccess) return attr2;
+            gram_tc32_kernel<<<PB, 256, gram_smem_bytes(32, true), s>>>(X, Y, dim, c.part);
+        } else if (gram_ring(R, X, Y)) {
             const cudaError_t attr2 = cudaFuncSetAttribute(
                 gram_dots_sym_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(gram_smem_bytes(32, true)));
             if (attr2 != cudaSuccess) return attr2;
@@ -835,6 +1097,13 @@ cudaError_t cpd_update(const Plan &p, const float *M, float *B, int R, float *fs
     const bool ring = R % 8 == 0 && R <= 32 && aligned16(M);
     const size_t rb = ring ? ring_bytes(1, R) : 0;
     cudaError_t e;
+    if (R == 32 && ring && use_tensor_cores()) {
+        if ((e = cudaFuncSetAttribute(apply_tc32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(rb))) != cudaSuccess)
+            return e;
+        apply_tc32_kernel<<<PB, 256, rb, s>>>(M, W, p.dim, B, skip);
+        return cudaGetLastError();
+    }
     switch ((R + 7) / 8) {
         case 1: e = launch_apply_inverse<8>(PB, rb, s, M, W, p.dim, R, B, skip, ring); break;
         case 2: e = launch_apply_inverse<16>(PB, rb, s, M, W, p.dim, R, B, skip, ring); break;

@@ -1045,3 +1045,31 @@ def test_large_nnz_closed_form(systec):
         assert np.array_equal(C[:, r].astype(np.float64), want), r
     assert launch["dynamic"] == 1
     print(f"nnz={nnz}: all {C.size} elements exact")
+
+
+@pytest.mark.parametrize("order,dim,nnz", [(3, 5000, 60000), (4, 300, 40000), (3, 1000, 3001)])
+def test_cp_als_tensor_core_passes(systec, order, dim, nnz, monkeypatch):
+    """R = 32: the dense passes run as 3xTF32 tensor-core MMAs (Gram of M with
+    permuted columns, M W with permuted K).  Iterates match the fp64 oracle
+    and the FFMA forms (SYSTEC_CPD_TC=0) to fp32 rounding; a dim that is not a
+    multiple of the 128-row tile exercises the ragged last tile."""
+    import torch
+    from oracle import cpd_ref
+    w = small_random(order, dim, nnz, 32, seed=nnz, diag_frac=0.1)
+    iters = 3
+    Bref, lref, fref = cpd_ref.cp_als_sym(order, dim, w.idx, w.vals, w.B, iters=iters)
+    di, dv, dB = to_dev(w.idx, w.vals, w.B)
+    plan = systec.Plan(order, dim, di, dv)
+    out = {}
+    for tc in ("1", "0"):
+        monkeypatch.setenv("SYSTEC_CPD_TC", tc)
+        B, lam, fits = plan.cp_als(dB.clone(), max_iters=iters, tol=0.0)
+        torch.cuda.synchronize()
+        out[tc] = (B.cpu().numpy(), lam.cpu().numpy(), np.asarray(fits))
+    for tc, (Bg, lg, fg) in out.items():
+        scale = np.abs(Bref).max()
+        assert np.max(np.abs(Bg - Bref)) / scale < 2e-4, tc
+        np.testing.assert_allclose(lg, lref, rtol=2e-4)
+        np.testing.assert_allclose(fg, fref, atol=2e-4)
+    assert np.max(np.abs(out["1"][0] - out["0"][0])) / np.abs(out["0"][0]).max() < 1e-5
+    plan.destroy()
