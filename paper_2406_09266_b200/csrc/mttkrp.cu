@@ -30,6 +30,15 @@ KernelFn pick(int order, int vw, int lpe, int vpl, bool pos1, bool pf) {
     }
 }
 
+KernelFn pick_full_naive(int order, int lpe) {
+    switch (order) {
+        case 3: return pick_full_naive_kernel<3>(lpe);
+        case 4: return pick_full_naive_kernel<4>(lpe);
+        case 5: return pick_full_naive_kernel<5>(lpe);
+        default: return nullptr;
+    }
+}
+
 KernelFn pick_full(int order, int lpe, bool pos1, bool occ) {
     switch (order) {
         case 3: return pick_full_kernel<3>(lpe, pos1, occ);
@@ -174,7 +183,9 @@ cudaError_t launch_mttkrp(const Plan &p, const float *B, int R, float *C, const 
     // the static split (order 2, dim 1e6, 10M nnz: R = 1 0.115 vs 0.123 ms,
     // R = 32 0.558 vs 0.568 ms static vs dynamic)
     // (the ablation builds keep the static split they were measured with)
-    const bool dyn = o.static_ranges <= 0 && o.ablation <= 0 && p.order >= 3 && R >= 8 && !p.general &&
+    // (the naive kernel over an expanded tensor gets the same distribution:
+    // it is the baseline of the paper's experiment, given its best form)
+    const bool dyn = o.static_ranges <= 0 && o.ablation <= 0 && p.order >= 3 && R >= 8 &&
                      p.nnz / 128 >= static_cast<int64_t>(sms) * 8;
     const int64_t rep_f = copies > 1 ? static_cast<int64_t>(copies) * plane : 0;
     const int64_t nctr = dyn ? counter_slots(R) : 0;
@@ -270,9 +281,9 @@ cudaError_t launch_mttkrp(const Plan &p, const float *B, int R, float *C, const 
     // fixed-rank build when R is exactly one float4 tile of 16 or 32 columns
     // (opts.fixed_rank: 0 auto = on, -1 off)
     bool full = false;
-    if (!v8 && o.fixed_rank >= 0 && vw == 4 && vpl == 1 && !pf && !p.general && tiles == 1 && R == lpe * 4 &&
+    if (!v8 && o.fixed_rank >= 0 && vw == 4 && vpl == 1 && !pf && tiles == 1 && R == lpe * 4 &&
         o.ablation <= 0 && K == default_K(E)) {
-        if (KernelFn ff = pick_full(p.order, lpe, pos1, occ5)) {
+        if (KernelFn ff = p.general ? pick_full_naive(p.order, lpe) : pick_full(p.order, lpe, pos1, occ5)) {
             fn = ff;
             full = true;
         }

@@ -542,6 +542,11 @@ template <int N> KernelFn pick_full_kernel(int lpe, bool pos1, bool occ);
 template <> KernelFn pick_full_kernel<3>(int lpe, bool pos1, bool occ);
 template <> KernelFn pick_full_kernel<4>(int lpe, bool pos1, bool occ);
 template <> KernelFn pick_full_kernel<5>(int lpe, bool pos1, bool occ);
+// fixed-rank builds of the naive (expanded-tensor) kernel: lpe 4 (R = 16) / 8 (R = 32)
+template <int N> KernelFn pick_full_naive_kernel(int lpe);
+template <> KernelFn pick_full_naive_kernel<3>(int lpe);
+template <> KernelFn pick_full_naive_kernel<4>(int lpe);
+template <> KernelFn pick_full_naive_kernel<5>(int lpe);
 // fixed-rank builds with 32-byte lanes (8 columns per lane, 256-bit gathers):
 // order 3 at R = 32 (4 lanes per entry), orders 4/5 at R = 16 (2 lanes)
 template <int N> KernelFn pick_full_v8_kernel(bool pos1);

@@ -96,4 +96,13 @@ KernelFn pick_full_v8_kernel<4>(bool pos1) {
                 : mttkrp_sym_kernel<4, 2, 1, 8, false, false, false, 0, 16>;
 }
 
+template <>
+KernelFn pick_full_naive_kernel<4>(int lpe) {
+    switch (lpe) {
+        case 4: return mttkrp_sym_kernel<4, 4, 1, 4, false, false, true, 0, 16>;
+        case 8: return mttkrp_sym_kernel<4, 8, 1, 4, false, false, true, 0, 32>;
+        default: return nullptr;
+    }
+}
+
 }  // namespace systec

@@ -456,10 +456,13 @@ def test_general_plan_vs_general_oracle(systec, n, dim, nnz, R):
         assert bplan.last_launch()["general"] == 1
 
 
-@pytest.mark.parametrize("n,dim,nnz,R", [(3, 60, 4000, 32), (4, 20, 3000, 16), (5, 12, 2000, 16)])
+@pytest.mark.parametrize("n,dim,nnz,R", [(3, 60, 4000, 32), (4, 20, 3000, 16), (5, 12, 2000, 16),
+                                          (3, 500, 200000, 32), (4, 60, 100000, 16), (5, 30, 40000, 16)])
 def test_general_plan_on_expansion_equals_symmetric(systec, n, dim, nnz, R):
     """The paper's comparison, on the GPU: the naive kernel over the expanded
-    tensor and the symmetric kernel over the canonical one agree."""
+    tensor and the symmetric kernel over the canonical one agree.  The larger
+    cases run the naive kernel in its fixed-rank build with the dynamic
+    distribution (as the symmetric kernel; static ranges checked too)."""
     import torch
     w = small_random(n, dim, nnz, R, seed=n + 5, diag_frac=0.2)
     Cref, S = oracle.mttkrp(n, dim, w.idx, w.vals, w.B)
@@ -469,6 +472,10 @@ def test_general_plan_on_expansion_equals_symmetric(systec, n, dim, nnz, R):
     C = plan.execute(dB)
     torch.cuda.synchronize()
     parity(C.cpu().numpy(), Cref, S)
+    if nnz >= 40000:
+        launch = plan.last_launch()
+        assert launch["general"] == 1 and launch["fixed_rank"] == 1 and launch["dynamic"] == 1
+        parity(plan.execute(dB, static_ranges=1, fixed_rank=-1).cpu().numpy(), Cref, S)
 
 
 # ---------------------------------------------------------------- ablation variants + graph capture
