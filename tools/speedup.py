@@ -61,9 +61,15 @@ def main():
         # (when the symmetric plan is banded) the same band shift on its last index
         shifts = [-1] + ([st["band_shift"]] if st["band_shift"] >= 0 else [])
         naive = {}
+        # ... and its best launch form: the default (fixed-rank build, dynamic
+        # units), software prefetch, static ranges, the general-rank build
+        forms = [{}, {"prefetch": 1}, {"static_ranges": 1}, {"fixed_rank": -1}, {"static_ranges": 1, "fixed_rank": -1}]
+        naive_forms = {}
         for sh in shifts:
             gen = systec.Plan(w.order, w.dim, ei, ev, general=True, band_shift=sh)
-            naive[sh] = (time_exec(gen, B, C2, a.reps, flush), time_exec(gen, B, C2, a.reps, flush, prefetch=1))
+            ts = [time_exec(gen, B, C2, a.reps, flush, **f) for f in forms]
+            naive[sh] = (ts[0], ts[1])
+            naive_forms[sh] = {",".join(f"{k}={v}" for k, v in f.items()) or "default": t for f, t in zip(forms, ts)}
             if sh != shifts[-1]:
                 gen.destroy()
         del ei, ev
@@ -75,11 +81,12 @@ def main():
         torch.cuda.synchronize()
         rel = float(((C1 - C2).abs().max() / C1.abs().max()).item())
         n = w.order
-        best_naive = min(min(v) for v in naive.values())
+        best_naive = min(min(v.values()) for v in naive_forms.values())
         print(json.dumps({
             "config": name, "order": n, "nnz": w.nnz, "expanded_nnz": m, "G": st["G"],
             "t_sym_ms": t_sym, "sym_band_shift": st["band_shift"], "t_naive_ms": t_naive, "t_naive_prefetch_ms": t_naive_pf,
             "t_naive_banded_ms": list(naive[shifts[-1]]) if len(shifts) > 1 else None, "t_naive_best_ms": best_naive,
+            "t_naive_forms_ms": {str(k): v for k, v in naive_forms.items()},
             "speedup": best_naive / t_sym,
             "expected_compute_ratio": math.factorial(n - 1), "expected_read_ratio": math.factorial(n),
             "paper_max_speedup_cpu": {3: 3.38, 4: 7.35, 5: 29.8}.get(n),
