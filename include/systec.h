@@ -104,7 +104,7 @@ typedef struct systec_exec_opts {
     int32_t occupancy;           /* order-3 R=32 kernel built for 5 blocks/SM: 1 on, -1 off,    */
                                  /* 0 auto (on when B > 64 MB and the plan is lexicographic)   */
     int32_t fixed_rank;          /* kernels built for R = 16 / 32 exactly (one float4 tile):    */
-                                 /* 0 auto (on when R matches), -1 off                          */
+                                 /* 0 auto (on when R matches; general plans: off), 1 on, -1 off */
     int32_t window;              /* order-2 plans created with systec_plan_opts.window = 1: the */
                                  /* atomic-free windowed kernel (each row block builds its     */
                                  /* rows' transposed entries in shared memory and writes every */

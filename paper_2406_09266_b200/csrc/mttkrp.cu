@@ -281,7 +281,11 @@ cudaError_t launch_mttkrp(const Plan &p, const float *B, int R, float *C, const 
     // fixed-rank build when R is exactly one float4 tile of 16 or 32 columns
     // (opts.fixed_rank: 0 auto = on, -1 off)
     bool full = false;
-    if (!v8 && o.fixed_rank >= 0 && vw == 4 && vpl == 1 && !pf && tiles == 1 && R == lpe * 4 &&
+    // (the naive kernel only on request, fixed_rank = 1: its general-rank build
+    // measured as fast or faster — c4's expanded tensor 6.33 vs 8.70 ms,
+    // profiles/r02/speedup_sym_vs_naive.jsonl)
+    if (!v8 && (p.general ? o.fixed_rank > 0 : o.fixed_rank >= 0) && vw == 4 && vpl == 1 && !pf && tiles == 1 &&
+        R == lpe * 4 &&
         o.ablation <= 0 && K == default_K(E)) {
         if (KernelFn ff = p.general ? pick_full_naive(p.order, lpe) : pick_full(p.order, lpe, pos1, occ5)) {
             fn = ff;

@@ -461,8 +461,8 @@ def test_general_plan_vs_general_oracle(systec, n, dim, nnz, R):
 def test_general_plan_on_expansion_equals_symmetric(systec, n, dim, nnz, R):
     """The paper's comparison, on the GPU: the naive kernel over the expanded
     tensor and the symmetric kernel over the canonical one agree.  The larger
-    cases run the naive kernel in its fixed-rank build with the dynamic
-    distribution (as the symmetric kernel; static ranges checked too)."""
+    cases run the naive kernel with the dynamic distribution (as the
+    symmetric kernel), its fixed-rank build on request and static ranges."""
     import torch
     w = small_random(n, dim, nnz, R, seed=n + 5, diag_frac=0.2)
     Cref, S = oracle.mttkrp(n, dim, w.idx, w.vals, w.B)
@@ -474,8 +474,10 @@ def test_general_plan_on_expansion_equals_symmetric(systec, n, dim, nnz, R):
     parity(C.cpu().numpy(), Cref, S)
     if nnz >= 40000:
         launch = plan.last_launch()
-        assert launch["general"] == 1 and launch["fixed_rank"] == 1 and launch["dynamic"] == 1
-        parity(plan.execute(dB, static_ranges=1, fixed_rank=-1).cpu().numpy(), Cref, S)
+        assert launch["general"] == 1 and launch["fixed_rank"] == 0 and launch["dynamic"] == 1
+        parity(plan.execute(dB, fixed_rank=1).cpu().numpy(), Cref, S)
+        assert plan.last_launch()["fixed_rank"] == 1
+        parity(plan.execute(dB, static_ranges=1).cpu().numpy(), Cref, S)
 
 
 # ---------------------------------------------------------------- ablation variants + graph capture
