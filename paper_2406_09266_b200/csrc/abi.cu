@@ -913,7 +913,11 @@ int mttkrp_host_pipelined(int order, int64_t dim, int64_t nnz, int bits, const i
         cudaPointerAttributes pa;
         const bool c_pinned = cudaPointerGetAttributes(&pa, C_host) == cudaSuccess && pa.type == cudaMemoryTypeHost;
         cudaGetLastError();  // clear a possible error from the query
-        ds = c_pinned ? copy_stream(1) : nullptr;
+        static const bool kEarly = [] {  // SYSTEC_HOST_EARLY=0: no early copies (measurements)
+            const char *v = std::getenv("SYSTEC_HOST_EARLY");
+            return !(v && v[0] == '0');
+        }();
+        ds = (c_pinned && kEarly) ? copy_stream(1) : nullptr;
         if (!ds) ds = s;
         bool bounds_sorted = true;  // chunk boundaries in canonical lexicographic order (host check)
         int64_t done_rows = 0;      // C rows [0, done_rows) already copied back
