@@ -895,12 +895,24 @@ int mttkrp_host_pipelined(int order, int64_t dim, int64_t nnz, int bits, const i
         if ((e = cudaMemsetAsync(d_C, 0, bb, s)) != cudaSuccess) break;
         if ((e = cudaEventRecord(ev[nch + 1], s)) != cudaSuccess) break;          // buffers exist
         if ((e = cudaStreamWaitEvent(cs, ev[nch + 1], 0)) != cudaSuccess) break;
+        // copy order: B and all values first (two copies), then the index
+        // chunks — every copy costs a fixed overhead on the copy engine, and
+        // the order does not change the total, only when chunk 0 can start
+        // (SYSTEC_HOST_VALS_CHUNKED=1: values per chunk, 2 copies per chunk)
+        static const bool kValsChunked = [] {
+            const char *v = std::getenv("SYSTEC_HOST_VALS_CHUNKED");
+            return v && v[0] == '1';
+        }();
         if ((e = cudaMemcpyAsync(d_B, B_host, bb, cudaMemcpyHostToDevice, cs)) != cudaSuccess) break;
+        if (!kValsChunked && (e = cudaMemcpyAsync(d_vals, vals_host, vb, cudaMemcpyHostToDevice, cs)) != cudaSuccess)
+            break;
         if ((e = cudaEventRecord(ev[nch], cs)) != cudaSuccess) break;
         for (int k = 0; k < nch && e == cudaSuccess; ++k) {
             const int64_t lo = k * per, n = std::min(per, nnz - lo);
             if ((e = cudaMemcpyAsync(d_idx + lo * order, idx_host + lo * order, n * order * 4, cudaMemcpyHostToDevice, cs)) != cudaSuccess) break;
-            if ((e = cudaMemcpyAsync(d_vals + lo, vals_host + lo, n * 4, cudaMemcpyHostToDevice, cs)) != cudaSuccess) break;
+            if (kValsChunked &&
+                (e = cudaMemcpyAsync(d_vals + lo, vals_host + lo, n * 4, cudaMemcpyHostToDevice, cs)) != cudaSuccess)
+                break;
             e = cudaEventRecord(ev[k], cs);
         }
         if (e != cudaSuccess) break;

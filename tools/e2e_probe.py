@@ -24,9 +24,12 @@ for _ in range(20):
     b.record(); b.synchronize(); ts.append(a.elapsed_time(b))
 print(json.dumps({"chunks": %s, "early": %s, "ms_min": min(ts), "ms_med": float(np.median(ts))}))
 '''
-for ch in (8, 16):
+for ch in (4, 8, 16):
     for early in (1, 0):
-        env = dict(os.environ, SYSTEC_HOST_CHUNKS=str(ch), SYSTEC_HOST_EARLY=str(early))
-        out = subprocess.run([sys.executable, "-c", CODE % (ROOT, ch, early)], env=env, capture_output=True, text=True,
-                             timeout=600)
-        print(out.stdout.strip() or out.stderr[-400:], flush=True)
+        for vc in (0, 1):
+            env = dict(os.environ, SYSTEC_HOST_CHUNKS=str(ch), SYSTEC_HOST_EARLY=str(early),
+                       SYSTEC_HOST_VALS_CHUNKED=str(vc))
+            out = subprocess.run([sys.executable, "-c", CODE % (ROOT, ch, early)], env=env, capture_output=True,
+                                 text=True, timeout=600)
+            print((out.stdout.strip()[:-1] + f', "vals_chunked": {vc}}}') if out.stdout.strip() else out.stderr[-400:],
+                  flush=True)
