@@ -494,8 +494,7 @@ cudaError_t cp_als_graph(Plan &p, float *B, int R, float *lambda, int max_iters,
             cudaSuccess)
             break;
         cudaError_t ce = launch_mttkrp(p, B, R, M, o, cs, scr);
-        if (ce == cudaSuccess) ce = cpd_fit_pieces(p, M, B, lambda, lambda, R, ds, fs, true, &st->skip_update, cs);
-        if (ce == cudaSuccess) ce = cpd_update(p, M, B, R, fs, &st->skip_update, cs);
+        if (ce == cudaSuccess) ce = cpd_step(p, M, B, R, ds, fs, true, false, &st->skip_update, cs);
         if (ce == cudaSuccess) ce = cpd_fit_check(ds, R, st, fits, tol, max_iters, h, cs);
         cudaGraph_t captured = nullptr;
         e = cudaStreamEndCapture(cs, &captured);
@@ -506,10 +505,11 @@ cudaError_t cp_als_graph(Plan &p, float *B, int R, float *lambda, int max_iters,
         if ((e = cpd_tensor_norm2(p, x2, s)) != cudaSuccess) break;
         if ((e = cpd_state_init(st, x2, max_iters, s)) != cudaSuccess) break;
         launched = true;
-        if ((e = cpd_init(p, B, R, ds, s)) != cudaSuccess) break;
+        if ((e = cpd_init(p, B, R, ds, fs, s)) != cudaSuccess) break;
         if ((e = launch_mttkrp(p, B, R, M, o, s, scr)) != cudaSuccess) break;
-        if ((e = cpd_step(p, M, B, lambda, R, ds, fs, false, false, s)) != cudaSuccess) break;
+        if ((e = cpd_step(p, M, B, R, ds, fs, false, false, nullptr, s)) != cudaSuccess) break;
         if ((e = cudaGraphLaunch(ge, s)) != cudaSuccess) break;
+        if ((e = cpd_finish(p, B, R, ds, lambda, s)) != cudaSuccess) break;
         CpdLoopState hst;
         if ((e = cudaMemcpyAsync(&hst, st, sizeof(hst), cudaMemcpyDeviceToHost, s)) != cudaSuccess) break;
         if ((e = cudaStreamSynchronize(s)) != cudaSuccess) break;
@@ -581,14 +581,14 @@ int systec_cp_als_sym(systec_plan plan, float *B, int R, float *lambda, int max_
         const double xn = sqrt(x2 > 0 ? x2 : 1e-300);
         double prev_fit = -1e300;
         double *scal = ds + systec::cpd_xhat2_offset(R);
-        if ((e = systec::cpd_init(*p, B, R, ds, s)) != cudaSuccess) break;
-        // iteration k: M = MTTKRP(X, B_k); the same pass yields fit(B_{k-1}-step iterate) pieces
+        if ((e = systec::cpd_init(*p, B, R, ds, fs, s)) != cudaSuccess) break;
+        // iteration k: M = MTTKRP(X, F_k); its pass yields the fit pieces of iterate k (k > 0)
         for (int it = 0; it <= max_iters; ++it) {
             systec_exec_opts o;
             std::memset(&o, 0, sizeof(o));
             if ((e = systec::launch_mttkrp(*p, B, R, M, o, s)) != cudaSuccess) break;
             const bool last = it == max_iters;
-            if ((e = systec::cpd_step(*p, M, B, lambda, R, ds, fs, it > 0, last, s)) != cudaSuccess) break;
+            if ((e = systec::cpd_step(*p, M, B, R, ds, fs, it > 0, last, nullptr, s)) != cudaSuccess) break;
             if (it > 0) {
                 if ((e = cudaMemcpyAsync(host, scal, 2 * sizeof(double), cudaMemcpyDeviceToHost, s)) != cudaSuccess) break;
                 if ((e = cudaStreamSynchronize(s)) != cudaSuccess) break;
@@ -602,6 +602,8 @@ int systec_cp_als_sym(systec_plan plan, float *B, int R, float *lambda, int max_
                 prev_fit = fit;
             }
         }
+        // B holds the factor scaled by lambda: unit columns, and lambda out
+        if (e == cudaSuccess) e = systec::cpd_finish(*p, B, R, ds, lambda, s);
     } while (false);
     cleanup();
     if (e != cudaSuccess) rc = systec::cuda_fail(e);

@@ -17,25 +17,34 @@
 //           ||X||^2   = sum_e v_e^2 * orbit_e   (each stored entry stands for its orbit),
 //           fit = 1 - sqrt(max(0, ||X||^2 - 2<X,Xhat> + ||Xhat||^2)) / ||X||.
 //
-// Dense passes per iteration (after the MTTKRP): TWO row passes over the
-// dim x R matrices, the normalisation folded into the R x R algebra.  Pass A
-// reads M and B once for G_M = M^T M and the column dots M o B; the Gram of
-// the current B, G_B = B^T B, is carried in fp64 from the previous iteration.
-// The small solve (one block, fp64) gives H^{-1}; then, since
-// B_new = M H^{-1} and H is symmetric,
-//     B_new^T B_new = H^{-1} G_M H^{-1}  =>  lambda_new = sqrt(diag(H^{-1} G_M H^{-1})),
-// so pass B writes the NORMALISED factor directly, B = M W with
-// W = H^{-1} diag(1/lambda_new), and the next G_B = diag(1/lambda) H^{-1} G_M
-// H^{-1} diag(1/lambda) needs no pass over B at all.  (Before: a Gram pass over
-// B, the apply pass, a column-norm reduction and a normalisation pass
-// reading and writing B again.)  The first iteration's G_B is one Gram pass
-// over the caller's B.
+// Dense work per iteration (after the MTTKRP): ONE row pass over the dim x R
+// matrices, the normalisation folded into the R x R algebra.  Two facts make
+// that possible:
+//   * B_new^T B_new = H^{-1} G_M H^{-1} for B_new = M H^{-1} (H symmetric), so
+//     the new lambda and the next G_B follow from G_M = M^T M alone;
+//   * MTTKRP is multilinear, MTTKRP(X, B diag(t)) = MTTKRP(X, B) diag(t)^{n-1},
+//     so the stored factor F may carry any known column scale t.
+// The pass reads M and F once: it accumulates G_M and the dots M o F (the
+// fit of the current iterate) and writes F_new = M W with W = diag(t)^{-(n-1)}
+// H^{-1} diag(1/lambda) — the current lambda predicts the new one, so F_new =
+// B_new diag(lambda_new / lambda) stays near unit columns.  The small solve
+// (one block, fp64, cp_small_kernel) then takes the exact new lambda and t from
+// diag(W^T G_M W) and builds the next W.  At R = 32 the pass is one fused
+// tensor-core kernel (pass_tc32_kernel); other ranks run it as a Gram/dots
+// launch and an apply launch.  Iteration 0 (the caller's factor, arbitrary
+// scale) runs the Gram first and writes B_1 normalised; the call ends with one
+// F /= t pass.  (Round 1: Gram of B, apply, column norms, normalise — four
+// passes; round 2 before this: Gram of M + apply — two.)  The first
+// iteration's G_B is one Gram pass over the caller's B.
 //
 // Every step runs in the kernels below (R <= 48; the small R x R algebra in
 // one block, in fp64).
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#ifdef SYSTEC_EXP_SMALL_CLOCKS
+#include <cstdio>
+#endif
 
 #include "internal.cuh"
 #include "ptx.cuh"
@@ -101,33 +110,36 @@ __device__ __forceinline__ void stage_rows(float *__restrict__ dst, const float 
 // (Double-buffered per-thread cp.async copies measured Gram 115 us on c3, the
 // bulk ring below is what runs now.)
 constexpr int kRingS = SYSTEC_CPD_RING;
-struct TileRing {
-    float *buf;       // [kRingS][NM][kTileRows * R]
-    uint64_t *bars;   // [kRingS]
+template <int S>
+struct TileRingT {
+    float *buf;       // [S][NM][kTileRows * R]
+    uint64_t *bars;   // [S]
     const float *X0, *X1;
     int NM, R;
     int64_t lo, hi;
     __device__ int64_t ntiles() const { return (hi - lo + kTileRows - 1) / kTileRows; }
     __device__ float *tile(int64_t k, int m) const {
-        return buf + (static_cast<size_t>(k % kRingS) * NM + m) * kTileRows * R;
+        return buf + (static_cast<size_t>(k % S) * NM + m) * kTileRows * R;
     }
     __device__ void init() const {  // thread 0, then a block barrier
-        for (int st = 0; st < kRingS; ++st) mbar_init(&bars[st], 1);
+        for (int st = 0; st < S; ++st) mbar_init(&bars[st], 1);
         fence_mbar_init();
     }
     __device__ void issue(int64_t k) const {  // thread 0
         const int64_t r0 = lo + k * kTileRows;
         const uint32_t bytes = static_cast<uint32_t>(min(static_cast<int64_t>(kTileRows), hi - r0) * R * 4);
-        uint64_t *bar = &bars[k % kRingS];
+        uint64_t *bar = &bars[k % S];
         const uint64_t pol = policy_evict_first();
         mbar_arrive_expect_tx(bar, bytes * NM);
         bulk_g2s(tile(k, 0), X0 + r0 * R, bytes, bar, pol);
         if (NM > 1) bulk_g2s(tile(k, 1), X1 + r0 * R, bytes, bar, pol);
     }
-    __device__ void wait(int64_t k) const { mbar_wait(&bars[k % kRingS], static_cast<uint32_t>((k / kRingS) & 1)); }
+    __device__ void wait(int64_t k) const { mbar_wait(&bars[k % S], static_cast<uint32_t>((k / S) & 1)); }
 };
+using TileRing = TileRingT<kRingS>;
+template <int S = kRingS>
 __host__ __device__ constexpr size_t ring_bytes(int NM, int R) {
-    return static_cast<size_t>(kRingS) * NM * kTileRows * R * 4 + kRingS * 8;
+    return static_cast<size_t>(S) * NM * kTileRows * R * 4 + S * 8;
 }
 
 __global__ void __launch_bounds__(256) gram_dots_partial_kernel(const float *__restrict__ B, const float *__restrict__ M,
@@ -235,8 +247,10 @@ __device__ __forceinline__ void mma_tf32(float (&d)[4], const uint32_t (&a)[4], 
 }
 __device__ __forceinline__ void mma3(float (&d)[4], const uint32_t (&ah)[4], const uint32_t (&al)[4], uint32_t bh0,
                                      uint32_t bh1, uint32_t bl0, uint32_t bl1) {
+#ifndef SYSTEC_EXP_1XTF32  // experiment builds only: one MMA (accuracy lost) to time the MMA share
     mma_tf32(d, al, bh0, bh1);  // small terms first
     mma_tf32(d, ah, bl0, bl1);
+#endif
     mma_tf32(d, ah, bh0, bh1);
 }
 
@@ -372,88 +386,207 @@ __global__ void __launch_bounds__(256) gram_tc32_kernel(const float *__restrict_
     }
 }
 
-// Pass B at R = 32 on tensor cores: Bout = M W.  Warp w computes rows
-// [16w, 16w+16) of each 128-row tile, all 32 columns (four n-tiles, four K
-// steps).  K is permuted so that thread (g, t) reads physical columns
-// 8t..8t+7 of its two rows (two LDS.128 each): logical k = 8 ks + kk maps to
-// physical column 8 (kk % 4) + 2 ks + kk / 4, and W's fragments (loaded once,
-// split hi/lo, in registers) use the same map.  The result is written over
-// the warp's own rows of the staged tile and stored with coalesced float4
-// stores.
-__global__ void __launch_bounds__(256) apply_tc32_kernel(const float *__restrict__ M, const float *__restrict__ W,
-                                                         int64_t dim, float *__restrict__ Bout, const int *skip) {
-    if (skip && *skip) return;
+// The one dense pass of an iteration at R = 32 (tensor cores, 3xTF32): every
+// 128-row tile of M and of the stored factor F arrives once through the
+// bulk-copy ring, and each warp, on its own 16 rows of the tile,
+//   (1) accumulates the Gram M^T M (gram_tc32_kernel's permuted-column MMAs),
+//   (2) accumulates the column dots M o F (the fit's <X, Xhat>; F is the
+//       factor the MTTKRP read),
+//   (3) computes F_new = M W with K permuted so that thread (g, t) reads
+//       physical columns 8t..8t+7 of its two rows (two LDS.128 each):
+//       logical k = 8 ks + kk maps to physical column 8 (kk % 4) + 2 ks + kk / 4,
+//       and W's fragments (loaded once, split hi/lo, in registers) use the
+//       same map; the result is stored over the same rows of F (unless a fit-only iteration:
+//       store == 0, or *skip set by the device loop).
+// Warp roles (16 warps, one block per SM): warps 0-7 do (1)-(2) and warps
+// 8-15 do (3) on the same 16-row slabs, so the two MMA streams interleave on
+// the tensor pipe (with 8 warps doing all three, 240 registers each, the pass
+// ran at 2 warps per scheduler: 102 us on c3, tensor pipe 42 % and DRAM 40 %
+// busy).  F's old rows are read by (2) from the ring, and (3) stores the new
+// rows straight to global memory: the ring slot is only refilled after the
+// tile's barrier.  kPassRing tiles in flight.
+#ifndef SYSTEC_CPD_PASS_RING
+#define SYSTEC_CPD_PASS_RING 5
+#endif
+constexpr int kPassRing = SYSTEC_CPD_PASS_RING;
+constexpr int kPassThreads = 512;
+__global__ void __launch_bounds__(kPassThreads, 1) pass_tc32_kernel(const float *__restrict__ M, float *F,
+                                                                    const float *__restrict__ W, int64_t dim,
+                                                                    double *__restrict__ part, int store,
+                                                                    const int *skip) {
     constexpr int R = 32;
     extern __shared__ __align__(16) unsigned char cpd_smem[];
+    const bool write = store && !(skip && *skip);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
-    uint32_t wh[4][4][2], wl[4][4][2];  // [k-step][n-tile][b0 / b1]
-#pragma unroll
-    for (int ks = 0; ks < 4; ++ks)
-#pragma unroll
-        for (int nb = 0; nb < 4; ++nb) {
-            const int k0 = 8 * t + 2 * ks, k1 = k0 + 1;  // physical rows of W for logical kk = t, t + 4
-            split_tf32(W[k0 * R + nb * 8 + g], wh[ks][nb][0], wl[ks][nb][0]);
-            split_tf32(W[k1 * R + nb * 8 + g], wh[ks][nb][1], wl[ks][nb][1]);
-        }
+    const bool gram_role = warp < 8;
+    const int w0 = (warp & 7) * 16;  // kTileRows == 128: one 16-row slab per warp of each role
     const int64_t rows = (dim + gridDim.x - 1) / gridDim.x;
     const int64_t lo = blockIdx.x * rows, hi = min(dim, lo + rows);
-    TileRing tr{reinterpret_cast<float *>(cpd_smem), reinterpret_cast<uint64_t *>(cpd_smem + ring_bytes(1, R) - kRingS * 8),
-                M, nullptr, 1, R, lo, hi};
+    TileRingT<kPassRing> tr{reinterpret_cast<float *>(cpd_smem),
+                            reinterpret_cast<uint64_t *>(cpd_smem + ring_bytes<kPassRing>(2, R) - kPassRing * 8),
+                            M, F, 2, R, lo, hi};
     const int64_t nt = lo < hi ? tr.ntiles() : 0;
     if (tid == 0) {
         tr.init();
-        for (int64_t q = 0; q < min(static_cast<int64_t>(kRingS - 1), nt); ++q) tr.issue(q);
+        for (int64_t q = 0; q < min(static_cast<int64_t>(kPassRing - 1), nt); ++q) tr.issue(q);
     }
     __syncthreads();
-    for (int64_t k = 0; k < nt; ++k) {
-        const int64_t r0g = lo + k * kTileRows;
-        const int nr = static_cast<int>(min(static_cast<int64_t>(kTileRows), hi - r0g));
-        if (tid == 0 && k + kRingS - 1 < nt) {
-            fence_proxy_async_smem();
-            tr.issue(k + kRingS - 1);
-        }
-        float *tm = tr.tile(k, 0);
-        tr.wait(k);
-        for (int w0 = warp * 16; w0 < nr; w0 += 8 * 16) {
-            const int ra = w0 + g, rb = ra + 8;  // rows past nr: garbage in, never stored
-            float acc[4][4];
+    constexpr int kTiles = 6;  // Gram output tiles (mb, nb): (0,0) (0,1) (0,2) (0,3) (1,2) (1,3)
+    double *red = reinterpret_cast<double *>(cpd_smem);  // [R][R] after the loop
+    double *dred = red + R * R;                           // [8 warps][4 row lanes][R]
+    if (gram_role) {
+        double acc[kTiles][4];
 #pragma unroll
-            for (int nb = 0; nb < 4; ++nb)
+        for (int q = 0; q < kTiles; ++q)
 #pragma unroll
-                for (int e = 0; e < 4; ++e) acc[nb][e] = 0.f;
-            const float4 a0 = *reinterpret_cast<const float4 *>(tm + ra * R + 8 * t);
-            const float4 a1 = *reinterpret_cast<const float4 *>(tm + ra * R + 8 * t + 4);
-            const float4 b0 = *reinterpret_cast<const float4 *>(tm + rb * R + 8 * t);
-            const float4 b1 = *reinterpret_cast<const float4 *>(tm + rb * R + 8 * t + 4);
-            const float ra8[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-            const float rb8[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
-#pragma unroll
-            for (int ks = 0; ks < 4; ++ks) {
-                // A fragment: (row g, kk = t) -> ra8[2 ks], (row g + 8, t) -> rb8[2 ks],
-                //             (row g, t + 4) -> ra8[2 ks + 1], (row g + 8, t + 4) -> rb8[2 ks + 1]
-                uint32_t ah[4], al[4];
-                split_tf32(ra8[2 * ks], ah[0], al[0]);
-                split_tf32(rb8[2 * ks], ah[1], al[1]);
-                split_tf32(ra8[2 * ks + 1], ah[2], al[2]);
-                split_tf32(rb8[2 * ks + 1], ah[3], al[3]);
-#pragma unroll
-                for (int nb = 0; nb < 4; ++nb)
-                    mma3(acc[nb], ah, al, wh[ks][nb][0], wh[ks][nb][1], wl[ks][nb][0], wl[ks][nb][1]);
+            for (int e = 0; e < 4; ++e) acc[q][e] = 0.0;
+        double dacc[4] = {0.0, 0.0, 0.0, 0.0};
+        const int dr = lane >> 3, dq = lane & 7;  // column dots: row dr + 4j of the slab, float4 column dq
+        for (int64_t k = 0; k < nt; ++k) {
+            const int nr = static_cast<int>(min(static_cast<int64_t>(kTileRows), hi - lo - k * kTileRows));
+            if (tid == 0 && k + kPassRing - 1 < nt) {
+                fence_proxy_async_smem();
+                tr.issue(k + kPassRing - 1);
             }
-            __syncwarp();  // every lane has read the warp's rows
+            const float *tx = tr.tile(k, 0), *ty = tr.tile(k, 1);
+            tr.wait(k);
+            if (w0 < nr) {
+                // (1) Gram
+                float f[kTiles][4];
+#pragma unroll
+                for (int q = 0; q < kTiles; ++q)
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) f[q][e] = 0.f;
+#pragma unroll
+                for (int ks = 0; ks < 2; ++ks) {
+                    const int q0 = w0 + ks * 8 + t, q1 = q0 + 4;  // rows past nr are zero-weighted
+                    const float4 v0 = q0 < nr ? *reinterpret_cast<const float4 *>(tx + q0 * R + 4 * g) : make_float4(0.f, 0.f, 0.f, 0.f);
+                    const float4 v1 = q1 < nr ? *reinterpret_cast<const float4 *>(tx + q1 * R + 4 * g) : make_float4(0.f, 0.f, 0.f, 0.f);
+                    uint32_t bh[4][2], bl[4][2];
+                    split_tf32(v0.x, bh[0][0], bl[0][0]); split_tf32(v1.x, bh[0][1], bl[0][1]);
+                    split_tf32(v0.y, bh[1][0], bl[1][0]); split_tf32(v1.y, bh[1][1], bl[1][1]);
+                    split_tf32(v0.z, bh[2][0], bl[2][0]); split_tf32(v1.z, bh[2][1], bl[2][1]);
+                    split_tf32(v0.w, bh[3][0], bl[3][0]); split_tf32(v1.w, bh[3][1], bl[3][1]);
+#pragma unroll
+                    for (int mb = 0; mb < 2; ++mb) {
+                        const uint32_t ah[4] = {bh[2 * mb][0], bh[2 * mb + 1][0], bh[2 * mb][1], bh[2 * mb + 1][1]};
+                        const uint32_t al[4] = {bl[2 * mb][0], bl[2 * mb + 1][0], bl[2 * mb][1], bl[2 * mb + 1][1]};
+#pragma unroll
+                        for (int nb = 2 * mb; nb < 4; ++nb) {
+                            const int q = mb == 0 ? nb : 2 + nb;
+                            mma3(f[q], ah, al, bh[nb][0], bh[nb][1], bl[nb][0], bl[nb][1]);
+                        }
+                    }
+                }
+#pragma unroll
+                for (int q = 0; q < kTiles; ++q)
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) acc[q][e] += f[q][e];
+                // (2) column dots M o F over the slab's rows
+                float4 d = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const int i = w0 + dr + 4 * j;
+                    if (i < nr) {
+                        const float4 x4 = *reinterpret_cast<const float4 *>(tx + i * R + 4 * dq);
+                        const float4 y4 = *reinterpret_cast<const float4 *>(ty + i * R + 4 * dq);
+                        d.x = fmaf(x4.x, y4.x, d.x);
+                        d.y = fmaf(x4.y, y4.y, d.y);
+                        d.z = fmaf(x4.z, y4.z, d.z);
+                        d.w = fmaf(x4.w, y4.w, d.w);
+                    }
+                }
+                dacc[0] += d.x;
+                dacc[1] += d.y;
+                dacc[2] += d.z;
+                dacc[3] += d.w;
+            }
+            __syncthreads();  // tile k consumed by every warp: its slot may be refilled
+        }
+        // the 8 gram warps' sums in shared memory in a fixed order (named
+        // barrier 1: these warps only; the ring is idle once every tile's
+        // block barrier has passed), un-permuted below
+        for (int w = 0; w < 8; ++w) {
+            if (warp == w) {
+#pragma unroll
+                for (int q = 0; q < kTiles; ++q) {
+                    const int mb = q < 4 ? 0 : 1, nb = q < 4 ? q : q - 2;
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const int m = mb * 16 + g + ((e & 2) ? 8 : 0);
+                        const int n = nb * 8 + 2 * t + (e & 1);
+                        const int pm = (m % 8) * 4 + m / 8, pn = (n % 8) * 4 + n / 8;
+                        double &slot = red[pm * R + pn];
+                        slot = (w == 0 ? 0.0 : slot) + acc[q][e];
+                    }
+                }
+            }
+            asm volatile("bar.sync 1, 256;" ::: "memory");
+        }
+#pragma unroll
+        for (int c = 0; c < 4; ++c) dred[(warp * 4 + dr) * R + 4 * dq + c] = dacc[c];
+    } else {
+        uint32_t wh[4][4][2], wl[4][4][2];  // W fragments, permuted K
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks)
 #pragma unroll
             for (int nb = 0; nb < 4; ++nb) {
-                *reinterpret_cast<float2 *>(tm + ra * R + nb * 8 + 2 * t) = make_float2(acc[nb][0], acc[nb][1]);
-                *reinterpret_cast<float2 *>(tm + rb * R + nb * 8 + 2 * t) = make_float2(acc[nb][2], acc[nb][3]);
+                const int k0 = 8 * t + 2 * ks, k1 = k0 + 1;
+                split_tf32(W[k0 * R + nb * 8 + g], wh[ks][nb][0], wl[ks][nb][0]);
+                split_tf32(W[k1 * R + nb * 8 + g], wh[ks][nb][1], wl[ks][nb][1]);
             }
-            __syncwarp();
-            const int nrow = min(16, nr - w0);
-            float4 *o4 = reinterpret_cast<float4 *>(Bout + (r0g + w0) * R);
-            const float4 *s4 = reinterpret_cast<const float4 *>(tm + w0 * R);
-            for (int q = lane; q < nrow * (R / 4); q += 32) o4[q] = s4[q];
+        for (int64_t k = 0; k < nt; ++k) {
+            const int64_t r0g = lo + k * kTileRows;
+            const int nr = static_cast<int>(min(static_cast<int64_t>(kTileRows), hi - r0g));
+            const float *tx = tr.tile(k, 0);
+            tr.wait(k);
+            if (write && w0 < nr) {
+                // (3) F_new = M W for the slab
+                const int ra = w0 + g, rb = ra + 8;  // rows past nr: computed, never stored
+                float o[4][4];
+#pragma unroll
+                for (int nb = 0; nb < 4; ++nb)
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) o[nb][e] = 0.f;
+                const float4 a0 = *reinterpret_cast<const float4 *>(tx + ra * R + 8 * t);
+                const float4 a1 = *reinterpret_cast<const float4 *>(tx + ra * R + 8 * t + 4);
+                const float4 b0 = *reinterpret_cast<const float4 *>(tx + rb * R + 8 * t);
+                const float4 b1 = *reinterpret_cast<const float4 *>(tx + rb * R + 8 * t + 4);
+                const float ra8[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+                const float rb8[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+                for (int ks = 0; ks < 4; ++ks) {
+                    uint32_t ah[4], al[4];
+                    split_tf32(ra8[2 * ks], ah[0], al[0]);
+                    split_tf32(rb8[2 * ks], ah[1], al[1]);
+                    split_tf32(ra8[2 * ks + 1], ah[2], al[2]);
+                    split_tf32(rb8[2 * ks + 1], ah[3], al[3]);
+#pragma unroll
+                    for (int nb = 0; nb < 4; ++nb)
+                        mma3(o[nb], ah, al, wh[ks][nb][0], wh[ks][nb][1], wl[ks][nb][0], wl[ks][nb][1]);
+                }
+                float *fa = F + (r0g + ra) * R + 2 * t, *fb = F + (r0g + rb) * R + 2 * t;
+#pragma unroll
+                for (int nb = 0; nb < 4; ++nb) {
+                    if (ra < nr) *reinterpret_cast<float2 *>(fa + nb * 8) = make_float2(o[nb][0], o[nb][1]);
+                    if (rb < nr) *reinterpret_cast<float2 *>(fb + nb * 8) = make_float2(o[nb][2], o[nb][3]);
+                }
+            }
+            __syncthreads();  // tile k consumed by every warp: its slot may be refilled
         }
-        fence_proxy_async_smem();  // this thread's writes to the slot precede the TMA refill
-        __syncthreads();           // tile k consumed: its slot may be refilled
+    }
+    __syncthreads();  // the ring is idle: its memory holds the reductions
+    constexpr int Wd = R * R + R;
+    double *out = part + static_cast<int64_t>(blockIdx.x) * Wd;
+    for (int q = tid; q < R * R; q += blockDim.x) {
+        const int a = q / R, b = q % R;
+        const int la = (a % 4) * 8 + a / 4, lb = (b % 4) * 8 + b / 4;
+        out[q] = (la / 16 <= lb / 16) ? red[q] : red[b * R + a];
+    }
+    if (tid < R) {
+        double d = 0.0;
+        for (int l = 0; l < 32; ++l) d += dred[l * R + tid];
+        out[R * R + tid] = d;
     }
 }
 
@@ -682,150 +815,323 @@ __global__ void tensor_norm_kernel(const int32_t *__restrict__ coords, int64_t l
     if ((threadIdx.x & 31) == 0) atomicAdd(out, acc);
 }
 
-// One block of 1024 threads: H = G^{.(n-1)} (+ a tiny relative ridge for
-// safety), Hinv = H^{-1} by Gauss-Jordan elimination on the tableau [H | I] (H
-// is SPD: no pivoting).  The tableau lives in registers: thread t owns row
-// t / TPR and the CW columns [k*CW, (k+1)*CW), k = t % TPR (TPR = 64, 32, 16
-// for R <= 16, 32, 48; CW = 1, 2, 6); each step publishes the pivot row and
-// the pivot column through shared memory (double-buffered: two barriers per
-// step).  With lam also the fit pieces ||Xhat||^2 = lam^T G^{.n} lam and
-// <X,Xhat> = lam . dots.
+// The R x R algebra of an iteration, one block of 1024 threads, fp64.
 //
-// Then, unless this is a fit-only iteration (update == 0, or *skip set by
-// the device loop), the update's R x R algebra in the same block:
-// P = H^{-1} G_M H^{-1} (= B_new^T B_new for B_new = M H^{-1}), lambda =
-// sqrt(diag P), W = H^{-1} diag(1/lambda) (fp32, for the apply pass) and the
-// next iteration's G = diag(1/lambda) P diag(1/lambda), written over G (read
-// only at the start).  A zero column (lambda = 0) is left unscaled, as
-// B_new's column is then 0.
-template <int CW>
-__global__ void __launch_bounds__(1024) small_solve_kernel(double *__restrict__ G, int R, int n,
-                                                           const float *__restrict__ lam,
-                                                           const double *__restrict__ dots,
-                                                           double *__restrict__ xhat2, const double *__restrict__ GM,
-                                                           float *__restrict__ W, float *__restrict__ lam_out,
-                                                           int update, const int *skip) {
-    constexpr int TPR = CW == 1 ? 64 : CW == 2 ? 32 : 16;
+// State (fp64, per column r): lambda_r of the current iterate B (unit
+// columns), the scale t_r of the stored factor F = B diag(t), and the divisor
+// lt_r folded into W when it was built.  G_B = B^T B is carried.  The MTTKRP
+// reads F, so M = MTTKRP(X, F) = MTTKRP(X, B) diag(t)^{n-1} (multilinearity).
+//   FIT      <X, Xhat> = sum_r lambda_r dots_r / t_r^n  (dots = sum_i M o F),
+//            ||Xhat||^2 = lambda^T G_B^{.n} lambda.
+//   UPDATE   the pass writes F_new = M W = B_new diag(lambda_new / lt), so
+//            P = F_new^T F_new = W^T G_M W,  t = sqrt(diag P),
+//            lambda = t lt,  G_B = diag(1/t) P diag(1/t).
+//   PRENORM  (two-pass form, iteration 0, before the pass writes)
+//            W <- W diag(1/t), t = 1: the pass then writes the unit-column
+//            B_new itself.  lambda_1 carries the caller's column norms c of
+//            B_0 (lambda_1 ~ c^{-(n-1)}), so the next prediction is taken
+//            as pf lambda with pf = c^{n-1} (a unit-column B_0's lambda_1).
+//   SOLVE    H = G_B^{.(n-1)} (+ a tiny relative ridge), H^{-1} by in-place
+//            Gauss-Jordan elimination (SPD: no pivoting), and the next
+//            pass's W = diag(t)^{-(n-1)} H^{-1} diag(1/lt) with lt = pf lambda
+//            (pf = 1 after iteration 0): B_new = MTTKRP(X, B) H^{-1}
+//            diag(1/lambda_new) and the current lambda predicts lambda_new,
+//            so the stored F stays near unit columns (t = lambda_new /
+//            lambda) without a pass of its own.
+// A zero column (lambda = 0) keeps t = lt = 1.  UPDATE, PRENORM and SOLVE
+// are dropped when *skip (the device loop's fit-only iteration).  H lives in
+// registers: thread t owns row t / TPR and the CW columns [k*CW, (k+1)*CW),
+// k = t % TPR (TPR = 16, 32, 16 for R <= 16, 32, 48; CW = 1, 1, 3); each
+// elimination step publishes the pivot row, column and reciprocal through
+// shared memory (double-buffered: one barrier per step).
+enum : int { kFit = 1, kUpdate = 2, kSolve = 4, kPrenorm = 8 };
+struct CpdCols {
+    double *lam, *t, *lt, *pf;  // [R] each
+};
+#ifndef SYSTEC_CPD_SMALL_T
+#define SYSTEC_CPD_SMALL_T 1024
+#endif
+constexpr int kSmallT = SYSTEC_CPD_SMALL_T;  // threads of the small block
+constexpr int pow2_floor(int x) { return x >= 2 ? 2 * pow2_floor(x / 2) : 1; }
+template <int RC>  // rank class: R <= RC (16, 32, 48)
+__global__ void __launch_bounds__(kSmallT, 1) cp_small_kernel(double *__restrict__ GB, int R, int n, CpdCols cols,
+                                                           const double *__restrict__ dots, double *__restrict__ xhat2,
+                                                           const double *__restrict__ GM, float *__restrict__ W,
+                                                           int flags, const int *skip) {
+    // H: thread t owns row t / TPR and the CW columns [k*CW, (k+1)*CW), k = t % TPR
+    constexpr int TPR = pow2_floor(kSmallT / RC) < RC ? pow2_floor(kSmallT / RC) : RC;
+    constexpr int CW = (RC + TPR - 1) / TPR;
+    constexpr int kPq = (kMaxCpR * kMaxCpR + kSmallT - 1) / kSmallT;
+    // every operand is staged in shared memory first (one coalesced load each):
+    // the block is a single SM, and dependent global loads were most of its time
+    extern __shared__ __align__(16) unsigned char cpd_smem[];
+    const int RR = R * R;
+    double *As = reinterpret_cast<double *>(cpd_smem);  // W
+    double *Gs = As + RR;                                // G_M
+    double *Ts = Gs + RR;                                // G_M W, then P, then G_B
+    double *Bs = Ts + RR;                                // G_B (current)
+    double *lam = Bs + RR, *ts = lam + R, *lt = ts + R, *pf = lt + R, *dt = pf + R;
     __shared__ double piv[2][2 * kMaxCpR];
-    __shared__ double Hs[kMaxCpR * kMaxCpR];  // H^{-1}, then the update's products
-    __shared__ double Ts[kMaxCpR * kMaxCpR];
-    __shared__ double inv[kMaxCpR];
     __shared__ double fcol[2][kMaxCpR];
-    __shared__ double red[1024];
+    __shared__ double pinv[2];
+    __shared__ double red[32];
     __shared__ double ridge_s;
-    const int tid = threadIdx.x, nt = blockDim.x;
-    const int W2 = 2 * R;
-    const int row = tid / TPR, k = tid % TPR;
-    const bool own = row < R;
-    const int c0 = k * CW;
-    if (tid < 32) {  // trace of H (one warp)
-        double tr = 0.0;
-        for (int a = tid; a < R; a += 32) {
-            double h = 1.0;
-            for (int q = 0; q < n - 1; ++q) h *= G[a * R + a];
-            tr += h;
+    const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5;
+    const bool skipped = skip && *skip;
+    const bool fit = flags & kFit, update = (flags & kUpdate) && !skipped, solve = (flags & kSolve) && !skipped;
+    const bool prenorm = (flags & kPrenorm) && !skipped;
+#ifdef SYSTEC_EXP_SMALL_CLOCKS  // experiment builds: phase timestamps of the small block
+    long long clk[8];
+    clk[0] = clock64();
+#define SMALL_CLK(i) (clk[i] = clock64())
+#else
+#define SMALL_CLK(i) ((void)0)
+#endif
+    for (int q = tid; q < RR; q += nt) {
+        Bs[q] = GB[q];
+        if (update) {
+            As[q] = W[q];
+            Gs[q] = GM[q];
         }
-#pragma unroll
-        for (int d = 16; d; d >>= 1) tr += __shfl_down_sync(0xffffffffu, tr, d);
-        if (tid == 0) ridge_s = 1e-12 * (tr / R + 1e-300);
+    }
+    if (tid < R) {
+        lam[tid] = cols.lam[tid];
+        ts[tid] = cols.t[tid];
+        lt[tid] = cols.lt[tid];
+        pf[tid] = cols.pf[tid];
+        dt[tid] = dots[tid];
     }
     __syncthreads();
-    double A[CW];
-    double fit_part = 0.0;
+    SMALL_CLK(1);
+    if (fit) {  // of the current iterate: before G_B, lambda, t change
+        double part = 0.0;
+        for (int q = tid; q < RR; q += nt) {
+            const int a = q / R, b = q % R;
+            const double gp = Bs[q];
+            double h = 1.0;
+            for (int e = 0; e < n; ++e) h *= gp;
+            part += lam[a] * lam[b] * h;
+        }
 #pragma unroll
-    for (int u = 0; u < CW; ++u) {
-        const int c = c0 + u;
-        double v = 0.0;
-        if (own && c < W2) {
-            if (c < R) {
-                const double gp = G[row * R + c];
-                double h = 1.0;
-                for (int q = 0; q < n - 1; ++q) h *= gp;
-                if (lam) fit_part += static_cast<double>(lam[row]) * lam[c] * h * gp;
-                v = h + (c == row ? ridge_s : 0.0);
-            } else {
-                v = (c - R == row) ? 1.0 : 0.0;
+        for (int d = 16; d; d >>= 1) part += __shfl_down_sync(0xffffffffu, part, d);
+        if (lane == 0) red[wid] = part;
+        __syncthreads();
+        if (tid < 32) {
+            double v = tid < nt / 32 ? red[tid] : 0.0;
+            double ip = 0.0;
+            for (int a = tid; a < R; a += 32) {
+                double tn = 1.0;
+                for (int e = 0; e < n; ++e) tn *= ts[a];
+                ip += lam[a] * dt[a] / tn;
+            }
+#pragma unroll
+            for (int d = 16; d; d >>= 1) {
+                v += __shfl_down_sync(0xffffffffu, v, d);
+                ip += __shfl_down_sync(0xffffffffu, ip, d);
+            }
+            if (tid == 0) {
+                xhat2[0] = v;
+                xhat2[1] = ip;
             }
         }
-        A[u] = v;
     }
-    red[tid] = fit_part;
+    SMALL_CLK(2);
+    if (!update && !solve) return;  // block-uniform
     __syncthreads();
-    for (int w = nt / 2; w > 0; w >>= 1) {  // block reduction (fixed order)
-        if (tid < w) red[tid] += red[tid + w];
+    if (update) {
+        // four independent partial sums per output (short dependent DFMA chains otherwise)
+        for (int q = tid; q < RR; q += nt) {  // T = G_M W
+            const int a = q / R, b = q % R;
+            const double *g = Gs + a * R;
+            double t0 = 0.0, t1 = 0.0, t2 = 0.0, t3 = 0.0;
+            int c = 0;
+            for (; c + 4 <= R; c += 4) {
+                t0 = fma(g[c], As[c * R + b], t0);
+                t1 = fma(g[c + 1], As[(c + 1) * R + b], t1);
+                t2 = fma(g[c + 2], As[(c + 2) * R + b], t2);
+                t3 = fma(g[c + 3], As[(c + 3) * R + b], t3);
+            }
+            for (; c < R; ++c) t0 = fma(g[c], As[c * R + b], t0);
+            Ts[q] = (t0 + t1) + (t2 + t3);
+        }
         __syncthreads();
+        double Pq[kPq];  // P = W^T T
+#pragma unroll
+        for (int u = 0; u < kPq; ++u) {
+            Pq[u] = 0.0;
+            const int q = tid + u * nt;
+            if (q < RR) {
+                const int a = q / R, b = q % R;
+                double t0 = 0.0, t1 = 0.0, t2 = 0.0, t3 = 0.0;
+                int c = 0;
+                for (; c + 4 <= R; c += 4) {
+                    t0 = fma(As[c * R + a], Ts[c * R + b], t0);
+                    t1 = fma(As[(c + 1) * R + a], Ts[(c + 1) * R + b], t1);
+                    t2 = fma(As[(c + 2) * R + a], Ts[(c + 2) * R + b], t2);
+                    t3 = fma(As[(c + 3) * R + a], Ts[(c + 3) * R + b], t3);
+                }
+                for (; c < R; ++c) t0 = fma(As[c * R + a], Ts[c * R + b], t0);
+                Pq[u] = (t0 + t1) + (t2 + t3);
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int u = 0; u < kPq; ++u)
+            if (tid + u * nt < RR) Ts[tid + u * nt] = Pq[u];
+        __syncthreads();
+        if (tid < R) {
+            const double d = Ts[tid * R + tid];
+            const double tn = sqrt(d > 0.0 ? d : 0.0);
+            lam[tid] = tn * lt[tid];
+            ts[tid] = tn > 0.0 ? tn : 1.0;
+            if (prenorm) {  // G_B still holds B_0's Gram: pf = c^{n-1}
+                const double c2 = Bs[tid * R + tid];
+                pf[tid] = c2 > 0.0 ? pow(c2, 0.5 * (n - 1)) : 1.0;
+            }
+        }
+        __syncthreads();
+        for (int q = tid; q < RR; q += nt) {
+            const int a = q / R, b = q % R;
+            const double g = Ts[q] / (ts[a] * ts[b]);
+            Ts[q] = g;
+            GB[q] = g;
+            if (prenorm) W[q] = static_cast<float>(As[q] / ts[b]);
+        }
+        __syncthreads();
+        if (prenorm && tid < R) ts[tid] = 1.0;
+    } else {
+        for (int q = tid; q < RR; q += nt) Ts[q] = Bs[q];
     }
-    if (tid == 0 && lam && xhat2) {
-        double ip = 0.0;
-        for (int a = 0; a < R; ++a) ip += static_cast<double>(lam[a]) * dots[a];
-        xhat2[0] = red[0];
-        xhat2[1] = ip;
-    }
-    for (int j = 0; j < R; ++j) {
-        const int bsel = j & 1;
-        // publish column j (every row) and row j's raw values
+    SMALL_CLK(3);
+    if (solve) {
+        __syncthreads();
+        // H = G_B^{.(n-1)}, inverted in place by Gauss-Jordan elimination
+        if (tid < 32) {
+            double tr = 0.0;
+            for (int a = tid; a < R; a += 32) {
+                double h = 1.0;
+                for (int q = 0; q < n - 1; ++q) h *= Ts[a * R + a];
+                tr += h;
+            }
+#pragma unroll
+            for (int d = 16; d; d >>= 1) tr += __shfl_down_sync(0xffffffffu, tr, d);
+            if (tid == 0) ridge_s = 1e-12 * (tr / R + 1e-300);
+        }
+        __syncthreads();
+        const int row = tid / TPR, k = tid % TPR;
+        const bool own = row < R;
+        const int c0 = k * CW;
+        double A[CW];
 #pragma unroll
         for (int u = 0; u < CW; ++u) {
             const int c = c0 + u;
-            if (own && c < W2) {
-                if (c == j) fcol[bsel][row] = A[u];
-                if (row == j) piv[bsel][c] = A[u];
+            double v = 0.0;
+            if (own && c < R) {
+                const double gp = Ts[row * R + c];
+                double h = 1.0;
+                for (int q = 0; q < n - 1; ++q) h *= gp;
+                v = h + (c == row ? ridge_s : 0.0);
             }
+            A[u] = v;
         }
-        __syncthreads();
-        if (own) {
-            const double inv = 1.0 / piv[bsel][j];
-            const double f = fcol[bsel][row];
+        SMALL_CLK(4);
+        // in place: after step j, column j holds the inverse's column; the
+        // pivot row / column / reciprocal are double-buffered in shared
+        // memory, so one barrier per step suffices (a thread can only
+        // overwrite a buffer after every thread passed the next step's barrier)
+        for (int j = 0; j < R; ++j) {
+            const int bsel = j & 1;
 #pragma unroll
             for (int u = 0; u < CW; ++u) {
                 const int c = c0 + u;
-                if (c < W2) {
-                    const double pj = piv[bsel][c] * inv;
-                    A[u] = (row == j) ? pj : fma(-f, pj, A[u]);
+                if (own && c < R) {
+                    if (c == j) fcol[bsel][row] = A[u];
+                    if (row == j) piv[bsel][c] = A[u];
+                    if (row == j && c == j) pinv[bsel] = 1.0 / A[u];  // one division per step
+                }
+            }
+            __syncthreads();
+            if (own) {
+                const double pv = pinv[bsel];
+                const double f = fcol[bsel][row] * pv;
+#pragma unroll
+                for (int u = 0; u < CW; ++u) {
+                    const int c = c0 + u;
+                    if (c < R) {
+                        if (row == j) A[u] = (c == j) ? pv : A[u] * pv;
+                        else A[u] = (c == j) ? -f : fma(-f, piv[bsel][c], A[u]);
+                    }
                 }
             }
         }
-        __syncthreads();  // buffers of step j free for step j + 2
-    }
-    if (!update || (skip && *skip)) return;  // block-uniform
+        SMALL_CLK(5);
+        // W = diag(t)^{-(n-1)} H^{-1} diag(1/lt), lt = pf lambda
 #pragma unroll
-    for (int u = 0; u < CW; ++u) {
-        const int c = c0 + u;
-        if (own && c >= R && c < W2) Hs[row * R + (c - R)] = A[u];
+        for (int u = 0; u < CW; ++u) {
+            const int c = c0 + u;
+            if (own && c < R) {
+                double tp = 1.0;
+                for (int q = 0; q < n - 1; ++q) tp *= ts[row];
+                const double lb = lam[c] > 0.0 ? lam[c] * pf[c] : 1.0;
+                W[row * R + c] = static_cast<float>(A[u] / (tp * lb));
+            }
+        }
     }
     __syncthreads();
-    const int RR = R * R;
-    for (int q = tid; q < RR; q += nt) {          // T = G_M H^{-1}
-        const int a = q / R, b = q % R;
-        double t = 0.0;
-        for (int c = 0; c < R; ++c) t = fma(GM[a * R + c], Hs[c * R + b], t);
-        Ts[q] = t;
+#ifdef SYSTEC_EXP_SMALL_CLOCKS
+    if (tid == 0) {
+        SMALL_CLK(6);
+        printf("small flags=%d R=%d cycles: stage %lld fit %lld upd %lld build %lld gj %lld w %lld\n", flags, R,
+               clk[1] - clk[0], clk[2] - clk[1], clk[3] - clk[2], clk[4] - clk[3], clk[5] - clk[4], clk[6] - clk[5]);
     }
-    __syncthreads();
-    double Pq[3];                                  // P = H^{-1} T (H^{-1} symmetric); R*R <= 3 * 1024
-    for (int u = 0, q = tid; q < RR; ++u, q += nt) {
-        const int a = q / R, b = q % R;
-        double t = 0.0;
-        for (int c = 0; c < R; ++c) t = fma(Hs[c * R + a], Ts[c * R + b], t);
-        Pq[u] = t;
-    }
-    __syncthreads();
-    for (int u = 0, q = tid; q < RR; ++u, q += nt) Ts[q] = Pq[u];
-    __syncthreads();
+#endif
     if (tid < R) {
-        const double l = sqrt(Ts[tid * R + tid] > 0.0 ? Ts[tid * R + tid] : 0.0);
-        inv[tid] = l > 0.0 ? 1.0 / l : 1.0;
-        lam_out[tid] = static_cast<float>(l);
-    }
-    __syncthreads();
-    for (int q = tid; q < RR; q += nt) {
-        const int a = q / R, b = q % R;
-        G[q] = Ts[q] * inv[a] * inv[b];
-        W[q] = static_cast<float>(Hs[q] * inv[b]);
+        cols.lam[tid] = lam[tid];
+        cols.t[tid] = ts[tid];
+        if (solve) {
+            cols.lt[tid] = lam[tid] > 0.0 ? lam[tid] * pf[tid] : 1.0;
+            cols.pf[tid] = 1.0;
+        } else {
+            cols.pf[tid] = pf[tid];
+        }
     }
 }
+size_t small_smem_bytes(int R) { return (4ull * R * R + 5ull * R) * sizeof(double); }
 
-// Bout = M W (W = H^{-1} diag(1/lambda): the normalised new factor).  RT = R
+// F /= t column-wise (the unit-column factor on return; one float
+// reciprocal per column, float4 lanes when R % 4 == 0) and lambda (fp32)
+__global__ void cp_finish_kernel(float *__restrict__ F, int64_t dim, int R, CpdCols cols, float *__restrict__ lam) {
+    __shared__ float rinv[kMaxCpR];
+    if (threadIdx.x < R) rinv[threadIdx.x] = static_cast<float>(1.0 / cols.t[threadIdx.x]);
+    __syncthreads();
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    const int64_t first = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (R % 4 == 0 && (reinterpret_cast<uintptr_t>(F) & 15u) == 0) {
+        float4 *F4 = reinterpret_cast<float4 *>(F);
+        const int R4 = R / 4;
+        const int64_t total4 = dim * R4;
+        for (int64_t q = first; q < total4; q += stride) {
+            const int c = static_cast<int>(q % R4) * 4;
+            float4 v = F4[q];
+            v.x *= rinv[c];
+            v.y *= rinv[c + 1];
+            v.z *= rinv[c + 2];
+            v.w *= rinv[c + 3];
+            F4[q] = v;
+        }
+    } else {
+        for (int64_t q = first; q < dim * R; q += stride) F[q] *= rinv[q % R];
+    }
+    if (blockIdx.x == 0 && threadIdx.x < R) lam[threadIdx.x] = static_cast<float>(cols.lam[threadIdx.x]);
+}
+
+// the caller's factor is the iterate itself: lambda = t = lt = pf = 1
+__global__ void cp_cols_init_kernel(CpdCols cols, int R) {
+    if (threadIdx.x < R)
+        cols.lam[threadIdx.x] = cols.t[threadIdx.x] = cols.lt[threadIdx.x] = cols.pf[threadIdx.x] = 1.0;
+}
+
+// Bout = M W (the FFMA form of the pass's F_new = M W; see cp_small_kernel).  RT = R
 // rounded up to a multiple of 8: thread (column b, row group) keeps W[:, b] in
 // registers and reads each staged M row as 16-byte broadcasts.
 template <int RT>
@@ -988,14 +1294,17 @@ size_t gram_smem_bytes(int R, bool ring) {
 }
 
 // scratch (doubles), in this order:
-//   GX[R*R], dots[R]   (contiguous: one reduction) — the pass-A Gram and dots
-//   GB[R*R]            the Gram of the current factor, carried across iterations
-//   H[R*R]             H^{-1} (fp64)
+//   GX[R*R], dots[R]   (contiguous: one reduction) — the pass's G_M and dots
+//   GB[R*R]            the Gram of the current (unit-column) iterate, carried
+//   H[R*R]             (spare)
 //   xhat2[2]           {||Xhat||^2, <X,Xhat>}
+//   lam[R], t[R], lt[R], pf[R]  per column: lambda, the stored factor's scale,
+//                      W's divisor, the next divisor's correction
 //   part[PB][R*R+R]    per-block partials
-// floats: W[R*R] (the apply pass's matrix)
+// floats: W[R*R] (the pass's matrix, F_new = M W)
 struct CpdScratch {
     double *GX, *dots, *GB, *H, *xhat2, *part;
+    CpdCols cols;
 };
 CpdScratch layout(double *ds, int R) {
     CpdScratch c;
@@ -1004,7 +1313,11 @@ CpdScratch layout(double *ds, int R) {
     c.GB = c.dots + R;
     c.H = c.GB + R * R;
     c.xhat2 = c.H + R * R;
-    c.part = c.xhat2 + 2;
+    c.cols.lam = c.xhat2 + 2;
+    c.cols.t = c.cols.lam + R;
+    c.cols.lt = c.cols.t + R;
+    c.cols.pf = c.cols.lt + R;
+    c.part = c.cols.pf + R;
     return c;
 }
 
@@ -1012,7 +1325,7 @@ int partial_blocks(int64_t dim) {
     return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(cpd_partial_blocks(), (dim + 31) / 32)));
 }
 
-// pass A: part = per-block {X^T X, column dots X o Y}; then GX, dots = their sums
+// part = per-block {X^T X, column dots X o Y}; then GX, dots = their sums
 cudaError_t gram_dots(const float *X, const float *Y, int64_t dim, int R, const CpdScratch &c, cudaStream_t s) {
     const int PB = partial_blocks(dim);
     const int W = R * R + R;
@@ -1044,12 +1357,54 @@ cudaError_t gram_dots(const float *X, const float *Y, int64_t dim, int R, const 
     return cudaGetLastError();
 }
 
+// F = M W (skipped when *skip): the FFMA forms
+cudaError_t apply_pass(int64_t dim, const float *M, float *F, int R, const float *W, const int *skip, cudaStream_t s) {
+    const int PB = partial_blocks(dim);
+    // ring form for R in {8, 16, 24, 32} (rows of exactly RT floats), aligned M
+    const bool ring = R % 8 == 0 && R <= 32 && aligned16(M);
+    const size_t rb = ring ? ring_bytes(1, R) : 0;
+    cudaError_t e;
+    switch ((R + 7) / 8) {
+        case 1: e = launch_apply_inverse<8>(PB, rb, s, M, W, dim, R, F, skip, ring); break;
+        case 2: e = launch_apply_inverse<16>(PB, rb, s, M, W, dim, R, F, skip, ring); break;
+        case 3: e = launch_apply_inverse<24>(PB, rb, s, M, W, dim, R, F, skip, ring); break;
+        case 4: e = launch_apply_inverse<32>(PB, rb, s, M, W, dim, R, F, skip, ring); break;
+        case 5: e = launch_apply_inverse<40>(PB, rb, s, M, W, dim, R, F, skip, ring); break;
+        default: e = launch_apply_inverse<48>(PB, rb, s, M, W, dim, R, F, skip, ring); break;
+    }
+    if (e != cudaSuccess) return e;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_small(const Plan &p, int R, const CpdScratch &c, float *W, int flags, const int *skip,
+                         cudaStream_t s) {
+    const size_t smem = small_smem_bytes(R);
+    cudaError_t e;
+    if (R <= 16) {
+        if ((e = cudaFuncSetAttribute(cp_small_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(smem))) != cudaSuccess)
+            return e;
+        cp_small_kernel<16><<<1, kSmallT, smem, s>>>(c.GB, R, p.order, c.cols, c.dots, c.xhat2, c.GX, W, flags, skip);
+    } else if (R <= 32) {
+        if ((e = cudaFuncSetAttribute(cp_small_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(smem))) != cudaSuccess)
+            return e;
+        cp_small_kernel<32><<<1, kSmallT, smem, s>>>(c.GB, R, p.order, c.cols, c.dots, c.xhat2, c.GX, W, flags, skip);
+    } else {
+        if ((e = cudaFuncSetAttribute(cp_small_kernel<48>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(smem))) != cudaSuccess)
+            return e;
+        cp_small_kernel<48><<<1, kSmallT, smem, s>>>(c.GB, R, p.order, c.cols, c.dots, c.xhat2, c.GX, W, flags, skip);
+    }
+    return cudaGetLastError();
+}
+
 }  // namespace
 
 int cpd_max_rank() { return kMaxCpR; }
 
 int64_t cpd_scratch_doubles(int R) {
-    return 3ll * R * R + R + 2 + static_cast<int64_t>(cpd_partial_blocks()) * (R * R + R);
+    return 3ll * R * R + 5ll * R + 2 + static_cast<int64_t>(cpd_partial_blocks()) * (R * R + R);
 }
 
 int64_t cpd_xhat2_offset(int R) { return 3ll * R * R + R; }
@@ -1068,59 +1423,53 @@ cudaError_t cpd_tensor_norm2(const Plan &p, double *out, cudaStream_t s) {
     return cudaGetLastError();
 }
 
-cudaError_t cpd_init(const Plan &p, const float *B, int R, double *dscratch, cudaStream_t s) {
+cudaError_t cpd_init(const Plan &p, const float *B, int R, double *dscratch, float *fscratch, cudaStream_t s) {
     const CpdScratch c = layout(dscratch, R);
     cudaError_t e = gram_dots(B, B, p.dim, R, c, s);  // G_B of the caller's factor (its dots unused)
     if (e != cudaSuccess) return e;
-    return cudaMemcpyAsync(c.GB, c.GX, sizeof(double) * R * R, cudaMemcpyDeviceToDevice, s);
+    if ((e = cudaMemcpyAsync(c.GB, c.GX, sizeof(double) * R * R, cudaMemcpyDeviceToDevice, s)) != cudaSuccess) return e;
+    cp_cols_init_kernel<<<1, 64, 0, s>>>(c.cols, R);
+    return launch_small(p, R, c, fscratch, kSolve, nullptr, s);  // W for iteration 0
 }
 
-cudaError_t cpd_fit_pieces(const Plan &p, const float *M, const float *B, const float *lam, float *lam_out, int R,
-                           double *dscratch, float *fscratch, bool update, const int *skip, cudaStream_t s) {
+cudaError_t cpd_step(const Plan &p, const float *M, float *F, int R, double *dscratch, float *fscratch,
+                     bool have_lam, bool fit_only, const int *skip, cudaStream_t s) {
     const CpdScratch c = layout(dscratch, R);
-    cudaError_t e = gram_dots(M, B, p.dim, R, c, s);  // pass A: G_M = M^T M, dots = sum_i M o B
-    if (e != cudaSuccess) return e;
-    // H = G_B^{.(n-1)} -> H^{-1}; fit pieces of the current iterate from G_B, lam, dots;
-    // then (update) lambda_new, W = H^{-1} diag(1/lambda_new) and the next G_B
-    const int up = update ? 1 : 0;
-    if (R <= 16) small_solve_kernel<1><<<1, 1024, 0, s>>>(c.GB, R, p.order, lam, c.dots, c.xhat2, c.GX, fscratch, lam_out, up, skip);
-    else if (R <= 32) small_solve_kernel<2><<<1, 1024, 0, s>>>(c.GB, R, p.order, lam, c.dots, c.xhat2, c.GX, fscratch, lam_out, up, skip);
-    else small_solve_kernel<6><<<1, 1024, 0, s>>>(c.GB, R, p.order, lam, c.dots, c.xhat2, c.GX, fscratch, lam_out, up, skip);
-    return cudaGetLastError();
-}
-
-cudaError_t cpd_update(const Plan &p, const float *M, float *B, int R, float *fscratch, const int *skip,
-                       cudaStream_t s) {
-    const float *W = fscratch;  // written by the solve: pass B, B = M W (normalised)
-    const int PB = partial_blocks(p.dim);
-    // ring form for R in {8, 16, 24, 32} (rows of exactly RT floats), aligned M
-    const bool ring = R % 8 == 0 && R <= 32 && aligned16(M);
-    const size_t rb = ring ? ring_bytes(1, R) : 0;
+    const float *W = fscratch;
     cudaError_t e;
-    if (R == 32 && ring && use_tensor_cores()) {
-        if ((e = cudaFuncSetAttribute(apply_tc32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(rb))) != cudaSuccess)
+    if (!have_lam) {  // iteration 0: no fit yet
+        if (fit_only) return cudaSuccess;
+        // two passes: the caller's factor has an arbitrary scale, so lambda_1 is
+        // taken from G_M before the apply writes the unit-column B_1
+        if ((e = gram_dots(M, F, p.dim, R, c, s)) != cudaSuccess) return e;
+        if ((e = launch_small(p, R, c, fscratch, kUpdate | kPrenorm, nullptr, s)) != cudaSuccess) return e;
+        if ((e = apply_pass(p.dim, M, F, R, W, nullptr, s)) != cudaSuccess) return e;
+        return launch_small(p, R, c, fscratch, kSolve, nullptr, s);
+    }
+    if (R == 32 && gram_ring(R, M, F) && use_tensor_cores()) {
+        // the fused pass: G_M, dots M o F and F = M W in one read of M and F
+        const int PB = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(sm_count(), (p.dim + 127) / 128)));
+        const size_t smem = ring_bytes<kPassRing>(2, 32);
+        if ((e = cudaFuncSetAttribute(pass_tc32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(smem))) != cudaSuccess)
             return e;
-        apply_tc32_kernel<<<PB, 256, rb, s>>>(M, W, p.dim, B, skip);
-        return cudaGetLastError();
+        pass_tc32_kernel<<<PB, kPassThreads, smem, s>>>(M, F, W, p.dim, c.part, fit_only ? 0 : 1, skip);
+        const int Wd = R * R + R;
+        reduce_partials_kernel<<<(Wd + 7) / 8, 256, 0, s>>>(c.part, PB, Wd, c.GX, nullptr);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    } else {
+        if ((e = gram_dots(M, F, p.dim, R, c, s)) != cudaSuccess) return e;  // G_M, dots M o F (the old F)
+        if (!fit_only && (e = apply_pass(p.dim, M, F, R, W, skip, s)) != cudaSuccess) return e;
     }
-    switch ((R + 7) / 8) {
-        case 1: e = launch_apply_inverse<8>(PB, rb, s, M, W, p.dim, R, B, skip, ring); break;
-        case 2: e = launch_apply_inverse<16>(PB, rb, s, M, W, p.dim, R, B, skip, ring); break;
-        case 3: e = launch_apply_inverse<24>(PB, rb, s, M, W, p.dim, R, B, skip, ring); break;
-        case 4: e = launch_apply_inverse<32>(PB, rb, s, M, W, p.dim, R, B, skip, ring); break;
-        case 5: e = launch_apply_inverse<40>(PB, rb, s, M, W, p.dim, R, B, skip, ring); break;
-        default: e = launch_apply_inverse<48>(PB, rb, s, M, W, p.dim, R, B, skip, ring); break;
-    }
-    if (e != cudaSuccess) return e;
-    return cudaGetLastError();
+    return launch_small(p, R, c, fscratch, kFit | (fit_only ? 0 : kUpdate | kSolve), skip, s);
 }
 
-cudaError_t cpd_step(const Plan &p, const float *M, float *B, float *lam, int R, double *dscratch,
-                     float *fscratch, bool have_lam, bool fit_only, cudaStream_t s) {
-    cudaError_t e = cpd_fit_pieces(p, M, B, have_lam ? lam : nullptr, lam, R, dscratch, fscratch, !fit_only, nullptr, s);
-    if (e != cudaSuccess || fit_only) return e;
-    return cpd_update(p, M, B, R, fscratch, nullptr, s);
+cudaError_t cpd_finish(const Plan &p, float *F, int R, const double *dscratch, float *lam, cudaStream_t s) {
+    const CpdScratch c = layout(const_cast<double *>(dscratch), R);
+    const int64_t total = p.dim * R;
+    const int blocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(sm_count() * 8, (total + 255) / 256)));
+    cp_finish_kernel<<<blocks, 256, 0, s>>>(F, p.dim, R, c.cols, lam);
+    return cudaGetLastError();
 }
 
 cudaError_t cpd_state_init(CpdLoopState *st, const double *x2, int max_iters, cudaStream_t s) {

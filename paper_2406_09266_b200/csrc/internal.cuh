@@ -110,10 +110,17 @@ int cpd_max_rank();
 int64_t cpd_scratch_doubles(int R);
 int64_t cpd_xhat2_offset(int R);  // doubles into the scratch: {||Xhat||^2, <X,Xhat>}
 cudaError_t cpd_tensor_norm2(const Plan &p, double *out, cudaStream_t s);
-// the Gram of the caller's factor, carried from then on in the scratch (before iteration 0)
-cudaError_t cpd_init(const Plan &p, const float *B, int R, double *dscratch, cudaStream_t s);
-cudaError_t cpd_step(const Plan &p, const float *M, float *B, float *lam, int R, double *dscratch,
-                     float *fscratch, bool have_lam, bool fit_only, cudaStream_t s);
+// before iteration 0: the Gram of the caller's factor (carried from then on in
+// the scratch), lambda = 1, and the first pass's W
+cudaError_t cpd_init(const Plan &p, const float *B, int R, double *dscratch, float *fscratch, cudaStream_t s);
+// one iteration after its MTTKRP M = MTTKRP(X, F): the dense pass (G_M, dots
+// M o F, and F = M W unless fit_only or *skip), then the R x R algebra (the
+// fit of the current iterate when have_lam; the new lambda, G_B and the next
+// W unless fit_only or *skip).  F is stored with column scale lambda.
+cudaError_t cpd_step(const Plan &p, const float *M, float *F, int R, double *dscratch, float *fscratch,
+                     bool have_lam, bool fit_only, const int *skip, cudaStream_t s);
+// after the last iteration: F /= lambda (unit columns), lam = lambda (fp32)
+cudaError_t cpd_finish(const Plan &p, float *F, int R, const double *dscratch, float *lam, cudaStream_t s);
 // device-resident CP-ALS loop (one conditional-WHILE graph): state + pieces
 struct CpdLoopState {
     double x2;         // ||X||^2
@@ -123,13 +130,6 @@ struct CpdLoopState {
     int iters_done;
     int pad;
 };
-// fit pieces of the current iterate (pass A + the small solve); with update
-// (and *skip == 0) also lambda_new -> lam_out, W -> fscratch, next G_B
-cudaError_t cpd_fit_pieces(const Plan &p, const float *M, const float *B, const float *lam, float *lam_out, int R,
-                           double *dscratch, float *fscratch, bool update, const int *skip, cudaStream_t s);
-// pass B: B = M W (skipped when *skip)
-cudaError_t cpd_update(const Plan &p, const float *M, float *B, int R, float *fscratch, const int *skip,
-                       cudaStream_t s);
 cudaError_t cpd_state_init(CpdLoopState *st, const double *x2, int max_iters, cudaStream_t s);
 cudaError_t cpd_fit_check(const double *dscratch, int R, CpdLoopState *st, double *fits, double tol, int max_iters,
                           cudaGraphConditionalHandle h, cudaStream_t s);
