@@ -342,7 +342,6 @@ cudaError_t launch_mttkrp(const Plan &p, const float *B, int R, float *C, const 
     kp.stages = stages;
     kp.hints = o.l2_hints >= 0 ? 1 : 0;
     kp.ctr = ctr;
-    kp.cold_shift = p.band_shift;  // read only by SYSTEC_COLD_HINT experiment builds
     // unit size: one chunk balances best (c2 0.476 vs 0.486 ms with 4), but a
     // leading run spanning thousands of chunks (c3's hub row: 10M entries) is
     // then flushed by a different warp at every chunk — tens of thousands of

@@ -66,9 +66,6 @@ struct KParams {
     // nnz-balanced range of `span` entries per warp
     unsigned int *ctr;
     int unit;
-    // experiment (SYSTEC_COLD_HINT): banded plans, shift of the bands; >= 0 marks
-    // position-1 rows outside the entry's band (and outside band 0) evict-first
-    int cold_shift;
 };
 
 using KernelFn = void (*)(KParams);
@@ -83,9 +80,6 @@ template <> struct VecT<4> {
     static __device__ __forceinline__ T load(const float *p, uint64_t pol) { return ldg4_hint(p, pol); }
     static __device__ __forceinline__ void red(float *p, T v) { red_add4(p, v); }
     static __device__ __forceinline__ void red_if(float *p, T v, bool pred) { red_add4_if(p, v, pred); }
-    static __device__ __forceinline__ void red_if_hint(float *p, T v, bool pred, uint64_t pol) {
-        red_add4_if_hint(p, v, pred, pol);
-    }
     static __device__ __forceinline__ T shfl_down(T v, int d) {
         return make_float4(__shfl_down_sync(0xffffffffu, v.x, d), __shfl_down_sync(0xffffffffu, v.y, d),
                            __shfl_down_sync(0xffffffffu, v.z, d), __shfl_down_sync(0xffffffffu, v.w, d));
@@ -115,10 +109,6 @@ template <> struct VecT<8> {
         red_add4_if(p, v.lo, pred);
         red_add4_if(p + 4, v.hi, pred);
     }
-    static __device__ __forceinline__ void red_if_hint(float *p, T v, bool pred, uint64_t pol) {
-        red_add4_if_hint(p, v.lo, pred, pol);
-        red_add4_if_hint(p + 4, v.hi, pred, pol);
-    }
     static __device__ __forceinline__ T shfl_down(T v, int d) {
         return T{VecT<4>::shfl_down(v.lo, d), VecT<4>::shfl_down(v.hi, d)};
     }
@@ -133,7 +123,6 @@ template <> struct VecT<1> {
     static __device__ __forceinline__ T load(const float *p, uint64_t pol) { return ldg1_hint(p, pol); }
     static __device__ __forceinline__ void red(float *p, T v) { red_add1(p, v); }
     static __device__ __forceinline__ void red_if(float *p, T v, bool pred) { red_add1_if(p, v, pred); }
-    static __device__ __forceinline__ void red_if_hint(float *p, T v, bool pred, uint64_t) { red_add1_if(p, v, pred); }
     static __device__ __forceinline__ T shfl_down(T v, int d) { return __shfl_down_sync(0xffffffffu, v, d); }
     static __device__ __forceinline__ T shfl(T v, int src) { return __shfl_sync(0xffffffffu, v, src); }
 };
@@ -285,17 +274,6 @@ __device__ __forceinline__ void mttkrp_sym_body(const KParams &p) {
     // into a wide multiply, an OR of the lane offset and a 64-bit add)
     auto rowB = [&](int32_t c, int q) { return reinterpret_cast<const float *>(mad_wide(c, Rb, Bq[q])); };
     auto rowC = [&](int32_t c, int q) { return reinterpret_cast<float *>(mad_wide(c, Rb, Cq[q])); };
-#ifdef SYSTEC_COLD_HINT
-    // experiment: a middle position's row outside the entry's band (the band
-    // of c_{n-1}) and outside band 0 is touched about once per band: its
-    // gather and reduction are marked evict-first so they do not push the
-    // band's window out of L2
-    auto cold_of = [&](int32_t c, int32_t clast, int t) {
-        return p.cold_shift >= 0 && t >= 1 && t <= N - 2 && (c >> p.cold_shift) != (clast >> p.cold_shift) &&
-               (c >> p.cold_shift) != 0;
-    };
-    bool cold1 = false;
-#endif
 
     // running sums: position 0 (carried across chunks) and position 1
     int cur0 = -1;
@@ -359,15 +337,9 @@ __device__ __forceinline__ void mttkrp_sym_body(const KParams &p) {
             assert(cb + i < p.nnz && i < CH);
 #endif
 #pragma unroll
-            for (int t = NAIVE ? 1 : 0; t < N; ++t) {  // the naive kernel never reads B[c_0]
-#ifdef SYSTEC_COLD_HINT
-                const uint64_t pol_t = cold_of(x.c[t], x.c[N - 1], t) ? pol_stream : pol_keep;
-#else
-                const uint64_t pol_t = pol_keep;
-#endif
+            for (int t = NAIVE ? 1 : 0; t < N; ++t)  // the naive kernel never reads B[c_0]
 #pragma unroll
-                for (int q = 0; q < VPL; ++q) x.b[t][q] = V::load(rowB(x.c[t], q), pol_t);
-            }
+                for (int q = 0; q < VPL; ++q) x.b[t][q] = V::load(rowB(x.c[t], q), pol_keep);
         };
         auto consume = [&](const Slot &x) {
             T u[N][VPL];
@@ -439,32 +411,17 @@ __device__ __forceinline__ void mttkrp_sym_body(const KParams &p) {
                 const bool take = first[1];
 #pragma unroll
                 for (int q = 0; q < VPL; ++q) {
-#ifdef SYSTEC_COLD_HINT
-                    V::red_if_hint(rowC(cur1, q), acc1[q], flush && has1 && act[q], cold1 ? pol_stream : pol_keep);
-#else
                     V::red_if(rowC(cur1, q), acc1[q], flush && has1 && act[q]);
-#endif
                     const T base = flush ? V::zero() : acc1[q];
                     acc1[q] = take ? V::add(base, u[1][q]) : base;
                 }
-#ifdef SYSTEC_COLD_HINT
-                if (flush) cold1 = cold_of(x.c[1], x.c[N - 1], 1);
-#endif
                 has1 = flush ? take : (has1 || take);
                 cur1 = x.c[1];
             }
 #pragma unroll
-            for (int t = POS1 ? 2 : 1; t < N; ++t) {
-#ifdef SYSTEC_COLD_HINT
-                const bool cold = cold_of(x.c[t], x.c[N - 1], t);
-#pragma unroll
-                for (int q = 0; q < VPL; ++q)
-                    V::red_if_hint(rowC(x.c[t], q), u[t][q], first[t] && act[q], cold ? pol_stream : pol_keep);
-#else
+            for (int t = POS1 ? 2 : 1; t < N; ++t)
 #pragma unroll
                 for (int q = 0; q < VPL; ++q) V::red_if(rowC(x.c[t], q), u[t][q], first[t] && act[q]);
-#endif
-            }
         };
 
         if (PF) {
@@ -492,11 +449,7 @@ __device__ __forceinline__ void mttkrp_sym_body(const KParams &p) {
         if (POS1) {
 #pragma unroll
             for (int q = 0; q < VPL; ++q) {
-#ifdef SYSTEC_COLD_HINT
-                V::red_if_hint(rowC(cur1, q), acc1[q], has1 && act[q], cold1 ? pol_stream : pol_keep);
-#else
                 V::red_if(rowC(cur1, q), acc1[q], has1 && act[q]);
-#endif
                 acc1[q] = V::zero();
             }
             has1 = false;

@@ -117,13 +117,6 @@ __device__ __forceinline__ void red_add4_if(float *p, float4 v, bool pred) {
         "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "r"(static_cast<int>(pred))
         : "memory");
 }
-__device__ __forceinline__ void red_add4_if_hint(float *p, float4 v, bool pred, uint64_t policy) {
-    asm volatile(
-        "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %5, 0;\n\t"
-        "@q red.global.add.L2::cache_hint.v4.f32 [%0], {%1,%2,%3,%4}, %6;\n\t}" ::"l"(p),
-        "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "r"(static_cast<int>(pred)), "l"(policy)
-        : "memory");
-}
 __device__ __forceinline__ void red_add1_if(float *p, float v, bool pred) {
     asm volatile(
         "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t"
