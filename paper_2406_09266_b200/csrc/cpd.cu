@@ -831,8 +831,9 @@ __global__ void tensor_norm_kernel(const int32_t *__restrict__ coords, int64_t l
 //            B_new itself.  lambda_1 carries the caller's column norms c of
 //            B_0 (lambda_1 ~ c^{-(n-1)}), so the next prediction is taken
 //            as pf lambda with pf = c^{n-1} (a unit-column B_0's lambda_1).
-//   SOLVE    H = G_B^{.(n-1)} (+ a tiny relative ridge), H^{-1} by in-place
-//            Gauss-Jordan elimination (SPD: no pivoting), and the next
+//   SOLVE    H = G_B^{.(n-1)}, equilibrated to unit diagonal with a 1e-12
+//            ridge, H^{-1} by in-place Gauss-Jordan elimination (SPD: no
+//            pivoting), and the next
 //            pass's W = diag(t)^{-(n-1)} H^{-1} diag(1/lt) with lt = pf lambda
 //            (pf = 1 after iteration 0): B_new = MTTKRP(X, B) H^{-1}
 //            diag(1/lambda_new) and the current lambda predicts lambda_new,
@@ -870,12 +871,11 @@ __global__ void __launch_bounds__(kSmallT, 1) cp_small_kernel(double *__restrict
     double *Gs = As + RR;                                // G_M
     double *Ts = Gs + RR;                                // G_M W, then P, then G_B
     double *Bs = Ts + RR;                                // G_B (current)
-    double *lam = Bs + RR, *ts = lam + R, *lt = ts + R, *pf = lt + R, *dt = pf + R;
+    double *lam = Bs + RR, *ts = lam + R, *lt = ts + R, *pf = lt + R, *dt = pf + R, *eq = dt + R;
     __shared__ double piv[2][2 * kMaxCpR];
     __shared__ double fcol[2][kMaxCpR];
     __shared__ double pinv[2];
     __shared__ double red[32];
-    __shared__ double ridge_s;
     const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5;
     const bool skipped = skip && *skip;
     const bool fit = flags & kFit, update = (flags & kUpdate) && !skipped, solve = (flags & kSolve) && !skipped;
@@ -1005,17 +1005,14 @@ __global__ void __launch_bounds__(kSmallT, 1) cp_small_kernel(double *__restrict
     SMALL_CLK(3);
     if (solve) {
         __syncthreads();
-        // H = G_B^{.(n-1)}, inverted in place by Gauss-Jordan elimination
-        if (tid < 32) {
-            double tr = 0.0;
-            for (int a = tid; a < R; a += 32) {
-                double h = 1.0;
-                for (int q = 0; q < n - 1; ++q) h *= Ts[a * R + a];
-                tr += h;
-            }
-#pragma unroll
-            for (int d = 16; d; d >>= 1) tr += __shfl_down_sync(0xffffffffu, tr, d);
-            if (tid == 0) ridge_s = 1e-12 * (tr / R + 1e-300);
+        // H = G_B^{.(n-1)}, equilibrated to unit diagonal (eq = diag(H)^{-1/2};
+        // the caller's factor may scale its columns arbitrarily) with a 1e-12
+        // ridge, inverted in place by Gauss-Jordan elimination:
+        // H^{-1} = diag(eq) (diag(eq) H diag(eq) + 1e-12 I)^{-1} diag(eq)
+        if (tid < R) {
+            double h = 1.0;
+            for (int q = 0; q < n - 1; ++q) h *= Ts[tid * R + tid];
+            eq[tid] = h > 0.0 ? 1.0 / sqrt(h) : 1.0;
         }
         __syncthreads();
         const int row = tid / TPR, k = tid % TPR;
@@ -1030,7 +1027,7 @@ __global__ void __launch_bounds__(kSmallT, 1) cp_small_kernel(double *__restrict
                 const double gp = Ts[row * R + c];
                 double h = 1.0;
                 for (int q = 0; q < n - 1; ++q) h *= gp;
-                v = h + (c == row ? ridge_s : 0.0);
+                v = h * eq[row] * eq[c] + (c == row ? 1e-12 : 0.0);
             }
             A[u] = v;
         }
@@ -1073,7 +1070,7 @@ __global__ void __launch_bounds__(kSmallT, 1) cp_small_kernel(double *__restrict
                 double tp = 1.0;
                 for (int q = 0; q < n - 1; ++q) tp *= ts[row];
                 const double lb = lam[c] > 0.0 ? lam[c] * pf[c] : 1.0;
-                W[row * R + c] = static_cast<float>(A[u] / (tp * lb));
+                W[row * R + c] = static_cast<float>(A[u] * eq[row] * eq[c] / (tp * lb));
             }
         }
     }
@@ -1096,7 +1093,7 @@ __global__ void __launch_bounds__(kSmallT, 1) cp_small_kernel(double *__restrict
         }
     }
 }
-size_t small_smem_bytes(int R) { return (4ull * R * R + 5ull * R) * sizeof(double); }
+size_t small_smem_bytes(int R) { return (4ull * R * R + 6ull * R) * sizeof(double); }
 
 // F /= t column-wise (the unit-column factor on return; one float
 // reciprocal per column, float4 lanes when R % 4 == 0) and lambda (fp32)
