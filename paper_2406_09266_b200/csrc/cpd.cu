@@ -410,6 +410,11 @@ __global__ void __launch_bounds__(256) gram_tc32_kernel(const float *__restrict_
 #endif
 constexpr int kPassRing = SYSTEC_CPD_PASS_RING;
 constexpr int kPassThreads = 512;
+#ifdef SYSTEC_EXP_PASS_EMPTY  // experiment builds only: the ring alone (no MMAs, dots or stores)
+constexpr bool kPassCompute = false;
+#else
+constexpr bool kPassCompute = true;
+#endif
 __global__ void __launch_bounds__(kPassThreads, 1) pass_tc32_kernel(const float *__restrict__ M, float *F,
                                                                     const float *__restrict__ W, int64_t dim,
                                                                     double *__restrict__ part, int store,
@@ -450,7 +455,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) pass_tc32_kernel(const float 
             }
             const float *tx = tr.tile(k, 0), *ty = tr.tile(k, 1);
             tr.wait(k);
-            if (w0 < nr) {
+            if (kPassCompute && w0 < nr) {
                 // (1) Gram
                 float f[kTiles][4];
 #pragma unroll
@@ -540,7 +545,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) pass_tc32_kernel(const float 
             const int nr = static_cast<int>(min(static_cast<int64_t>(kTileRows), hi - r0g));
             const float *tx = tr.tile(k, 0);
             tr.wait(k);
-            if (write && w0 < nr) {
+            if (kPassCompute && write && w0 < nr) {
                 // (3) F_new = M W for the slab
                 const int ra = w0 + g, rb = ra + 8;  // rows past nr: computed, never stored
                 float o[4][4];
