@@ -241,6 +241,25 @@ SYSTEC_API int systec_cp_als_sym(systec_plan plan, float *B, int R, float *lambd
                                  double *fit_host, int *iters_done, systec_stream_t stream);
 
 /*
+ * Testing entry point: ONE CP-ALS dense pass at R = 32 — the iteration's only
+ * dim x R pass (PAPER.md:853-857 for the update; reading X25 for the
+ * one-pass form) — in a chosen kernel form, so that the tensor-core forms can
+ * be checked against a reference and against each other:
+ *   form 0: legacy mma.sync (m16n8k8 TF32) 3xTF32 kernel;
+ *   form 1: tcgen05.mma kind::tf32 3xTF32 kernel, accumulators in TMEM.
+ * M, F: [dim][32] device fp32, 16-byte aligned; W: [32][32] device fp32.
+ * part: device fp64, room for 1024 blocks of (32*32 + 32): block b receives
+ * {sum over its rows of M^T M (row-major 32 x 32), sum over its rows of M o F
+ * (32 column dots)}; the sums over the returned number of blocks are the pass's
+ * totals.  store != 0: F is overwritten with M W after its dots are taken.
+ * Async on `stream`.  Returns the number of blocks written (>= 1), or
+ * -SYSTEC_ERR_ARG / -SYSTEC_ERR_UNSUPPORTED (form not available: misaligned,
+ * or no tensor-map encoder) / -SYSTEC_ERR_CUDA.
+ */
+SYSTEC_API int systec_testing_cpd_pass(int form, int64_t dim, const float *M, float *F, const float *W, double *part,
+                                       int store, systec_stream_t stream);
+
+/*
  * Single-source shortest paths by Bellman-Ford over a symmetric sparse matrix
  * of edge weights (an order-2 plan: stored (i, j, w) is the undirected edge
  * i-j): dist [dim] (device, out) starts at +inf except dist[source] = 0 and is

@@ -5,7 +5,7 @@ C ABI of ``include/systec.h``); this package is the thin ctypes binding with
 the same names.  See DESIGN.md.
 """
 from .systec import (EXPORTS, LIB_PATH, Plan, SystecError, expand_symmetric, load, mttkrp, mttkrp_host,
-                     plan_create, plan_create_general)
+                     plan_create, plan_create_general, testing_cpd_pass)
 
 __all__ = ["EXPORTS", "LIB_PATH", "Plan", "SystecError", "expand_symmetric", "load", "mttkrp", "mttkrp_host",
-           "plan_create", "plan_create_general"]
+           "plan_create", "plan_create_general", "testing_cpd_pass"]

@@ -537,6 +537,25 @@ cudaError_t cp_als_graph(Plan &p, float *B, int R, float *lambda, int max_iters,
 }  // namespace
 }  // namespace systec
 
+int systec_testing_cpd_pass(int form, int64_t dim, const float *M, float *F, const float *W, double *part,
+                            int store, systec_stream_t stream) {
+    systec::NvtxRange nvtx_range_("systec_testing_cpd_pass");
+    if ((form != 0 && form != 1) || dim < 1 || !M || !F || !W || !part) return -SYSTEC_ERR_ARG;
+    if ((reinterpret_cast<uintptr_t>(M) & 15) || (reinterpret_cast<uintptr_t>(F) & 15)) return -SYSTEC_ERR_UNSUPPORTED;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (form == 1) {
+        const cudaError_t e = systec::launch_pass_umma32(M, F, W, dim, part, store, nullptr, s);
+        if (e == cudaErrorNotSupported) {
+            cudaGetLastError();
+            return -SYSTEC_ERR_UNSUPPORTED;
+        }
+        return e == cudaSuccess ? systec::cpd_umma_blocks(dim) : -systec::cuda_fail(e);
+    }
+    cudaError_t e = cudaSuccess;
+    const int pb = systec::cpd_pass_r32(0, dim, M, F, W, part, store, nullptr, s, &e);
+    return pb > 0 ? pb : -systec::cuda_fail(e);
+}
+
 int systec_cp_als_sym(systec_plan plan, float *B, int R, float *lambda, int max_iters, double tol,
                       double *fit_host, int *iters_done, systec_stream_t stream) {
     systec::NvtxRange nvtx_range_("systec_cp_als_sym");

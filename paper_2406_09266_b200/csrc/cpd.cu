@@ -1285,6 +1285,13 @@ bool use_tensor_cores() {
     const char *v = std::getenv("SYSTEC_CPD_TC");  // read per call: the tests switch it
     return !(v && v[0] == '0');
 }
+// the tcgen05 form of the R = 32 pass (cpd_umma.cu) on request
+// (SYSTEC_CPD_UMMA=1): correct, but measured slower than the mma.sync form on
+// c3 (127 vs 101 us: its 3xTF32 operand copies make it shared-memory bound)
+bool use_umma() {
+    const char *v = std::getenv("SYSTEC_CPD_UMMA");
+    return v && v[0] == '1';
+}
 
 // ring form: R % 4 == 0 (contiguous 16-byte rows), R <= 32, 16-byte aligned bases
 bool gram_ring(int R, const float *B, const float *M) { return R % 4 == 0 && R <= 32 && aligned16(B) && aligned16(M); }
@@ -1403,6 +1410,33 @@ cudaError_t launch_small(const Plan &p, int R, const CpdScratch &c, float *W, in
 
 }  // namespace
 
+int cpd_pass_r32(int form, int64_t dim, const float *M, float *F, const float *W, double *part, int store,
+                 const int *skip, cudaStream_t s, cudaError_t *err) {
+    *err = cudaSuccess;
+    if (form == 1) {
+        const cudaError_t e = launch_pass_umma32(M, F, W, dim, part, store, skip, s);
+        if (e == cudaSuccess) return cpd_umma_blocks(dim);
+        if (e != cudaErrorNotSupported) {
+            *err = e;
+            return -1;
+        }
+        cudaGetLastError();  // not available here: the mma.sync form runs
+    }
+    const int PB = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(sm_count(), (dim + 127) / 128)));
+    const size_t smem = ring_bytes<kPassRing>(2, 32);
+    cudaError_t e = cudaFuncSetAttribute(pass_tc32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e == cudaSuccess) {
+        pass_tc32_kernel<<<PB, kPassThreads, smem, s>>>(M, F, W, dim, part, store, skip);
+        e = cudaGetLastError();
+    }
+    if (e != cudaSuccess) {
+        *err = e;
+        return -1;
+    }
+    return PB;
+}
+
 int cpd_max_rank() { return kMaxCpR; }
 
 int64_t cpd_scratch_doubles(int R) {
@@ -1450,12 +1484,9 @@ cudaError_t cpd_step(const Plan &p, const float *M, float *F, int R, double *dsc
     }
     if (R == 32 && gram_ring(R, M, F) && use_tensor_cores()) {
         // the fused pass: G_M, dots M o F and F = M W in one read of M and F
-        const int PB = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(sm_count(), (p.dim + 127) / 128)));
-        const size_t smem = ring_bytes<kPassRing>(2, 32);
-        if ((e = cudaFuncSetAttribute(pass_tc32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(smem))) != cudaSuccess)
-            return e;
-        pass_tc32_kernel<<<PB, kPassThreads, smem, s>>>(M, F, W, p.dim, c.part, fit_only ? 0 : 1, skip);
+        // (the tcgen05 form when SYSTEC_CPD_UMMA=1 and it can run here)
+        const int PB = cpd_pass_r32(use_umma() ? 1 : 0, p.dim, M, F, W, c.part, fit_only ? 0 : 1, skip, s, &e);
+        if (PB < 0) return e;
         const int Wd = R * R + R;
         reduce_partials_kernel<<<(Wd + 7) / 8, 256, 0, s>>>(c.part, PB, Wd, c.GX, nullptr);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;

@@ -119,6 +119,14 @@ cudaError_t cpd_init(const Plan &p, const float *B, int R, double *dscratch, flo
 // W unless fit_only or *skip).  F is stored with column scale lambda.
 cudaError_t cpd_step(const Plan &p, const float *M, float *F, int R, double *dscratch, float *fscratch,
                      bool have_lam, bool fit_only, const int *skip, cudaStream_t s);
+// the R = 32 dense pass in one form (0: mma.sync, 1: tcgen05; cpd_umma.cu):
+// part[blocks] = {M^T M, dots M o F}, F = M W when store; returns the blocks
+// used, or -1 when the form cannot run (form 1: misaligned / no encoder)
+int cpd_pass_r32(int form, int64_t dim, const float *M, float *F, const float *W, double *part, int store,
+                 const int *skip, cudaStream_t s, cudaError_t *err);
+cudaError_t launch_pass_umma32(const float *M, float *F, const float *W, int64_t dim, double *part, int store,
+                               const int *skip, cudaStream_t s);
+int cpd_umma_blocks(int64_t dim);
 // after the last iteration: F /= lambda (unit columns), lam = lambda (fp32)
 cudaError_t cpd_finish(const Plan &p, float *F, int R, const double *dscratch, float *lam, cudaStream_t s);
 // device-resident CP-ALS loop (one conditional-WHILE graph): state + pieces

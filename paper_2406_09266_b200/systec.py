@@ -48,7 +48,7 @@ EXPORTS = ["systec_mttkrp", "systec_mttkrp_host", "systec_plan_create", "systec_
            "systec_status_string", "systec_last_cuda_error", "systec_version", "systec_last_bad_entry",
            "systec_plan_create_general", "systec_expand_symmetric", "systec_plan_minplus",
            "systec_cp_als_sym", "systec_plan_ttm", "systec_ttm_unpack", "systec_plan_sssp",
-           "systec_plan_create_ex"]
+           "systec_plan_create_ex", "systec_testing_cpd_pass"]
 
 _lib = None
 
@@ -75,6 +75,7 @@ def load(path: str | None = None):
     lib.systec_plan_sssp.argtypes = [vp, i64, vp, i32, ctypes.POINTER(i32), vp]
     lib.systec_ttm_unpack.argtypes = [i64, i32, vp, vp, vp]
     lib.systec_cp_als_sym.argtypes = [vp, vp, i32, vp, i32, ctypes.c_double, vp, ctypes.POINTER(i32), vp]
+    lib.systec_testing_cpd_pass.argtypes = [i32, i64, vp, vp, vp, vp, i32, vp]
     lib.systec_expand_symmetric.argtypes = [i32, i64, i64, vp, vp, i64, vp, vp, ctypes.POINTER(i64), vp]
     lib.systec_plan_execute_ex.argtypes = [vp, vp, i32, vp, ctypes.POINTER(SystecExecOpts), vp]
     lib.systec_plan_stats.argtypes = [vp, ctypes.POINTER(SystecStats)]
@@ -366,3 +367,21 @@ def mttkrp_host(order: int, dim: int, idx, vals, B, C=None, stream=None):
     _check(lib.systec_mttkrp_host(order, dim, nnz, ip, vp_, bp, R, cp, _stream_handle(stream)),
            "systec_mttkrp_host")
     return C
+
+
+def testing_cpd_pass(form: int, M, F, W, store: bool = True, stream=None):
+    """``systec_testing_cpd_pass``: one R = 32 CP-ALS dense pass in kernel form
+    ``form`` (0 mma.sync, 1 tcgen05).  Returns (G [32][32] = M^T M, dots [32]
+    = sum_i M o F) as fp64 CUDA tensors summed over the blocks; F is
+    overwritten with M W when ``store``."""
+    import torch
+    if M.dim() != 2 or M.shape[1] != 32 or F.shape != M.shape or tuple(W.shape) != (32, 32):
+        raise ValueError("M, F must be [dim][32] and W [32][32]")
+    part = torch.zeros((1024, 32 * 32 + 32), dtype=torch.float64, device=M.device)
+    rc = load().systec_testing_cpd_pass(form, int(M.shape[0]), _dev(M, torch.float32, "M"), _dev(F, torch.float32, "F"),
+                                        _dev(W, torch.float32, "W"), _dev(part, torch.float64, "part"), int(store),
+                                        _stream_handle(stream))
+    if rc < 0:
+        _check(-rc, "systec_testing_cpd_pass")
+    tot = part[:rc].sum(dim=0)
+    return tot[:1024].reshape(32, 32), tot[1024:]

@@ -1120,3 +1120,38 @@ def test_cp_als_tensor_core_passes(systec, order, dim, nnz, monkeypatch):
         np.testing.assert_allclose(fg, fref, atol=2e-4)
     assert np.max(np.abs(out["1"][0] - out["0"][0])) / np.abs(out["0"][0]).max() < 1e-5
     plan.destroy()
+
+
+@pytest.mark.parametrize("dim", [1, 127, 128, 1000, 5000, 100003])
+def test_cpd_pass_forms_vs_fp64(systec, dim):
+    """The R = 32 CP-ALS dense pass in both kernel forms — legacy mma.sync
+    (form 0) and tcgen05.mma kind::tf32 with TMEM accumulators (form 1) — on
+    random M, F, W, against the fp64 products: the Gram M^T M, the column dots
+    sum_i M o F (taken before F is overwritten) and F_new = M W.  3xTF32
+    keeps fp32-level accuracy; dims cover one partial tile, exact tiles and a
+    ragged tail over many blocks."""
+    import torch
+    rng = np.random.default_rng(dim)
+    M = rng.standard_normal((dim, 32)).astype(np.float32)
+    F = rng.standard_normal((dim, 32)).astype(np.float32)
+    W = rng.standard_normal((32, 32)).astype(np.float32)
+    M64, F64, W64 = M.astype(np.float64), F.astype(np.float64), W.astype(np.float64)
+    G_ref, d_ref, Fn_ref = M64.T @ M64, np.sum(M64 * F64, axis=0), M64 @ W64
+    gscale = np.sum(M64 * M64)               # |entries| of M^T M are bounded by its trace
+    out = {}
+    for form in (0, 1):
+        dM, dF, dW = (torch.from_numpy(a).cuda() for a in (M, F, W))
+        G, d = systec.testing_cpd_pass(form, dM, dF, dW, store=True)
+        torch.cuda.synchronize()
+        G, d, Fn = G.cpu().numpy(), d.cpu().numpy(), dF.cpu().numpy()
+        eg = np.max(np.abs(G - G_ref)) / gscale
+        ed = np.max(np.abs(d - d_ref)) / np.sum(np.abs(M64 * F64))
+        ef = np.max(np.abs(Fn - Fn_ref) / (np.abs(M64) @ np.abs(W64)))
+        print(f"cpd pass form {form} dim {dim}: gram {eg:.2e} dots {ed:.2e} M W {ef:.2e}")
+        assert eg < 1e-6 and ed < 1e-6 and ef < 1e-5, (form, eg, ed, ef)
+        out[form] = (G, d, Fn)
+        # fit-only: F untouched
+        dF2 = torch.from_numpy(F).cuda()
+        systec.testing_cpd_pass(form, dM, dF2, dW, store=False)
+        torch.cuda.synchronize()
+        assert np.array_equal(dF2.cpu().numpy(), F)
