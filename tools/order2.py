@@ -41,6 +41,8 @@ def main():
     ap.add_argument("--band", type=int, default=64)
     ap.add_argument("--ranks", default="1,32")
     ap.add_argument("--no-sssp", action="store_true")
+    ap.add_argument("--band-shifts", default="", help="also time band-ordered plans (symmetric and naive) "
+                                                      "with these band shifts (bands on the column index)")
     a = ap.parse_args()
     import numpy as np
     import torch
@@ -73,6 +75,24 @@ def main():
                           "expanded_nnz": m, "t_sym_ms": t_sym, "t_naive_ms": t_gen, "speedup": t_gen / t_sym,
                           "gnnz_s": a.nnz / t_sym / 1e6, "eff_gbs": eff, "paper_ssymv_speedup_vs_naive_finch": 1.45,
                           "max_rel_diff": rel}), flush=True)
+    for sh in (int(x) for x in filter(None, a.band_shifts.split(","))):
+        symb = systec.Plan(2, a.dim, di, dv, band_shift=sh)
+        genb = systec.Plan(2, a.dim, ei, ev, band_shift=sh, general=True)
+        for R in (int(r) for r in a.ranks.split(",")):
+            B = torch.from_numpy(rng.uniform(-1, 1, (a.dim, R)).astype(np.float32)).cuda()
+            C1 = torch.empty((a.dim, R), device="cuda")
+            C2 = torch.empty((a.dim, R), device="cuda")
+            t_sym = timed(lambda: symb.execute(B, C1), a.reps, flush)
+            t_gen = timed(lambda: genb.execute(B, C2), a.reps, flush)
+            t_gen_lex = timed(lambda: gen.execute(B, C2), a.reps, flush)
+            rel = float(((C1 - C2).abs().max() / C1.abs().max()).item())
+            print(json.dumps({"kernel": "SSYMV" if R == 1 else f"SSYMM R={R}", "matrix": a.mode, "band_shift": sh,
+                              "plan_band_shift": symb.stats()["band_shift"], "t_sym_banded_ms": t_sym,
+                              "t_naive_banded_ms": t_gen, "t_naive_lex_ms": t_gen_lex,
+                              "speedup_vs_best_naive": min(t_gen, t_gen_lex) / t_sym, "max_rel_diff": rel}),
+                  flush=True)
+        symb.destroy()
+        genb.destroy()
     if a.variants:
         B = torch.from_numpy(rng.uniform(-1, 1, (a.dim, 1)).astype(np.float32)).cuda()
         C1 = torch.empty((a.dim, 1), device="cuda")
