@@ -65,6 +65,11 @@ def test_host_argument_checks_need_no_gpu(lib):
     out = ctypes.c_void_p()
     assert lib.systec_plan_create(ctypes.byref(out), 6, 10, 0, None, None, None) == 2
     assert not out.value
+    # the testing pass entry: bad form / dim / null -> -ARG, misaligned -> -UNSUPPORTED
+    assert lib.systec_testing_cpd_pass(2, 10, vp(16), vp(16), vp(16), vp(16), 1, None) == -1
+    assert lib.systec_testing_cpd_pass(0, 0, vp(16), vp(16), vp(16), vp(16), 1, None) == -1
+    assert lib.systec_testing_cpd_pass(1, 10, None, vp(16), vp(16), vp(16), 1, None) == -1
+    assert lib.systec_testing_cpd_pass(1, 10, vp(20), vp(16), vp(16), vp(16), 1, None) == -2
 
 
 def test_product_path_has_no_oracle_dependency():
