@@ -1155,3 +1155,34 @@ def test_cpd_pass_forms_vs_fp64(systec, dim):
         systec.testing_cpd_pass(form, dM, dF2, dW, store=False)
         torch.cuda.synchronize()
         assert np.array_equal(dF2.cpu().numpy(), F)
+
+
+def test_cp_als_with_tcgen05_pass(systec, monkeypatch):
+    """CP-ALS at R = 32 with its dense pass in the tcgen05 form
+    (SYSTEC_CPD_UMMA=1) in both loop forms (the device loop's fit-only
+    iteration sets the pass's skip flag) matches the fp64 oracle and the
+    default (mma.sync) form."""
+    import torch
+    from oracle import cpd_ref
+    w = small_random(3, 4000, 60000, 32, seed=321, diag_frac=0.1)
+    iters = 5
+    Bref, lref, fref = cpd_ref.cp_als_sym(3, 4000, w.idx, w.vals, w.B, iters=iters)
+    di, dv, dB = to_dev(w.idx, w.vals, w.B)
+    plan = systec.Plan(3, 4000, di, dv)
+    out = {}
+    for umma in ("1", "0"):
+        for loop in ("host", "graph"):
+            monkeypatch.setenv("SYSTEC_CPD_UMMA", umma)
+            monkeypatch.setenv("SYSTEC_CPALS_LOOP", loop)
+            B, lam, fits = plan.cp_als(dB.clone(), max_iters=iters, tol=0.0)
+            torch.cuda.synchronize()
+            out[(umma, loop)] = (B.cpu().numpy(), lam.cpu().numpy(), np.asarray(fits))
+    scale = np.abs(Bref).max()
+    for key, (Bg, lg, fg) in out.items():
+        assert np.max(np.abs(Bg - Bref)) / scale < 2e-4, key
+        np.testing.assert_allclose(lg, lref, rtol=2e-4)
+        np.testing.assert_allclose(fg, fref, atol=2e-4)
+    d = np.max(np.abs(out[("1", "host")][0] - out[("0", "host")][0])) / scale
+    print(f"cp_als tcgen05 vs mma.sync pass: max|dB|/max|B| = {d:.2e}")
+    assert d < 1e-5
+    plan.destroy()
