@@ -23,9 +23,15 @@ def main():
     tot_i = sum(float(x[i_col] or 0) for x in rows)
     print(f"samples {tot_s:.0f}  warp instructions {tot_i:.0f}")
     rows.sort(key=lambda x: -float(x[s_col] or 0))
+    reasons = [k for k in h if k.startswith("stall_") and "Not Issued" not in k]
+    tot_r = {k: sum(float(x[ci[k]] or 0) for x in rows) for k in reasons}
+    print("stall reasons (samples):", ", ".join(f"{k[6:]} {v:.0f}" for k, v in
+                                              sorted(tot_r.items(), key=lambda kv: -kv[1]) if v > 0))
     for x in rows[:n]:
+        top = sorted(((float(x[ci[k]] or 0), k[6:]) for k in reasons), reverse=True)[:2]
+        why = " ".join(f"{k}:{v:.0f}" for v, k in top if v > 0)
         print(f'{x[ci["Address"]][-5:]} {float(x[s_col] or 0):7.0f} {float(x[i_col] or 0):8.0f}  '
-              f'{x[ci["Source"]].strip()[:90]}')
+              f'{x[ci["Source"]].strip()[:70]:70s} {why}')
 
 
 if __name__ == "__main__":
