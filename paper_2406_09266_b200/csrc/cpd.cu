@@ -398,24 +398,32 @@ __global__ void __launch_bounds__(256) gram_tc32_kernel(const float *__restrict_
 //       and W's fragments (loaded once, split hi/lo, in registers) use the
 //       same map; the result is stored over the same rows of F (unless a fit-only iteration:
 //       store == 0, or *skip set by the device loop).
-// Warp roles (16 warps, one block per SM): warps 0-7 do (1)-(2) and warps
-// 8-15 do (3) on the same 16-row slabs, so the two MMA streams interleave on
-// the tensor pipe (with 8 warps doing all three, 240 registers each, the pass
-// ran at 2 warps per scheduler: 102 us on c3, tensor pipe 42 % and DRAM 40 %
-// busy).  F's old rows are read by (2) from the ring, and (3) stores the new
+// Warp roles: warps [0, W) do (1)-(2) and warps [W, 2W) do (3) on the same
+// 16-row slabs, each warp taking slabs rw, rw + W, ... of a tile, so the two
+// MMA streams interleave on the tensor pipe (with 8 warps doing all three,
+// 240 registers each, the pass ran at 2 warps per scheduler: 102 us on c3,
+// tensor pipe 42 % and DRAM 40 % busy; 16 warps in one block per SM: 94 us;
+// W = 4 with two 256-thread blocks per SM, each with its own 3-deep ring:
+// 88 us).  F's old rows are read by (2) from the ring, and (3) stores the new
 // rows straight to global memory: the ring slot is only refilled after the
-// tile's barrier.  kPassRing tiles in flight.
+// tile's barrier.
+#ifndef SYSTEC_CPD_PASS_WARPS
+#define SYSTEC_CPD_PASS_WARPS 4  // warps per role: 4 = 256-thread blocks, two per SM (c3 pass 88 us);
+                                 // 8 = 512 threads, one per SM, 5-deep ring (94 us)
+#endif
 #ifndef SYSTEC_CPD_PASS_RING
-#define SYSTEC_CPD_PASS_RING 5
+#define SYSTEC_CPD_PASS_RING (SYSTEC_CPD_PASS_WARPS == 8 ? 5 : 3)
 #endif
 constexpr int kPassRing = SYSTEC_CPD_PASS_RING;
-constexpr int kPassThreads = 512;
+constexpr int kRoleWarps = SYSTEC_CPD_PASS_WARPS;
+constexpr int kPassThreads = 64 * kRoleWarps;
+constexpr int kPassBlocksPerSm = 8 / kRoleWarps;
 #ifdef SYSTEC_EXP_PASS_EMPTY  // experiment builds only: the ring alone (no MMAs, dots or stores)
 constexpr bool kPassCompute = false;
 #else
 constexpr bool kPassCompute = true;
 #endif
-__global__ void __launch_bounds__(kPassThreads, 1) pass_tc32_kernel(const float *__restrict__ M, float *F,
+__global__ void __launch_bounds__(kPassThreads, kPassBlocksPerSm) pass_tc32_kernel(const float *__restrict__ M, float *F,
                                                                     const float *__restrict__ W, int64_t dim,
                                                                     double *__restrict__ part, int store,
                                                                     const int *skip) {
@@ -423,8 +431,8 @@ __global__ void __launch_bounds__(kPassThreads, 1) pass_tc32_kernel(const float 
     extern __shared__ __align__(16) unsigned char cpd_smem[];
     const bool write = store && !(skip && *skip);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
-    const bool gram_role = warp < 8;
-    const int w0 = (warp & 7) * 16;  // kTileRows == 128: one 16-row slab per warp of each role
+    const bool gram_role = warp < kRoleWarps;
+    const int rw = warp % kRoleWarps;  // the warp's slabs: rows 16 (rw + kRoleWarps i) of each 128-row tile
     const int64_t rows = (dim + gridDim.x - 1) / gridDim.x;
     const int64_t lo = blockIdx.x * rows, hi = min(dim, lo + rows);
     TileRingT<kPassRing> tr{reinterpret_cast<float *>(cpd_smem),
@@ -455,6 +463,9 @@ __global__ void __launch_bounds__(kPassThreads, 1) pass_tc32_kernel(const float 
             }
             const float *tx = tr.tile(k, 0), *ty = tr.tile(k, 1);
             tr.wait(k);
+#pragma unroll 1
+            for (int sl = 0; sl < 8 / kRoleWarps; ++sl) {
+            const int w0 = (rw + kRoleWarps * sl) * 16;
             if (kPassCompute && w0 < nr) {
                 // (1) Gram
                 float f[kTiles][4];
@@ -506,12 +517,13 @@ __global__ void __launch_bounds__(kPassThreads, 1) pass_tc32_kernel(const float 
                 dacc[2] += d.z;
                 dacc[3] += d.w;
             }
+            }
             __syncthreads();  // tile k consumed by every warp: its slot may be refilled
         }
         // the 8 gram warps' sums in shared memory in a fixed order (named
         // barrier 1: these warps only; the ring is idle once every tile's
         // block barrier has passed), un-permuted below
-        for (int w = 0; w < 8; ++w) {
+        for (int w = 0; w < kRoleWarps; ++w) {
             if (warp == w) {
 #pragma unroll
                 for (int q = 0; q < kTiles; ++q) {
@@ -526,7 +538,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) pass_tc32_kernel(const float 
                     }
                 }
             }
-            asm volatile("bar.sync 1, 256;" ::: "memory");
+            asm volatile("bar.sync 1, %0;" ::"n"(32 * kRoleWarps) : "memory");
         }
 #pragma unroll
         for (int c = 0; c < 4; ++c) dred[(warp * 4 + dr) * R + 4 * dq + c] = dacc[c];
@@ -545,6 +557,9 @@ __global__ void __launch_bounds__(kPassThreads, 1) pass_tc32_kernel(const float 
             const int nr = static_cast<int>(min(static_cast<int64_t>(kTileRows), hi - r0g));
             const float *tx = tr.tile(k, 0);
             tr.wait(k);
+#pragma unroll 1
+            for (int sl = 0; sl < 8 / kRoleWarps; ++sl) {
+            const int w0 = (rw + kRoleWarps * sl) * 16;
             if (kPassCompute && write && w0 < nr) {
                 // (3) F_new = M W for the slab
                 const int ra = w0 + g, rb = ra + 8;  // rows past nr: computed, never stored
@@ -577,6 +592,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) pass_tc32_kernel(const float 
                     if (rb < nr) *reinterpret_cast<float2 *>(fb + nb * 8) = make_float2(o[nb][2], o[nb][3]);
                 }
             }
+            }
             __syncthreads();  // tile k consumed by every warp: its slot may be refilled
         }
     }
@@ -590,7 +606,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) pass_tc32_kernel(const float 
     }
     if (tid < R) {
         double d = 0.0;
-        for (int l = 0; l < 32; ++l) d += dred[l * R + tid];
+        for (int l = 0; l < 4 * kRoleWarps; ++l) d += dred[l * R + tid];
         out[R * R + tid] = d;
     }
 }
@@ -1464,7 +1480,8 @@ int cpd_pass_r32(int form, int64_t dim, const float *M, float *F, const float *W
         }
         cudaGetLastError();  // not available here: the mma.sync form runs
     }
-    const int PB = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(sm_count(), (dim + 127) / 128)));
+    const int PB = static_cast<int>(
+        std::max<int64_t>(1, std::min<int64_t>(static_cast<int64_t>(sm_count()) * kPassBlocksPerSm, (dim + 127) / 128)));
     const size_t smem = ring_bytes<kPassRing>(2, 32);
     cudaError_t e = cudaFuncSetAttribute(pass_tc32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
