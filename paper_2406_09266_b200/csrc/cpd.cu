@@ -418,6 +418,8 @@ constexpr int kPassRing = SYSTEC_CPD_PASS_RING;
 constexpr int kRoleWarps = SYSTEC_CPD_PASS_WARPS;
 constexpr int kPassThreads = 64 * kRoleWarps;
 constexpr int kPassBlocksPerSm = 8 / kRoleWarps;
+static_assert(kRoleWarps == 4 || kRoleWarps == 8, "warps per role: 4 or 8");
+static_assert(kPassBlocksPerSm <= SYSTEC_CPD_BPS, "the partial-sum scratch holds SYSTEC_CPD_BPS blocks per SM");
 #ifdef SYSTEC_EXP_PASS_EMPTY  // experiment builds only: the ring alone (no MMAs, dots or stores)
 constexpr bool kPassCompute = false;
 #else
