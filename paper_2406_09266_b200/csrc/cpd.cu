@@ -872,20 +872,21 @@ enum : int { kFit = 1, kUpdate = 2, kSolve = 4, kPrenorm = 8 };
 struct CpdCols {
     double *lam, *t, *lt, *pf;  // [R] each
 };
-// threads of the small block: 1024 at every rank class — the inverse's pivot
-// steps run fastest with one column per thread (460 cycles per step at R =
-// 32, against 1,150 with 256 threads, 4 columns each, and 1,230 on one warp
-// holding the rows in registers with shuffled pivots; clock64 phases,
+// threads of the small block: the inverse's pivot steps run fastest with one
+// column per thread (460 cycles per step at R = 32, against 1,150 with 256
+// threads, 4 columns each, and 1,230 on one warp holding the rows in
+// registers with shuffled pivots; clock64 phases,
 // profiles/r02/cpd_small_phase_clocks.log)
-constexpr int small_threads(int) { return 1024; }
+constexpr int kSmallThreads = 1024;
 constexpr int pow2_floor(int x) { return x >= 2 ? 2 * pow2_floor(x / 2) : 1; }
 template <int RC>  // rank class: R <= RC (16, 32, 48)
-__global__ void __launch_bounds__(small_threads(RC), 1) cp_small_kernel(double *__restrict__ GB, int R, int n, CpdCols cols,
-                                                           const double *__restrict__ dots, double *__restrict__ xhat2,
-                                                           const double *__restrict__ GM, float *__restrict__ W,
-                                                           int flags, const int *skip) {
+__global__ void __launch_bounds__(kSmallThreads, 1) cp_small_kernel(double *__restrict__ GB, int R, int n,
+                                                                    CpdCols cols, const double *__restrict__ dots,
+                                                                    double *__restrict__ xhat2,
+                                                                    const double *__restrict__ GM,
+                                                                    float *__restrict__ W, int flags, const int *skip) {
     // H: thread t owns row t / TPR and the CW columns [k*CW, (k+1)*CW), k = t % TPR
-    constexpr int kT = small_threads(RC);
+    constexpr int kT = kSmallThreads;
     constexpr int TPR = pow2_floor(kT / RC) < RC ? pow2_floor(kT / RC) : RC;
     constexpr int CW = (RC + TPR - 1) / TPR;
     constexpr int kPq = (kMaxCpR * kMaxCpR + kT - 1) / kT;
@@ -966,40 +967,40 @@ __global__ void __launch_bounds__(small_threads(RC), 1) cp_small_kernel(double *
     __syncthreads();
     if constexpr (RC <= 32) {
         if (update) {
-        // T = G_M W, then P = W^T T: warp w < 8 owns rows w, w + 8, w + 16,
-        // w + 24, lane b the column; each W (or T) element read serves four
-        // rows (6.8k against 10k cycles for one output per thread of 1024)
-        const int b = wid < 8 ? lane : R;
-        double acc[4] = {0.0, 0.0, 0.0, 0.0};
-        if (b < R)
-            for (int c = 0; c < R; ++c) {
-                const double wcb = As[c * R + b];
+            // T = G_M W, then P = W^T T: warp w < 8 owns rows w, w + 8, w + 16,
+            // w + 24, lane b the column; each W (or T) element read serves four
+            // rows (6.8k against 10k cycles for one output per thread of 1024)
+            const int b = wid < 8 ? lane : R;
+            double acc[4] = {0.0, 0.0, 0.0, 0.0};
+            if (b < R)
+                for (int c = 0; c < R; ++c) {
+                    const double wcb = As[c * R + b];
 #pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    const int a = wid + 8 * i;
-                    if (a < R) acc[i] = fma(Gs[a * R + c], wcb, acc[i]);
+                    for (int i = 0; i < 4; ++i) {
+                        const int a = wid + 8 * i;
+                        if (a < R) acc[i] = fma(Gs[a * R + c], wcb, acc[i]);
+                    }
                 }
-            }
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
-            if (wid + 8 * i < R && b < R) Ts[(wid + 8 * i) * R + b] = acc[i];
-        __syncthreads();
+            for (int i = 0; i < 4; ++i)
+                if (wid + 8 * i < R && b < R) Ts[(wid + 8 * i) * R + b] = acc[i];
+            __syncthreads();
 #pragma unroll
-        for (int i = 0; i < 4; ++i) acc[i] = 0.0;
-        if (b < R)
-            for (int c = 0; c < R; ++c) {
-                const double tcb = Ts[c * R + b];
+            for (int i = 0; i < 4; ++i) acc[i] = 0.0;
+            if (b < R)
+                for (int c = 0; c < R; ++c) {
+                    const double tcb = Ts[c * R + b];
 #pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    const int a = wid + 8 * i;
-                    if (a < R) acc[i] = fma(As[c * R + a], tcb, acc[i]);
+                    for (int i = 0; i < 4; ++i) {
+                        const int a = wid + 8 * i;
+                        if (a < R) acc[i] = fma(As[c * R + a], tcb, acc[i]);
+                    }
                 }
-            }
-        __syncthreads();
+            __syncthreads();
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
-            if (wid + 8 * i < R && b < R) Ts[(wid + 8 * i) * R + b] = acc[i];
-        __syncthreads();
+            for (int i = 0; i < 4; ++i)
+                if (wid + 8 * i < R && b < R) Ts[(wid + 8 * i) * R + b] = acc[i];
+            __syncthreads();
         }
     } else if (update) {
         // four independent partial sums per output (short dependent DFMA chains otherwise)
@@ -1453,17 +1454,17 @@ cudaError_t launch_small(const Plan &p, int R, const CpdScratch &c, float *W, in
         if ((e = cudaFuncSetAttribute(cp_small_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(smem))) != cudaSuccess)
             return e;
-        cp_small_kernel<16><<<1, small_threads(16), smem, s>>>(c.GB, R, p.order, c.cols, c.dots, c.xhat2, c.GX, W, flags, skip);
+        cp_small_kernel<16><<<1, kSmallThreads, smem, s>>>(c.GB, R, p.order, c.cols, c.dots, c.xhat2, c.GX, W, flags, skip);
     } else if (R <= 32) {
         if ((e = cudaFuncSetAttribute(cp_small_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(smem))) != cudaSuccess)
             return e;
-        cp_small_kernel<32><<<1, small_threads(32), smem, s>>>(c.GB, R, p.order, c.cols, c.dots, c.xhat2, c.GX, W, flags, skip);
+        cp_small_kernel<32><<<1, kSmallThreads, smem, s>>>(c.GB, R, p.order, c.cols, c.dots, c.xhat2, c.GX, W, flags, skip);
     } else {
         if ((e = cudaFuncSetAttribute(cp_small_kernel<48>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(smem))) != cudaSuccess)
             return e;
-        cp_small_kernel<48><<<1, small_threads(48), smem, s>>>(c.GB, R, p.order, c.cols, c.dots, c.xhat2, c.GX, W, flags, skip);
+        cp_small_kernel<48><<<1, kSmallThreads, smem, s>>>(c.GB, R, p.order, c.cols, c.dots, c.xhat2, c.GX, W, flags, skip);
     }
     return cudaGetLastError();
 }
