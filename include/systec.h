@@ -226,7 +226,8 @@ SYSTEC_API int systec_plan_minplus(systec_plan plan, const float *d, float *y, s
  *     M = MTTKRP(X, B);  B = M ((B^T B)^{.(n-1)})^{-1};  lambda = column norms;  B /= lambda
  * (R = 1 is the symmetric higher-order power method).  B [dim][R] (device) holds
  * the initial factor on entry and the unit-column factor on return; lambda [R]
- * (device) receives the weights.  Runs up to max_iters iterations and stops
+ * (device) receives the weights (max_iters = 0: B is returned unchanged and
+ * lambda = 1).  Runs up to max_iters iterations and stops
  * early when the fit changes by less than tol; fit_host [max_iters] (host, may
  * be NULL) receives fit_k = 1 - ||X - Xhat_k|| / ||X|| of each iterate;
  * *iters_done the number of iterations run.  1 <= R <= 48.  For runs of
