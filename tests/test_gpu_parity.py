@@ -1186,3 +1186,17 @@ def test_cp_als_with_tcgen05_pass(systec, monkeypatch):
     print(f"cp_als tcgen05 vs mma.sync pass: max|dB|/max|B| = {d:.2e}")
     assert d < 1e-5
     plan.destroy()
+
+
+def test_cp_als_zero_iterations(systec):
+    """max_iters = 0: no update, B returned unchanged, lambda = 1, no fits."""
+    import torch
+    w = small_random(3, 300, 5000, 8, seed=3, diag_frac=0.1)
+    di, dv, dB = to_dev(w.idx, w.vals, w.B)
+    plan = systec.Plan(3, 300, di, dv)
+    B, lam, fits = plan.cp_als(dB.clone(), max_iters=0)
+    torch.cuda.synchronize()
+    assert np.array_equal(B.cpu().numpy(), w.B)
+    assert np.array_equal(lam.cpu().numpy(), np.ones(8, np.float32))
+    assert len(fits) == 0
+    plan.destroy()
