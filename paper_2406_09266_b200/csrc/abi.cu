@@ -437,11 +437,12 @@ int systec_plan_minplus(systec_plan plan, const float *d, float *y, systec_strea
 namespace systec {
 namespace {
 
-// CP-ALS with the whole iteration loop on the device: iteration 0 runs
-// eagerly, iterations 1..max_iters are the body of a conditional WHILE node of
-// one CUDA graph (MTTKRP -> fit pieces + R x R update -> apply pass -> device
-// convergence test, which also flags the next run as fit-only when it is the
-// last), so there is no host round trip per iteration — one launch, one
+// CP-ALS with the whole iteration loop on the device: iteration 0 and the
+// first MTTKRP run eagerly, iterations 1..max_iters are the body of a
+// conditional WHILE node of one CUDA graph (the dense pass, then the R x R
+// algebra + device convergence test — which also flags the next run as
+// fit-only when it is the last — beside the next iteration's MTTKRP), so
+// there is no host round trip per iteration — one launch, one
 // synchronisation at the end.  Returns cudaErrorNotSupported (nothing
 // launched) when the graph cannot be built; the caller then runs the host loop.
 cudaError_t cp_als_graph(Plan &p, float *B, int R, float *lambda, int max_iters, double tol, double *fit_host,
@@ -455,12 +456,16 @@ cudaError_t cp_als_graph(Plan &p, float *B, int R, float *lambda, int max_iters,
     CpdLoopState *st = nullptr;
     cudaGraph_t g = nullptr;
     cudaGraphExec_t ge = nullptr;
-    cudaStream_t cs = nullptr;
+    cudaStream_t cs = nullptr, cs2 = nullptr;
+    cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
     bool launched = false;
     auto cleanup = [&]() {
         if (ge) cudaGraphExecDestroy(ge);
         if (g) cudaGraphDestroy(g);
         if (cs) cudaStreamDestroy(cs);
+        if (cs2) cudaStreamDestroy(cs2);
+        if (fork_ev) cudaEventDestroy(fork_ev);
+        if (join_ev) cudaEventDestroy(join_ev);
         for (void *q : {static_cast<void *>(M), static_cast<void *>(fs), static_cast<void *>(scr),
                         static_cast<void *>(ds), static_cast<void *>(fits), static_cast<void *>(x2),
                         static_cast<void *>(st)})
@@ -490,12 +495,24 @@ cudaError_t cp_als_graph(Plan &p, float *B, int R, float *lambda, int max_iters,
         if ((e = cudaGraphAddNode(&node, g, nullptr, 0, &cp)) != cudaSuccess) break;
         cudaGraph_t body = cp.conditional.phGraph_out[0];
         if ((e = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking)) != cudaSuccess) break;
+        if ((e = cudaStreamCreateWithFlags(&cs2, cudaStreamNonBlocking)) != cudaSuccess) break;
+        if ((e = cudaEventCreateWithFlags(&fork_ev, cudaEventDisableTiming)) != cudaSuccess) break;
+        if ((e = cudaEventCreateWithFlags(&join_ev, cudaEventDisableTiming)) != cudaSuccess) break;
         if ((e = cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal)) !=
             cudaSuccess)
             break;
-        cudaError_t ce = launch_mttkrp(p, B, R, M, o, cs, scr);
-        if (ce == cudaSuccess) ce = cpd_step(p, M, B, R, ds, fs, true, false, &st->skip_update, cs);
+        // body j (M = MTTKRP(X, F_j) on entry): the dense pass writes F_{j+1}, then
+        // the R x R algebra + convergence test and MTTKRP(X, F_{j+1}) run side by
+        // side (the MTTKRP needs only F_{j+1}; the algebra only the pass's
+        // partial sums); the last body's MTTKRP is computed and not used
+        cudaError_t ce = cpd_step_pass(p, M, B, R, ds, fs, false, &st->skip_update, cs);
+        if (ce == cudaSuccess) ce = cudaEventRecord(fork_ev, cs);
+        if (ce == cudaSuccess) ce = cudaStreamWaitEvent(cs2, fork_ev, 0);
+        if (ce == cudaSuccess) ce = launch_mttkrp(p, B, R, M, o, cs2, scr);
+        if (ce == cudaSuccess) ce = cudaEventRecord(join_ev, cs2);
+        if (ce == cudaSuccess) ce = cpd_step_algebra(p, R, ds, fs, false, &st->skip_update, cs);
         if (ce == cudaSuccess) ce = cpd_fit_check(ds, R, st, fits, tol, max_iters, h, cs);
+        if (ce == cudaSuccess) ce = cudaStreamWaitEvent(cs, join_ev, 0);
         cudaGraph_t captured = nullptr;
         e = cudaStreamEndCapture(cs, &captured);
         if (ce != cudaSuccess) e = ce;
@@ -508,6 +525,7 @@ cudaError_t cp_als_graph(Plan &p, float *B, int R, float *lambda, int max_iters,
         if ((e = cpd_init(p, B, R, ds, fs, s)) != cudaSuccess) break;
         if ((e = launch_mttkrp(p, B, R, M, o, s, scr)) != cudaSuccess) break;
         if ((e = cpd_step(p, M, B, R, ds, fs, false, false, nullptr, s)) != cudaSuccess) break;
+        if ((e = launch_mttkrp(p, B, R, M, o, s, scr)) != cudaSuccess) break;  // the first body's M
         if ((e = cudaGraphLaunch(ge, s)) != cudaSuccess) break;
         if ((e = cpd_finish(p, B, R, ds, lambda, s)) != cudaSuccess) break;
         CpdLoopState hst;

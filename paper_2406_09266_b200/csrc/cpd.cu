@@ -1544,6 +1544,15 @@ cudaError_t cpd_step(const Plan &p, const float *M, float *F, int R, double *dsc
         if ((e = apply_pass(p.dim, M, F, R, W, nullptr, s)) != cudaSuccess) return e;
         return launch_small(p, R, c, fscratch, kSolve, nullptr, s);
     }
+    if ((e = cpd_step_pass(p, M, F, R, dscratch, fscratch, fit_only, skip, s)) != cudaSuccess) return e;
+    return cpd_step_algebra(p, R, dscratch, fscratch, fit_only, skip, s);
+}
+
+cudaError_t cpd_step_pass(const Plan &p, const float *M, float *F, int R, double *dscratch, const float *fscratch,
+                          bool fit_only, const int *skip, cudaStream_t s) {
+    const CpdScratch c = layout(dscratch, R);
+    const float *W = fscratch;
+    cudaError_t e;
     if (R == 32 && gram_ring(R, M, F) && use_tensor_cores()) {
         // the fused pass: G_M, dots M o F and F = M W in one read of M and F
         // (the tcgen05 form when SYSTEC_CPD_UMMA=1 and it can run here)
@@ -1551,11 +1560,16 @@ cudaError_t cpd_step(const Plan &p, const float *M, float *F, int R, double *dsc
         if (PB < 0) return e;
         const int Wd = R * R + R;
         reduce_partials_kernel<<<(Wd + 7) / 8, 256, 0, s>>>(c.part, PB, Wd, c.GX, nullptr);
-        if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    } else {
-        if ((e = gram_dots(M, F, p.dim, R, c, s)) != cudaSuccess) return e;  // G_M, dots M o F (the old F)
-        if (!fit_only && (e = apply_pass(p.dim, M, F, R, W, skip, s)) != cudaSuccess) return e;
+        return cudaGetLastError();
     }
+    if ((e = gram_dots(M, F, p.dim, R, c, s)) != cudaSuccess) return e;  // G_M, dots M o F (the old F)
+    if (!fit_only && (e = apply_pass(p.dim, M, F, R, W, skip, s)) != cudaSuccess) return e;
+    return cudaSuccess;
+}
+
+cudaError_t cpd_step_algebra(const Plan &p, int R, double *dscratch, float *fscratch, bool fit_only, const int *skip,
+                             cudaStream_t s) {
+    const CpdScratch c = layout(dscratch, R);
     return launch_small(p, R, c, fscratch, kFit | (fit_only ? 0 : kUpdate | kSolve), skip, s);
 }
 

@@ -127,6 +127,13 @@ int cpd_pass_r32(int form, int64_t dim, const float *M, float *F, const float *W
 cudaError_t launch_pass_umma32(const float *M, float *F, const float *W, int64_t dim, double *part, int store,
                                const int *skip, cudaStream_t s);
 int cpd_umma_blocks(int64_t dim);
+// cpd_step (have_lam) in two parts: the dense pass with its partial-sum
+// reduction, then the R x R algebra (the device loop runs the next MTTKRP
+// beside the algebra: it only needs the F the pass wrote)
+cudaError_t cpd_step_pass(const Plan &p, const float *M, float *F, int R, double *dscratch, const float *fscratch,
+                          bool fit_only, const int *skip, cudaStream_t s);
+cudaError_t cpd_step_algebra(const Plan &p, int R, double *dscratch, float *fscratch, bool fit_only, const int *skip,
+                             cudaStream_t s);
 // after the last iteration: F /= lambda (unit columns), lam = lambda (fp32)
 cudaError_t cpd_finish(const Plan &p, float *F, int R, const double *dscratch, float *lam, cudaStream_t s);
 // device-resident CP-ALS loop (one conditional-WHILE graph): state + pieces
