@@ -232,8 +232,9 @@ SYSTEC_API int systec_plan_minplus(systec_plan plan, const float *d, float *y, s
  * be NULL) receives fit_k = 1 - ||X - Xhat_k|| / ||X|| of each iterate;
  * *iters_done the number of iterations run.  1 <= R <= 48.  For runs of
  * max_iters >= 16 the iteration loop is device-resident: one CUDA graph whose
- * conditional WHILE node repeats MTTKRP -> fit -> device convergence test ->
- * update, synchronising `stream` once at the end; shorter runs use a host loop
+ * conditional WHILE node repeats the dense pass -> (the fit, the R x R update
+ * and a device convergence test, beside the next MTTKRP), synchronising
+ * `stream` once at the end; shorter runs use a host loop
  * that synchronises once per iteration to read the fit (the graph costs
  * ~0.4 ms to build).  Environment SYSTEC_CPALS_LOOP=host|graph overrides.
  * Errors: ARG, UNSUPPORTED (general plan, R > 48), ALIAS, NOMEM, CUDA.
