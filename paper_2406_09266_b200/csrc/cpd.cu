@@ -388,11 +388,11 @@ __global__ void __launch_bounds__(256) gram_tc32_kernel(const float *__restrict_
 
 // The one dense pass of an iteration at R = 32 (tensor cores, 3xTF32): every
 // 128-row tile of M and of the stored factor F arrives once through the
-// bulk-copy ring, and each warp, on its own 16 rows of the tile,
-//   (1) accumulates the Gram M^T M (gram_tc32_kernel's permuted-column MMAs),
-//   (2) accumulates the column dots M o F (the fit's <X, Xhat>; F is the
+// bulk-copy ring, and per 16-row slab of the tile the warps
+//   (1) accumulate the Gram M^T M (gram_tc32_kernel's permuted-column MMAs),
+//   (2) accumulate the column dots M o F (the fit's <X, Xhat>; F is the
 //       factor the MTTKRP read),
-//   (3) computes F_new = M W with K permuted so that thread (g, t) reads
+//   (3) compute F_new = M W with K permuted so that thread (g, t) reads
 //       physical columns 8t..8t+7 of its two rows (two LDS.128 each):
 //       logical k = 8 ks + kk maps to physical column 8 (kk % 4) + 2 ks + kk / 4,
 //       and W's fragments (loaded once, split hi/lo, in registers) use the
