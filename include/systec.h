@@ -55,7 +55,7 @@ typedef struct CUstream_st *systec_stream_t;   /* == cudaStream_t */
 typedef enum {
     SYSTEC_OK = 0,
     SYSTEC_ERR_ARG = 1,          /* null pointer with nnz>0, dim<1, nnz<0, R<1, bad option   */
-    SYSTEC_ERR_UNSUPPORTED = 2,  /* order outside 2..5, order*ceil(log2 dim) > 64, nnz>=2^31 */
+    SYSTEC_ERR_UNSUPPORTED = 2,  /* order outside 2..5, dim >= 2^31, nnz >= 2^31 - 64 */
     SYSTEC_ERR_INDEX = 3,        /* some idx outside [0, dim) (detected on the device)      */
     SYSTEC_ERR_ALIAS = 4,        /* C overlaps B, idx or vals                               */
     SYSTEC_ERR_NOMEM = 5,        /* device or host allocation failed                        */
@@ -67,7 +67,7 @@ typedef struct systec_stats {
     int64_t nnz;                 /* stored entries                                            */
     int64_t dim;
     int32_t order;
-    int32_t key_bits;            /* bits per index in the 64-bit sort key = ceil(log2 dim)     */
+    int32_t key_bits;            /* bits per index in the sort key = ceil(log2 dim); order*key_bits > 64: a wide plan */
     int64_t G;                   /* sum over entries of the number of distinct indices d_e     */
     int64_t expanded;            /* sum over entries of the orbit size n!/prod m! (naive work) */
     int64_t pattern_hist[16];    /* entries per equality-pattern code (bit t: c_t == c_{t+1})  */

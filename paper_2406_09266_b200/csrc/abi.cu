@@ -63,9 +63,7 @@ int check_shape(int order, int64_t dim, int64_t nnz, int *bits_out) {
     if (dim < 1 || nnz < 0) return SYSTEC_ERR_ARG;
     if (order < 2 || order > 5) return SYSTEC_ERR_UNSUPPORTED;
     if (dim > INT32_MAX || nnz > INT32_MAX - 64) return SYSTEC_ERR_UNSUPPORTED;
-    const int bits = ceil_log2(dim);
-    if (bits * order > 64) return SYSTEC_ERR_UNSUPPORTED;
-    *bits_out = bits;
+    *bits_out = ceil_log2(dim);  // order * bits > 64: a wide plan (no packed 64-bit key; prepare.cu)
     return SYSTEC_OK;
 }
 
@@ -226,9 +224,11 @@ int plan_create_impl(Plan **out, int order, int64_t dim, int64_t nnz, const int3
     hst.bad_entry = ULLONG_MAX;
     if ((e = cudaMemcpyAsync(dst, &hst, sizeof(hst), cudaMemcpyHostToDevice, s)) != cudaSuccess) return fail(e);
 
-    // a1: validate + canonicalise + pack keys
-    if ((e = launch_canonicalize(order, dim, nnz, bits, idx, keys, perm, dst, s, !general)) != cudaSuccess)
-        return fail(e);
+    // a1: validate + canonicalise + pack keys (wide plans: validate only, no keys)
+    const bool wide = bits * order > 64;
+    e = wide ? launch_validate_wide(order, dim, nnz, idx, perm, dst, s, !general)
+             : launch_canonicalize(order, dim, nnz, bits, idx, keys, perm, dst, s, !general);
+    if (e != cudaSuccess) return fail(e);
     if ((e = cudaMemcpyAsync(&hst, dst, sizeof(hst), cudaMemcpyDeviceToHost, s)) != cudaSuccess) return fail(e);
     if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return fail(e);  // sync 1: validation verdict
     if (hst.err) {
@@ -245,12 +245,21 @@ int plan_create_impl(Plan **out, int order, int64_t dim, int64_t nnz, const int3
     if (!sorted && nnz > 1) {
         if ((e = cudaMallocAsync(&keys2, nk * 8, s)) != cudaSuccess) return fail(e);
         if ((e = cudaMallocAsync(&perm2, nk * 4, s)) != cudaSuccess) return fail(e);
-        if ((e = sort_keys(nnz, bits * order, keys, keys2, perm, perm2, s)) != cudaSuccess) return fail(e);
-        skeys = keys2;
-        sperm = perm2;
+        if (wide) {
+            uint32_t *sorted_perm = nullptr;
+            if ((e = sort_wide(order, dim, nnz, bits, idx, keys, keys2, perm, perm2, &sorted_perm, s, !general)) !=
+                cudaSuccess)
+                return fail(e);
+            sperm = sorted_perm;
+        } else {
+            if ((e = sort_keys(nnz, bits * order, keys, keys2, perm, perm2, s)) != cudaSuccess) return fail(e);
+            skeys = keys2;
+            sperm = perm2;
+        }
     }
-    if ((e = launch_gather(order, nnz, p->ld, bits, skeys, sperm, vals, p->coords, p->vals, s)) != cudaSuccess)
-        return fail(e);
+    e = wide ? launch_gather_wide(order, nnz, p->ld, p->ld, dim, idx, sperm, vals, p->coords, p->vals, s, !general)
+             : launch_gather(order, nnz, p->ld, bits, skeys, sperm, vals, p->coords, p->vals, s);
+    if (e != cudaSuccess) return fail(e);
     if ((e = launch_stats(order, nnz, p->ld, p->coords, -1, dst, s)) != cudaSuccess) return fail(e);
     if ((e = cudaMemcpyAsync(&hst, dst, sizeof(hst), cudaMemcpyDeviceToHost, s)) != cudaSuccess) return fail(e);
     // order-2 symmetric plans: the windowed kernel's row / column pointers and
@@ -976,9 +985,17 @@ int mttkrp_host_pipelined(int order, int64_t dim, int64_t nnz, int bits, const i
         for (int k = 0; k < nch; ++k) {
             const int64_t lo = k * per, n = std::min(per, nnz - lo);
             if ((e = cudaStreamWaitEvent(s, ev[k], 0)) != cudaSuccess) break;
-            if ((e = launch_canonicalize(order, dim, n, bits, d_idx + lo * order, keys, perm, dst, s, true, lo)) != cudaSuccess)
-                break;
-            if ((e = launch_gather_range(order, n, ld, bits, keys, d_vals + lo, coords + lo, svals + lo, s)) != cudaSuccess) break;
+            if (bits * order > 64) {  // wide plan: no packed keys (the last chunk's padding tail is never read)
+                if ((e = launch_validate_wide(order, dim, n, d_idx + lo * order, perm, dst, s, true, lo)) != cudaSuccess)
+                    break;
+                if ((e = launch_gather_wide(order, n, n, ld, dim, d_idx + lo * order, nullptr, d_vals + lo, coords + lo,
+                                            svals + lo, s, true)) != cudaSuccess)
+                    break;
+            } else {
+                if ((e = launch_canonicalize(order, dim, n, bits, d_idx + lo * order, keys, perm, dst, s, true, lo)) != cudaSuccess)
+                    break;
+                if ((e = launch_gather_range(order, n, ld, bits, keys, d_vals + lo, coords + lo, svals + lo, s)) != cudaSuccess) break;
+            }
             if (k == 0) {  // chunk-0 statistics decide position-1 accumulation (one sync)
                 if ((e = launch_stats(order, n, ld, coords, -1, dst, s)) != cudaSuccess) break;
                 if ((e = cudaMemcpyAsync(&hst, dst, sizeof(hst), cudaMemcpyDeviceToHost, s)) != cudaSuccess) break;

@@ -91,6 +91,17 @@ cudaError_t launch_permute(int order, int64_t nnz, int64_t ld, const uint32_t *p
 cudaError_t launch_gather_range(int order, int64_t n, int64_t ld, int bits, const unsigned long long *keys,
                                 const float *vals_in, int32_t *coords, float *vals_out, cudaStream_t s);
 
+// wide plans (order * ceil(log2 dim) > 64): no packed keys
+cudaError_t launch_validate_wide(int order, int64_t dim, int64_t nnz, const int32_t *idx, uint32_t *perm,
+                                 DevStats *st, cudaStream_t s, bool canonicalise = true, int64_t e_offset = 0);
+cudaError_t sort_wide(int order, int64_t dim, int64_t nnz, int bits, const int32_t *idx, unsigned long long *keys,
+                      unsigned long long *keys2, uint32_t *perm, uint32_t *perm2, uint32_t **perm_out,
+                      cudaStream_t s, bool canonicalise = true);
+// span: entries written (ld for a whole plan incl. its zero padding, nnz for one chunk of the host pipeline)
+cudaError_t launch_gather_wide(int order, int64_t nnz, int64_t span, int64_t ld, int64_t dim, const int32_t *idx,
+                               const uint32_t *perm /* null = identity */, const float *vals_in, int32_t *coords,
+                               float *vals_out, cudaStream_t s, bool canonicalise = true);
+
 // expand.cu
 cudaError_t expand_count(int order, int64_t dim, int64_t nnz, const int32_t *idx, unsigned long long *sizes,
                          unsigned long long *offsets, DevStats *st, cudaStream_t s);

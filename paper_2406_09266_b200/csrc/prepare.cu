@@ -115,6 +115,78 @@ __global__ void gather_range_kernel(int64_t n, int64_t ld, int bits, const unsig
     }
 }
 
+// ---- wide plans: order * ceil(log2 dim) > 64, the canonical tuple does not
+// fit one 64-bit key.  Nothing is packed: validation compares neighbouring
+// tuples directly, the sort is an LSD radix sort over words of `cpw`
+// coordinates each (last word first, every pass stable, carrying only the
+// permutation), and the gather re-reads the caller's tuples through it.
+
+template <int N, bool CANON>
+__global__ void validate_wide_kernel(const int32_t *__restrict__ idx, int64_t nnz, int64_t dim,
+                                     uint32_t *__restrict__ perm, DevStats *st, int64_t e_offset) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        int32_t c[N];
+        perm[e] = static_cast<uint32_t>(e);
+        if (!load_canonical<N, CANON>(idx, e, dim, c)) {
+            atomicOr(&st->err, 1ull);
+            atomicMin(&st->bad_entry, static_cast<unsigned long long>(e + e_offset));
+            continue;
+        }
+        if (e > 0) {
+            int32_t q[N];
+            if (load_canonical<N, CANON>(idx, e - 1, dim, q)) {
+                int cmp = 0;  // sign of q - c in lexicographic order
+#pragma unroll
+                for (int t = 0; t < N; ++t)
+                    if (cmp == 0) cmp = (q[t] > c[t]) - (q[t] < c[t]);
+                if (cmp > 0) st->unsorted = 1ull;
+            }
+        }
+    }
+}
+
+// keys[e] = coordinates [first, first + count) of the canonical tuple of entry perm[e]
+template <int N, bool CANON>
+__global__ void word_keys_kernel(const int32_t *__restrict__ idx, int64_t nnz, int64_t dim, int bits, int first,
+                                 int count, const uint32_t *__restrict__ perm,
+                                 unsigned long long *__restrict__ keys) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        int32_t c[N];
+        load_canonical<N, CANON>(idx, perm[e], dim, c);
+        unsigned long long k = 0;
+#pragma unroll
+        for (int t = 0; t < N; ++t)
+            if (t >= first && t < first + count)
+                k = (k << bits) | static_cast<unsigned long long>(static_cast<uint32_t>(c[t]));
+        keys[e] = k;
+    }
+}
+
+template <int N, bool CANON>
+__global__ void gather_wide_kernel(int64_t nnz, int64_t span, int64_t ld, int64_t dim,
+                                   const int32_t *__restrict__ idx, const uint32_t *__restrict__ perm,
+                                   const float *__restrict__ vals_in, int32_t *__restrict__ coords,
+                                   float *__restrict__ vals_out) {
+    // span = ld for a whole plan (entries past nnz are padding), = nnz for one chunk of the host pipeline
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < span;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        if (e < nnz) {
+            const int64_t src = perm ? static_cast<int64_t>(perm[e]) : e;
+            int32_t c[N];
+            load_canonical<N, CANON>(idx, src, dim, c);
+#pragma unroll
+            for (int t = 0; t < N; ++t) coords[t * ld + e] = c[t];
+            vals_out[e] = vals_in[src];
+        } else {  // padding (see gather_kernel)
+#pragma unroll
+            for (int t = 0; t < N; ++t) coords[t * ld + e] = 0;
+            vals_out[e] = 0.0f;
+        }
+    }
+}
+
 // banded stream order (systec_plan_opts.band_shift): the band number of each
 // prepared entry, c_{N-1} >> band_shift, with its position
 template <int N>
@@ -290,6 +362,57 @@ cudaError_t launch_gather(int order, int64_t nnz, int64_t ld, int bits, const un
     if (ld == 0) return cudaSuccess;
     const int th = 256;
     SYSTEC_ORDER_SWITCH(order, gather_kernel<N><<<grid_for(ld, th), th, 0, s>>>(nnz, ld, bits, keys, perm, vals_in, coords, vals_out));
+    return cudaGetLastError();
+}
+
+cudaError_t launch_validate_wide(int order, int64_t dim, int64_t nnz, const int32_t *idx, uint32_t *perm,
+                                 DevStats *st, cudaStream_t s, bool canonicalise, int64_t e_offset) {
+    if (nnz == 0) return cudaSuccess;
+    const int th = 256;
+    if (canonicalise) {
+        SYSTEC_ORDER_SWITCH(order, validate_wide_kernel<N, true><<<grid_for(nnz, th), th, 0, s>>>(idx, nnz, dim, perm, st, e_offset));
+    } else {
+        SYSTEC_ORDER_SWITCH(order, validate_wide_kernel<N, false><<<grid_for(nnz, th), th, 0, s>>>(idx, nnz, dim, perm, st, e_offset));
+    }
+    return cudaGetLastError();
+}
+
+// Lexicographic sort of the canonical tuples for wide plans: perm (identity on
+// entry) becomes the sorting permutation.  keys/keys2 [nnz] 64-bit and perm2
+// [nnz] are scratch; the result is in *perm_out (perm or perm2).
+cudaError_t sort_wide(int order, int64_t dim, int64_t nnz, int bits, const int32_t *idx, unsigned long long *keys,
+                      unsigned long long *keys2, uint32_t *perm, uint32_t *perm2, uint32_t **perm_out,
+                      cudaStream_t s, bool canonicalise) {
+    const int cpw = 64 / bits;                    // coordinates per 64-bit word (bits <= 31: at least 2)
+    const int words = (order + cpw - 1) / cpw;
+    const int th = 256;
+    uint32_t *in = perm, *out = perm2;
+    for (int w = words - 1; w >= 0; --w) {
+        const int first = w * cpw, count = order - first < cpw ? order - first : cpw;
+        if (canonicalise) {
+            SYSTEC_ORDER_SWITCH(order, word_keys_kernel<N, true><<<grid_for(nnz, th), th, 0, s>>>(idx, nnz, dim, bits, first, count, in, keys));
+        } else {
+            SYSTEC_ORDER_SWITCH(order, word_keys_kernel<N, false><<<grid_for(nnz, th), th, 0, s>>>(idx, nnz, dim, bits, first, count, in, keys));
+        }
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+        if ((e = sort_keys(nnz, bits * count, keys, keys2, in, out, s)) != cudaSuccess) return e;
+        uint32_t *t = in; in = out; out = t;
+    }
+    *perm_out = in;
+    return cudaSuccess;
+}
+
+cudaError_t launch_gather_wide(int order, int64_t nnz, int64_t span, int64_t ld, int64_t dim, const int32_t *idx,
+                               const uint32_t *perm, const float *vals_in, int32_t *coords, float *vals_out,
+                               cudaStream_t s, bool canonicalise) {
+    if (span == 0) return cudaSuccess;
+    const int th = 256;
+    if (canonicalise) {
+        SYSTEC_ORDER_SWITCH(order, gather_wide_kernel<N, true><<<grid_for(span, th), th, 0, s>>>(nnz, span, ld, dim, idx, perm, vals_in, coords, vals_out));
+    } else {
+        SYSTEC_ORDER_SWITCH(order, gather_wide_kernel<N, false><<<grid_for(span, th), th, 0, s>>>(nnz, span, ld, dim, idx, perm, vals_in, coords, vals_out));
+    }
     return cudaGetLastError();
 }
 

@@ -51,8 +51,9 @@ def test_host_argument_checks_need_no_gpu(lib):
     # dim < 1, nnz < 0 -> ARG
     assert lib.systec_mttkrp(3, 0, 0, None, None, vp(16), 4, vp(4096), None) == 1
     assert lib.systec_mttkrp(3, 10, -1, None, None, vp(16), 4, vp(4096), None) == 1
-    # key wider than 64 bits (5 * 20 bits) -> UNSUPPORTED
-    assert lib.systec_mttkrp(5, 1 << 20, 0, None, None, vp(16), 4, vp(1 << 30), None) == 2
+    # dim or nnz beyond int32 -> UNSUPPORTED (a sort key wider than 64 bits is supported: wide plans)
+    assert lib.systec_mttkrp(5, 1 << 31, 0, None, None, vp(16), 4, vp(1 << 30), None) == 2
+    assert lib.systec_mttkrp(5, 10, (1 << 31) - 64, vp(16), vp(16), vp(16), 4, vp(1 << 30), None) == 2
     # null idx with nnz > 0 -> ARG
     assert lib.systec_mttkrp(3, 10, 5, None, None, vp(16), 4, vp(4096), None) == 1
     # R < 1 -> ARG

@@ -551,6 +551,107 @@ def test_key_width_limits(systec, order, bits, R):
     plan.destroy()
 
 
+def _crowded_tuples(order, dim, nnz, seed):
+    """Shuffled, non-canonical tuples crowded at both ends of [0, dim) with every
+    equality pattern present (duplicates included: they add)."""
+    rng = np.random.default_rng(seed)
+    top = rng.integers(dim - 8, dim, (nnz // 2, order))
+    low = rng.integers(0, 8, (nnz // 4, order))
+    mid = rng.integers(0, dim, (nnz - nnz // 2 - nnz // 4, order))
+    mid[::7, 1] = mid[::7, 0]                          # forced repeats away from the ends
+    mid[::11, order - 1] = mid[::11, order - 2]
+    idx = np.concatenate([top, low, mid]).astype(np.int32)
+    idx[0] = dim - 1                                  # the all-equal top entry
+    idx = idx[rng.permutation(nnz)]
+    vals = rng.uniform(-1, 1, nnz).astype(np.float32)
+    return idx, vals, rng
+
+
+@pytest.mark.parametrize("order,dim,R", [(3, (1 << 21) + 1, 4), (3, 3_000_001, 4), (3, (1 << 28) - 1, 1),
+                                         (4, 100_003, 8), (4, (1 << 22) + 7, 2), (5, 4097, 8), (5, 10_007, 8),
+                                         (5, (1 << 25) + 3, 1)])
+def test_wide_plans(systec, order, dim, R):
+    """order * ceil(log2 dim) > 64 (66..135 bits: two or three sort words): the
+    canonical tuple does not fit one 64-bit key.  The prepared stream equals a
+    numpy lexsort of the canonical tuples (stable: values in input order among
+    equal tuples), the statistics match, touched rows equal the oracle row by
+    row, untouched rows are exactly zero; sorted input skips the sort; the
+    one-shot device and host calls agree."""
+    import torch
+    nnz = 20011
+    assert order * int(np.ceil(np.log2(dim))) > 64
+    idx, vals, rng = _crowded_tuples(order, dim, nnz, seed=order * 1000 + R)
+    B = rng.uniform(-1, 1, (dim, R)).astype(np.float32)
+    di, dv, dB = to_dev(idx, vals, B)
+    plan = systec.Plan(order, dim, di, dv)
+    canon = np.sort(idx, axis=1)
+    p = np.lexsort(canon.T[::-1])                     # stable, first coordinate most significant
+    coords, pv = plan.prepared()
+    torch.cuda.synchronize()
+    assert np.array_equal(coords.cpu().numpy().T, canon[p])
+    assert np.array_equal(pv.cpu().numpy(), vals[p])
+    st = plan.stats()
+    c = canon[p].astype(np.int64)
+    assert st["input_was_sorted"] == 0
+    assert st["G"] == int(np.sum(1 + np.sum(c[:, 1:] != c[:, :-1], axis=1)))
+    assert st["lead_runs"] == len(np.unique(c[:, 0]))
+    assert st["expanded"] == oracle.count_expanded(order, canon[p])
+    C = plan.execute(dB)
+    torch.cuda.synchronize()
+    Cg = C.cpu().numpy()
+    touched = np.unique(idx)
+    rows = np.unique(np.concatenate([touched[:150], touched[-150:], rng.choice(touched, 100)]))
+    Cref, S = oracle.mttkrp_rows(order, dim, idx, vals, B, rows)
+    err = parity(Cg[rows], Cref, S)
+    mask = np.ones(dim, bool)
+    mask[touched] = False
+    assert not np.any(Cg[mask]), "row with no stored index is not zero"
+    plan.destroy()
+    # sorted canonical input: recognised, no sort, same stream
+    ds, dvs = to_dev(canon[p].astype(np.int32), vals[p])
+    plan2 = systec.Plan(order, dim, ds, dvs)
+    assert plan2.stats()["input_was_sorted"] == 1
+    c2, v2 = plan2.prepared()
+    assert np.array_equal(c2.cpu().numpy().T, canon[p]) and np.array_equal(v2.cpu().numpy(), vals[p])
+    C2 = plan2.execute(dB)
+    torch.cuda.synchronize()
+    parity(C2.cpu().numpy()[rows], Cref, S)
+    plan2.destroy()
+    # one-shot device call and the (unchunked) host call
+    C3 = systec.mttkrp(order, dim, di, dv, dB)
+    torch.cuda.synchronize()
+    parity(C3.cpu().numpy()[rows], Cref, S)
+    if dim * R <= 1 << 25:
+        Ch = systec.mttkrp_host(order, dim, idx, vals, B)
+        parity(Ch[rows], Cref, S)
+        assert not np.any(Ch[mask])
+    # a bad index is still located
+    bad = idx.copy()
+    bad[nnz // 3, order - 1] = dim
+    with pytest.raises(IndexError, match=f"first bad entry {nnz // 3}"):
+        systec.Plan(order, dim, *to_dev(bad, vals))
+    print(f"wide order {order} dim {dim}: max_rel_err={err:.3e}")
+
+
+@pytest.mark.parametrize("shuffle", [False, True])
+def test_wide_host_call_pipelined(systec, shuffle):
+    """The chunked host call (nnz >= 2^20) on a wide shape (order 5, 14 bits per
+    index = 70), every element against the oracle; shuffled input too."""
+    order, dim, nnz, R = 5, 10_007, (1 << 20) + 4099, 4
+    rng = np.random.default_rng(77)
+    idx = np.sort(rng.integers(0, dim, (nnz, order)), axis=1).astype(np.int32)
+    idx[::9, 2] = idx[::9, 1]
+    idx = idx[np.lexsort(np.sort(idx, axis=1).T[::-1])]
+    vals = rng.uniform(-1, 1, nnz).astype(np.float32)
+    if shuffle:
+        idx, vals = scramble(idx, vals, seed=5)
+    B = rng.uniform(-1, 1, (dim, R)).astype(np.float32)
+    Cref, S = oracle.mttkrp(order, dim, idx, vals, B)
+    Ch = systec.mttkrp_host(order, dim, idx, vals, B)
+    err = parity(Ch, Cref, S)
+    print(f"wide host call shuffle={shuffle}: max_rel_err={err:.3e}")
+
+
 def test_work_distribution_modes(systec):
     """Dynamic units when the problem has at least one unit per resident warp,
     the static split otherwise or on request; same result either way."""
