@@ -174,9 +174,12 @@ SYSTEC_API int systec_mttkrp_host(int order, int64_t dim, int64_t nnz, const int
  * input already is), and store the prepared structure-of-arrays copy
  * (order x int32 + 1 x fp32 per entry, owned by the plan).  idx and vals may
  * be freed once this returns.  The plan belongs to the device current at
- * creation; execute it there.  Synchronises `stream` twice: once to read the
- * device validation verdict (which also decides whether the sort can be
- * skipped) and once to read the statistics.
+ * creation; execute it there.  Input already in storage order (canonical
+ * forms sorted lexicographically) is prepared in one device pass —
+ * validation, the structure-of-arrays copy, the sortedness verdict and the
+ * statistics — and ONE synchronisation of `stream`; any other order takes the
+ * sorting path after that verdict and synchronises once more to read the
+ * statistics of the sorted stream.
  * Errors: ARG, UNSUPPORTED, INDEX (plan not created, *out = NULL, and
  * systec_last_bad_entry() names the first offending entry), NOMEM, CUDA.
  */

@@ -218,69 +218,82 @@ int plan_create_impl(Plan **out, int order, int64_t dim, int64_t nnz, const int3
     };
     const size_t nk = static_cast<size_t>(nnz > 0 ? nnz : 1);
     if ((e = cudaMallocAsync(&dst, sizeof(DevStats), s)) != cudaSuccess) return fail(e);
-    if ((e = cudaMallocAsync(&keys, nk * 8, s)) != cudaSuccess) return fail(e);
-    if ((e = cudaMallocAsync(&perm, nk * 4, s)) != cudaSuccess) return fail(e);
     std::memset(&hst, 0, sizeof(hst));
     hst.bad_entry = ULLONG_MAX;
-    if ((e = cudaMemcpyAsync(dst, &hst, sizeof(hst), cudaMemcpyHostToDevice, s)) != cudaSuccess) return fail(e);
+    const DevStats hst0 = hst;
+    if ((e = cudaMemcpyAsync(dst, &hst0, sizeof(hst0), cudaMemcpyHostToDevice, s)) != cudaSuccess) return fail(e);
 
-    // a1: validate + canonicalise + pack keys (wide plans: validate only, no keys)
-    const bool wide = bits * order > 64;
-    e = wide ? launch_validate_wide(order, dim, nnz, idx, perm, dst, s, !general)
-             : launch_canonicalize(order, dim, nnz, bits, idx, keys, perm, dst, s, !general);
-    if (e != cudaSuccess) return fail(e);
+    // order-2 symmetric plans: the windowed kernel's row / column pointers and
+    // bandwidth, read back with the statistics (sym2_window.cu)
+    unsigned long long win_host[2] = {0, 0};  // {bandwidth, largest column count}
+    int32_t win_items = 0;
+    auto build_window = [&]() -> cudaError_t {
+        if (!(order == 2 && !general && window)) return cudaSuccess;
+        cudaError_t we;
+        if (!p->win_rowptr) {
+            const size_t wb = static_cast<size_t>(dim + 1) * 8 + 16;
+            void *w = nullptr;
+            if ((we = pooled ? cudaMallocAsync(&w, wb, s) : cudaMalloc(&w, wb)) != cudaSuccess) return we;
+            p->win_rowptr = static_cast<int32_t *>(w);
+            p->win_colptr = p->win_rowptr + (dim + 1);
+        }
+        auto *wv = reinterpret_cast<unsigned long long *>(p->win_colptr + (dim + 1));
+        if ((we = win_build(*p, p->win_rowptr, p->win_colptr, wv, wv + 1, s)) != cudaSuccess) return we;
+        if ((we = cudaMemcpyAsync(win_host, wv, 16, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return we;
+        return cudaMemcpyAsync(&win_items, p->win_colptr + dim, 4, cudaMemcpyDeviceToHost, s);
+    };
+
+    // a1 + a2 in one pass, for input already in storage order (the common case):
+    // validation, canonical tuples written straight into the SoA stream, the
+    // sortedness flag and the statistics — one kernel, one synchronisation.
+    if ((e = launch_prepare_sorted(order, dim, nnz, p->ld, idx, vals, p->coords, p->vals, dst, s, !general)) !=
+        cudaSuccess)
+        return fail(e);
     if ((e = cudaMemcpyAsync(&hst, dst, sizeof(hst), cudaMemcpyDeviceToHost, s)) != cudaSuccess) return fail(e);
-    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return fail(e);  // sync 1: validation verdict
+    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return fail(e);  // sync 1: verdict + statistics
     if (hst.err) {
         g_last_bad_entry = static_cast<int64_t>(hst.bad_entry);
         cleanup();
+        free_window(p, pooled, s);
         if (pooled) cudaFreeAsync(p->storage, s); else cudaFree(p->storage);
         delete p;
         return SYSTEC_ERR_INDEX;
     }
-    const bool sorted = hst.unsorted == 0;
-    // a2: lexicographic sort (only when needed) + SoA gather
-    const unsigned long long *skeys = keys;
-    const uint32_t *sperm = nullptr;
-    if (!sorted && nnz > 1) {
+    const bool sorted = hst.unsorted == 0 || nnz < 2;
+    if (!sorted) {
+        // a1/a2, sorting path: pack keys (wide plans: none), lexicographic radix
+        // sort, SoA gather through the permutation, statistics of the sorted stream
+        const bool wide = bits * order > 64;
+        if ((e = cudaMallocAsync(&keys, nk * 8, s)) != cudaSuccess) return fail(e);
+        if ((e = cudaMallocAsync(&perm, nk * 4, s)) != cudaSuccess) return fail(e);
         if ((e = cudaMallocAsync(&keys2, nk * 8, s)) != cudaSuccess) return fail(e);
         if ((e = cudaMallocAsync(&perm2, nk * 4, s)) != cudaSuccess) return fail(e);
+        if ((e = cudaMemcpyAsync(dst, &hst0, sizeof(hst0), cudaMemcpyHostToDevice, s)) != cudaSuccess) return fail(e);
+        e = wide ? launch_validate_wide(order, dim, nnz, idx, perm, dst, s, !general)
+                 : launch_canonicalize(order, dim, nnz, bits, idx, keys, perm, dst, s, !general);
+        if (e != cudaSuccess) return fail(e);
+        const uint32_t *sperm = perm2;
         if (wide) {
             uint32_t *sorted_perm = nullptr;
             if ((e = sort_wide(order, dim, nnz, bits, idx, keys, keys2, perm, perm2, &sorted_perm, s, !general)) !=
                 cudaSuccess)
                 return fail(e);
             sperm = sorted_perm;
-        } else {
-            if ((e = sort_keys(nnz, bits * order, keys, keys2, perm, perm2, s)) != cudaSuccess) return fail(e);
-            skeys = keys2;
-            sperm = perm2;
-        }
-    }
-    e = wide ? launch_gather_wide(order, nnz, p->ld, p->ld, dim, idx, sperm, vals, p->coords, p->vals, s, !general)
-             : launch_gather(order, nnz, p->ld, bits, skeys, sperm, vals, p->coords, p->vals, s);
-    if (e != cudaSuccess) return fail(e);
-    if ((e = launch_stats(order, nnz, p->ld, p->coords, -1, dst, s)) != cudaSuccess) return fail(e);
-    if ((e = cudaMemcpyAsync(&hst, dst, sizeof(hst), cudaMemcpyDeviceToHost, s)) != cudaSuccess) return fail(e);
-    // order-2 symmetric plans: the windowed kernel's row / column pointers and
-    // bandwidth, read back with the statistics (sym2_window.cu)
-    unsigned long long win_host[2] = {0, 0};  // {bandwidth, largest column count}
-    int32_t win_items = 0;
-    if (order == 2 && !general && window) {
-        const size_t wb = static_cast<size_t>(dim + 1) * 8 + 16;
-        void *w = nullptr;
-        if ((e = pooled ? cudaMallocAsync(&w, wb, s) : cudaMalloc(&w, wb)) != cudaSuccess) return fail(e);
-        p->win_rowptr = static_cast<int32_t *>(w);
-        p->win_colptr = p->win_rowptr + (dim + 1);
-        auto *wv = reinterpret_cast<unsigned long long *>(p->win_colptr + (dim + 1));
-        if ((e = win_build(*p, p->win_rowptr, p->win_colptr, wv, wv + 1, s)) != cudaSuccess) return fail(e);
-        if ((e = cudaMemcpyAsync(win_host, wv, 16, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return fail(e);
-        if ((e = cudaMemcpyAsync(&win_items, p->win_colptr + dim, 4, cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+        } else if ((e = sort_keys(nnz, bits * order, keys, keys2, perm, perm2, s)) != cudaSuccess) {
             return fail(e);
+        }
+        e = wide ? launch_gather_wide(order, nnz, p->ld, p->ld, dim, idx, sperm, vals, p->coords, p->vals, s, !general)
+                 : launch_gather(order, nnz, p->ld, bits, keys2, sperm, vals, p->coords, p->vals, s);
+        if (e != cudaSuccess) return fail(e);
+        if ((e = cudaMemcpyAsync(dst, &hst0, sizeof(hst0), cudaMemcpyHostToDevice, s)) != cudaSuccess) return fail(e);
+        if ((e = launch_stats(order, nnz, p->ld, p->coords, -1, dst, s)) != cudaSuccess) return fail(e);
+        if ((e = cudaMemcpyAsync(&hst, dst, sizeof(hst), cudaMemcpyDeviceToHost, s)) != cudaSuccess) return fail(e);
     }
+    if ((e = build_window()) != cudaSuccess) return fail(e);  // order-2 window plans only (reads the sorted stream)
     cleanup();
     dst = nullptr; keys = nullptr; keys2 = nullptr; perm = nullptr; perm2 = nullptr;
-    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) {  // sync 2: statistics
+    // sync 2: only on the sorting path (its statistics) and for window plans
+    if ((!sorted || p->win_rowptr) && (e = cudaStreamSynchronize(s)) != cudaSuccess) {
         free_window(p, pooled, s);
         if (pooled) cudaFreeAsync(p->storage, s); else cudaFree(p->storage);
         delete p;

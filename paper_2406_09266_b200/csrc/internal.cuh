@@ -91,6 +91,10 @@ cudaError_t launch_permute(int order, int64_t nnz, int64_t ld, const uint32_t *p
 cudaError_t launch_gather_range(int order, int64_t n, int64_t ld, int bits, const unsigned long long *keys,
                                 const float *vals_in, int32_t *coords, float *vals_out, cudaStream_t s);
 
+// one pass for input already in storage order: SoA stream + validation + sortedness + statistics
+cudaError_t launch_prepare_sorted(int order, int64_t dim, int64_t nnz, int64_t ld, const int32_t *idx,
+                                  const float *vals_in, int32_t *coords, float *vals_out, DevStats *st,
+                                  cudaStream_t s, bool canonicalise = true, int64_t e_offset = 0);
 // wide plans (order * ceil(log2 dim) > 64): no packed keys
 cudaError_t launch_validate_wide(int order, int64_t dim, int64_t nnz, const int32_t *idx, uint32_t *perm,
                                  DevStats *st, cudaStream_t s, bool canonicalise = true, int64_t e_offset = 0);

@@ -8,6 +8,8 @@
 // The concordant, sorted traversal order corresponds to building the CSF /
 // concordising step of PAPER.md:482-503.  The paper excludes this
 // rearrangement from its timings; so do we (plan creation).
+#include <algorithm>
+
 #include <cub/device/device_radix_sort.cuh>
 
 #include "internal.cuh"
@@ -277,7 +279,9 @@ __global__ void stats_kernel(int64_t nnz, int64_t ld, const int32_t *__restrict_
             maxrun = len > maxrun ? len : maxrun;
         }
     }
-    // warp reductions, then one atomic per warp and counter
+    // warp reductions, block totals in shared memory, then one atomic per
+    // counter and block (the counters share a 128-byte line: same-line atomics
+    // serialise at their L2 slice)
     auto wsum = [](unsigned long long v) {
         for (int d = 16; d; d >>= 1) v += __shfl_down_sync(0xffffffffu, v, d);
         return v;
@@ -289,6 +293,8 @@ __global__ void stats_kernel(int64_t nnz, int64_t ld, const int32_t *__restrict_
         }
         return v;
     };
+    constexpr int NS = 5 + NC;  // G, expanded, lead, pos1, maxrun, hist[NC]
+    __shared__ unsigned long long part[32][NS];
     G = wsum(G);
     expanded = wsum(expanded);
     lead = wsum(lead);
@@ -296,15 +302,225 @@ __global__ void stats_kernel(int64_t nnz, int64_t ld, const int32_t *__restrict_
     maxrun = wmax(maxrun);
 #pragma unroll
     for (int q = 0; q < NC; ++q) hist[q] = wsum(hist[q]);
+    const int warps = (blockDim.x + 31) >> 5;
     if ((threadIdx.x & 31) == 0) {
-        atomicAdd(&st->G, G);
-        atomicAdd(&st->expanded, expanded);
-        atomicAdd(&st->lead_runs, lead);
-        atomicAdd(&st->pos1_runs, pos1);
-        if (maxrun) atomicMax(&st->max_lead_run, maxrun);
+        unsigned long long *row = part[threadIdx.x >> 5];
+        row[0] = G; row[1] = expanded; row[2] = lead; row[3] = pos1; row[4] = maxrun;
 #pragma unroll
-        for (int q = 0; q < NC; ++q)
-            if (hist[q]) atomicAdd(&st->hist[q], hist[q]);
+        for (int q = 0; q < NC; ++q) row[5 + q] = hist[q];
+    }
+    __syncthreads();
+    if (threadIdx.x < NS) {
+        const int k = threadIdx.x;
+        unsigned long long tot = 0;
+        for (int w = 0; w < warps; ++w) tot = k == 4 ? (part[w][k] > tot ? part[w][k] : tot) : tot + part[w][k];
+        if (tot) {
+            if (k == 4) atomicMax(&st->max_lead_run, tot);
+            else atomicAdd(k == 0 ? &st->G : k == 1 ? &st->expanded : k == 2 ? &st->lead_runs
+                           : k == 3 ? &st->pos1_runs : &st->hist[k - 5], tot);
+        }
+    }
+}
+
+// ---- one-pass prepare for input that is already in storage order (the
+// north_star's format: canonical tuples sorted lexicographically; tuples
+// spelled in another order still qualify when their canonical forms are
+// sorted).  Reads the caller's tuples once and writes the structure-of-arrays
+// stream, the validation verdict, the sortedness flag and the plan statistics
+// — what canonicalize + gather + stats do in three passes over packed keys.
+// No keys: any order * ceil(log2 dim).  When the flag comes back "unsorted"
+// the stream it wrote is discarded and the sorting path runs.
+// A block stages a contiguous tile of kPrepTile tuples in shared memory with
+// coalesced loads (the tuples are 4N bytes apart: read per thread they would
+// be strided), then every thread takes U of them; an entry's predecessor comes
+// from the tile too (the tile's first entry loads its own).  The longest
+// leading run is found by max_lead_run_kernel right after: a search per run
+// end is bounded work only on sorted input, so that kernel first reads the flag.
+constexpr int kPrepThreads = 256;
+constexpr int kPrepU = 4;
+constexpr int kPrepTile = kPrepThreads * kPrepU;
+
+template <int N, bool CANON>
+__global__ void __launch_bounds__(kPrepThreads) prepare_sorted_kernel(const int32_t *__restrict__ idx,
+                                                                      const float *__restrict__ vals_in, int64_t nnz,
+                                                                      int64_t ld, int64_t dim,
+                                                                      int32_t *__restrict__ coords,
+                                                                      float *__restrict__ vals_out, DevStats *st,
+                                                                      int64_t e_offset) {
+    constexpr int NC = 1 << (N - 1);  // equality patterns
+    constexpr int U = kPrepU;
+    __shared__ int32_t tile[kPrepTile * N];
+    unsigned hist[NC];  // per-thread counts fit 32 bits (a thread sees < 2^31 / threads entries)
+#pragma unroll
+    for (int c = 0; c < NC; ++c) hist[c] = 0;
+    unsigned G = 0, expanded = 0, lead = 0, pos1 = 0;
+    long long bad_at = -1;
+    bool unsorted = false;
+    const int tid = threadIdx.x;
+    const int64_t tiles = (ld + kPrepTile - 1) / kPrepTile;
+    auto canonical = [&](const int32_t *w, int32_t (&c)[N]) {  // tuple at w -> canonical c; in range?
+        bool ok = true;
+#pragma unroll
+        for (int t = 0; t < N; ++t) {
+            c[t] = w[t];
+            ok &= (c[t] >= 0) & (static_cast<int64_t>(c[t]) < dim);
+        }
+        if (CANON) sort_net<N>(c);
+        return ok;
+    };
+    for (int64_t tl = blockIdx.x; tl < tiles; tl += gridDim.x) {
+        const int64_t base = tl * kPrepTile;
+        const int64_t have = min(static_cast<int64_t>(kPrepTile), nnz - base);  // tuples of this tile (<= 0: padding only)
+        const int64_t words = have > 0 ? have * N : 0;
+        float v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t e = base + tid + u * kPrepThreads;
+            v[u] = e < nnz ? vals_in[e] : 0.0f;
+        }
+        __syncthreads();  // the previous tile is consumed
+#pragma unroll
+        for (int k = 0; k < U * N; ++k) {
+            const int w = tid + k * kPrepThreads;
+            if (w < words) tile[w] = idx[base * N + w];
+        }
+        __syncthreads();
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int i = tid + u * kPrepThreads;
+            const int64_t e = base + i;
+            if (e >= ld) continue;
+            if (e >= nnz) {  // the padding read by the last chunk's bulk copies, never used
+#pragma unroll
+                for (int t = 0; t < N; ++t) coords[t * ld + e] = 0;
+                vals_out[e] = 0.0f;
+                continue;
+            }
+            int32_t c[N], q[N];
+            const bool ok = canonical(tile + i * N, c);
+#pragma unroll
+            for (int t = 0; t < N; ++t) coords[t * ld + e] = ok ? c[t] : 0;
+            vals_out[e] = v[u];
+            if (!ok) {
+                if (bad_at < 0) bad_at = e;
+                continue;
+            }
+            bool new_lead = true, new_pos1 = true;
+            if (e > 0 && canonical(i > 0 ? tile + (i - 1) * N : idx + (e - 1) * N, q)) {
+                int cmp = 0;  // sign of q - c in lexicographic order
+#pragma unroll
+                for (int t = 0; t < N; ++t)
+                    if (cmp == 0) cmp = (q[t] > c[t]) - (q[t] < c[t]);
+                unsorted |= cmp > 0;
+                new_lead = q[0] != c[0];
+                new_pos1 = q[1 % N] != c[1 % N];
+            }
+            int code = 0, distinct = 1, run = 1;
+            int denom = 1;
+#pragma unroll
+            for (int t = 1; t < N; ++t) {
+                if (c[t] == c[t - 1]) {
+                    code |= 1 << (t - 1);
+                    ++run;
+                } else {
+                    ++distinct;
+                    denom *= static_cast<int>(dfact(run));
+                    run = 1;
+                }
+            }
+            denom *= static_cast<int>(dfact(run));
+            G += distinct;
+            expanded += static_cast<unsigned>(static_cast<int>(dfact(N)) / denom);
+#pragma unroll
+            for (int w = 0; w < NC; ++w) hist[w] += (code == w);
+            lead += new_lead;
+            pos1 += new_pos1;
+        }
+    }
+    if (bad_at >= 0) {
+        atomicOr(&st->err, 1ull);
+        atomicMin(&st->bad_entry, static_cast<unsigned long long>(bad_at + e_offset));
+    }
+    if (unsorted) st->unsorted = 1ull;
+    // block totals in shared memory, then one atomic per counter and block:
+    // the counters share one 128-byte line, and same-line atomics serialise at
+    // their L2 slice (one set per warp cost more than the streaming itself)
+    constexpr int NS = 4 + NC;
+    __shared__ unsigned long long part[kPrepThreads / 32][NS];
+    auto wsum = [](unsigned long long x) {
+        for (int d = 16; d; d >>= 1) x += __shfl_down_sync(0xffffffffu, x, d);
+        return x;
+    };
+    const unsigned long long Gs = wsum(G), xs = wsum(expanded), ls = wsum(lead), ps = wsum(pos1);
+    unsigned long long hs[NC];
+#pragma unroll
+    for (int w = 0; w < NC; ++w) hs[w] = wsum(hist[w]);
+    if ((tid & 31) == 0) {
+        unsigned long long *row = part[tid >> 5];
+        row[0] = Gs; row[1] = xs; row[2] = ls; row[3] = ps;
+#pragma unroll
+        for (int w = 0; w < NC; ++w) row[4 + w] = hs[w];
+    }
+    __syncthreads();
+    if (tid < NS) {
+        unsigned long long tot = 0;
+#pragma unroll
+        for (int w = 0; w < kPrepThreads / 32; ++w) tot += part[w][tid];
+        unsigned long long *dst = tid == 0 ? &st->G : tid == 1 ? &st->expanded : tid == 2 ? &st->lead_runs
+                                  : tid == 3 ? &st->pos1_runs : &st->hist[tid - 4];
+        if (tot) atomicAdd(dst, tot);
+    }
+}
+
+// longest run of equal c_0 in a sorted SoA stream (c0 16-byte aligned, padded
+// to a multiple of 4); returns at once when the one-pass prepare found the
+// input unsorted (st->unsorted, final by stream order)
+__global__ void __launch_bounds__(256) max_lead_run_kernel(const int32_t *__restrict__ c0, int64_t nnz, DevStats *st) {
+    if (*reinterpret_cast<volatile unsigned long long *>(&st->unsorted) != 0ull) return;
+    unsigned long long maxrun = 0;
+    const int lane = threadIdx.x & 31;
+    const int64_t quads = (nnz + 3) >> 2;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i - lane < quads;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int4 w = make_int4(0, 0, 0, 0);
+        if (i < quads) w = reinterpret_cast<const int4 *>(c0)[i];
+        int32_t nxt = __shfl_down_sync(0xffffffffu, w.x, 1);
+        if (lane == 31 && 4 * i + 4 < nnz) nxt = c0[4 * i + 4];
+        const int32_t me[5] = {w.x, w.y, w.z, w.w, nxt};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int64_t e = 4 * i + k;
+            if (e < nnz && (e == nnz - 1 || me[k + 1] != me[k])) {
+                // end of a leading run: its start by a galloping search backwards
+                // (probes stay within twice the run's length of e), then bisection
+                int64_t step = 1, hi = e;
+                while (hi - step >= 0 && c0[hi - step] >= me[k]) {
+                    hi -= step;
+                    step <<= 1;
+                }
+                int64_t lo = hi - step >= 0 ? hi - step + 1 : 0;  // c0[lo - 1] < me[k] (or lo == 0); c0[hi] == me[k]
+                while (lo < hi) {
+                    const int64_t mid = (lo + hi) >> 1;
+                    if (c0[mid] < me[k]) lo = mid + 1; else hi = mid;
+                }
+                const unsigned long long len = static_cast<unsigned long long>(e - lo + 1);
+                maxrun = len > maxrun ? len : maxrun;
+            }
+        }
+    }
+    for (int d = 16; d; d >>= 1) {
+        const unsigned long long o = __shfl_down_sync(0xffffffffu, maxrun, d);
+        maxrun = o > maxrun ? o : maxrun;
+    }
+    // one atomic per block at most, and none when the running maximum already
+    // covers it (same-address atomics serialise at their L2 slice)
+    __shared__ unsigned long long wmax[8];
+    if (lane == 0) wmax[threadIdx.x >> 5] = maxrun;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long m = 0;
+        for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) m = wmax[w] > m ? wmax[w] : m;
+        if (m > *reinterpret_cast<volatile unsigned long long *>(&st->max_lead_run)) atomicMax(&st->max_lead_run, m);
     }
 }
 
@@ -362,6 +578,23 @@ cudaError_t launch_gather(int order, int64_t nnz, int64_t ld, int bits, const un
     if (ld == 0) return cudaSuccess;
     const int th = 256;
     SYSTEC_ORDER_SWITCH(order, gather_kernel<N><<<grid_for(ld, th), th, 0, s>>>(nnz, ld, bits, keys, perm, vals_in, coords, vals_out));
+    return cudaGetLastError();
+}
+
+cudaError_t launch_prepare_sorted(int order, int64_t dim, int64_t nnz, int64_t ld, const int32_t *idx,
+                                  const float *vals_in, int32_t *coords, float *vals_out, DevStats *st,
+                                  cudaStream_t s, bool canonicalise, int64_t e_offset) {
+    if (ld == 0) return cudaSuccess;
+    const int th = kPrepThreads;
+    const int grid = std::max(1, grid_for((ld + kPrepU - 1) / kPrepU, th) / 2);  // one tile per block and round, 8 blocks per SM
+    if (canonicalise) {
+        SYSTEC_ORDER_SWITCH(order, prepare_sorted_kernel<N, true><<<grid, th, 0, s>>>(idx, vals_in, nnz, ld, dim, coords, vals_out, st, e_offset));
+    } else {
+        SYSTEC_ORDER_SWITCH(order, prepare_sorted_kernel<N, false><<<grid, th, 0, s>>>(idx, vals_in, nnz, ld, dim, coords, vals_out, st, e_offset));
+    }
+    // one quad per thread, uncapped grid: a warp that meets a run end waits for that lane's
+    // search, so no warp is given a second round behind it
+    if (nnz > 0) max_lead_run_kernel<<<static_cast<unsigned>(((nnz + 3) / 4 + th - 1) / th), th, 0, s>>>(coords, nnz, st);
     return cudaGetLastError();
 }
 
