@@ -74,9 +74,25 @@ template <int VW> struct VecT;
 template <> struct VecT<4> {
     using T = float4;
     static __device__ __forceinline__ T zero() { return make_float4(0.f, 0.f, 0.f, 0.f); }
-    static __device__ __forceinline__ T mul(T a, T b) { return make_float4(a.x * b.x, a.y * b.y, a.z * b.z, a.w * b.w); }
-    static __device__ __forceinline__ T scale(float s, T a) { return make_float4(s * a.x, s * a.y, s * a.z, s * a.w); }
-    static __device__ __forceinline__ T add(T a, T b) { return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w); }
+    // two packed-pair operations per float4 (FMUL2 / FADD2, ptx.cuh)
+    static __device__ __forceinline__ T mul(T a, T b) {
+        T r;
+        mul2(r.x, r.y, a.x, a.y, b.x, b.y);
+        mul2(r.z, r.w, a.z, a.w, b.z, b.w);
+        return r;
+    }
+    static __device__ __forceinline__ T scale(float s, T a) {
+        T r;
+        mul2(r.x, r.y, s, s, a.x, a.y);
+        mul2(r.z, r.w, s, s, a.z, a.w);
+        return r;
+    }
+    static __device__ __forceinline__ T add(T a, T b) {
+        T r;
+        add2(r.x, r.y, a.x, a.y, b.x, b.y);
+        add2(r.z, r.w, a.z, a.w, b.z, b.w);
+        return r;
+    }
     static __device__ __forceinline__ T load(const float *p, uint64_t pol) { return ldg4_hint(p, pol); }
     static __device__ __forceinline__ void red(float *p, T v) { red_add4(p, v); }
     static __device__ __forceinline__ void red_if(float *p, T v, bool pred) { red_add4_if(p, v, pred); }

@@ -109,6 +109,31 @@ __device__ __forceinline__ void red_add1(float *p, float v) {
     asm volatile("red.global.add.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
 }
 
+// Packed fp32 pairs (sm_100a FMUL2 / FADD2: two IEEE round-to-nearest fp32
+// operations per lane in one issue slot; element results identical to
+// FMUL / FADD).  -DSYSTEC_NO_F32X2 builds the scalar forms for A/B runs.
+#ifndef SYSTEC_NO_F32X2
+__device__ __forceinline__ void mul2(float &r0, float &r1, float a0, float a1, float b0, float b1) {
+    asm("{\n\t.reg .b64 ra, rb, rc;\n\tmov.b64 ra, {%2,%3};\n\tmov.b64 rb, {%4,%5};\n\t"
+        "mul.rn.f32x2 rc, ra, rb;\n\tmov.b64 {%0,%1}, rc;\n\t}"
+        : "=f"(r0), "=f"(r1) : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
+}
+__device__ __forceinline__ void add2(float &r0, float &r1, float a0, float a1, float b0, float b1) {
+    asm("{\n\t.reg .b64 ra, rb, rc;\n\tmov.b64 ra, {%2,%3};\n\tmov.b64 rb, {%4,%5};\n\t"
+        "add.rn.f32x2 rc, ra, rb;\n\tmov.b64 {%0,%1}, rc;\n\t}"
+        : "=f"(r0), "=f"(r1) : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
+}
+#else
+__device__ __forceinline__ void mul2(float &r0, float &r1, float a0, float a1, float b0, float b1) {
+    r0 = a0 * b0;
+    r1 = a1 * b1;
+}
+__device__ __forceinline__ void add2(float &r0, float &r1, float a0, float a1, float b0, float b1) {
+    r0 = a0 + b0;
+    r1 = a1 + b1;
+}
+#endif
+
 // predicated forms: one REDG issued under a predicate, no branch
 __device__ __forceinline__ void red_add4_if(float *p, float4 v, bool pred) {
     asm volatile(
