@@ -10,6 +10,8 @@
 // rearrangement from its timings; so do we (plan creation).
 #include <algorithm>
 
+#include <cuda_pipeline.h>
+
 #include <cub/device/device_radix_sort.cuh>
 
 #include "internal.cuh"
@@ -349,7 +351,7 @@ __global__ void __launch_bounds__(kPrepThreads) prepare_sorted_kernel(const int3
                                                                       int64_t e_offset) {
     constexpr int NC = 1 << (N - 1);  // equality patterns
     constexpr int U = kPrepU;
-    __shared__ int32_t tile[kPrepTile * N];
+    __shared__ int32_t tiles_s[2][kPrepTile * N];
     unsigned hist[NC];  // per-thread counts fit 32 bits (a thread sees < 2^31 / threads entries)
 #pragma unroll
     for (int c = 0; c < NC; ++c) hist[c] = 0;
@@ -368,22 +370,33 @@ __global__ void __launch_bounds__(kPrepThreads) prepare_sorted_kernel(const int3
         if (CANON) sort_net<N>(c);
         return ok;
     };
-    for (int64_t tl = blockIdx.x; tl < tiles; tl += gridDim.x) {
+    // two-stage pipeline: the next tile's tuples (4-byte cp.async into the other
+    // shared buffer) and values (registers) are in flight while this one is consumed
+    auto issue = [&](int64_t tl, int32_t *dst, float (&vv)[U]) {
         const int64_t base = tl * kPrepTile;
-        const int64_t have = min(static_cast<int64_t>(kPrepTile), nnz - base);  // tuples of this tile (<= 0: padding only)
+        const int64_t have = min(static_cast<int64_t>(kPrepTile), nnz - base);  // tuples of the tile (<= 0: padding only)
         const int64_t words = have > 0 ? have * N : 0;
-        float v[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int64_t e = base + tid + u * kPrepThreads;
-            v[u] = e < nnz ? vals_in[e] : 0.0f;
-        }
-        __syncthreads();  // the previous tile is consumed
 #pragma unroll
         for (int k = 0; k < U * N; ++k) {
             const int w = tid + k * kPrepThreads;
-            if (w < words) tile[w] = idx[base * N + w];
+            if (w < words) __pipeline_memcpy_async(dst + w, idx + base * N + w, 4);
         }
+        __pipeline_commit();
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t e = base + tid + u * kPrepThreads;
+            vv[u] = e < nnz ? vals_in[e] : 0.0f;
+        }
+    };
+    float v[U], vn[U];
+    int buf = 0;
+    if (blockIdx.x < tiles) issue(blockIdx.x, tiles_s[0], v);
+    for (int64_t tl = blockIdx.x; tl < tiles; tl += gridDim.x) {
+        const int64_t base = tl * kPrepTile;
+        const int32_t *tile = tiles_s[buf];
+        const bool more = tl + gridDim.x < tiles;
+        if (more) issue(tl + gridDim.x, tiles_s[buf ^ 1], vn);
+        if (more) __pipeline_wait_prior(1); else __pipeline_wait_prior(0);
         __syncthreads();
 #pragma unroll
         for (int u = 0; u < U; ++u) {
@@ -436,6 +449,10 @@ __global__ void __launch_bounds__(kPrepThreads) prepare_sorted_kernel(const int3
             lead += new_lead;
             pos1 += new_pos1;
         }
+        __syncthreads();  // this buffer is consumed: the next round's copies may overwrite it
+        buf ^= 1;
+#pragma unroll
+        for (int u = 0; u < U; ++u) v[u] = vn[u];
     }
     if (bad_at >= 0) {
         atomicOr(&st->err, 1ull);
@@ -474,38 +491,73 @@ __global__ void __launch_bounds__(kPrepThreads) prepare_sorted_kernel(const int3
 
 // longest run of equal c_0 in a sorted SoA stream (c0 16-byte aligned, padded
 // to a multiple of 4); returns at once when the one-pass prepare found the
-// input unsorted (st->unsorted, final by stream order)
+// input unsorted (st->unsorted, final by stream order).  A lane holds 16
+// consecutive entries, a warp a window of 512.  A run that ends in the window
+// starts right after the previous run end: inside the lane, or in an earlier
+// lane (an exclusive max-scan of the lanes' last ends), else before the window
+// — then, and only for the window's first run end, by a galloping search
+// backwards from the window's start (probes stay within twice the run's
+// length) and a bisection.  One search per warp at most: with a search per
+// run end the kernel was a chain of dependent loads per warp (43 us on c2).
+constexpr int kRunQuads = 4;  // int4 loads per lane
 __global__ void __launch_bounds__(256) max_lead_run_kernel(const int32_t *__restrict__ c0, int64_t nnz, DevStats *st) {
-    if (*reinterpret_cast<volatile unsigned long long *>(&st->unsorted) != 0ull) return;
-    unsigned long long maxrun = 0;
+    if (__ldg(&st->unsorted) != 0ull) return;  // cached load: one L2 request per SM, not one per warp
+    constexpr int PER = 4 * kRunQuads;
     const int lane = threadIdx.x & 31;
-    const int64_t quads = (nnz + 3) >> 2;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i - lane < quads;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        int4 w = make_int4(0, 0, 0, 0);
-        if (i < quads) w = reinterpret_cast<const int4 *>(c0)[i];
-        int32_t nxt = __shfl_down_sync(0xffffffffu, w.x, 1);
-        if (lane == 31 && 4 * i + 4 < nnz) nxt = c0[4 * i + 4];
-        const int32_t me[5] = {w.x, w.y, w.z, w.w, nxt};
+    const int64_t first = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * PER;  // grid covers nnz: one window per warp
+    const int64_t wstart = first - static_cast<int64_t>(lane) * PER;
+    unsigned long long maxrun = 0;
+    if (wstart < nnz) {  // warp-uniform
+        int32_t me[PER + 1];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const int64_t e = 4 * i + k;
-            if (e < nnz && (e == nnz - 1 || me[k + 1] != me[k])) {
-                // end of a leading run: its start by a galloping search backwards
-                // (probes stay within twice the run's length of e), then bisection
-                int64_t step = 1, hi = e;
-                while (hi - step >= 0 && c0[hi - step] >= me[k]) {
-                    hi -= step;
+        for (int q = 0; q < kRunQuads; ++q) {
+            int4 w = make_int4(0, 0, 0, 0);
+            if (first + 4 * q < nnz) w = reinterpret_cast<const int4 *>(c0 + first)[q];  // padded to a multiple of 4
+            me[4 * q] = w.x; me[4 * q + 1] = w.y; me[4 * q + 2] = w.z; me[4 * q + 3] = w.w;
+        }
+        me[PER] = __shfl_down_sync(0xffffffffu, me[0], 1);
+        if (lane == 31 && first + PER < nnz) me[PER] = c0[first + PER];
+        // this lane's run ends (bit k: entry first + k ends a leading run)
+        unsigned ends = 0;
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            const int64_t e = first + k;
+            if (e < nnz && (e == nnz - 1 || me[k + 1] != me[k])) ends |= 1u << k;
+        }
+        // last run end in earlier lanes of the window (-1: none)
+        long long last = ends ? first + (31 - __clz(ends)) : -1;
+        long long before = __shfl_up_sync(0xffffffffu, last, 1);
+        if (lane == 0) before = -1;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const long long o = __shfl_up_sync(0xffffffffu, before, d);
+            if (lane >= d) before = o > before ? o : before;
+        }
+        long long prev = before;
+        while (ends) {
+            const int k = __ffs(ends) - 1;
+            ends &= ends - 1;
+            const int64_t e = first + k;
+            int64_t start;
+            if (prev >= 0) {
+                start = prev + 1;
+            } else {  // the window's first run end: every entry from the window's start to e equals me[k]
+                const int32_t val = c0[e];
+                int64_t step = 1, hi2 = wstart;
+                while (hi2 - step >= 0 && c0[hi2 - step] >= val) {
+                    hi2 -= step;
                     step <<= 1;
                 }
-                int64_t lo = hi - step >= 0 ? hi - step + 1 : 0;  // c0[lo - 1] < me[k] (or lo == 0); c0[hi] == me[k]
-                while (lo < hi) {
-                    const int64_t mid = (lo + hi) >> 1;
-                    if (c0[mid] < me[k]) lo = mid + 1; else hi = mid;
+                int64_t lo2 = hi2 - step >= 0 ? hi2 - step + 1 : 0;  // c0[lo2 - 1] < val (or lo2 == 0); c0[hi2] == val
+                while (lo2 < hi2) {
+                    const int64_t mid = (lo2 + hi2) >> 1;
+                    if (c0[mid] < val) lo2 = mid + 1; else hi2 = mid;
                 }
-                const unsigned long long len = static_cast<unsigned long long>(e - lo + 1);
-                maxrun = len > maxrun ? len : maxrun;
+                start = lo2;
             }
+            const unsigned long long len = static_cast<unsigned long long>(e - start + 1);
+            maxrun = len > maxrun ? len : maxrun;
+            prev = e;
         }
     }
     for (int d = 16; d; d >>= 1) {
@@ -586,15 +638,26 @@ cudaError_t launch_prepare_sorted(int order, int64_t dim, int64_t nnz, int64_t l
                                   cudaStream_t s, bool canonicalise, int64_t e_offset) {
     if (ld == 0) return cudaSuccess;
     const int th = kPrepThreads;
-    const int grid = std::max(1, grid_for((ld + kPrepU - 1) / kPrepU, th) / 2);  // one tile per block and round, 8 blocks per SM
+    // persistent grid of exactly the resident blocks (tiles are taken round-robin: a second,
+    // partial wave of blocks would leave the SMs half empty behind it), at most one block per tile
+    auto resident = [&](auto kernel) {
+        int dev = 0, sms = 148, per_sm = 1;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, th, 0) != cudaSuccess || per_sm < 1) per_sm = 1;
+        const int64_t tiles = (ld + kPrepTile - 1) / kPrepTile;
+        return static_cast<int>(std::min<int64_t>(tiles, static_cast<int64_t>(sms) * per_sm));
+    };
     if (canonicalise) {
-        SYSTEC_ORDER_SWITCH(order, prepare_sorted_kernel<N, true><<<grid, th, 0, s>>>(idx, vals_in, nnz, ld, dim, coords, vals_out, st, e_offset));
+        SYSTEC_ORDER_SWITCH(order, prepare_sorted_kernel<N, true><<<resident(prepare_sorted_kernel<N, true>), th, 0, s>>>(idx, vals_in, nnz, ld, dim, coords, vals_out, st, e_offset));
     } else {
-        SYSTEC_ORDER_SWITCH(order, prepare_sorted_kernel<N, false><<<grid, th, 0, s>>>(idx, vals_in, nnz, ld, dim, coords, vals_out, st, e_offset));
+        SYSTEC_ORDER_SWITCH(order, prepare_sorted_kernel<N, false><<<resident(prepare_sorted_kernel<N, false>), th, 0, s>>>(idx, vals_in, nnz, ld, dim, coords, vals_out, st, e_offset));
     }
-    // one quad per thread, uncapped grid: a warp that meets a run end waits for that lane's
-    // search, so no warp is given a second round behind it
-    if (nnz > 0) max_lead_run_kernel<<<static_cast<unsigned>(((nnz + 3) / 4 + th - 1) / th), th, 0, s>>>(coords, nnz, st);
+    // one 512-entry window per warp, uncapped grid
+    if (nnz > 0) {
+        const int64_t per_block = static_cast<int64_t>(th) * 4 * kRunQuads;
+        max_lead_run_kernel<<<static_cast<unsigned>((nnz + per_block - 1) / per_block), th, 0, s>>>(coords, nnz, st);
+    }
     return cudaGetLastError();
 }
 
