@@ -251,7 +251,9 @@ int plan_create_impl(Plan **out, int order, int64_t dim, int64_t nnz, const int3
         return fail(e);
     if ((e = cudaMemcpyAsync(&hst, dst, sizeof(hst), cudaMemcpyDeviceToHost, s)) != cudaSuccess) return fail(e);
     if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return fail(e);  // sync 1: verdict + statistics
-    if (hst.err) {
+    // (a pass that also saw a disorder stopped early: its first bad entry need not be
+    // the first one — the sorting path below validates every entry and reports)
+    if (hst.err && hst.unsorted == 0) {
         g_last_bad_entry = static_cast<int64_t>(hst.bad_entry);
         cleanup();
         free_window(p, pooled, s);
@@ -285,7 +287,9 @@ int plan_create_impl(Plan **out, int order, int64_t dim, int64_t nnz, const int3
         e = wide ? launch_gather_wide(order, nnz, p->ld, p->ld, dim, idx, sperm, vals, p->coords, p->vals, s, !general)
                  : launch_gather(order, nnz, p->ld, bits, keys2, sperm, vals, p->coords, p->vals, s);
         if (e != cudaSuccess) return fail(e);
-        if ((e = cudaMemcpyAsync(dst, &hst0, sizeof(hst0), cudaMemcpyHostToDevice, s)) != cudaSuccess) return fail(e);
+        // (no reset here: the one-pass kernel stops at the first tile after a disorder is
+        // published, so this path's validation verdict is the complete one; the
+        // canonicalise kernels write only the verdict fields, the counters are still zero)
         if ((e = launch_stats(order, nnz, p->ld, p->coords, -1, dst, s)) != cudaSuccess) return fail(e);
         if ((e = cudaMemcpyAsync(&hst, dst, sizeof(hst), cudaMemcpyDeviceToHost, s)) != cudaSuccess) return fail(e);
     }
@@ -298,6 +302,13 @@ int plan_create_impl(Plan **out, int order, int64_t dim, int64_t nnz, const int3
         if (pooled) cudaFreeAsync(p->storage, s); else cudaFree(p->storage);
         delete p;
         return cuda_fail(e);
+    }
+    if (hst.err) {  // sorting path: a bad index in a tile the one-pass kernel never reached
+        g_last_bad_entry = static_cast<int64_t>(hst.bad_entry);
+        free_window(p, pooled, s);
+        if (pooled) cudaFreeAsync(p->storage, s); else cudaFree(p->storage);
+        delete p;
+        return SYSTEC_ERR_INDEX;
     }
     if (p->win_rowptr) {
         p->win_bw = static_cast<int64_t>(win_host[0]);

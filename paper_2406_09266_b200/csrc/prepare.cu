@@ -352,6 +352,7 @@ __global__ void __launch_bounds__(kPrepThreads) prepare_sorted_kernel(const int3
     constexpr int NC = 1 << (N - 1);  // equality patterns
     constexpr int U = kPrepU;
     __shared__ int32_t tiles_s[2][kPrepTile * N];
+    __shared__ bool stop;
     unsigned hist[NC];  // per-thread counts fit 32 bits (a thread sees < 2^31 / threads entries)
 #pragma unroll
     for (int c = 0; c < NC; ++c) hist[c] = 0;
@@ -397,7 +398,13 @@ __global__ void __launch_bounds__(kPrepThreads) prepare_sorted_kernel(const int3
         const bool more = tl + gridDim.x < tiles;
         if (more) issue(tl + gridDim.x, tiles_s[buf ^ 1], vn);
         if (more) __pipeline_wait_prior(1); else __pipeline_wait_prior(0);
+        // unsorted input: some block has said so — stop (what this pass wrote is discarded anyway)
+        if (tid == 0) stop = *reinterpret_cast<volatile unsigned long long *>(&st->unsorted) != 0ull;
         __syncthreads();
+        if (stop) {  // block-uniform
+            __pipeline_wait_prior(0);
+            break;
+        }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int i = tid + u * kPrepThreads;
@@ -449,7 +456,9 @@ __global__ void __launch_bounds__(kPrepThreads) prepare_sorted_kernel(const int3
             lead += new_lead;
             pos1 += new_pos1;
         }
-        __syncthreads();  // this buffer is consumed: the next round's copies may overwrite it
+        // this buffer is consumed (the next round's copies may overwrite it); a disorder
+        // seen in this tile is published at once
+        if (__syncthreads_or(unsorted) && tid == 0) *reinterpret_cast<volatile unsigned long long *>(&st->unsorted) = 1ull;
         buf ^= 1;
 #pragma unroll
         for (int u = 0; u < U; ++u) v[u] = vn[u];
@@ -458,7 +467,6 @@ __global__ void __launch_bounds__(kPrepThreads) prepare_sorted_kernel(const int3
         atomicOr(&st->err, 1ull);
         atomicMin(&st->bad_entry, static_cast<unsigned long long>(bad_at + e_offset));
     }
-    if (unsorted) st->unsorted = 1ull;
     // block totals in shared memory, then one atomic per counter and block:
     // the counters share one 128-byte line, and same-line atomics serialise at
     // their L2 slice (one set per warp cost more than the streaming itself)

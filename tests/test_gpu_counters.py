@@ -29,7 +29,10 @@ pytestmark = pytest.mark.gpu
 
 METRICS = ["l1tex__m_xbar2l1tex_read_bytes_mem_global_op_tma_ld.sum", "lts__t_requests_srcunit_tex_op_red.sum",
            "sm__sass_thread_inst_executed_op_fmul_pred_on.sum", "sm__sass_thread_inst_executed_op_fadd_pred_on.sum",
-           "sm__sass_thread_inst_executed_op_ffma_pred_on.sum"]
+           "sm__sass_thread_inst_executed_op_ffma_pred_on.sum",
+           # packed fp32 pairs (FMUL2 / FADD2 / FFMA2): two operations per thread instruction
+           "sm__sass_thread_inst_executed_op_fmul2_pred_on.sum", "sm__sass_thread_inst_executed_op_fadd2_pred_on.sum",
+           "sm__sass_thread_inst_executed_op_ffma2_pred_on.sum"]
 
 
 def ncu_counts(tool_args):
@@ -58,7 +61,8 @@ def ncu_counts(tool_args):
 
 
 def fp_ops(c):
-    return sum(c[m] for m in METRICS[2:])
+    """fp32 multiply / add / fma operations: scalar instructions + 2 x packed-pair instructions."""
+    return sum(c[m] for m in METRICS[2:5]) + 2 * sum(c[m] for m in METRICS[5:8])
 
 
 # R = 32: one 128-byte line per reduced row, so one L2 request per row; the

@@ -177,6 +177,26 @@ def test_index_out_of_range_reports_entry(systec):
         systec.mttkrp(3, 20, di, dv, dB)
 
 
+@pytest.mark.parametrize("n,dim", [(3, 500), (5, 10_007)])          # narrow keys / wide plan
+def test_bad_index_in_unsorted_input_is_the_first_one(systec, n, dim):
+    """Shuffled input: the one-pass prepare stops at the first published
+    disorder, so the verdict comes from the sorting path, which validates every
+    entry — the reported entry is the first bad one, wherever the others are."""
+    nnz = 300_000
+    rng = np.random.default_rng(n)
+    idx = rng.integers(0, dim, (nnz, n)).astype(np.int32)
+    vals = rng.uniform(-1, 1, nnz).astype(np.float32)
+    for bad_at in ([nnz - 5], [250_001, 299_000], [7, 123_456]):
+        bad = idx.copy()
+        for k, e in enumerate(bad_at):
+            bad[e, (e + k) % n] = dim if k % 2 == 0 else -1
+        with pytest.raises(IndexError, match=f"first bad entry {min(bad_at)}\\b"):
+            systec.Plan(n, dim, *to_dev(bad, vals))
+    plan = systec.Plan(n, dim, *to_dev(idx, vals))      # the clean spelling still plans
+    assert plan.stats()["input_was_sorted"] == 0
+    plan.destroy()
+
+
 def test_misaligned_views_take_scalar_path(systec):
     import torch
     w = small_random(3, 64, 3000, 8, seed=6, diag_frac=0.2)
