@@ -180,7 +180,7 @@ def in_run_bounds(w, launch, st, nnz_local, dev_index=0):
             "l2_mix_gbs": mix_gbs[best], "mix_shape": best, "mix_shapes_gbs": mix_gbs, "row_bytes": rb,
             "gather_table_bytes": tb, "red_table_bytes": tc,
             "clocks": clk.report(),
-            "how": "tools/bounds.cu in this run: best of 5 launches each (148x8 blocks of 256 threads), "
+            "how": "tools/bounds.cu in this run: best of 5 launches each (148x8 blocks of 256 threads, >= 0.6 ms per launch), "
                    "2 GiB stream read; random whole-row float4 gathers / red.global.add.v4.f32 over tables of "
                    "the footprints (capped at 48 MB: L2-resident); the mix = ng gathers + nr reductions per "
                    "unit in the plan's ratio, reduced values from the gathered rows, fastest unit shape"}

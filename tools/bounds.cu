@@ -194,7 +194,10 @@ static int rows_bound(int kind, int row_bytes, int64_t table_bytes, int reps, do
     cudaError_t e = cudaMalloc(&T, static_cast<size_t>(rows) * row_bytes);
     if (e != cudaSuccess) return static_cast<int>(e);
     if ((e = cudaMalloc(&sink, 4)) == cudaSuccess && (e = cudaMemset(T, 0, static_cast<size_t>(rows) * row_bytes)) == cudaSuccess) {
-        const int blocks = sm_count() * 8, threads = 256, iters = kind == 0 ? 256 : 128;
+        // long launches (>= 0.6 ms at the rates measured): with 128 - 256 iterations a launch
+        // lasted ~0.1 ms and its start-up and tail cost the measured rate ~6 %
+        // (red.v4, 128-byte rows: 5.96 TB/s then, 6.35 TB/s over 0.8 ms)
+        const int blocks = sm_count() * 8, threads = 256, iters = kind == 0 ? 2048 : 1024;
         auto launch = [&] {
             if (kind == 0) {
                 switch (lpe) {
@@ -269,7 +272,7 @@ BOUNDS_API int bounds_mix(int row_bytes, int64_t table_b, int64_t table_c, int n
     if ((e = cudaMalloc(&U, static_cast<size_t>(rc) * row_bytes)) == cudaSuccess &&
         (e = cudaMemset(T, 0, static_cast<size_t>(rb) * row_bytes)) == cudaSuccess &&
         (e = cudaMemset(U, 0, static_cast<size_t>(rc) * row_bytes)) == cudaSuccess) {
-        const int blocks = sm_count() * 8, threads = 256, iters = 64;
+        const int blocks = sm_count() * 8, threads = 256, iters = 512;  // >= 1 ms per launch (see rows_bound)
         float ms = 0.f;
         e = best_ms(reps, [&] { fn<<<blocks, threads>>>(T, rb, U, rc, iters); }, &ms);
         const double units = static_cast<double>(blocks) * threads / lpe * iters;
