@@ -256,6 +256,50 @@ def test_prepare_canonicalises_sorts_and_counts(systec):
     assert plan2.stats()["input_was_sorted"] == 1
 
 
+@pytest.mark.parametrize("order", [2, 3, 4, 5])
+def test_one_pass_prepare_edge_sizes(systec, order):
+    """The one-pass prepare (input already in storage order) at sizes around
+    its tile (1,024 entries), quad (4) and warp-window (512) boundaries, with
+    duplicates and long runs: the prepared stream, every statistic and the
+    padding equal numpy's; the same entries shuffled go through the sorting
+    path to the same stream."""
+    import math
+    import torch
+    rng = np.random.default_rng(100 + order)
+    for nnz in (1, 2, 3, 4, 5, 7, 511, 512, 513, 1023, 1024, 1025, 2047, 2049, 4096, 5000, 12289):
+        dim = int(rng.integers(1, 40))
+        idx = np.sort(rng.integers(0, dim, (nnz, order)), axis=1).astype(np.int32)
+        idx = idx[np.lexsort(idx.T[::-1])]                      # canonical, lexicographic, duplicates kept
+        vals = rng.uniform(-1, 1, nnz).astype(np.float32)
+        for shuffled in (False, True):
+            pi = rng.permutation(nnz) if shuffled else np.arange(nnz)
+            src_i, src_v = idx[pi], vals[pi]
+            if shuffled:                                        # and a non-canonical spelling of every tuple
+                src_i = np.take_along_axis(src_i, np.argsort(rng.random(src_i.shape), axis=1), axis=1)
+            plan = systec.Plan(order, dim, *to_dev(np.ascontiguousarray(src_i), np.ascontiguousarray(src_v)))
+            coords, pv = plan.prepared()
+            torch.cuda.synchronize()
+            assert np.array_equal(coords.cpu().numpy().T, idx), (order, nnz, shuffled)
+            if not shuffled:
+                assert np.array_equal(pv.cpu().numpy(), vals)
+            else:                                               # equal tuples keep their input order (stable sort)
+                want = src_v[np.lexsort(np.sort(src_i, axis=1).T[::-1])]
+                assert np.array_equal(pv.cpu().numpy(), want)
+            st = plan.stats()
+            c = idx.astype(np.int64)
+            eq = c[:, 1:] == c[:, :-1]
+            code = (eq * (1 << np.arange(order - 1))).sum(axis=1)
+            assert st["G"] == int(np.sum(order - eq.sum(axis=1))), (order, nnz, shuffled)
+            assert st["pattern_hist"][:1 << (order - 1)] == np.bincount(code, minlength=1 << (order - 1)).tolist()
+            assert st["lead_runs"] == len(np.unique(c[:, 0]))
+            assert st["max_lead_run"] == int(np.bincount(c[:, 0]).max())
+            assert st["pos1_runs"] == 1 + int(np.sum(c[1:, 1] != c[:-1, 1]))
+            assert st["expanded"] == oracle.count_expanded(order, idx)
+            sorted_now = bool(np.array_equal(np.sort(src_i, axis=1), idx))   # a shuffle of few entries can be the identity
+            assert st["input_was_sorted"] == int(sorted_now), (order, nnz, shuffled)
+            plan.destroy()
+
+
 @pytest.mark.parametrize("name", ["c1"])
 def test_config_c1_full(systec, name):
     w = generate(name)
