@@ -298,6 +298,17 @@ def test_one_pass_prepare_edge_sizes(systec, order):
             sorted_now = bool(np.array_equal(np.sort(src_i, axis=1), idx))   # a shuffle of few entries can be the identity
             assert st["input_was_sorted"] == int(sorted_now), (order, nnz, shuffled)
             plan.destroy()
+        if nnz in (5, 1025, 5000):      # idx / vals 4 bytes off a 16-byte boundary: the 4-byte staging and scalar value loads
+            bi = torch.zeros(nnz * order + 1, dtype=torch.int32, device="cuda")
+            bv = torch.zeros(nnz + 1, dtype=torch.float32, device="cuda")
+            bi[1:] = torch.from_numpy(idx.reshape(-1)).cuda()
+            bv[1:] = torch.from_numpy(vals).cuda()
+            plan = systec.Plan(order, dim, bi[1:].view(nnz, order), bv[1:])
+            coords, pv = plan.prepared()
+            torch.cuda.synchronize()
+            assert np.array_equal(coords.cpu().numpy().T, idx) and np.array_equal(pv.cpu().numpy(), vals)
+            assert plan.stats()["input_was_sorted"] == 1
+            plan.destroy()
 
 
 @pytest.mark.parametrize("name", ["c1"])
