@@ -74,7 +74,7 @@ template <int VW> struct VecT;
 template <> struct VecT<4> {
     using T = float4;
     static __device__ __forceinline__ T zero() { return make_float4(0.f, 0.f, 0.f, 0.f); }
-    // two packed-pair operations per float4 (FMUL2 / FADD2, ptx.cuh)
+    // mul2 / add2: scalar pairs by default, packed FMUL2 / FADD2 with -DSYSTEC_F32X2 (ptx.cuh)
     static __device__ __forceinline__ T mul(T a, T b) {
         T r;
         mul2(r.x, r.y, a.x, a.y, b.x, b.y);

@@ -111,8 +111,11 @@ __device__ __forceinline__ void red_add1(float *p, float v) {
 
 // Packed fp32 pairs (sm_100a FMUL2 / FADD2: two IEEE round-to-nearest fp32
 // operations per lane in one issue slot; element results identical to
-// FMUL / FADD).  -DSYSTEC_NO_F32X2 builds the scalar forms for A/B runs.
-#ifndef SYSTEC_NO_F32X2
+// FMUL / FADD).  Opt-in (-DSYSTEC_F32X2): measured, 18 % fewer instructions
+// per entry change no symmetric kernel's time and make the naive baseline
+// kernel 1.5 % (c2) to 5 % (c4) slower (profiles/r02/s4/f32x2_ab.txt), so the
+// default build keeps the scalar forms.
+#ifdef SYSTEC_F32X2
 __device__ __forceinline__ void mul2(float &r0, float &r1, float a0, float a1, float b0, float b1) {
     asm("{\n\t.reg .b64 ra, rb, rc;\n\tmov.b64 ra, {%2,%3};\n\tmov.b64 rb, {%4,%5};\n\t"
         "mul.rn.f32x2 rc, ra, rb;\n\tmov.b64 {%0,%1}, rc;\n\t}"
